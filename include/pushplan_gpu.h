@@ -1,0 +1,213 @@
+/*
+ * pushplan_gpu.h — C-ABI of the B200-native PMBS batched-rollout hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, int return codes, no
+ * exceptions and no torch types.  Each entry point names the reference
+ * interface (arxiv 2207.06649 "pushplan", /root/reference/proj/core) that it
+ * replaces.  A host binding (C++ adapter, ctypes, ...) marshals the reference
+ * value types into the flat arrays below; see INTEGRATION.md.
+ *
+ * Array conventions (all host pointers unless a function name ends in _dev):
+ *   poses     [E][n][3]  double  (x, y, theta) per object, reference Pose
+ *                               (world.hpp:49-56)
+ *   pushes    [E][4]     double  (x_s, y_s, x_e, y_e), reference PushAction
+ *                               (world.hpp:79-85)
+ *   status    [E]        int32   PPG_OK / PPG_START_COLLISION / PPG_NOT_CONVERGED
+ *                               (the two SimError throw sites push_sim.cpp:60-62
+ *                               and :123-128)
+ *   shapes    one table per environment or one table shared by all, see
+ *             ppg_shapes (reference ObjectShape world.hpp:33-46).
+ */
+#ifndef PUSHPLAN_GPU_H_
+#define PUSHPLAN_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPG_MAX_OBJECTS 32
+#define PPG_MAX_VERTICES 8
+
+/* return codes */
+#define PPG_SUCCESS 0
+#define PPG_EINVAL -1       /* bad argument (reference: SimError / SearchError on size checks) */
+#define PPG_ECUDA -2        /* CUDA runtime failure */
+#define PPG_ENOLEGAL -3     /* root has no legal push (reference SearchError mcts.cpp:244, pmbs.cpp:248) */
+#define PPG_ENODEVICE -4    /* no CUDA device: the product has no CPU fallback */
+
+/* per-element status (reference PushResult.error, push_sim.hpp:38-43) */
+#define PPG_OK 0
+#define PPG_START_COLLISION 1  /* push_sim.cpp:60-62 */
+#define PPG_NOT_CONVERGED 2    /* push_sim.cpp:123-128 */
+
+/* object kinds (reference ObjectShape::Kind, world.hpp:34) */
+#define PPG_DISC 0
+#define PPG_POLYGON 1
+
+/* Scene shapes.  n_tables == 1: every environment shares the table (a PMBS
+ * search: only poses differ between tree nodes); n_tables == E: one table per
+ * environment (reference batch_resolve over arbitrary WorldStates). */
+typedef struct ppg_shapes {
+  int32_t n_objects;            /* objects per environment, 1..PPG_MAX_OBJECTS */
+  int32_t n_tables;             /* 1 or E */
+  const int32_t* kind;          /* [n_tables][n_objects] PPG_DISC / PPG_POLYGON */
+  const double* radius;         /* [n_tables][n_objects] disc radius */
+  const int32_t* n_vertices;    /* [n_tables][n_objects]; NULL when all discs */
+  const double* vertices;       /* [n_tables][n_objects][PPG_MAX_VERTICES][2] local CCW; NULL when all discs */
+  const int32_t* target_index;  /* [n_tables] (WorldState::target_index, world.hpp:66) */
+  double side_length;           /* Workspace::side_length (world.hpp:18) */
+  double boundary_margin;       /* Workspace::boundary_margin (world.hpp:19) */
+} ppg_shapes;
+
+/* Every knob of the reference config structs, flattened.  ppg_params_default
+ * fills the reference defaults. */
+typedef struct ppg_params {
+  /* GripperTip (world.hpp:86-89) */
+  double tip_radius;            /* 0.012 */
+  double tip_clearance;         /* 0.002 */
+  /* SimParams (push_sim.hpp:14-20) */
+  double push_distance;         /* 0.05 */
+  int32_t substeps;             /* 64 */
+  int32_t max_projection_iters; /* 32 */
+  double eps_pen;               /* 1e-4 */
+  double rotation_gain;         /* 1.0 */
+  /* GraspGeometry (actions.hpp:21-26) */
+  double finger_width;          /* 0.02 */
+  double finger_thickness;      /* 0.01 */
+  double opening;               /* 0.085 */
+  double approach_clearance;    /* 0.003 */
+  /* SearchConfig (mcts.hpp:30-44) */
+  double gamma;                 /* 0.8 */
+  double c_explore;             /* 0.3 */
+  int32_t tree_depth;           /* 7 */
+  int32_t rollout_depth;        /* 3 */
+  int32_t pushes_per_object;    /* 16 */
+  double margin_threshold;      /* 0.003 */
+  uint64_t rng_seed;            /* 0 */
+  int32_t rank_by_ucb;          /* 0 */
+  int32_t budget_iterations;    /* 1: Budget::iterations(max_iterations); 0: Budget::seconds(max_seconds) */
+  int64_t max_iterations;       /* 0 */
+  double max_seconds;           /* 60.0 */
+  /* ParallelConfig (pmbs.hpp:24-28) */
+  int32_t n_envs;               /* 64 */
+  int32_t leaf_parallel;        /* 1 */
+} ppg_params;
+
+typedef struct ppg_ctx ppg_ctx;
+
+/* Search statistics (reference SearchStats, mcts.hpp:80-85). */
+typedef struct ppg_search_stats {
+  int64_t iterations;
+  int64_t expansions;
+  double elapsed_s;
+  int32_t stop_reason;          /* 0 budget, 1 explored, 2 early_stop */
+  int32_t final_tree_depth;     /* SearchTree::tree_depth at return */
+  int64_t env_steps;            /* resolve_push calls: expansions + rollout steps */
+  int64_t rollout_steps;        /* RolloutCursor::step calls that ran a push */
+  int64_t lockstep_rounds;
+  uint64_t signature_fnv;       /* FNV-1a-64 of tree_signature() text (mcts.cpp:296-300) */
+  int64_t n_nodes;
+} ppg_search_stats;
+
+/* Fills the reference defaults. */
+void ppg_params_default(ppg_params* p);
+
+/* Version / build string, e.g. "pmbs_b200 sm_100a fmad=false". */
+const char* ppg_version(void);
+
+/* Number of visible CUDA devices (0 on a host without a GPU; never touches a
+ * kernel). */
+int ppg_device_count(void);
+
+/* Creates a context on `device` (the WorkerPool seam of the reference:
+ * pmbs.cpp:250-251, push_sim.cpp:146-150).  Returns NULL and sets *err on
+ * failure.  One context per host thread. */
+ppg_ctx* ppg_create(int device, const ppg_params* params, int* err);
+void ppg_destroy(ppg_ctx* ctx);
+const char* ppg_last_error(ppg_ctx* ctx);
+
+/* Replaces the context's parameters (takes effect on the next call). */
+int ppg_set_params(ppg_ctx* ctx, const ppg_params* params);
+
+/* Installs the shared scene shapes used by ppg_expand / ppg_simulate /
+ * ppg_run_pmbs (SearchTree::create, mcts.cpp:28-39, fixes the shapes of a
+ * search).  shapes->n_tables must be 1. */
+int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes);
+
+/* batch_resolve (push_sim.hpp:48-51, push_sim.cpp:132-152): element-wise
+ * resolve_push (push_sim.cpp:58-130) with per-element status; never aborts
+ * siblings.  residual[e] = final max pairwise penetration (NULL allowed).
+ * shapes == NULL uses the context scene.  Synchronous w.r.t. host buffers. */
+int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in,
+                      const double* pushes, int E, double* poses_out, int32_t* status,
+                      double* residual);
+
+/* Same on device-resident buffers (all pointers are device pointers; shape
+ * arrays too), enqueued on `stream` (a cudaStream_t, NULL = default stream),
+ * asynchronous. */
+int ppg_batch_resolve_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, const double* poses_in,
+                          const double* pushes, int E, double* poses_out, int32_t* status,
+                          double* residual, void* stream);
+
+/* sample_pushes (actions.hpp:39-40, actions.cpp:51-73) for E states sharing
+ * the context scene: out[e][k] for k < count[e] in (object, angle) order,
+ * capacity n_objects * pushes_per_object per state. */
+int ppg_sample_pushes(ppg_ctx* ctx, const double* poses, int E, double* out, int32_t* count);
+
+/* graspable (actions.hpp:47-48, actions.cpp:113-147) for E states sharing the
+ * context scene: flag, margin, best (x, y, angle_index; angle_index -1 when no
+ * feasible pose). */
+int ppg_graspable(ppg_ctx* ctx, const double* poses, int E, uint8_t* graspable,
+                  double* margin, double* best_x, double* best_y, int32_t* best_angle);
+
+/* batch_expand prepare step (pmbs.hpp:51-52, pmbs.cpp:82-93): per pair,
+ * resolve_push -> sample_pushes (full list) -> graspable.  child_poses and
+ * untried follow the conventions above; untried capacity per pair is
+ * n_objects * pushes_per_object. */
+int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, int P,
+               double* child_poses, int32_t* status, uint8_t* graspable, int32_t* n_untried,
+               double* untried);
+
+/* batch_simulate / lockstep_simulate (pmbs.hpp:73-82, pmbs.cpp:133-234): the
+ * leaf-parallel lockstep rollouts of n_envs environments over n_nodes new
+ * nodes; env e uses the MT19937-64 stream keyed (seed, iteration, e)
+ * (rng.hpp:21-23).  node_meta[i] = {depth, graspable, dead}.  depth_cap =
+ * tree_depth + rollout_depth as they stand after this iteration's expansion
+ * (pmbs.cpp:230-231).  rewards_out[i] = max over node i's rollouts.
+ * counters (optional, 4 x int64): rollout steps, rounds, re-purposes, resolve
+ * calls. */
+int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes,
+                 int n_envs, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap,
+                 double* rewards_out, int64_t* counters);
+
+/* run_pmbs (pmbs.hpp:91, pmbs.cpp:242-292) on the context scene and poses:
+ * the full PMBS planning decision.  Tree kept on the host (C++), batched
+ * expansion and lockstep rollouts on the device.  action_out[4] = chosen push.
+ * Returns PPG_ENOLEGAL when the root has no legal push. */
+int ppg_run_pmbs(ppg_ctx* ctx, const double* root_poses, double* action_out,
+                 ppg_search_stats* stats);
+
+/* Same, and also writes the tree_signature text (mcts.cpp:284-300) into
+ * sig_buf (NUL-terminated, truncated to sig_cap); *sig_len = full length. */
+int ppg_run_pmbs_sig(ppg_ctx* ctx, const double* root_poses, double* action_out,
+                     ppg_search_stats* stats, char* sig_buf, int64_t sig_cap, int64_t* sig_len);
+
+/* FNV-1a state digest (world.cpp:166-191) of E states sharing `shapes`
+ * (n_tables 1 or E): bit-exact state identity. Host-only helper. */
+int ppg_state_digest(const ppg_shapes* shapes, const double* poses, int E, uint64_t* out);
+
+/* Algorithmic FP64 work counters for ppg_batch_resolve (SURVEY 8d formula):
+ * runs an instrumented variant of the physics kernel on device buffers and
+ * writes per-env counts [E][8] = {T_b, T_n, H_t, P_b, P_n, H_p, S, P_final}. */
+int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev,
+                                const double* poses_in, const double* pushes, int E,
+                                int64_t* counts_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PUSHPLAN_GPU_H_ */

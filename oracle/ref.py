@@ -1,0 +1,243 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes binding of oracle/_ref/libpushplan_ref.so,
+the unmodified reference (arxiv 2207.06649 pushplan core) + oracle/ref_shim.cpp."""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint64, c_void_p
+
+import numpy as np
+
+from paper_2207_06649_b200.abi import (PPG_MAX_VERTICES, PpgParams, PpgSearchStats, PpgShapes,
+                                       STOP_REASONS, dptr, i64ptr, iptr, u64ptr)
+from paper_2207_06649_b200.world import ShapeTable, WorldState
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_LIB = os.path.join(HERE, "_ref", "libpushplan_ref.so")
+_LIB = None
+
+
+def available() -> bool:
+    return os.path.exists(REF_LIB)
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not available():
+            raise RuntimeError(f"{REF_LIB} missing (build with `make -C oracle ref` where /root/reference exists)")
+        L = ctypes.CDLL(REF_LIB)
+        L.ref_states_new.restype = c_void_p
+        L.ref_states_new.argtypes = [POINTER(PpgShapes), POINTER(c_double), c_int]
+        L.ref_states_free.argtypes = [c_void_p]
+        L.ref_state_n.argtypes = [c_void_p, c_int]
+        L.ref_state_export.argtypes = [c_void_p, c_int, POINTER(c_int32), POINTER(c_double), POINTER(c_int32),
+                                       POINTER(c_double), POINTER(c_double), POINTER(c_int32),
+                                       POINTER(c_double), POINTER(c_double)]
+        L.ref_generate_case.restype = c_void_p
+        L.ref_generate_case.argtypes = [c_int, c_int, c_double, c_uint64]
+        L.ref_load_scene.restype = c_void_p
+        L.ref_load_scene.argtypes = [c_char_p]
+        L.ref_fixture.restype = c_void_p
+        L.ref_fixture.argtypes = [c_char_p, c_double, c_int]
+        L.ref_state_digest.restype = c_uint64
+        L.ref_state_digest.argtypes = [c_void_p, c_int]
+        L.ref_batch_resolve.argtypes = [c_void_p, POINTER(c_double), POINTER(PpgParams), c_int, POINTER(c_double)]
+        L.ref_batch_results.argtypes = [c_void_p, POINTER(c_double), POINTER(c_int32), POINTER(c_uint64)]
+        L.ref_sample_pushes.argtypes = [c_void_p, c_int, POINTER(PpgParams), POINTER(c_double), c_int]
+        L.ref_graspable.argtypes = [c_void_p, c_int, POINTER(PpgParams), POINTER(c_double), POINTER(c_double),
+                                    POINTER(c_double), POINTER(c_int32)]
+        L.ref_keyed_picks.argtypes = [c_uint64, c_uint64, c_uint64, c_int, c_uint64, POINTER(c_uint64)]
+        L.ref_keyed_raw.argtypes = [c_uint64, c_uint64, c_uint64, c_int, POINTER(c_uint64)]
+        L.ref_mix_keys.restype = c_uint64
+        L.ref_mix_keys.argtypes = [c_uint64, c_uint64, c_uint64]
+        L.ref_episode_seed.restype = c_uint64
+        L.ref_episode_seed.argtypes = [c_uint64, c_char_p, c_int]
+        L.ref_run_search.argtypes = [c_void_p, c_int, POINTER(PpgParams), c_int, c_int, POINTER(c_double),
+                                     POINTER(PpgSearchStats), c_char_p, c_int64, POINTER(c_int64)]
+        L.ref_first_iteration.argtypes = [c_void_p, c_int, POINTER(PpgParams), c_uint64, POINTER(c_double),
+                                          POINTER(c_int32), POINTER(c_double), POINTER(c_int32)]
+        L.ref_run_episode.argtypes = [c_void_p, c_int, c_char_p, c_int, POINTER(PpgParams), c_int, c_uint64,
+                                      c_int, POINTER(c_int32), POINTER(c_double)]
+        _LIB = L
+    return _LIB
+
+
+class Handle:
+    """Owns a std::vector<WorldState> inside the reference library."""
+
+    def __init__(self, ptr):
+        if not ptr:
+            raise RuntimeError("reference call failed")
+        self.ptr = ptr
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _LIB is not None:
+            _LIB.ref_states_free(self.ptr)
+            self.ptr = None
+
+    def export(self, i: int = 0) -> WorldState:
+        L = lib()
+        n = L.ref_state_n(self.ptr, i)
+        kind = np.zeros(n, np.int32)
+        radius = np.zeros(n, np.float64)
+        nv = np.zeros(n, np.int32)
+        verts = np.zeros((n, PPG_MAX_VERTICES, 2), np.float64)
+        poses = np.zeros((n, 3), np.float64)
+        tgt = c_int32()
+        side = c_double()
+        margin = c_double()
+        L.ref_state_export(self.ptr, i, iptr(kind), dptr(radius), iptr(nv), dptr(verts), dptr(poses),
+                           ctypes.byref(tgt), ctypes.byref(side), ctypes.byref(margin))
+        return WorldState(kind, radius, nv, verts, poses, tgt.value, side.value, margin.value)
+
+
+def states_handle(table: ShapeTable, poses: np.ndarray) -> Handle:
+    poses = np.ascontiguousarray(poses, np.float64)
+    E = poses.shape[0]
+    return Handle(lib().ref_states_new(ctypes.byref(table.struct()), dptr(poses), E))
+
+
+def state_handle(st: WorldState) -> Handle:
+    return states_handle(ShapeTable.shared(st), st.poses.reshape(1, st.n, 3))
+
+
+def generate_case(n_objects: int, polygon_fraction: float, seed: int, motif: int = 0) -> WorldState:
+    """bench::generate_case / generate_case_motif (bench.cpp:234-317)."""
+    h = Handle(lib().ref_generate_case(motif, n_objects, polygon_fraction, seed))
+    return h.export(0)
+
+
+def load_scene(path: str) -> WorldState:
+    h = Handle(lib().ref_load_scene(path.encode()))
+    return h.export(0)
+
+
+def fixture(name: str, arg: float = 0.0, iarg: int = 0) -> WorldState:
+    """tests/support/scenes.cpp fixtures."""
+    h = Handle(lib().ref_fixture(name.encode(), arg, iarg))
+    return h.export(0)
+
+
+def state_digest(st: WorldState) -> int:
+    h = state_handle(st)
+    return int(lib().ref_state_digest(h.ptr, 0))
+
+
+def batch_resolve(table: ShapeTable, poses: np.ndarray, pushes: np.ndarray, params: PpgParams,
+                  threads: int = 1):
+    """pushplan::batch_resolve (push_sim.cpp:132-152).  Returns poses_out,
+    status, digests, seconds (the reference call alone)."""
+    h = states_handle(table, poses)
+    pushes = np.ascontiguousarray(pushes, np.float64)
+    secs = c_double()
+    lib().ref_batch_resolve(h.ptr, dptr(pushes), ctypes.byref(params), threads, ctypes.byref(secs))
+    E = poses.shape[0]
+    out = np.zeros_like(np.ascontiguousarray(poses, np.float64))
+    status = np.zeros(E, np.int32)
+    dig = np.zeros(E, np.uint64)
+    lib().ref_batch_results(h.ptr, dptr(out), iptr(status), u64ptr(dig))
+    return out, status, dig, secs.value
+
+
+class PreparedBatch:
+    """States built once; ``run`` times only pushplan::batch_resolve."""
+
+    def __init__(self, table: ShapeTable, poses: np.ndarray, pushes: np.ndarray, params: PpgParams):
+        self.h = states_handle(table, poses)
+        self.pushes = np.ascontiguousarray(pushes, np.float64)
+        self.params = params
+        self.E = poses.shape[0]
+
+    def run(self, threads: int) -> float:
+        secs = c_double()
+        lib().ref_batch_resolve(self.h.ptr, dptr(self.pushes), ctypes.byref(self.params), threads,
+                                ctypes.byref(secs))
+        return secs.value
+
+
+def sample_pushes(st: WorldState, params: PpgParams) -> np.ndarray:
+    h = state_handle(st)
+    cap = st.n * params.pushes_per_object
+    out = np.zeros((cap, 4), np.float64)
+    k = lib().ref_sample_pushes(h.ptr, 0, ctypes.byref(params), dptr(out), cap)
+    return out[:k].copy()
+
+
+def graspable(st: WorldState, params: PpgParams):
+    h = state_handle(st)
+    m = c_double()
+    bx = c_double()
+    by = c_double()
+    bk = c_int32()
+    g = lib().ref_graspable(h.ptr, 0, ctypes.byref(params), ctypes.byref(m), ctypes.byref(bx),
+                            ctypes.byref(by), ctypes.byref(bk))
+    return bool(g), m.value, bx.value, by.value, bk.value
+
+
+def keyed_picks(seed: int, it: int, env: int, count: int, n: int) -> np.ndarray:
+    out = np.zeros(count, np.uint64)
+    lib().ref_keyed_picks(seed, it, env, count, n, u64ptr(out))
+    return out
+
+
+def keyed_raw(seed: int, it: int, env: int, count: int) -> np.ndarray:
+    out = np.zeros(count, np.uint64)
+    lib().ref_keyed_raw(seed, it, env, count, u64ptr(out))
+    return out
+
+
+def mix_keys(seed: int, a: int, b: int = 0) -> int:
+    return int(lib().ref_mix_keys(seed, a, b))
+
+
+def episode_seed(base: int, case_id: str, trial: int) -> int:
+    return int(lib().ref_episode_seed(base, case_id.encode(), trial))
+
+
+def run_search(st: WorldState, params: PpgParams, threads: int = 1, serial: bool = False,
+               want_sig: bool = False):
+    """run_pmbs (pmbs.cpp:242-292) / run_serial_mcts (mcts.cpp:237-282)."""
+    h = state_handle(st)
+    action = np.zeros(4, np.float64)
+    stats = PpgSearchStats()
+    slen = c_int64()
+    L = lib()
+    rc = L.ref_run_search(h.ptr, 0, ctypes.byref(params), threads, 1 if serial else 0, dptr(action),
+                          ctypes.byref(stats), None, 0, ctypes.byref(slen))
+    if rc != 0:
+        return {"rc": rc}
+    sig = None
+    if want_sig:
+        buf = ctypes.create_string_buffer(slen.value + 1)
+        L.ref_run_search(h.ptr, 0, ctypes.byref(params), threads, 1 if serial else 0, dptr(action),
+                         ctypes.byref(stats), buf, slen.value + 1, ctypes.byref(slen))
+        sig = buf.value.decode()
+    return {"rc": 0, "action": action, "iterations": stats.iterations, "expansions": stats.expansions,
+            "elapsed_s": stats.elapsed_s, "stop": STOP_REASONS[stats.stop_reason],
+            "final_tree_depth": stats.final_tree_depth, "sig_fnv": int(stats.signature_fnv),
+            "n_nodes": stats.n_nodes, "sig": sig}
+
+
+def first_iteration(st: WorldState, params: PpgParams, iteration: int = 0):
+    h = state_handle(st)
+    N = params.n_envs
+    poses = np.zeros((N, st.n, 3), np.float64)
+    meta = np.zeros((N, 3), np.int32)
+    rewards = np.zeros(N, np.float64)
+    cap = c_int32()
+    k = lib().ref_first_iteration(h.ptr, 0, ctypes.byref(params), iteration, dptr(poses), iptr(meta),
+                                  dptr(rewards), ctypes.byref(cap))
+    if k < 0:
+        raise RuntimeError("no legal push at the root")
+    return poses[:k].copy(), meta[:k].copy(), rewards[:k].copy(), cap.value
+
+
+def run_episode(st: WorldState, case_id: str, trial: int, params: PpgParams, threads: int = 1,
+                seed_base: int = 0, action_cap: int = 16):
+    h = state_handle(st)
+    comp = c_int32()
+    ps = c_double()
+    used = lib().ref_run_episode(h.ptr, 0, case_id.encode(), trial, ctypes.byref(params), threads,
+                                 seed_base, action_cap, ctypes.byref(comp), ctypes.byref(ps))
+    return {"actions_used": used, "completed": bool(comp.value), "planning_s": ps.value}
