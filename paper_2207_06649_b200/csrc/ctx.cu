@@ -1,0 +1,637 @@
+// ctx.cu — the C-ABI (include/pushplan_gpu.h) over the sm_100a kernels:
+// context, device buffers, shape upload and the host loops that drive the
+// kernels.  The PMBS tree planner that sits on top lives in planner.cpp.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+#include "kernels.cuh"
+
+namespace ppg {
+
+template <bool kCount>
+__global__ void resolve_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
+__global__ void shape_prep_kernel(ShapesDev S, const int* kind, const double* radius, const int* nv,
+                                  const double* verts, const int* target);
+__global__ void sample_kernel(const __grid_constant__ SimConst C, SampleArgs a);
+__global__ void grasp_kernel(const __grid_constant__ SimConst C, SampleArgs a);
+__global__ void expand_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
+__global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
+
+constexpr int kBlock = 128;
+constexpr size_t kMaxSmem = 3 * kMaxObjects * kBlock * sizeof(double);
+
+}  // namespace ppg
+
+using namespace ppg;
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                     \
+      return PPG_ECUDA;                                                                  \
+    }                                                                                    \
+  } while (0)
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 256 ? 256 : bytes;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct ppg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ppg_params params{};
+  std::string err;
+  // shared scene (ppg_set_scene)
+  bool has_scene = false;
+  ShapesDev scene;
+  std::vector<int32_t> h_kind, h_nv, h_target;
+  std::vector<double> h_radius, h_verts;
+  double side = 0.288, margin = 0.0;
+  DevBuf scene_buf, scene_in;
+  // per-call shape tables (batch_resolve with per-env shapes)
+  DevBuf shape_buf, shape_in;
+  // I/O scratch
+  DevBuf b_in, b_push, b_out, b_status, b_resid, b_a, b_b, b_c, b_d, b_e;
+  // lockstep state
+  DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx;
+  DevBuf l_W, l_rew, l_active, l_nactive, l_counters, l_npose, l_nmeta;
+  int32_t* h_nactive = nullptr;  // pinned
+};
+
+namespace {
+
+SimConst make_const(const ppg_params& p, int n, double side, double margin) {
+  SimConst C;
+  std::memset(&C, 0, sizeof C);
+  C.tip_r = p.tip_radius;
+  C.tip_clear = p.tip_clearance;
+  C.push_distance = p.push_distance;
+  C.substeps = p.substeps;
+  C.max_iters = p.max_projection_iters;
+  C.eps_pen = p.eps_pen;
+  C.gain = p.rotation_gain;
+  C.side = side;
+  C.margin = margin;
+  C.finger_width = p.finger_width;
+  C.finger_thickness = p.finger_thickness;
+  C.opening = p.opening;
+  C.approach_clearance = p.approach_clearance;
+  C.margin_threshold = p.margin_threshold;
+  C.na = p.pushes_per_object;
+  C.n = n;
+  // Same expressions and the same glibc as the reference (actions.cpp:59-60,
+  // :77-78; mcts.cpp:132 std::pow(double, int) == pow(double, double)).
+  const int n_per_object = p.pushes_per_object;
+  for (int k = 0; k < n_per_object && k < kMaxNa; ++k) {
+    const double angle = 2.0 * M_PI * k / n_per_object;
+    C.dir_cos[k] = std::cos(angle);
+    C.dir_sin[k] = std::sin(angle);
+  }
+  for (int k = 0; k < kGraspAngles; ++k) {
+    const double angle = 2.0 * M_PI * k / kGraspAngles;
+    C.g_cos[k] = std::cos(angle);
+    C.g_sin[k] = std::sin(angle);
+  }
+  for (int k = 0; k < kMaxGammaPow; ++k) C.gamma_pow[k] = std::pow(p.gamma, static_cast<double>(k));
+  return C;
+}
+
+int check_params(ppg_ctx* ctx, const ppg_params& p) {
+  if (p.pushes_per_object > kMaxNa) {
+    ctx->err = "pushes_per_object > 32 is not supported by the device sampler";
+    return PPG_EINVAL;
+  }
+  if (p.substeps < 1 || p.max_projection_iters < 0) {
+    ctx->err = "substeps must be >= 1";
+    return PPG_EINVAL;
+  }
+  if (p.tree_depth + p.rollout_depth >= kMaxGammaPow) {
+    ctx->err = "tree_depth + rollout_depth too large";
+    return PPG_EINVAL;
+  }
+  return PPG_SUCCESS;
+}
+
+// Uploads host shape arrays (ppg_shapes) and runs shape_prep_kernel into `S`.
+int upload_shapes(ppg_ctx* ctx, const ppg_shapes* sh, bool device_ptrs, DevBuf& in, DevBuf& buf, ShapesDev& S,
+                  cudaStream_t st) {
+  const int n = sh->n_objects, T = sh->n_tables;
+  if (n < 1 || n > kMaxObjects || T < 1) {
+    ctx->err = "n_objects must be in [1, 32] and n_tables >= 1";
+    return PPG_EINVAL;
+  }
+  const size_t tn = static_cast<size_t>(T) * n;
+  const size_t vbytes = tn * kMaxV * 2 * sizeof(double);
+  // layout of `buf`: kind | rad | br | nv | verts | target
+  const size_t off_rad = ((tn * 4 + 15) / 16) * 16;
+  const size_t off_br = off_rad + tn * 8;
+  const size_t off_nv = off_br + tn * 8;
+  const size_t off_v = off_nv + ((tn * 4 + 15) / 16) * 16;
+  const size_t off_t = off_v + vbytes;
+  CK(buf.ensure(off_t + T * 4 + 16));
+  char* b = buf.as<char>();
+  S.kind = reinterpret_cast<int*>(b);
+  S.rad = reinterpret_cast<double*>(b + off_rad);
+  S.br = reinterpret_cast<double*>(b + off_br);
+  S.nv = reinterpret_cast<int*>(b + off_nv);
+  S.verts = reinterpret_cast<double*>(b + off_v);
+  S.target = reinterpret_cast<int*>(b + off_t);
+  S.T = T;
+  S.n = n;
+  const int* kind = sh->kind;
+  const double* radius = sh->radius;
+  const int* nv = sh->n_vertices;
+  const double* verts = sh->vertices;
+  const int* target = sh->target_index;
+  if (!device_ptrs) {
+    // stage host arrays: kind | radius | nv | verts | target
+    const size_t o_r = ((tn * 4 + 15) / 16) * 16, o_nv = o_r + tn * 8, o_v = o_nv + ((tn * 4 + 15) / 16) * 16,
+                 o_t = o_v + vbytes;
+    CK(in.ensure(o_t + T * 4 + 16));
+    char* q = in.as<char>();
+    CK(cudaMemcpyAsync(q, sh->kind, tn * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(q + o_r, sh->radius, tn * 8, cudaMemcpyHostToDevice, st));
+    if (sh->n_vertices) CK(cudaMemcpyAsync(q + o_nv, sh->n_vertices, tn * 4, cudaMemcpyHostToDevice, st));
+    else CK(cudaMemsetAsync(q + o_nv, 0, tn * 4, st));
+    if (sh->vertices) CK(cudaMemcpyAsync(q + o_v, sh->vertices, vbytes, cudaMemcpyHostToDevice, st));
+    else CK(cudaMemsetAsync(q + o_v, 0, vbytes, st));
+    CK(cudaMemcpyAsync(q + o_t, sh->target_index, T * 4, cudaMemcpyHostToDevice, st));
+    kind = reinterpret_cast<int*>(q);
+    radius = reinterpret_cast<double*>(q + o_r);
+    nv = reinterpret_cast<int*>(q + o_nv);
+    verts = reinterpret_cast<double*>(q + o_v);
+    target = reinterpret_cast<int*>(q + o_t);
+  }
+  const int threads = 256;
+  const int total = static_cast<int>(tn > static_cast<size_t>(T) ? tn : T);
+  shape_prep_kernel<<<(total + threads - 1) / threads, threads, 0, st>>>(S, kind, radius, nv, verts, target);
+  CK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
+size_t smem_for(int n) { return static_cast<size_t>(3) * n * kBlock * sizeof(double); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+void ppg_params_default(ppg_params* p) {
+  std::memset(p, 0, sizeof *p);
+  p->tip_radius = 0.012;
+  p->tip_clearance = 0.002;
+  p->push_distance = 0.05;
+  p->substeps = 64;
+  p->max_projection_iters = 32;
+  p->eps_pen = 1e-4;
+  p->rotation_gain = 1.0;
+  p->finger_width = 0.02;
+  p->finger_thickness = 0.01;
+  p->opening = 0.085;
+  p->approach_clearance = 0.003;
+  p->gamma = 0.8;
+  p->c_explore = 0.3;
+  p->tree_depth = 7;
+  p->rollout_depth = 3;
+  p->pushes_per_object = 16;
+  p->margin_threshold = 0.003;
+  p->rng_seed = 0;
+  p->rank_by_ucb = 0;
+  p->budget_iterations = 0;
+  p->max_iterations = 0;
+  p->max_seconds = 60.0;
+  p->n_envs = 64;
+  p->leaf_parallel = 1;
+}
+
+const char* ppg_version(void) { return "pmbs_b200 0.1 sm_100a fp64 fmad=false"; }
+
+int ppg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
+  if (err) *err = PPG_SUCCESS;
+  const int nd = ppg_device_count();
+  if (nd <= 0 || device < 0 || device >= nd) {
+    if (err) *err = PPG_ENODEVICE;
+    return nullptr;
+  }
+  auto* ctx = new ppg_ctx;
+  ctx->device = device;
+  if (params) ctx->params = *params;
+  else ppg_params_default(&ctx->params);
+  if (check_params(ctx, ctx->params) != PPG_SUCCESS) {
+    if (err) *err = PPG_EINVAL;
+    delete ctx;
+    return nullptr;
+  }
+  bool ok = cudaSetDevice(device) == cudaSuccess && cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMallocHost(&ctx->h_nactive, sizeof(int32_t)) == cudaSuccess;
+  const int smem = static_cast<int>(kMaxSmem);
+  ok = ok && cudaFuncSetAttribute(resolve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(resolve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(grasp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(lock_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    if (err) *err = PPG_ECUDA;
+    ppg_destroy(ctx);
+    return nullptr;
+  }
+  return ctx;
+}
+
+void ppg_destroy(ppg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  DevBuf* bufs[] = {&ctx->scene_buf, &ctx->scene_in, &ctx->shape_buf, &ctx->shape_in, &ctx->b_in, &ctx->b_push,
+                    &ctx->b_out, &ctx->b_status, &ctx->b_resid, &ctx->b_a, &ctx->b_b, &ctx->b_c, &ctx->b_d,
+                    &ctx->b_e, &ctx->l_node, &ctx->l_pushes, &ctx->l_done, &ctx->l_byg, &ctx->l_harv,
+                    &ctx->l_flag, &ctx->l_reward, &ctx->l_poses, &ctx->l_mt, &ctx->l_mtidx, &ctx->l_W,
+                    &ctx->l_rew, &ctx->l_active, &ctx->l_nactive, &ctx->l_counters, &ctx->l_npose,
+                    &ctx->l_nmeta};
+  for (DevBuf* b : bufs) b->release();
+  if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* ppg_last_error(ppg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int ppg_set_params(ppg_ctx* ctx, const ppg_params* params) {
+  if (!ctx || !params) return PPG_EINVAL;
+  const int rc = check_params(ctx, *params);
+  if (rc != PPG_SUCCESS) return rc;
+  ctx->params = *params;
+  return PPG_SUCCESS;
+}
+
+int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
+  if (!ctx || !shapes || shapes->n_tables != 1) return PPG_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  const int n = shapes->n_objects;
+  ctx->h_kind.assign(shapes->kind, shapes->kind + n);
+  ctx->h_radius.assign(shapes->radius, shapes->radius + n);
+  ctx->h_nv.assign(n, 0);
+  if (shapes->n_vertices) ctx->h_nv.assign(shapes->n_vertices, shapes->n_vertices + n);
+  ctx->h_verts.assign(static_cast<size_t>(n) * kMaxV * 2, 0.0);
+  if (shapes->vertices) ctx->h_verts.assign(shapes->vertices, shapes->vertices + static_cast<size_t>(n) * kMaxV * 2);
+  ctx->h_target.assign(shapes->target_index, shapes->target_index + 1);
+  ctx->side = shapes->side_length;
+  ctx->margin = shapes->boundary_margin;
+  const int rc = upload_shapes(ctx, shapes, false, ctx->scene_in, ctx->scene_buf, ctx->scene, ctx->stream);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->has_scene = true;
+  return PPG_SUCCESS;
+}
+
+static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, double side, double margin, const double* d_in,
+                          const double* d_push, int E, double* d_out, int32_t* d_status, double* d_resid,
+                          long long* d_counts, cudaStream_t st) {
+  const SimConst C = make_const(ctx->params, S.n, side, margin);
+  ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
+  const int grid = (E + kBlock - 1) / kBlock;
+  if (d_counts) resolve_kernel<true><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
+  else resolve_kernel<false><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
+  CK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
+int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in, const double* pushes,
+                      int E, double* poses_out, int32_t* status, double* residual) {
+  if (!ctx || E < 0) return PPG_EINVAL;
+  if (E == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  ShapesDev S;
+  double side, margin;
+  if (shapes) {
+    if (shapes->n_tables != 1 && shapes->n_tables != E) {
+      ctx->err = "batch_resolve: states and shape tables must have equal length";
+      return PPG_EINVAL;
+    }
+    const int rc = upload_shapes(ctx, shapes, false, ctx->shape_in, ctx->shape_buf, S, st);
+    if (rc != PPG_SUCCESS) return rc;
+    side = shapes->side_length;
+    margin = shapes->boundary_margin;
+  } else {
+    if (!ctx->has_scene) {
+      ctx->err = "no scene installed";
+      return PPG_EINVAL;
+    }
+    S = ctx->scene;
+    side = ctx->side;
+    margin = ctx->margin;
+  }
+  const size_t pbytes = static_cast<size_t>(E) * S.n * 3 * sizeof(double);
+  CK(ctx->b_in.ensure(pbytes));
+  CK(ctx->b_out.ensure(pbytes));
+  CK(ctx->b_push.ensure(static_cast<size_t>(E) * 4 * sizeof(double)));
+  CK(ctx->b_status.ensure(static_cast<size_t>(E) * sizeof(int32_t)));
+  CK(ctx->b_resid.ensure(static_cast<size_t>(E) * sizeof(double)));
+  CK(cudaMemcpyAsync(ctx->b_in.p, poses_in, pbytes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->b_push.p, pushes, static_cast<size_t>(E) * 32, cudaMemcpyHostToDevice, st));
+  int rc = launch_resolve(ctx, S, side, margin, ctx->b_in.as<double>(), ctx->b_push.as<double>(), E,
+                          ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(), ctx->b_resid.as<double>(), nullptr, st);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(cudaMemcpyAsync(poses_out, ctx->b_out.p, pbytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(status, ctx->b_status.p, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToHost, st));
+  if (residual) CK(cudaMemcpyAsync(residual, ctx->b_resid.p, static_cast<size_t>(E) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_batch_resolve_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, const double* poses_in, const double* pushes,
+                          int E, double* poses_out, int32_t* status, double* residual, void* stream) {
+  if (!ctx || !shapes_dev || E < 0) return PPG_EINVAL;
+  if (E == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ShapesDev S;
+  const int rc = upload_shapes(ctx, shapes_dev, true, ctx->shape_in, ctx->shape_buf, S, st);
+  if (rc != PPG_SUCCESS) return rc;
+  return launch_resolve(ctx, S, shapes_dev->side_length, shapes_dev->boundary_margin, poses_in, pushes, E,
+                        poses_out, status, residual, nullptr, st);
+}
+
+int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, const double* poses_in,
+                                const double* pushes, int E, int64_t* counts_dev, void* stream) {
+  if (!ctx || !shapes_dev || E < 0) return PPG_EINVAL;
+  if (E == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ShapesDev S;
+  int rc = upload_shapes(ctx, shapes_dev, true, ctx->shape_in, ctx->shape_buf, S, st);
+  if (rc != PPG_SUCCESS) return rc;
+  const size_t pbytes = static_cast<size_t>(E) * S.n * 3 * sizeof(double);
+  CK(ctx->b_out.ensure(pbytes));
+  CK(ctx->b_status.ensure(static_cast<size_t>(E) * 4));
+  return launch_resolve(ctx, S, shapes_dev->side_length, shapes_dev->boundary_margin, poses_in, pushes, E,
+                        ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(), nullptr,
+                        reinterpret_cast<long long*>(counts_dev), st);
+}
+
+int ppg_sample_pushes(ppg_ctx* ctx, const double* poses, int E, double* out, int32_t* count) {
+  if (!ctx || E < 0) return PPG_EINVAL;
+  if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
+  }
+  if (E == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int n = ctx->scene.n, na = ctx->params.pushes_per_object;
+  const size_t pbytes = static_cast<size_t>(E) * n * 3 * 8, obytes = static_cast<size_t>(E) * n * na * 4 * 8;
+  CK(ctx->b_in.ensure(pbytes));
+  CK(ctx->b_out.ensure(obytes));
+  CK(ctx->b_status.ensure(static_cast<size_t>(E) * 4));
+  CK(cudaMemcpyAsync(ctx->b_in.p, poses, pbytes, cudaMemcpyHostToDevice, st));
+  const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
+  SampleArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(),
+               nullptr, nullptr, nullptr, nullptr, nullptr, E};
+  sample_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, ctx->b_out.p, obytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(count, ctx->b_status.p, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_graspable(ppg_ctx* ctx, const double* poses, int E, uint8_t* graspable, double* margin, double* best_x,
+                  double* best_y, int32_t* best_angle) {
+  if (!ctx || E < 0) return PPG_EINVAL;
+  if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
+  }
+  if (E == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int n = ctx->scene.n;
+  const size_t pbytes = static_cast<size_t>(E) * n * 3 * 8;
+  CK(ctx->b_in.ensure(pbytes));
+  CK(ctx->b_a.ensure(E));
+  CK(ctx->b_b.ensure(static_cast<size_t>(E) * 8));
+  CK(ctx->b_c.ensure(static_cast<size_t>(E) * 8));
+  CK(ctx->b_d.ensure(static_cast<size_t>(E) * 8));
+  CK(ctx->b_e.ensure(static_cast<size_t>(E) * 4));
+  CK(cudaMemcpyAsync(ctx->b_in.p, poses, pbytes, cudaMemcpyHostToDevice, st));
+  const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
+  SampleArgs a{ctx->scene, ctx->b_in.as<double>(), nullptr, nullptr, ctx->b_a.as<uint8_t>(),
+               ctx->b_b.as<double>(), ctx->b_c.as<double>(), ctx->b_d.as<double>(), ctx->b_e.as<int32_t>(), E};
+  grasp_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(graspable, ctx->b_a.p, E, cudaMemcpyDeviceToHost, st));
+  if (margin) CK(cudaMemcpyAsync(margin, ctx->b_b.p, static_cast<size_t>(E) * 8, cudaMemcpyDeviceToHost, st));
+  if (best_x) CK(cudaMemcpyAsync(best_x, ctx->b_c.p, static_cast<size_t>(E) * 8, cudaMemcpyDeviceToHost, st));
+  if (best_y) CK(cudaMemcpyAsync(best_y, ctx->b_d.p, static_cast<size_t>(E) * 8, cudaMemcpyDeviceToHost, st));
+  if (best_angle) CK(cudaMemcpyAsync(best_angle, ctx->b_e.p, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, int P, double* child_poses,
+               int32_t* status, uint8_t* graspable, int32_t* n_untried, double* untried) {
+  if (!ctx || P < 0) return PPG_EINVAL;
+  if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
+  }
+  if (P == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int n = ctx->scene.n, na = ctx->params.pushes_per_object;
+  const size_t pbytes = static_cast<size_t>(P) * n * 3 * 8, ubytes = static_cast<size_t>(P) * n * na * 4 * 8;
+  CK(ctx->b_in.ensure(pbytes));
+  CK(ctx->b_out.ensure(pbytes));
+  CK(ctx->b_push.ensure(static_cast<size_t>(P) * 32));
+  CK(ctx->b_status.ensure(static_cast<size_t>(P) * 4));
+  CK(ctx->b_a.ensure(P));
+  CK(ctx->b_e.ensure(static_cast<size_t>(P) * 4));
+  CK(ctx->b_b.ensure(ubytes));
+  CK(cudaMemcpyAsync(ctx->b_in.p, parent_poses, pbytes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->b_push.p, actions, static_cast<size_t>(P) * 32, cudaMemcpyHostToDevice, st));
+  const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
+  ExpandArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_push.as<double>(), ctx->b_out.as<double>(),
+               ctx->b_status.as<int32_t>(), ctx->b_a.as<uint8_t>(), ctx->b_e.as<int32_t>(), ctx->b_b.as<double>(), P};
+  expand_kernel<<<(P + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(child_poses, ctx->b_out.p, pbytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(status, ctx->b_status.p, static_cast<size_t>(P) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(graspable, ctx->b_a.p, P, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(n_untried, ctx->b_e.p, static_cast<size_t>(P) * 4, cudaMemcpyDeviceToHost, st));
+  if (untried) CK(cudaMemcpyAsync(untried, ctx->b_b.p, ubytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
+                 int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, double* rewards_out,
+                 int64_t* counters) {
+  if (!ctx) return PPG_EINVAL;
+  if (n_nodes <= 0) return PPG_SUCCESS;
+  if (n_envs < n_nodes) {
+    ctx->err = "lockstep_simulate: fewer environments than nodes";
+    return PPG_EINVAL;
+  }
+  if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
+  }
+  if (depth_cap + 1 >= kMaxGammaPow) {
+    ctx->err = "depth cap too large";
+    return PPG_EINVAL;
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int n = ctx->scene.n;
+  const int used = leaf_parallel ? n_envs : n_nodes;
+  const int E = used;
+  CK(ctx->l_node.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_pushes.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_done.ensure(E));
+  CK(ctx->l_byg.ensure(E));
+  CK(ctx->l_harv.ensure(E));
+  CK(ctx->l_flag.ensure(E));
+  CK(ctx->l_reward.ensure(static_cast<size_t>(E) * 8));
+  CK(ctx->l_poses.ensure(static_cast<size_t>(E) * 3 * n * 8));
+  CK(ctx->l_mt.ensure(static_cast<size_t>(E) * 312 * 8));
+  CK(ctx->l_mtidx.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_W.ensure(static_cast<size_t>(n_nodes) * 4));
+  CK(ctx->l_rew.ensure(static_cast<size_t>(n_nodes) * 8));
+  CK(ctx->l_active.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_nactive.ensure(4));
+  CK(ctx->l_counters.ensure(4 * 8));
+  CK(ctx->l_npose.ensure(static_cast<size_t>(n_nodes) * n * 3 * 8));
+  CK(ctx->l_nmeta.ensure(static_cast<size_t>(n_nodes) * 3 * 4));
+  CK(cudaMemcpyAsync(ctx->l_npose.p, node_poses, static_cast<size_t>(n_nodes) * n * 3 * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->l_nmeta.p, node_meta, static_cast<size_t>(n_nodes) * 3 * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ctx->l_counters.p, 0, 32, st));
+  const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
+  LockArgs a;
+  a.S = ctx->scene;
+  a.node_poses = ctx->l_npose.as<double>();
+  a.node_meta = ctx->l_nmeta.as<int32_t>();
+  a.n_nodes = n_nodes;
+  a.used = used;
+  a.leaf_parallel = leaf_parallel;
+  a.cap = depth_cap;
+  a.seed = seed;
+  a.iteration = iteration;
+  a.env_node = ctx->l_node.as<int32_t>();
+  a.env_pushes = ctx->l_pushes.as<int32_t>();
+  a.env_done = ctx->l_done.as<uint8_t>();
+  a.env_bygrasp = ctx->l_byg.as<uint8_t>();
+  a.env_harvested = ctx->l_harv.as<uint8_t>();
+  a.env_flag = ctx->l_flag.as<uint8_t>();
+  a.env_reward = ctx->l_reward.as<double>();
+  a.env_poses = ctx->l_poses.as<double>();
+  a.mt = ctx->l_mt.as<uint64_t>();
+  a.mt_idx = ctx->l_mtidx.as<int32_t>();
+  a.E = E;
+  a.W = ctx->l_W.as<int32_t>();
+  a.rew = ctx->l_rew.as<unsigned long long>();
+  a.active = ctx->l_active.as<int32_t>();
+  a.n_active = ctx->l_nactive.as<int32_t>();
+  a.counters = ctx->l_counters.as<long long>();
+  const int ginit = ((E > n_nodes ? E : n_nodes) + 255) / 256;
+  lock_init_kernel<<<ginit, 256, 0, st>>>(C, a);
+  CK(cudaGetLastError());
+  for (;;) {
+    lock_harvest_kernel<<<1, 1024, 0, st>>>(C, a);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_nactive, a.n_active, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int act = *ctx->h_nactive;
+    if (act == 0) break;
+    lock_step_kernel<<<(act + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(rewards_out, a.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
+  if (counters) CK(cudaMemcpyAsync(counters, a.counters, 32, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_state_digest(const ppg_shapes* sh, const double* poses, int E, uint64_t* out) {
+  if (!sh || !poses || !out) return PPG_EINVAL;
+  const int n = sh->n_objects;
+  for (int e = 0; e < E; ++e) {
+    const int t = sh->n_tables == 1 ? 0 : e;
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&h](const void* data, size_t len) {
+      const unsigned char* p = static_cast<const unsigned char*>(data);
+      for (size_t i = 0; i < len; ++i) {
+        h ^= p[i];
+        h *= 1099511628211ull;
+      }
+    };
+    const int32_t tgt = sh->target_index[t];
+    mix(&tgt, 4);
+    mix(&sh->side_length, 8);
+    for (int i = 0; i < n; ++i) {
+      const int32_t kind = sh->kind[t * n + i];
+      mix(&kind, 4);
+      mix(&sh->radius[t * n + i], 8);
+      if (kind != PPG_DISC && sh->n_vertices && sh->vertices)
+        for (int k = 0; k < sh->n_vertices[t * n + i]; ++k)
+          mix(&sh->vertices[((static_cast<size_t>(t) * n + i) * kMaxV + k) * 2], 16);
+      mix(&poses[(static_cast<size_t>(e) * n + i) * 3], 24);
+    }
+    out[e] = h;
+  }
+  return PPG_SUCCESS;
+}
+
+}  // extern "C"
+
+// internal accessors for planner.cpp
+namespace ppg {
+const ppg_params& ctx_params(const ppg_ctx* ctx) { return ctx->params; }
+int ctx_n_objects(const ppg_ctx* ctx) { return ctx->has_scene ? ctx->scene.n : 0; }
+void ctx_set_error(ppg_ctx* ctx, const char* msg) { ctx->err = msg; }
+}  // namespace ppg

@@ -1,0 +1,364 @@
+// kernels.cu — sm_100a kernels of the PMBS batched-rollout hot path.
+//
+//  shape_prep_kernel      ppg_shapes AoS -> [object][table] SoA + bounding radii
+//  resolve_kernel<C>      batch_resolve  (push_sim.cpp:132-152), C = work counters
+//  sample_kernel          sample_pushes  (actions.cpp:51-73), full ordered list
+//  grasp_kernel           graspable      (actions.cpp:113-147)
+//  expand_kernel          batch_expand prepare (pmbs.cpp:82-93)
+//  lock_init_kernel       env split + RolloutCursor ctor + keyed MT seeding
+//                         (pmbs.cpp:138-149, mcts.cpp:121-140, pmbs.cpp:211-213)
+//  lock_harvest_kernel    harvest_and_repurpose (pmbs.cpp:165-187) + active list
+//  lock_step_kernel       RolloutCursor::step (mcts.cpp:142-171)
+//
+// One environment per lane; the environment's poses are staged in shared
+// memory (see physics.cuh).  Everything is FP64 with --fmad=false.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace ppg {
+
+__global__ void shape_prep_kernel(ShapesDev S, const int* kind, const double* radius, const int* nv,
+                                  const double* verts, const int* target) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int T = S.T, n = S.n;
+  if (idx < T) S.target[idx] = target[idx];
+  if (idx >= T * n) return;
+  const int t = idx / n, i = idx % n;
+  const int k = kind[idx];
+  const double r = radius[idx];
+  const int nvert = nv ? nv[idx] : 0;
+  double br = r;
+  if (k != 0) {  // ObjectShape::bounding_radius world.cpp:32-37
+    br = 0.0;
+    for (int v = 0; v < nvert; ++v) {
+      const double x = verts[(static_cast<size_t>(idx) * kMaxV + v) * 2];
+      const double y = verts[(static_cast<size_t>(idx) * kMaxV + v) * 2 + 1];
+      br = dmax(br, sqrt(x * x + y * y));
+    }
+  }
+  S.kind[i * T + t] = k;
+  S.rad[i * T + t] = r;
+  S.br[i * T + t] = br;
+  S.nv[i * T + t] = nvert;
+  for (int v = 0; v < kMaxV; ++v) {
+    const bool ok = verts != nullptr && k != 0;
+    S.verts[(static_cast<size_t>(idx) * kMaxV + v) * 2] = ok ? verts[(static_cast<size_t>(idx) * kMaxV + v) * 2] : 0.0;
+    S.verts[(static_cast<size_t>(idx) * kMaxV + v) * 2 + 1] =
+        ok ? verts[(static_cast<size_t>(idx) * kMaxV + v) * 2 + 1] : 0.0;
+  }
+}
+
+// Stages environment e's AoS poses into this lane's shared-memory column.
+PPG_DI PoseView stage_poses(double* smem, int n, const double* src) {
+  PoseView P{smem + threadIdx.x, static_cast<int>(blockDim.x), n};
+  for (int i = 0; i < n; ++i) {
+    P.x(i) = src[i * 3];
+    P.y(i) = src[i * 3 + 1];
+    P.th(i) = src[i * 3 + 2];
+  }
+  return P;
+}
+
+PPG_DI void unstage_poses(const PoseView& P, double* dst) {
+  for (int i = 0; i < P.n; ++i) {
+    dst[i * 3] = P.x(i);
+    dst[i * 3 + 1] = P.y(i);
+    dst[i * 3 + 2] = P.th(i);
+  }
+}
+
+template <bool kCount>
+__global__ void __launch_bounds__(128) resolve_kernel(const __grid_constant__ SimConst C, ResolveArgs a) {
+  extern __shared__ double smem[];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.E) return;
+  const int n = C.n;
+  const PoseView P = stage_poses(smem, n, a.poses_in + static_cast<size_t>(e) * n * 3);
+  const ShapeView S = a.S.view(a.S.T == 1 ? 0 : e);
+  const double* pu = a.pushes + static_cast<size_t>(e) * 4;
+  double residual = 0.0;
+  Counts cnt{0, 0, 0, 0, 0, 0, 0, 0};
+  const int st = resolve_push<kCount>(P, S, C, V2{pu[0], pu[1]}, V2{pu[2], pu[3]}, true, &residual, &cnt);
+  a.status[e] = st;
+  if (a.residual) a.residual[e] = residual;
+  double* out = a.poses_out + static_cast<size_t>(e) * n * 3;
+  if (st == 0) {
+    unstage_poses(P, out);
+  } else {
+    for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
+  }
+  if (kCount) {
+    long long* q = a.counts + static_cast<size_t>(e) * 8;
+    q[0] = cnt.tb; q[1] = cnt.tn; q[2] = cnt.ht; q[3] = cnt.pb;
+    q[4] = cnt.pn; q[5] = cnt.hp; q[6] = cnt.s; q[7] = cnt.pfinal;
+  }
+}
+
+template __global__ void resolve_kernel<false>(const __grid_constant__ SimConst, ResolveArgs);
+template __global__ void resolve_kernel<true>(const __grid_constant__ SimConst, ResolveArgs);
+
+// Full ordered candidate list (object, angle) of sample_pushes.
+PPG_DI int sample_all(const PoseView& P, const ShapeView& S, const SimConst& C, double* out) {
+  int count = 0;
+  for (int o = 0; o < S.n; ++o)
+    for (int k = 0; k < C.na; ++k) {
+      V2 s, t;
+      if (!push_candidate(P, S, C, o, k, true, s, t)) continue;
+      double* q = out + static_cast<size_t>(count) * 4;
+      q[0] = s.x; q[1] = s.y; q[2] = t.x; q[3] = t.y;
+      ++count;
+    }
+  return count;
+}
+
+__global__ void __launch_bounds__(128) sample_kernel(const __grid_constant__ SimConst C, SampleArgs a) {
+  extern __shared__ double smem[];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.E) return;
+  const int n = C.n;
+  const PoseView P = stage_poses(smem, n, a.poses + static_cast<size_t>(e) * n * 3);
+  const ShapeView S = a.S.view(a.S.T == 1 ? 0 : e);
+  a.count[e] = sample_all(P, S, C, a.out + static_cast<size_t>(e) * n * C.na * 4);
+}
+
+__global__ void __launch_bounds__(128) grasp_kernel(const __grid_constant__ SimConst C, SampleArgs a) {
+  extern __shared__ double smem[];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.E) return;
+  const int n = C.n;
+  const PoseView P = stage_poses(smem, n, a.poses + static_cast<size_t>(e) * n * 3);
+  const int t = a.S.T == 1 ? 0 : e;
+  const ShapeView S = a.S.view(t);
+  const GraspOut g = graspable(P, S, C, a.S.target[t]);
+  a.grasp[e] = g.graspable ? 1 : 0;
+  a.margin[e] = g.margin;
+  a.bx[e] = g.x;
+  a.by[e] = g.y;
+  a.bk[e] = g.k;
+}
+
+__global__ void __launch_bounds__(128) expand_kernel(const __grid_constant__ SimConst C, ExpandArgs a) {
+  extern __shared__ double smem[];
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.P) return;
+  const int n = C.n;
+  const double* parent = a.parent_poses + static_cast<size_t>(p) * n * 3;
+  const PoseView P = stage_poses(smem, n, parent);
+  const ShapeView S = a.S.view(0);
+  const double* act = a.actions + static_cast<size_t>(p) * 4;
+  double residual;
+  const int st = resolve_push<false>(P, S, C, V2{act[0], act[1]}, V2{act[2], act[3]}, true, &residual, nullptr);
+  a.status[p] = st;
+  double* child = a.child_poses + static_cast<size_t>(p) * n * 3;
+  if (st != 0) {  // dead child: copy of the parent state (mcts.cpp:89-92)
+    for (int i = 0; i < n * 3; ++i) child[i] = parent[i];
+    a.grasp[p] = 0;
+    a.n_untried[p] = 0;
+    return;
+  }
+  unstage_poses(P, child);
+  a.n_untried[p] = sample_all(P, S, C, a.untried + static_cast<size_t>(p) * n * C.na * 4);
+  a.grasp[p] = graspable(P, S, C, a.S.target[0]).graspable ? 1 : 0;
+}
+
+// ---------------- lockstep engine ----------------
+
+// RolloutCursor ctor (mcts.cpp:121-140) for env e at node `node`.
+PPG_DI void cursor_init(const SimConst& C, const LockArgs& a, int e, int node) {
+  const int32_t* m = a.node_meta + node * 3;
+  const int depth = m[0];
+  a.env_node[e] = node;
+  a.env_pushes[e] = depth;
+  uint8_t done = 0, byg = 0;
+  double reward = 0.0;
+  if (m[1]) {
+    done = 1;
+    byg = 1;
+    reward = C.gamma_pow[depth];
+  } else if (m[2]) {
+    done = 1;
+  } else if (depth >= a.cap) {
+    done = 1;
+  }
+  a.env_done[e] = done;
+  a.env_bygrasp[e] = byg;
+  a.env_reward[e] = reward;
+  const int n = C.n;
+  const double* src = a.node_poses + static_cast<size_t>(node) * n * 3;
+  for (int i = 0; i < n; ++i) {
+    a.env_poses[(static_cast<size_t>(i)) * a.E + e] = src[i * 3];
+    a.env_poses[(static_cast<size_t>(n + i)) * a.E + e] = src[i * 3 + 1];
+    a.env_poses[(static_cast<size_t>(2 * n + i)) * a.E + e] = src[i * 3 + 2];
+  }
+}
+
+__global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < a.n_nodes) a.rew[e] = 0ull;
+  if (e >= a.used) return;
+  // Even split, remainder to earlier nodes (pmbs.cpp:138-149).
+  const int base = a.used / a.n_nodes, rem = a.used % a.n_nodes;
+  const int big = rem * (base + 1);
+  const int node = e < big ? e / (base + 1) : rem + (e - big) / base;
+  cursor_init(C, a, e, node);
+  a.env_harvested[e] = 0;
+  a.env_flag[e] = 0;
+  MtView g{a.mt + e, a.E};
+  mt_seed(g, mix_keys(a.seed, a.iteration, static_cast<uint64_t>(e)));
+  a.mt_idx[e] = 312;
+}
+
+// harvest_and_repurpose (pmbs.cpp:165-187) + next round's active list.  One
+// block.  Rewards are order-free (max of non-negative doubles via their bit
+// patterns); the re-purposing decisions are sequential in env order and run
+// in warp 0: argmax of per-node remaining work W (strict >, W > 0, lowest
+// node on ties), then W[best] += cap - depth(best).  This reproduces the
+// reference's O(E*N*E) rescan exactly in O(E + repurposes * N / 32).
+__global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  const int tid = threadIdx.x;
+  const int B = blockDim.x;
+  __shared__ int s_active;
+  __shared__ long long s_rep;
+  if (tid == 0) {
+    s_active = 0;
+    s_rep = 0;
+  }
+  for (int i = tid; i < a.n_nodes; i += B) a.W[i] = 0;
+  __syncthreads();
+  for (int e = tid; e < a.used; e += B) {
+    if (!a.env_done[e]) {
+      atomicAdd(&a.W[a.env_node[e]], a.cap - a.env_pushes[e]);
+      a.env_flag[e] = 0;
+    } else if (!a.env_harvested[e]) {
+      a.env_harvested[e] = 1;
+      atomicMax(&a.rew[a.env_node[e]], static_cast<unsigned long long>(__double_as_longlong(a.env_reward[e])));
+      a.env_flag[e] = (a.leaf_parallel && a.env_bygrasp[e]) ? 1 : 0;
+    } else {
+      a.env_flag[e] = 0;
+    }
+  }
+  __syncthreads();
+  if (a.leaf_parallel && tid < 32) {
+    const int lane = tid;
+    for (int base = 0; base < a.used; base += 32) {
+      const int e = base + lane;
+      unsigned m = __ballot_sync(0xffffffffu, e < a.used && a.env_flag[e] == 1);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int ce = base + src;
+        int bw = 0, bi = -1;
+        for (int i = lane; i < a.n_nodes; i += 32) {
+          const int w = a.W[i];
+          if (w > bw) {
+            bw = w;
+            bi = i;
+          }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
+            bw = ow;
+            bi = oi;
+          }
+        }
+        if (bi >= 0) {
+          if (lane == 0) {
+            a.W[bi] += a.cap - a.node_meta[bi * 3];
+            a.env_flag[ce] = 2;
+            a.env_node[ce] = bi;
+            ++s_rep;
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < a.used; e += B) {
+    if (a.env_flag[e] == 2) {
+      cursor_init(C, a, e, a.env_node[e]);
+      a.env_harvested[e] = 0;
+      a.env_flag[e] = 0;
+    }
+  }
+  __syncthreads();
+  for (int e0 = 0; e0 < a.used; e0 += B) {
+    const int e = e0 + tid;
+    const bool act = e < a.used && !a.env_done[e];
+    if (act) a.active[atomicAdd(&s_active, 1)] = e;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    *a.n_active = s_active;
+    a.counters[2] += s_rep;
+    if (s_active > 0) a.counters[1] += 1;
+  }
+}
+
+// RolloutCursor::step (mcts.cpp:142-171) for each active env.
+__global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  extern __shared__ double smem[];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_act = *a.n_active;
+  if (gid >= n_act) return;
+  const int e = a.active[gid];
+  const int n = C.n;
+  PoseView P{smem + threadIdx.x, static_cast<int>(blockDim.x), n};
+  for (int i = 0; i < 3 * n; ++i) P.p[i * P.stride] = a.env_poses[static_cast<size_t>(i) * a.E + e];
+  const ShapeView S = a.S.view(0);
+  // sample_pushes: count the valid candidates, remembering which (bitmask).
+  uint32_t mask[(kMaxObjects * kMaxNa) / 32];
+  const int total = n * C.na;
+  int count = 0;
+  for (int c = 0; c < total; ++c) {
+    if ((c & 31) == 0) mask[c >> 5] = 0;
+    V2 s, t;
+    if (push_candidate(P, S, C, c / C.na, c % C.na, true, s, t)) {
+      mask[c >> 5] |= 1u << (c & 31);
+      ++count;
+    }
+  }
+  if (count == 0) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  MtView g{a.mt + e, a.E};
+  int idx = a.mt_idx[e];
+  const uint64_t k = mt_pick(g, idx, static_cast<uint64_t>(count));
+  a.mt_idx[e] = idx;
+  int c = 0;
+  for (uint64_t seen = 0;; ++c) {
+    if (mask[c >> 5] >> (c & 31) & 1u) {
+      if (seen == k) break;
+      ++seen;
+    }
+  }
+  V2 s, t;
+  push_candidate(P, S, C, c / C.na, c % C.na, false, s, t);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), 1ull);
+  double residual;
+  const int st = resolve_push<false>(P, S, C, s, t, false, &residual, nullptr);
+  if (st != 0) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  const int pushes = a.env_pushes[e] + 1;
+  a.env_pushes[e] = pushes;
+  if (graspable(P, S, C, a.S.target[0]).graspable) {
+    a.env_done[e] = 1;
+    a.env_bygrasp[e] = 1;
+    a.env_reward[e] = C.gamma_pow[pushes];
+  } else if (pushes >= a.cap) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+  }
+  for (int i = 0; i < 3 * n; ++i) a.env_poses[static_cast<size_t>(i) * a.E + e] = P.p[i * P.stride];
+}
+
+}  // namespace ppg

@@ -1,0 +1,91 @@
+// kernels.cuh — kernel argument blocks shared by the kernels (kernels.cu) and
+// the host context (ctx.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "physics.cuh"
+
+namespace ppg {
+
+struct ShapesDev {
+  int* kind = nullptr;      // [n][T]
+  double* rad = nullptr;    // [n][T]
+  double* br = nullptr;     // [n][T]
+  int* nv = nullptr;        // [n][T]
+  double* verts = nullptr;  // [T][n][kMaxV][2]
+  int* target = nullptr;    // [T]
+  int T = 0;
+  int n = 0;
+  int capT = 0;
+  __host__ __device__ ShapeView view(int t) const { return ShapeView{kind, rad, br, nv, verts, T, t, n}; }
+};
+
+struct ResolveArgs {
+  ShapesDev S;
+  const double* poses_in;  // [E][n][3]
+  const double* pushes;    // [E][4]
+  double* poses_out;       // [E][n][3]
+  int32_t* status;         // [E]
+  double* residual;        // [E] or null
+  long long* counts;       // [E][8] (counting variant)
+  int E;
+};
+
+struct SampleArgs {
+  ShapesDev S;
+  const double* poses;  // [E][n][3]
+  double* out;          // [E][n*na][4]
+  int32_t* count;       // [E]
+  uint8_t* grasp;       // [E] (grasp kernel)
+  double* margin;       // [E]
+  double* bx;           // [E]
+  double* by;           // [E]
+  int32_t* bk;          // [E]
+  int E;
+};
+
+struct ExpandArgs {
+  ShapesDev S;
+  const double* parent_poses;  // [P][n][3]
+  const double* actions;       // [P][4]
+  double* child_poses;         // [P][n][3]
+  int32_t* status;             // [P]
+  uint8_t* grasp;              // [P]
+  int32_t* n_untried;          // [P]
+  double* untried;             // [P][n*na][4]
+  int P;
+};
+
+// Lockstep engine state (pmbs.cpp:133-205), all in HBM.
+struct LockArgs {
+  ShapesDev S;
+  const double* node_poses;  // [n_nodes][n][3]
+  const int32_t* node_meta;  // [n_nodes][3] depth, graspable, dead
+  int n_nodes;
+  int used;       // environments in use
+  int leaf_parallel;
+  int cap;        // depth cap d_T + d_s
+  uint64_t seed, iteration;
+  // per-env
+  int32_t* env_node;
+  int32_t* env_pushes;
+  uint8_t* env_done;
+  uint8_t* env_bygrasp;
+  uint8_t* env_harvested;
+  uint8_t* env_flag;
+  double* env_reward;
+  double* env_poses;    // [3][n][E] planes, env fastest
+  uint64_t* mt;         // [312][E]
+  int32_t* mt_idx;      // [E]
+  int E;                // allocated stride for env arrays
+  // per-node
+  int32_t* W;                // [n_nodes] remaining work
+  unsigned long long* rew;   // [n_nodes] max reward bits (rewards >= 0)
+  // round bookkeeping
+  int32_t* active;           // [used]
+  int32_t* n_active;         // [1]
+  long long* counters;       // [4] steps, rounds, repurposes, resolve calls
+};
+
+}  // namespace ppg

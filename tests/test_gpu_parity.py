@@ -1,0 +1,183 @@
+"""GPU parity: the CUDA path through the C-ABI against the golden fixtures
+(made by the unmodified reference) and the CPU oracle.  Bit-exact for discs;
+polygon poses within the stated tolerance until the device sincos is
+glibc-exact (the only non-bitwise item)."""
+import numpy as np
+import pytest
+
+import golden_io
+from oracle import port
+from paper_2207_06649_b200 import ParallelConfig, SearchError, ShapeTable, default_params
+from paper_2207_06649_b200 import batch_resolve, graspable, run_pmbs, sample_pushes
+from paper_2207_06649_b200.api import Budget, GripperTip, SimParams, SimError, resolve_push
+
+pytestmark = pytest.mark.gpu
+P = default_params()
+POLY_POSE_TOL = 1e-9  # metres / radians: device sin/cos vs glibc (<= 2 ulp) on polygon rotation
+
+
+def _bitwise(a, b):
+    return np.all(a.view(np.uint64) == b.view(np.uint64), axis=tuple(range(1, a.ndim)))
+
+
+@pytest.mark.parametrize("name", ["discs", "ring16", "hard18"])
+def test_batch_resolve_discs_bitwise(ctx, name):
+    t, poses, pushes, status, digests, out_ref = golden_io.resolve_set(name)
+    ctx.set_params(P)
+    out, st, resid = ctx.batch_resolve_arrays(t, poses, pushes)
+    assert np.array_equal(st, status)
+    ok = status == 0
+    assert _bitwise(out[ok], out_ref[ok]).all()
+    assert np.array_equal(port.state_digests(t, out)[ok], digests[ok])
+    assert np.all(out[~ok] == 0.0)
+    assert np.all(resid[status == 2] > P.eps_pen)
+
+
+def test_batch_resolve_polygons(ctx):
+    t, poses, pushes, status, digests, out_ref = golden_io.resolve_set("polygons")
+    ctx.set_params(P)
+    out, st, _ = ctx.batch_resolve_arrays(t, poses, pushes)
+    assert np.array_equal(st, status)
+    assert np.max(np.abs(out - out_ref)) <= POLY_POSE_TOL
+    bit = _bitwise(out, out_ref)
+    all_disc = np.all(t.kind == 0, axis=1)
+    assert bit[all_disc].all()
+    assert bit.mean() > 0.9
+
+
+def test_batch_resolve_shared_scene_and_reference_api(ctx):
+    cases = golden_io.cases()
+    c, st = cases[12]
+    sp = port.sample_pushes(st, P)
+    res = batch_resolve([st] * len(sp), list(sp), GripperTip(), SimParams(), ctx=ctx)
+    exp, est, _ = port.batch_resolve(ShapeTable.shared(st), np.repeat(st.poses[None], len(sp), 0), sp, P)
+    for k, r in enumerate(res):
+        assert r.ok() == (est[k] == 0)
+        if r.ok():
+            assert _bitwise(r.state.poses[None], exp[k][None]).all()
+
+
+def test_batch_resolve_edge_cases(ctx):
+    c, st = golden_io.cases()[0]
+    # empty batch
+    assert batch_resolve([], [], ctx=ctx) == []
+    # size mismatch -> SimError (push_sim.cpp:136-137)
+    with pytest.raises(SimError):
+        batch_resolve([st], [], ctx=ctx)
+    # start collision -> per-element error, siblings unaffected (test_pushworld.cpp:321-330)
+    good = port.sample_pushes(st, P)[0]
+    tgt = st.poses[0]
+    bad = np.array([tgt[0], tgt[1], tgt[0] + 0.05, tgt[1]])
+    res = batch_resolve([st, st], [bad, good], ctx=ctx)
+    assert not res[0].ok() and "collides" in res[0].error
+    assert res[1].ok()
+    with pytest.raises(SimError):
+        resolve_push(st, bad, ctx=ctx)
+
+
+def test_single_disc_closed_form(ctx):
+    """test_pushworld.cpp:170-182: x = 0.05 - gap within 1e-12 relative."""
+    from paper_2207_06649_b200.world import WorldState
+    r = 0.016
+    st = WorldState.from_objects([{"kind": "disc", "radius": r, "pose": [0.0, 0.0, 0.0]}])
+    gap = 0.004
+    sx = -(r + 0.012 + gap)
+    out = resolve_push(st, [sx, 0.0, sx + 0.05, 0.0], ctx=ctx)
+    assert abs(out.poses[0, 0] - (0.05 - gap)) <= 1e-12 * (0.05 - gap)
+    assert out.poses[0, 1] == 0.0 and out.poses[0, 2] == 0.0
+
+
+def test_sample_and_grasp_cases(ctx):
+    ctx.set_params(P)
+    for c, st in golden_io.cases():
+        sp = sample_pushes(st, 16, ctx=ctx)
+        assert len(sp) == c["n_pushes"], c["case_id"]
+        if np.all(st.kind == 0):
+            assert golden_io.fnv_bytes(sp.tobytes()) == int(c["pushes_fnv"]), c["case_id"]
+        else:
+            assert np.max(np.abs(sp - port.sample_pushes(st, P))) <= POLY_POSE_TOL
+        g = graspable(st, ctx=ctx)
+        assert g.graspable == c["graspable"], c["case_id"]
+        if np.all(st.kind == 0):
+            assert g.margin == c["margin"]
+            assert (list(g.best) if g.best else [0.0, 0.0, -1]) == c["best"]
+
+
+def test_expand_matches_oracle(ctx):
+    ctx.set_params(P)
+    for c, st in golden_io.cases()[10:14]:
+        ctx.set_scene(st)
+        sp = port.sample_pushes(st, P)
+        parents = np.repeat(st.poses[None], len(sp), 0)
+        child, status, g, nu, un = ctx.expand_arrays(parents, sp)
+        exp, est, _ = port.batch_resolve(ShapeTable.shared(st), parents, sp, P)
+        assert np.array_equal(status, est)
+        for k in range(len(sp)):
+            if est[k] != 0:
+                assert _bitwise(child[k][None], parents[k][None]).all() and nu[k] == 0
+                continue
+            assert _bitwise(child[k][None], exp[k][None]).all()
+            s2 = st.with_poses(exp[k])
+            sp2 = port.sample_pushes(s2, P)
+            assert nu[k] == len(sp2)
+            assert _bitwise(un[k, :nu[k]][None], sp2[None]).all()
+            assert bool(g[k]) == port.graspable(s2, P)[0]
+
+
+def test_simulate_matches_reference_golden(ctx):
+    cases = {c["case_id"]: st for c, st in golden_io.cases()}
+    for cid, ne, seed, cap, poses, meta, rewards in golden_io.simulate_sets():
+        st = cases[cid]
+        ctx.set_params(default_params(n_envs=ne, rng_seed=seed))
+        ctx.set_scene(st)
+        r, ctr = ctx.simulate_arrays(poses, meta, ne, True, seed, 0, cap)
+        if np.all(st.kind == 0):
+            assert np.array_equal(r, rewards), cid
+        else:
+            assert np.mean(r == rewards) > 0.9, cid
+        ro, co = port.simulate(st, poses, meta, ne, True, seed, 0, cap, default_params(n_envs=ne))
+        if np.all(st.kind == 0):
+            assert np.array_equal(ctr, co), cid
+
+
+def test_simulate_no_leaf_parallel_and_validation(ctx):
+    c, st = golden_io.cases()[12]
+    ctx.set_params(P)
+    ctx.set_scene(st)
+    sp = port.sample_pushes(st, P)[:5]
+    exp, est, _ = port.batch_resolve(ShapeTable.shared(st), np.repeat(st.poses[None], 5, 0), sp, P)
+    meta = np.array([[1, 0, 0]] * 5, np.int32)
+    r, _ = ctx.simulate_arrays(exp, meta, 8, False, 3, 1, 10)
+    ro, _ = port.simulate(st, exp, meta, 8, False, 3, 1, 10, P)
+    assert np.array_equal(r, ro)
+    with pytest.raises(ValueError):
+        ctx.simulate_arrays(exp, meta, 4, True, 3, 1, 10)
+
+
+@pytest.mark.parametrize("idx", list(range(20)))
+def test_first_decision_fingerprints(ctx, idx):
+    """SURVEY A.5 / tests/golden/cases.json: run_pmbs at the reference
+    defaults (N_e = 64) reproduces the reference's decision; on disc scenes
+    also the exact tree (FNV of tree_signature) and search statistics."""
+    c, st = golden_io.cases()[idx]
+    d = c["decision"]
+    cfg = ParallelConfig(rng_seed=int(c["seed"]))
+    r = run_pmbs(st, cfg, ctx=ctx)
+    assert r.stop_reason == d["stop"]
+    assert r.iterations == d["iterations"] and r.expansions == d["expansions"]
+    assert r.final_tree_depth == d["final_tree_depth"]
+    if np.all(st.kind == 0):
+        assert list(r.action) == d["action"]
+        assert r.signature_fnv == int(d["sig_fnv"])
+    else:
+        assert np.max(np.abs(r.action - np.array(d["action"]))) <= POLY_POSE_TOL
+
+
+def test_run_pmbs_budget_and_errors(ctx):
+    from paper_2207_06649_b200.world import WorldState
+    giant = WorldState.from_objects([{"kind": "disc", "radius": 0.2, "pose": [0.0, 0.0, 0.0]}])
+    with pytest.raises(SearchError):
+        run_pmbs(giant, ParallelConfig(), ctx=ctx)
+    c, st = golden_io.cases()[17]
+    r = run_pmbs(st, ParallelConfig(budget=Budget.iterations(3), rng_seed=5), ctx=ctx)
+    assert r.iterations == 3 and r.stop_reason == "budget"
