@@ -42,7 +42,6 @@ def test_batch_resolve_polygons(ctx):
     bit = _bitwise(out, out_ref)
     all_disc = np.all(t.kind == 0, axis=1)
     assert bit[all_disc].all()
-    assert bit.mean() > 0.9
 
 
 def test_batch_resolve_shared_scene_and_reference_api(ctx):
