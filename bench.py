@@ -1,0 +1,389 @@
+"""bench.py — BASELINE.json config 2 on B200: batched push-physics throughput.
+
+One step = one batch_resolve (push_sim.cpp:132-152) over E = 65,536 synthetic
+10-disc clutter scenes (generate_case(10, ShapeMix{0.0}, 1000 + k), bench.cpp:
+234-259) with one sampled push each (sample_pushes(scene, 16)[pick(keyed_rng(7,
+k))]), i.e. the single-push-action rollout horizon.  Metric:
+simulated env-steps/s (one env-step = one resolve_push, SimError included).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+ours:      `value` = device-resident throughput (CUDA events on the launching
+           stream, L2 flushed between steps, max over ranks); `e2e` = the same
+           metric through the host C-ABI call ppg_batch_resolve with pinned
+           host buffers (H2D + kernel + D2H per step); `roofline` = FP64-pipe
+           fraction of the physics kernel; `cpu_baseline` = the reference
+           (oracle/_ref, or the C restatement) on a bounded sample, rank 0, N=1.
+reference: the unmodified reference batch_resolve (oracle/_ref) with every
+           host thread, on a bounded sample of the same workload; rank 0 only.
+Multi-GPU (torchrun): each rank simulates its own E scenes (weak scaling; the
+environments are independent, so there is no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated env-steps/sec (batch_resolve, 10-disc clutter, 1 push per env)"
+UNIT = "env-steps/s"
+E_DEFAULT = 65536
+N_OBJ = 10
+
+
+def formula_ops(counts: np.ndarray, n: int) -> np.ndarray:
+    """Algorithmic FP64 ops of resolve_push per env: +,-,*,/,sqrt
+    each 1; counts columns T_b, T_n, H_t, P_b, P_n, H_p, S, P_final."""
+    tb, tn, ht, pb, pn, hp, s, pf = (counts[:, i].astype(np.float64) for i in range(8))
+    return (7 * tb + 15 * tn + 4 * ht + 7 * pb + 15 * pn + 10 * hp + 4 * s + 17 * n
+            + 7 * n * (n - 1) / 2 + 15 * pf)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def dist_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_sample(table, poses, pushes, params, sample: int, min_seconds: float, threads: int):
+    """The reference batch_resolve (oracle/_ref) on the first `sample` envs,
+    repeated until min_seconds; falls back to the C restatement (port)."""
+    from oracle import port, ref
+    from paper_2207_06649_b200.scenes import _take
+    idx = np.arange(sample)
+    t = _take(table, idx)
+    if ref.available():
+        pb = ref.PreparedBatch(t, poses[:sample], pushes[:sample], params)
+        pb.run(threads)  # warm-up
+        total, reps = 0.0, 0
+        while total < min_seconds:
+            total += pb.run(threads)
+            reps += 1
+        return {"value": sample * reps / total, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": f"first {sample} envs of the workload x {reps} passes, pushplan::batch_resolve "
+                          f"(oracle/_ref, unmodified reference, -O3) with WorkerPool({threads})"}
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < min_seconds:
+        port.batch_resolve(t, poses[:sample], pushes[:sample], params)
+        reps += 1
+    dt = time.perf_counter() - t0
+    return {"value": sample * reps / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"first {sample} envs x {reps} passes, oracle/pmbs_oracle.c (1 thread)"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle import ref
+    from paper_2207_06649_b200.abi import default_params
+    params = default_params()
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample
+    cfg = {"workload": f"C2 batch_resolve, E={args.envs} generate_case({N_OBJ}) disc scenes, 1 push/env",
+           "envs": args.envs, "objects": N_OBJ, "polygon_fraction": 0.0, "l2": "n/a (CPU)"}
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "metric": METRIC, "unit": UNIT,
+                          "unavailable": "oracle/_ref/libpushplan_ref.so not built (needs /root/reference)"}))
+        return
+    # Inputs built by the reference itself: generate_case + sample_pushes + keyed pick.
+    states, pushes = [], []
+    k = 0
+    seed = 1000
+    while len(states) < sample:
+        try:
+            s = ref.generate_case(N_OBJ, 0.0, seed)
+        except RuntimeError:
+            seed += 1
+            continue
+        sp = ref.sample_pushes(s, params)
+        if len(sp):
+            states.append(s)
+            pushes.append(sp[int(ref.keyed_picks(7, k, 0, 1, len(sp))[0])])
+            k += 1
+        seed += 1
+    from paper_2207_06649_b200.world import ShapeTable
+    t = ShapeTable.per_env(states)
+    pb = ref.PreparedBatch(t, np.stack([s.poses for s in states]), np.stack(pushes), params)
+    for _ in range(args.warmup):
+        pb.run(threads)
+    total = sum(pb.run(threads) for _ in range(args.steps))
+    value = sample * args.steps / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generate_case scenes, reference-sampled pushes)", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{sample} envs per step, pushplan::batch_resolve with WorkerPool({threads})"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2207_06649_b200 import Context, abi
+    from paper_2207_06649_b200.abi import PpgShapes, default_params
+    from paper_2207_06649_b200.scenes import c2_workload
+
+    torch.cuda.set_device(local)
+    params = default_params()
+    ctx = Context(local, params)
+    E = args.envs
+    t0 = time.perf_counter()
+    table, poses, pushes, seeds = c2_workload(ctx, E, N_OBJ, 0.0, seed_base=1000 + rank * 2 * E)
+    gen_s = time.perf_counter() - t0
+    n = N_OBJ
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    d_poses = torch.from_numpy(poses).to(dev)
+    d_push = torch.from_numpy(pushes).to(dev)
+    d_kind = torch.from_numpy(table.kind).to(dev)
+    d_rad = torch.from_numpy(table.radius).to(dev)
+    d_tgt = torch.from_numpy(table.target_index).to(dev)
+    d_out = torch.empty_like(d_poses)
+    d_status = torch.empty(E, dtype=torch.int32, device=dev)
+    d_resid = torch.empty(E, dtype=torch.float64, device=dev)
+    sh = PpgShapes(n, E, ctypes.cast(d_kind.data_ptr(), ctypes.POINTER(ctypes.c_int32)),
+                   ctypes.cast(d_rad.data_ptr(), ctypes.POINTER(ctypes.c_double)), None, None,
+                   ctypes.cast(d_tgt.data_ptr(), ctypes.POINTER(ctypes.c_int32)), 0.288, 0.0)
+    lib = ctx.lib
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+
+    def step(e=E):
+        rc = lib.ppg_batch_resolve_dev(ctx.ptr, ctypes.byref(sh), d_poses.data_ptr(), d_push.data_ptr(), e,
+                                       d_out.data_ptr(), d_status.data_ptr(), d_resid.data_ptr(), sptr)
+        if rc != 0:
+            raise RuntimeError(lib.ppg_last_error(ctx.ptr).decode())
+
+    # algorithmic work of this exact workload (instrumented kernel, untimed)
+    d_counts = torch.zeros((E, 8), dtype=torch.int64, device=dev)
+    rc = lib.ppg_batch_resolve_count_dev(ctx.ptr, ctypes.byref(sh), d_poses.data_ptr(), d_push.data_ptr(), E,
+                                         d_counts.data_ptr(), sptr)
+    assert rc == 0, lib.ppg_last_error(ctx.ptr)
+    torch.cuda.synchronize(dev)
+    ops_total = float(formula_ops(d_counts.cpu().numpy(), n).sum())
+    peak = ctypes.c_double()
+    lib.ppg_measure_fp64_peak(ctx.ptr, ctypes.byref(peak), None)
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    dist_barrier(world)
+    torch.cuda.synchronize(dev)
+    for k in range(args.steps):
+        flush.zero_()
+        starts[k].record(stream)
+        step()
+        ends[k].record(stream)
+    torch.cuda.synchronize(dev)
+    dist_barrier(world)
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_s = dist_max(sum(step_ms) * 1e-3, world)
+    status = d_status.cpu().numpy()
+    value = E * world * args.steps / total_s
+    ms_per_step = 1e3 * total_s / args.steps
+    launch_s = sum(step_ms) * 1e-3 / args.steps
+    achieved = ops_total / launch_s
+    roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
+            "frac": achieved / peak.value, "traffic": None,
+            "note": "algorithmic FP64 ops (+,-,*,/,sqrt = 1 each, SURVEY 8d formula, counted on this workload) per "
+                    "step / step time; peak = measured DFMA instr/s (= FP64 FLOP/s / 2) on this GPU; HBM is not "
+                    "the bound (" + f"{(E * (n * 3 * 8 * 2 + 32 + 4 + 8 + n * 12)) / launch_s / 1e9:.1f}" +
+                    " GB/s algorithmic vs 6548 measured)",
+            "ops_per_env_step": ops_total / E}
+
+    # e2e through the host C-ABI (pinned host buffers; H2D + kernels + D2H in the region)
+    h_poses = torch.from_numpy(poses).pin_memory()
+    h_push = torch.from_numpy(pushes).pin_memory()
+    h_kind = torch.from_numpy(table.kind).pin_memory()
+    h_rad = torch.from_numpy(table.radius).pin_memory()
+    h_tgt = torch.from_numpy(table.target_index).pin_memory()
+    h_out = torch.empty_like(h_poses).pin_memory()
+    h_status = torch.empty(E, dtype=torch.int32).pin_memory()
+    h_resid = torch.empty(E, dtype=torch.float64).pin_memory()
+    hsh = PpgShapes(n, E, ctypes.cast(h_kind.data_ptr(), ctypes.POINTER(ctypes.c_int32)),
+                    ctypes.cast(h_rad.data_ptr(), ctypes.POINTER(ctypes.c_double)), None, None,
+                    ctypes.cast(h_tgt.data_ptr(), ctypes.POINTER(ctypes.c_int32)), 0.288, 0.0)
+
+    def e2e_step():
+        rc = lib.ppg_batch_resolve(ctx.ptr, ctypes.byref(hsh),
+                                   ctypes.cast(h_poses.data_ptr(), ctypes.POINTER(ctypes.c_double)),
+                                   ctypes.cast(h_push.data_ptr(), ctypes.POINTER(ctypes.c_double)), E,
+                                   ctypes.cast(h_out.data_ptr(), ctypes.POINTER(ctypes.c_double)),
+                                   ctypes.cast(h_status.data_ptr(), ctypes.POINTER(ctypes.c_int32)),
+                                   ctypes.cast(h_resid.data_ptr(), ctypes.POINTER(ctypes.c_double)))
+        if rc != 0:
+            raise RuntimeError(lib.ppg_last_error(ctx.ptr).decode())
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    e2e_total = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        e2e_step()
+        e2e_total += time.perf_counter() - t1
+    e2e_total = dist_max(e2e_total, world)
+    assert np.array_equal(h_status.numpy(), status), "e2e and device-resident results differ"
+    h2d = poses.nbytes + pushes.nbytes + table.kind.nbytes + table.radius.nbytes + table.target_index.nbytes
+    d2h = poses.nbytes + E * 4 + E * 8
+
+    # E sweep 1K..64K (config 2's range), device-resident, same timing rules
+    sweep = {}
+    for e in (1024, 2048, 4096, 8192, 16384, 32768, 65536):
+        if e > E:
+            break
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for _ in range(5):
+            flush.zero_()
+            st.record(stream)
+            step(e)
+            en.record(stream)
+            torch.cuda.synchronize(dev)
+            tot += st.elapsed_time(en) * 1e-3
+        sweep[str(e)] = e * 5 / tot
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: generate_case(10, ShapeMix{0.0}, seed) scenes (host generator, bit-identical to "
+                    "the reference's), push = sample_pushes(scene,16)[keyed_rng(7,k) pick]",
+            "config": {"workload": f"C2 batch_resolve: E={E} envs per GPU x {N_OBJ} discs, single push-action "
+                                   "horizon (BASELINE configs[1])", "envs_per_gpu": E, "objects": N_OBJ,
+                       "polygon_fraction": 0.0, "l2": "flushed between steps (256 MB write)",
+                       "parallelism": f"{world} independent env shards (weak)"},
+            "e2e": {"value": E * world * args.steps / e2e_total, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "api": "ppg_batch_resolve (host C-ABI, pinned buffers)"},
+            "roofline": roof, "clocks": clk, "gpu_launches": 2 * args.steps,
+            "status_counts": np.bincount(status, minlength=3).tolist(), "sweep_env_steps_per_s": sweep,
+            "workload_gen_s": gen_s}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_reference_sample(table, poses, pushes, params, min(args.ref_sample, E),
+                                                    args.cpu_seconds, os.cpu_count() or 1)
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--envs", type=int, default=E_DEFAULT)
+    ap.add_argument("--ref-sample", type=int, default=8192)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        # rank 0 alone times the CPU reference; other ranks exit without work
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
+    world, rank, local = dist_setup(args.gpus)
+    if True:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

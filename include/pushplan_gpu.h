@@ -152,10 +152,11 @@ int ppg_batch_resolve_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, const doub
                           const double* pushes, int E, double* poses_out, int32_t* status,
                           double* residual, void* stream);
 
-/* sample_pushes (actions.hpp:39-40, actions.cpp:51-73) for E states sharing
- * the context scene: out[e][k] for k < count[e] in (object, angle) order,
- * capacity n_objects * pushes_per_object per state. */
-int ppg_sample_pushes(ppg_ctx* ctx, const double* poses, int E, double* out, int32_t* count);
+/* sample_pushes (actions.hpp:39-40, actions.cpp:51-73) for E states:
+ * out[e][k] for k < count[e] in (object, angle) order, capacity n_objects *
+ * pushes_per_object per state.  shapes == NULL uses the context scene. */
+int ppg_sample_pushes(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses, int E, double* out,
+                      int32_t* count);
 
 /* graspable (actions.hpp:47-48, actions.cpp:113-147) for E states sharing the
  * context scene: flag, margin, best (x, y, angle_index; angle_index -1 when no
@@ -205,6 +206,29 @@ int ppg_state_digest(const ppg_shapes* shapes, const double* poses, int E, uint6
 int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev,
                                 const double* poses_in, const double* pushes, int E,
                                 int64_t* counts_dev, void* stream);
+
+/* Measurement helper (not on the hot path): the FP64 CUDA-core pipe peak in
+ * DFMA instructions per second, from a dependent-chain microbenchmark on the
+ * context's device — the roofline denominator of the FP64 kernels. */
+int ppg_measure_fp64_peak(ppg_ctx* ctx, double* dfma_per_s, double* seconds);
+
+/* ---- host-side input generators (no device needed) ---- */
+
+/* bench::generate_case / generate_case_motif (bench.cpp:234-317): one scene
+ * per seed, bit-identical to the reference generator (same libstdc++
+ * std::mt19937_64 and distributions, same glibc).  motif 0 random, 1 ring,
+ * 2 wall.  Outputs are [count][n_objects] tables in the ppg_shapes layout
+ * plus poses [count][n_objects][3]; ok[c] = 0 where the reference throws
+ * (rejection sampling exhausted).  `threads` host threads split the seeds. */
+int ppg_generate_cases(int motif, int n_objects, double polygon_fraction, const uint64_t* seeds, int count,
+                       int32_t* kind, double* radius, int32_t* n_vertices, double* vertices, double* poses,
+                       int32_t* target_index, int32_t* ok, int threads);
+
+/* out[c] = std::uniform_int_distribution<size_t>(0, n[c]-1) applied once to
+ * keyed_rng(seed, a[c], b[c]) (rng.hpp:21-23, mcts.cpp:151-152); a or b may
+ * be NULL (0). */
+int ppg_keyed_picks(uint64_t seed, const uint64_t* a, const uint64_t* b, const uint64_t* n, int count,
+                    uint64_t* out);
 
 #ifdef __cplusplus
 }

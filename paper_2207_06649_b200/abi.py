@@ -147,7 +147,7 @@ SIGNATURES = {
                                   c_int, POINTER(c_double), POINTER(c_int32), POINTER(c_double)]),
     "ppg_batch_resolve_dev": (c_int, [c_void_p, POINTER(PpgShapes), c_void_p, c_void_p, c_int,
                                       c_void_p, c_void_p, c_void_p, c_void_p]),
-    "ppg_sample_pushes": (c_int, [c_void_p, POINTER(c_double), c_int, POINTER(c_double),
+    "ppg_sample_pushes": (c_int, [c_void_p, POINTER(PpgShapes), POINTER(c_double), c_int, POINTER(c_double),
                                   POINTER(c_int32)]),
     "ppg_graspable": (c_int, [c_void_p, POINTER(c_double), c_int, POINTER(c_uint8), POINTER(c_double),
                               POINTER(c_double), POINTER(c_double), POINTER(c_int32)]),
@@ -161,6 +161,12 @@ SIGNATURES = {
     "ppg_state_digest": (c_int, [POINTER(PpgShapes), POINTER(c_double), c_int, POINTER(c_uint64)]),
     "ppg_batch_resolve_count_dev": (c_int, [c_void_p, POINTER(PpgShapes), c_void_p, c_void_p, c_int,
                                             c_void_p, c_void_p]),
+    "ppg_measure_fp64_peak": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
+    "ppg_generate_cases": (c_int, [c_int, c_int, c_double, POINTER(c_uint64), c_int, POINTER(c_int32),
+                                   POINTER(c_double), POINTER(c_int32), POINTER(c_double), POINTER(c_double),
+                                   POINTER(c_int32), POINTER(c_int32), c_int]),
+    "ppg_keyed_picks": (c_int, [c_uint64, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64), c_int,
+                                POINTER(c_uint64)]),
 }
 
 _LIB = None

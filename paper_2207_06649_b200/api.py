@@ -204,13 +204,15 @@ class Context:
                                                dptr(resid)), "ppg_batch_resolve")
         return out, status, resid
 
-    def sample_pushes_arrays(self, poses: np.ndarray):
+    def sample_pushes_arrays(self, poses: np.ndarray, table: Optional[ShapeTable] = None):
         poses = np.ascontiguousarray(poses, np.float64)
         E, n = poses.shape[0], poses.shape[1]
         cap = n * self.params.pushes_per_object
         out = np.empty((E, cap, 4), np.float64)
         cnt = np.empty(E, np.int32)
-        self._check(self.lib.ppg_sample_pushes(self.ptr, dptr(poses), E, dptr(out), iptr(cnt)), "ppg_sample_pushes")
+        sh = ctypes.byref(table.struct()) if table is not None else None
+        self._check(self.lib.ppg_sample_pushes(self.ptr, sh, dptr(poses), E, dptr(out), iptr(cnt)),
+                    "ppg_sample_pushes")
         return out, cnt
 
     def graspable_arrays(self, poses: np.ndarray):

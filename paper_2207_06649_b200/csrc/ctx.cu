@@ -24,6 +24,7 @@ __global__ void expand_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
 __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
 
 constexpr int kBlock = 128;
 constexpr size_t kMaxSmem = 3 * kMaxObjects * kBlock * sizeof(double);
@@ -415,23 +416,36 @@ int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, cons
                         reinterpret_cast<long long*>(counts_dev), st);
 }
 
-int ppg_sample_pushes(ppg_ctx* ctx, const double* poses, int E, double* out, int32_t* count) {
+int ppg_sample_pushes(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses, int E, double* out,
+                      int32_t* count) {
   if (!ctx || E < 0) return PPG_EINVAL;
-  if (!ctx->has_scene) {
+  if (!shapes && !ctx->has_scene) {
     ctx->err = "no scene installed";
     return PPG_EINVAL;
   }
   if (E == 0) return PPG_SUCCESS;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
-  const int n = ctx->scene.n, na = ctx->params.pushes_per_object;
+  ShapesDev S = ctx->scene;
+  double side = ctx->side, margin = ctx->margin;
+  if (shapes) {
+    if (shapes->n_tables != 1 && shapes->n_tables != E) {
+      ctx->err = "sample_pushes: shape tables must be 1 or E";
+      return PPG_EINVAL;
+    }
+    const int rc = upload_shapes(ctx, shapes, false, ctx->shape_in, ctx->shape_buf, S, st);
+    if (rc != PPG_SUCCESS) return rc;
+    side = shapes->side_length;
+    margin = shapes->boundary_margin;
+  }
+  const int n = S.n, na = ctx->params.pushes_per_object;
   const size_t pbytes = static_cast<size_t>(E) * n * 3 * 8, obytes = static_cast<size_t>(E) * n * na * 4 * 8;
   CK(ctx->b_in.ensure(pbytes));
   CK(ctx->b_out.ensure(obytes));
   CK(ctx->b_status.ensure(static_cast<size_t>(E) * 4));
   CK(cudaMemcpyAsync(ctx->b_in.p, poses, pbytes, cudaMemcpyHostToDevice, st));
-  const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
-  SampleArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(),
+  const SimConst C = make_const(ctx->params, n, side, margin);
+  SampleArgs a{S, ctx->b_in.as<double>(), ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(),
                nullptr, nullptr, nullptr, nullptr, nullptr, E};
   sample_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
   CK(cudaGetLastError());
@@ -594,6 +608,37 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   CK(cudaMemcpyAsync(rewards_out, a.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
   if (counters) CK(cudaMemcpyAsync(counters, a.counters, 32, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_measure_fp64_peak(ppg_ctx* ctx, double* dfma_per_s, double* seconds) {
+  if (!ctx || !dfma_per_s) return PPG_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int blocks = sms * 8, threads = 256, iters = 1 << 16;
+  CK(ctx->b_e.ensure(static_cast<size_t>(blocks) * 8));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  double best = 0.0, best_s = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    CK(cudaEventRecord(e0, ctx->stream));
+    fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(ctx->b_e.as<double>(), iters, 0.999999, 1e-7);
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    const double rate = static_cast<double>(blocks) * threads * 8.0 * iters / (ms * 1e-3);
+    if (rate > best) {
+      best = rate;
+      best_s = ms * 1e-3;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *dfma_per_s = best;
+  if (seconds) *seconds = best_s;
   return PPG_SUCCESS;
 }
 

@@ -8,6 +8,7 @@
 // state digest (world.cpp:166-191) sees.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 
 #ifndef M_PI
@@ -16,32 +17,40 @@
 
 namespace ppg {
 
+#ifdef __CUDACC__
 #define PPG_DI __device__ __forceinline__
+#define PPG_HD __host__ __device__ __forceinline__
+#else
+#define PPG_DI inline
+#define PPG_HD inline
+#endif
+
+PPG_HD double inf_d() { return __builtin_huge_val(); }
 
 struct V2 {
   double x, y;
 };
 
-PPG_DI V2 mk(double x, double y) { return V2{x, y}; }
-PPG_DI V2 operator+(V2 a, V2 b) { return V2{a.x + b.x, a.y + b.y}; }  // geometry.hpp:12
-PPG_DI V2 operator-(V2 a, V2 b) { return V2{a.x - b.x, a.y - b.y}; }  // geometry.hpp:13
-PPG_DI V2 operator*(V2 a, double s) { return V2{a.x * s, a.y * s}; }  // geometry.hpp:14
-PPG_DI V2 operator-(V2 a) { return V2{-a.x, -a.y}; }                  // geometry.hpp:15
-PPG_DI double dot(V2 a, V2 b) { return a.x * b.x + a.y * b.y; }       // geometry.hpp:20
-PPG_DI double cross(V2 a, V2 b) { return a.x * b.y - a.y * b.x; }     // geometry.hpp:21
-PPG_DI double norm2(V2 a) { return a.x * a.x + a.y * a.y; }           // geometry.hpp:22
-PPG_DI double norm(V2 a) { return sqrt(norm2(a)); }                   // geometry.hpp:23
-PPG_DI V2 perp(V2 a) { return V2{-a.y, a.x}; }                        // geometry.hpp:24
-PPG_DI V2 normalized(V2 a) {                                          // geometry.hpp:25-28
+PPG_HD V2 mk(double x, double y) { return V2{x, y}; }
+PPG_HD V2 operator+(V2 a, V2 b) { return V2{a.x + b.x, a.y + b.y}; }  // geometry.hpp:12
+PPG_HD V2 operator-(V2 a, V2 b) { return V2{a.x - b.x, a.y - b.y}; }  // geometry.hpp:13
+PPG_HD V2 operator*(V2 a, double s) { return V2{a.x * s, a.y * s}; }  // geometry.hpp:14
+PPG_HD V2 operator-(V2 a) { return V2{-a.x, -a.y}; }                  // geometry.hpp:15
+PPG_HD double dot(V2 a, V2 b) { return a.x * b.x + a.y * b.y; }       // geometry.hpp:20
+PPG_HD double cross(V2 a, V2 b) { return a.x * b.y - a.y * b.x; }     // geometry.hpp:21
+PPG_HD double norm2(V2 a) { return a.x * a.x + a.y * a.y; }           // geometry.hpp:22
+PPG_HD double norm(V2 a) { return sqrt(norm2(a)); }                   // geometry.hpp:23
+PPG_HD V2 perp(V2 a) { return V2{-a.y, a.x}; }                        // geometry.hpp:24
+PPG_HD V2 normalized(V2 a) {                                          // geometry.hpp:25-28
   const double n = norm(a);
   return n > 0.0 ? V2{a.x / n, a.y / n} : V2{0.0, 0.0};
 }
-PPG_DI double dmax(double a, double b) { return a < b ? b : a; }
-PPG_DI double dmin(double a, double b) { return b < a ? b : a; }
-PPG_DI double dclamp(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+PPG_HD double dmax(double a, double b) { return a < b ? b : a; }
+PPG_HD double dmin(double a, double b) { return b < a ? b : a; }
+PPG_HD double dclamp(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
 
 // geometry.cpp:8-13.  fmod is exact on both sides.
-PPG_DI double wrap_angle(double theta) {
+PPG_HD double wrap_angle(double theta) {
   const double two_pi = 2.0 * M_PI;
   double t = fmod(theta + M_PI, two_pi);
   if (t < 0.0) t += two_pi;
@@ -49,7 +58,7 @@ PPG_DI double wrap_angle(double theta) {
 }
 
 // geometry.cpp:15-22
-PPG_DI V2 closest_point_on_segment(V2 p, V2 a, V2 b) {
+PPG_HD V2 closest_point_on_segment(V2 p, V2 a, V2 b) {
   const V2 ab = b - a;
   const double len2 = norm2(ab);
   if (len2 == 0.0) return a;
@@ -59,12 +68,12 @@ PPG_DI V2 closest_point_on_segment(V2 p, V2 a, V2 b) {
 }
 
 // geometry.cpp:24-26
-PPG_DI double dist_point_segment(V2 p, V2 a, V2 b) {
+PPG_HD double dist_point_segment(V2 p, V2 a, V2 b) {
   return norm(p - closest_point_on_segment(p, a, b));
 }
 
 // geometry.cpp:28-40
-PPG_DI double dist_segment_segment(V2 a0, V2 a1, V2 b0, V2 b1) {
+PPG_HD double dist_segment_segment(V2 a0, V2 a1, V2 b0, V2 b1) {
   const double d1 = cross(a1 - a0, b0 - a0);
   const double d2 = cross(a1 - a0, b1 - a0);
   const double d3 = cross(b1 - b0, a0 - b0);
@@ -83,7 +92,7 @@ struct Poly {
 };
 
 // geometry.cpp:56-64
-PPG_DI bool point_in_convex(V2 p, const Poly& poly) {
+PPG_HD bool point_in_convex(V2 p, const Poly& poly) {
   for (int i = 0; i < poly.n; ++i) {
     const V2 a = poly.p[i];
     const V2 b = poly.p[i + 1 == poly.n ? 0 : i + 1];
@@ -93,7 +102,7 @@ PPG_DI bool point_in_convex(V2 p, const Poly& poly) {
 }
 
 // geometry.cpp:66-79
-PPG_DI V2 polygon_centroid(const Poly& poly) {
+PPG_HD V2 polygon_centroid(const Poly& poly) {
   double area2 = 0.0;
   V2 c{0.0, 0.0};
   for (int i = 0; i < poly.n; ++i) {
@@ -110,16 +119,16 @@ PPG_DI V2 polygon_centroid(const Poly& poly) {
 }
 
 // geometry.cpp:81-85
-PPG_DI double support_extent(const Poly& poly, V2 dir) {
-  double best = -__longlong_as_double(0x7ff0000000000000ll);
+PPG_HD double support_extent(const Poly& poly, V2 dir) {
+  double best = -inf_d();
   for (int i = 0; i < poly.n; ++i) best = dmax(best, dot(poly.p[i], dir));
   return best;
 }
 
 // geometry.cpp:87-100
-PPG_DI V2 closest_point_on_polygon(V2 p, const Poly& poly) {
+PPG_HD V2 closest_point_on_polygon(V2 p, const Poly& poly) {
   V2 best{0.0, 0.0};
-  double best_d = __longlong_as_double(0x7ff0000000000000ll);
+  double best_d = inf_d();
   for (int i = 0; i < poly.n; ++i) {
     const V2 q = closest_point_on_segment(p, poly.p[i], poly.p[i + 1 == poly.n ? 0 : i + 1]);
     const double d = norm2(p - q);
@@ -132,7 +141,7 @@ PPG_DI V2 closest_point_on_polygon(V2 p, const Poly& poly) {
 }
 
 // geometry.cpp:102-105
-PPG_DI double signed_dist_point_polygon(V2 p, const Poly& poly) {
+PPG_HD double signed_dist_point_polygon(V2 p, const Poly& poly) {
   const double d = norm(p - closest_point_on_polygon(p, poly));
   return point_in_convex(p, poly) ? -d : d;
 }
@@ -144,7 +153,7 @@ struct Overlap {
 };
 
 // geometry.cpp:107-115
-PPG_DI Overlap disc_disc_overlap(V2 ca, double ra, V2 cb, double rb) {
+PPG_HD Overlap disc_disc_overlap(V2 ca, double ra, V2 cb, double rb) {
   Overlap o;
   const V2 d = cb - ca;
   const double dist = norm(d);
@@ -155,7 +164,7 @@ PPG_DI Overlap disc_disc_overlap(V2 ca, double ra, V2 cb, double rb) {
 }
 
 // geometry.cpp:117-132
-PPG_DI Overlap disc_polygon_overlap(V2 c, double r, const Poly& poly) {
+PPG_HD Overlap disc_polygon_overlap(V2 c, double r, const Poly& poly) {
   Overlap o;
   const V2 q = closest_point_on_polygon(c, poly);
   const V2 d = q - c;
@@ -167,7 +176,7 @@ PPG_DI Overlap disc_polygon_overlap(V2 c, double r, const Poly& poly) {
 }
 
 // geometry.cpp:137-152
-PPG_DI bool sat_min_overlap(const Poly& a, const Poly& b, double& depth, V2& axis) {
+PPG_HD bool sat_min_overlap(const Poly& a, const Poly& b, double& depth, V2& axis) {
   for (int i = 0; i < a.n; ++i) {
     const V2 edge = a.p[i + 1 == a.n ? 0 : i + 1] - a.p[i];
     const V2 normal = normalized(V2{edge.y, -edge.x});
@@ -184,16 +193,16 @@ PPG_DI bool sat_min_overlap(const Poly& a, const Poly& b, double& depth, V2& axi
 }
 
 // geometry.cpp:191-195
-PPG_DI bool polygons_intersect(const Poly& a, const Poly& b) {
-  double depth = __longlong_as_double(0x7ff0000000000000ll);
+PPG_HD bool polygons_intersect(const Poly& a, const Poly& b) {
+  double depth = inf_d();
   V2 axis{0.0, 0.0};
   return sat_min_overlap(a, b, depth, axis) && sat_min_overlap(b, a, depth, axis);
 }
 
 // geometry.cpp:176-184
-PPG_DI double dist_polygon_polygon(const Poly& a, const Poly& b) {
+PPG_HD double dist_polygon_polygon(const Poly& a, const Poly& b) {
   if (polygons_intersect(a, b)) return 0.0;
-  double best = __longlong_as_double(0x7ff0000000000000ll);
+  double best = inf_d();
   for (int i = 0; i < a.n; ++i)
     for (int j = 0; j < b.n; ++j)
       best = dmin(best, dist_segment_segment(a.p[i], a.p[i + 1 == a.n ? 0 : i + 1], b.p[j],
@@ -206,10 +215,10 @@ PPG_DI double dist_polygon_polygon(const Poly& a, const Poly& b) {
 // path (push_sim.cpp:96, :110; world.cpp:148 via max with 0.0) only tests
 // depth > 0 or takes max(., 0.0) of it, so `exact_separation` = false skips
 // that distance and returns depth = -0.0 (same decisions, same bits).
-PPG_DI Overlap polygon_polygon_overlap(const Poly& a, const Poly& b, bool exact_separation) {
+PPG_HD Overlap polygon_polygon_overlap(const Poly& a, const Poly& b, bool exact_separation) {
   Overlap o;
   o.contact = V2{0.0, 0.0};
-  double depth = __longlong_as_double(0x7ff0000000000000ll);
+  double depth = inf_d();
   V2 axis{0.0, 0.0};
   const bool ab = sat_min_overlap(a, b, depth, axis);
   const bool ba = ab && sat_min_overlap(b, a, depth, axis);

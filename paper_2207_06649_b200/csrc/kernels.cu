@@ -362,3 +362,20 @@ __global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ 
 }
 
 }  // namespace ppg
+
+namespace ppg {
+
+// Measurement only (not on the hot path): the FP64 CUDA-core pipe peak, as
+// the denominator of the roofline.  8 independent DFMA chains per thread.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, double b, double c) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-3, a2 = a0 + 2e-3, a3 = a0 + 3e-3;
+  double a4 = a0 + 4e-3, a5 = a0 + 5e-3, a6 = a0 + 6e-3, a7 = a0 + 7e-3;
+  for (int i = 0; i < iters; ++i) {
+    a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains alive
+}
+
+}  // namespace ppg

@@ -276,7 +276,7 @@ PPG_DI bool push_candidate(const PoseView& P, const ShapeView& S, const SimConst
 // actions.cpp:32-39
 PPG_DI double rect_min_wall_clearance(const Poly& rect, double side) {
   const double h = side / 2.0;
-  double best = __longlong_as_double(0x7ff0000000000000ll);
+  double best = inf_d();
   for (int i = 0; i < rect.n; ++i)
     best = dmin(best, dmin(h - fabs(rect.p[i].x), h - fabs(rect.p[i].y)));
   return best;

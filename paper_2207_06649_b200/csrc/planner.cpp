@@ -172,7 +172,7 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
     root.poses.assign(root_poses, root_poses + n * 3);
     std::vector<double> buf(cap_untried * 4);
     int32_t cnt = 0;
-    if ((rc = ppg_sample_pushes(ctx, root_poses, 1, buf.data(), &cnt)) != PPG_SUCCESS) return rc;
+    if ((rc = ppg_sample_pushes(ctx, nullptr, root_poses, 1, buf.data(), &cnt)) != PPG_SUCCESS) return rc;
     root.untried.resize(cnt);
     std::memcpy(root.untried.data(), buf.data(), sizeof(double) * 4 * cnt);
     uint8_t g = 0;
