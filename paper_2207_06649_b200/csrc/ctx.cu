@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,8 +26,13 @@ __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a)
 __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
+template <int NMAX>
+__global__ void resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a, int* next_env);
 
 constexpr int kBlock = 128;
+constexpr int kDiscBlock = 128;  // resolve_disc.cu kDB
+constexpr int kNumDisc = 8;
+constexpr int kDiscSizes[kNumDisc] = {4, 6, 8, 10, 11, 12, 14, 16};
 constexpr size_t kMaxSmem = 3 * kMaxObjects * kBlock * sizeof(double);
 
 }  // namespace ppg
@@ -77,6 +83,7 @@ struct ppg_ctx {
   std::string err;
   // shared scene (ppg_set_scene)
   bool has_scene = false;
+  bool scene_all_discs = false;
   ShapesDev scene;
   std::vector<int32_t> h_kind, h_nv, h_target;
   std::vector<double> h_radius, h_verts;
@@ -89,7 +96,12 @@ struct ppg_ctx {
   // lockstep state
   DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx;
   DevBuf l_W, l_rew, l_active, l_nactive, l_counters, l_npose, l_nmeta;
+  DevBuf b_counter;              // persistent-kernel work counter
   int32_t* h_nactive = nullptr;  // pinned
+  int num_sms = 148;
+  int disc_blocks_per_sm[kNumDisc] = {};  // resolve_disc_kernel<kDiscSizes[k]>
+  bool disc_kernels = false;
+  bool force_generic = false;             // PPG_FORCE_GENERIC=1: A/B the generic kernel
 };
 
 namespace {
@@ -203,6 +215,28 @@ int upload_shapes(ppg_ctx* ctx, const ppg_shapes* sh, bool device_ptrs, DevBuf& 
   return PPG_SUCCESS;
 }
 
+bool host_all_discs(const ppg_shapes* sh) {
+  if (!sh->n_vertices && !sh->vertices) return true;
+  const size_t tn = static_cast<size_t>(sh->n_tables) * sh->n_objects;
+  for (size_t i = 0; i < tn; ++i)
+    if (sh->kind[i] != PPG_DISC) return false;
+  return true;
+}
+
+template <class F>
+bool for_each_disc_kernel(F&& f) {
+  const void* fns[kNumDisc] = {
+      reinterpret_cast<const void*>(&resolve_disc_kernel<4>), reinterpret_cast<const void*>(&resolve_disc_kernel<6>),
+      reinterpret_cast<const void*>(&resolve_disc_kernel<8>), reinterpret_cast<const void*>(&resolve_disc_kernel<10>),
+      reinterpret_cast<const void*>(&resolve_disc_kernel<11>), reinterpret_cast<const void*>(&resolve_disc_kernel<12>),
+      reinterpret_cast<const void*>(&resolve_disc_kernel<14>), reinterpret_cast<const void*>(&resolve_disc_kernel<16>)};
+  for (int k = 0; k < kNumDisc; ++k)
+    if (!f(k, fns[k])) return false;
+  return true;
+}
+
+size_t disc_smem(int nmax) { return static_cast<size_t>(3) * nmax * kDiscBlock * sizeof(double); }
+
 size_t smem_for(int n) { return static_cast<size_t>(3) * n * kBlock * sizeof(double); }
 
 }  // namespace
@@ -275,6 +309,19 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
   ok = ok && cudaFuncSetAttribute(grasp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(lock_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess;
+  ok = ok && for_each_disc_kernel([&](int k, const void* fn) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(disc_smem(kDiscSizes[k]))) == cudaSuccess &&
+           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->disc_blocks_per_sm[k], fn, kDiscBlock,
+                                                         disc_smem(kDiscSizes[k])) == cudaSuccess &&
+           ctx->disc_blocks_per_sm[k] > 0;
+  });
+  ctx->disc_kernels = ok;
+  {
+    const char* fg = std::getenv("PPG_FORCE_GENERIC");
+    ctx->force_generic = fg && fg[0] == '1';
+  }
   if (!ok) {
     cudaGetLastError();
     if (err) *err = PPG_ECUDA;
@@ -323,6 +370,7 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
   ctx->h_target.assign(shapes->target_index, shapes->target_index + 1);
   ctx->side = shapes->side_length;
   ctx->margin = shapes->boundary_margin;
+  ctx->scene_all_discs = host_all_discs(shapes);
   const int rc = upload_shapes(ctx, shapes, false, ctx->scene_in, ctx->scene_buf, ctx->scene, ctx->stream);
   if (rc != PPG_SUCCESS) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
@@ -330,17 +378,46 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
   return PPG_SUCCESS;
 }
 
-static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, double side, double margin, const double* d_in,
-                          const double* d_push, int E, double* d_out, int32_t* d_status, double* d_resid,
-                          long long* d_counts, cudaStream_t st) {
+// Kernel #1 dispatch: all-disc batches (shapes without vertex tables) run the
+// register-resident persistent kernel (resolve_disc.cu) sized to the object
+// count; polygons, n > 16 and the counting variant run the generic kernel.
+static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, double side, double margin,
+                          const double* d_in, const double* d_push, int E, double* d_out, int32_t* d_status,
+                          double* d_resid, long long* d_counts, cudaStream_t st) {
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
+  if (!d_counts && all_discs && S.n <= 16 && ctx->disc_kernels && !ctx->force_generic) {
+    CK(ctx->b_counter.ensure(16));
+    CK(cudaMemsetAsync(ctx->b_counter.p, 0, 4, st));
+    int slot = 0;
+    while (kDiscSizes[slot] < S.n) ++slot;
+    const int nmax = kDiscSizes[slot];
+    const int want = (E + kDiscBlock - 1) / kDiscBlock;
+    const int cap = ctx->disc_blocks_per_sm[slot] * ctx->num_sms;
+    const int grid = want < cap ? want : cap;
+    int* counter = ctx->b_counter.as<int>();
+    const size_t sm = disc_smem(nmax);
+    switch (nmax) {
+      case 4: resolve_disc_kernel<4><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+      case 6: resolve_disc_kernel<6><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+      case 8: resolve_disc_kernel<8><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+      case 10: resolve_disc_kernel<10><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+      case 11: resolve_disc_kernel<11><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+      case 12: resolve_disc_kernel<12><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+      case 14: resolve_disc_kernel<14><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+      default: resolve_disc_kernel<16><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    }
+    CK(cudaGetLastError());
+    return PPG_SUCCESS;
+  }
   const int grid = (E + kBlock - 1) / kBlock;
   if (d_counts) resolve_kernel<true><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
   else resolve_kernel<false><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
   CK(cudaGetLastError());
   return PPG_SUCCESS;
 }
+
+
 
 int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in, const double* pushes,
                       int E, double* poses_out, int32_t* status, double* residual) {
@@ -376,7 +453,8 @@ int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* pose
   CK(ctx->b_resid.ensure(static_cast<size_t>(E) * sizeof(double)));
   CK(cudaMemcpyAsync(ctx->b_in.p, poses_in, pbytes, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ctx->b_push.p, pushes, static_cast<size_t>(E) * 32, cudaMemcpyHostToDevice, st));
-  int rc = launch_resolve(ctx, S, side, margin, ctx->b_in.as<double>(), ctx->b_push.as<double>(), E,
+  const bool discs = shapes ? host_all_discs(shapes) : ctx->scene_all_discs;
+  int rc = launch_resolve(ctx, S, discs, side, margin, ctx->b_in.as<double>(), ctx->b_push.as<double>(), E,
                           ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(), ctx->b_resid.as<double>(), nullptr, st);
   if (rc != PPG_SUCCESS) return rc;
   CK(cudaMemcpyAsync(poses_out, ctx->b_out.p, pbytes, cudaMemcpyDeviceToHost, st));
@@ -395,7 +473,8 @@ int ppg_batch_resolve_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, const doub
   ShapesDev S;
   const int rc = upload_shapes(ctx, shapes_dev, true, ctx->shape_in, ctx->shape_buf, S, st);
   if (rc != PPG_SUCCESS) return rc;
-  return launch_resolve(ctx, S, shapes_dev->side_length, shapes_dev->boundary_margin, poses_in, pushes, E,
+  const bool discs = !shapes_dev->n_vertices && !shapes_dev->vertices;  // documented contract
+  return launch_resolve(ctx, S, discs, shapes_dev->side_length, shapes_dev->boundary_margin, poses_in, pushes, E,
                         poses_out, status, residual, nullptr, st);
 }
 
@@ -411,7 +490,7 @@ int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, cons
   const size_t pbytes = static_cast<size_t>(E) * S.n * 3 * sizeof(double);
   CK(ctx->b_out.ensure(pbytes));
   CK(ctx->b_status.ensure(static_cast<size_t>(E) * 4));
-  return launch_resolve(ctx, S, shapes_dev->side_length, shapes_dev->boundary_margin, poses_in, pushes, E,
+  return launch_resolve(ctx, S, false, shapes_dev->side_length, shapes_dev->boundary_margin, poses_in, pushes, E,
                         ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(), nullptr,
                         reinterpret_cast<long long*>(counts_dev), st);
 }

@@ -1,0 +1,392 @@
+// resolve_disc.cu — the disc-scene physics kernel (kernel #1 fast path):
+// resolve_push (push_sim.cpp:58-130) for batches whose objects are all discs
+// (every proj/cases disc scene, the C2 / C4 workloads), bit-identical to the
+// reference.
+//
+// Why a second kernel: the straight transcription (kernels.cu) spends ~90 %
+// of its algorithmic FP64 work in broad-phase tests (7 ops each, uniform
+// across lanes) but executes the rare narrow tests (sqrt + div, ~2 % of
+// pairs) whenever ANY lane of the warp needs them, and pays address
+// arithmetic on every shared-memory pose access.  Here, per projection
+// iteration and per lane (= environment):
+//
+//   1. tip broad phase over all objects from REGISTERS (fully unrolled, no
+//      divergence) -> candidate bitmask;
+//   2. tip narrow tests in a loop over the set bits (poses in shared memory,
+//      dynamic index) — objects are independent in the tip loop
+//      (push_sim.cpp:90-100), so any order is exact;
+//   3. pair broad phase over all i<j from registers -> flat pair bitmask;
+//   4. pair narrow tests in lexicographic order over the set bits.  A hit on
+//      (i,j) moves i and j, so every LATER pair touching i or j is re-queued
+//      for evaluation (its broad result is stale); a pair not re-queued has
+//      unchanged inputs, so its broad result still holds.  This reproduces
+//      the reference's in-place Gauss-Seidel sweep (push_sim.cpp:101-117)
+//      exactly while running ~1 narrow test per lane per iteration;
+//   5. clamp (push_sim.cpp:48-54) in registers, write back.
+//
+// The (substep, iteration) double loop is flattened per lane and lanes are
+// persistent: a lane that finishes its environment fetches the next one, so
+// warps stay full until the batch drains (no per-warp max-iteration tail).
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "kernels.cuh"
+
+namespace ppg {
+
+namespace {
+
+constexpr int kDB = 128;  // threads per block
+
+// Compile-time loops: the body receives std::integral_constant<int, I>, so
+// every register-array index below is a constant expression and the arrays
+// stay in registers.
+template <class F, int... Is>
+PPG_DI void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+PPG_DI void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// lexicographic pair p of n objects -> (i, j), evaluated at compile time
+__host__ __device__ constexpr int pair_i(int p, int n) {
+  int i = 0;
+  while (p >= n - 1 - i) {
+    p -= n - 1 - i;
+    ++i;
+  }
+  return i;
+}
+__host__ __device__ constexpr int pair_j(int p, int n) {
+  int i = 0;
+  while (p >= n - 1 - i) {
+    p -= n - 1 - i;
+    ++i;
+  }
+  return i + 1 + p;
+}
+
+template <int W>
+struct Mask {
+  uint64_t w[W];
+  PPG_DI void clear() {
+#pragma unroll
+    for (int k = 0; k < W; ++k) w[k] = 0;
+  }
+  PPG_DI bool any() const {
+    uint64_t o = 0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) o |= w[k];
+    return o != 0;
+  }
+  // pops the lowest set bit; returns its index (mask must be non-empty).
+  // Branch-free over words (constant indices only) so the mask stays in
+  // registers.
+  PPG_DI int pop() {
+    int idx = -1;
+    bool done = false;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const bool take = !done && w[k] != 0;
+      const int b = __ffsll(static_cast<long long>(w[k])) - 1;
+      idx = take ? k * 64 + b : idx;
+      w[k] = take ? (w[k] & (w[k] - 1)) : w[k];
+      done = done || take;
+    }
+    return idx;
+  }
+  PPG_DI void assign(int q, bool v) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const uint64_t bit = (q >> 6) == k ? (1ull << (q & 63)) : 0ull;
+      w[k] = v ? (w[k] | bit) : (w[k] & ~bit);
+    }
+  }
+  // this |= ((a | b) & m & bits strictly above p)
+  PPG_DI void or_above(const uint64_t* a, const uint64_t* b, const Mask& m, int p) {
+    const int pw = p >> 6, pb = p & 63;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const uint64_t above = k > pw ? ~0ull : (k < pw ? 0ull : (pb == 63 ? 0ull : (~0ull << (pb + 1))));
+      w[k] |= (a[k] | b[k]) & m.w[k] & above;
+    }
+  }
+};
+
+PPG_DI double fclampd(double v, double lo, double hi) {
+  // == std::clamp(v, lo, hi) for non-NaN v (positions are finite)
+  return fmin(fmax(v, lo), hi);
+}
+
+}  // namespace
+
+template <int NMAX>
+__global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a,
+                                                               int* next_env) {
+  constexpr int P = NMAX * (NMAX - 1) / 2;
+  constexpr int W = (P + 63) / 64;
+  extern __shared__ double dsm[];  // [x | y | r][NMAX][kDB]
+  __shared__ uint8_t pi_[P], pj_[P];
+  __shared__ uint64_t omask[NMAX][W];  // pairs touching object k
+
+  const int tid = threadIdx.x;
+  for (int q = tid; q < NMAX * W; q += kDB) (&omask[0][0])[q] = 0;
+  __syncthreads();
+  if (tid == 0) {
+    int p = 0;
+    for (int i = 0; i < NMAX; ++i)
+      for (int j = i + 1; j < NMAX; ++j, ++p) {
+        pi_[p] = static_cast<uint8_t>(i);
+        pj_[p] = static_cast<uint8_t>(j);
+        omask[i][p >> 6] |= 1ull << (p & 63);
+        omask[j][p >> 6] |= 1ull << (p & 63);
+      }
+  }
+  __syncthreads();
+
+  const int n = C.n;
+  const double tr = C.tip_r;
+  const double hcl = C.side / 2.0 - C.margin - 1e-9;
+  double* const xl = dsm + tid;
+  double* const yl = dsm + NMAX * kDB + tid;
+  double* const rl = dsm + 2 * NMAX * kDB + tid;
+
+  double x[NMAX], y[NMAX], r[NMAX];
+  uint32_t active = 0;
+  Mask<W> pact;  // pairs with both objects active
+  V2 start{0.0, 0.0}, delta{0.0, 0.0};
+  int step = 0, iter = 0;
+  const int total_threads = gridDim.x * kDB;
+  int e = blockIdx.x * kDB + tid;
+  bool have = false;
+  bool need_init = true;
+
+  while (true) {
+    // ---- environment init: load, precondition, active mask (push_sim.cpp:58-82)
+    if (need_init) {
+      need_init = false;
+      have = false;
+      while (e < a.E) {
+        const double* src = a.poses_in + static_cast<size_t>(e) * n * 3;
+        const int t = a.S.T == 1 ? 0 : e;
+        static_for<NMAX>([&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          const bool real = i < n;
+          x[i] = real ? src[i * 3] : 0.0;
+          y[i] = real ? src[i * 3 + 1] : 0.0;
+          r[i] = real ? __ldg(a.S.rad + i * a.S.T + t) : 0.0;
+          xl[i * kDB] = x[i];
+          yl[i * kDB] = y[i];
+          rl[i * kDB] = r[i];
+        });
+        const double* pu = a.pushes + static_cast<size_t>(e) * 4;
+        start = V2{pu[0], pu[1]};
+        const V2 end{pu[2], pu[3]};
+        // collides_gripper_start (world.cpp:154-164)
+        bool collide = false;
+        {
+          const double rr = C.tip_r + C.tip_clear;
+          const double h = C.side / 2.0;
+          if (start.x - rr < -h || start.x + rr > h || start.y - rr < -h || start.y + rr > h) collide = true;
+          static_for<NMAX>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            if (i < n && dmax(0.0, norm(start - V2{x[i], y[i]}) - r[i]) < rr) collide = true;
+          });
+        }
+        if (collide) {
+          a.status[e] = 1;
+          if (a.residual) a.residual[e] = 0.0;
+          double* out = a.poses_out + static_cast<size_t>(e) * n * 3;
+          for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
+          e = atomicAdd(next_env, 1) + total_threads;
+          continue;
+        }
+        delta = (end - start) * (1.0 / C.substeps);
+        double max_diam = 0.0;
+        static_for<NMAX>([&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          if (i < n) max_diam = dmax(max_diam, 2.0 * r[i]);
+        });
+        const double reach = (C.push_distance + C.tip_r) + 2.0 * max_diam;
+        active = 0;
+        static_for<NMAX>([&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          if (i < n && dist_point_segment(V2{x[i], y[i]}, start, end) <= reach + r[i]) active |= 1u << i;
+        });
+        pact.clear();
+        static_for<P>([&](auto pc) {
+          constexpr int p = decltype(pc)::value;
+          constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
+          if ((active >> i & 1u) && (active >> j & 1u)) pact.w[p >> 6] |= 1ull << (p & 63);
+        });
+        step = 1;
+        iter = 0;
+        if (C.max_iters < 1) step = C.substeps + 1;
+        have = true;
+        break;
+      }
+    }
+    if (!__any_sync(0xffffffffu, have)) break;
+    if (!have) continue;
+
+    if (step > C.substeps) {
+      // ---- final all-pairs penetration check + output (push_sim.cpp:123-128,
+      // world.cpp:139-152).  Once per environment, from shared memory.
+      double worst = 0.0;
+      for (int i = 0; i + 1 < n; ++i) {
+        const double xi = xl[i * kDB], yi = yl[i * kDB], ri = rl[i * kDB];
+        for (int j = i + 1; j < n; ++j) {
+          const double rj = rl[j * kDB];
+          const double bx = xi - xl[j * kDB], by = yi - yl[j * kDB];
+          const double rr = ri + rj;
+          const double d2 = bx * bx + by * by;
+          if (d2 > rr * rr) continue;
+          worst = dmax(worst, ri + rj - sqrt(d2));  // norm2(pos_j - pos_i) == d2 exactly
+        }
+      }
+      const int st = worst > C.eps_pen ? 2 : 0;
+      a.status[e] = st;
+      if (a.residual) a.residual[e] = worst;
+      double* out = a.poses_out + static_cast<size_t>(e) * n * 3;
+      if (st == 0) {
+        for (int i = 0; i < n; ++i) {
+          out[i * 3] = xl[i * kDB];
+          out[i * 3 + 1] = yl[i * kDB];
+          out[i * 3 + 2] = a.poses_in[(static_cast<size_t>(e) * n + i) * 3 + 2];  // discs never rotate
+        }
+      } else {
+        for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
+      }
+      e = atomicAdd(next_env, 1) + total_threads;
+      need_init = true;
+      have = false;
+      continue;
+    }
+
+    // ---- one projection iteration of substep `step` (push_sim.cpp:87-120)
+    const V2 tc = start + delta * static_cast<double>(step);
+    double max_pen = 0.0;
+    // 1-2. tip vs objects (push_sim.cpp:90-100)
+    uint32_t tcand = 0;
+    static_for<NMAX>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      const double dx = x[i] - tc.x, dy = y[i] - tc.y;
+      const double reach = tr + r[i];
+      if ((active >> i & 1u) && !(dx * dx + dy * dy > reach * reach)) tcand |= 1u << i;
+    });
+    if (tcand) {
+      do {
+        const int i = __ffs(tcand) - 1;
+        tcand &= tcand - 1;
+        const double xi = xl[i * kDB], yi = yl[i * kDB], ri = rl[i * kDB];
+        const double dx = xi - tc.x, dy = yi - tc.y;
+        const double dist = sqrt(dx * dx + dy * dy);
+        const double depth = tr + ri - dist;
+        if (depth > 0.0) {
+          double ux = 1.0, uy = 0.0;
+          if (dist > 0.0) {
+            const double inv = __drcp_rn(dist);  // == 1.0 / dist (both correctly rounded)
+            ux = dx * inv;
+            uy = dy * inv;
+          }
+          xl[i * kDB] = xi + ux * depth;
+          yl[i * kDB] = yi + uy * depth;
+          max_pen = dmax(max_pen, depth);
+        }
+      } while (tcand);
+      static_for<NMAX>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        x[i] = xl[i * kDB];
+        y[i] = yl[i * kDB];
+      });
+    }
+    // 3-4. object pairs, lexicographic Gauss-Seidel (push_sim.cpp:101-117)
+    Mask<W> cand;
+    cand.clear();
+    static_for<P>([&](auto pc) {
+      constexpr int p = decltype(pc)::value;
+      constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
+      const double dx = x[i] - x[j], dy = y[i] - y[j];
+      const double rr = r[i] + r[j];
+      if (!(dx * dx + dy * dy > rr * rr)) cand.w[p >> 6] |= 1ull << (p & 63);
+    });
+#pragma unroll
+    for (int k = 0; k < W; ++k) cand.w[k] &= pact.w[k];
+    bool moved = false;
+    while (cand.any()) {
+      const int p = cand.pop();
+      const int i = pi_[p], j = pj_[p];
+      const double xi = xl[i * kDB], yi = yl[i * kDB], xj = xl[j * kDB], yj = yl[j * kDB];
+      const double ri = rl[i * kDB], rj = rl[j * kDB];
+      const double bx = xi - xj, by = yi - yj;
+      const double rr = ri + rj;
+      const double d2 = bx * bx + by * by;
+      if (d2 > rr * rr) continue;  // stale candidate that no longer passes the broad test
+      const double dx = xj - xi, dy = yj - yi;
+      const double dist = sqrt(d2);  // norm2(pos_j - pos_i) == d2 bit for bit (negation is exact)
+      const double depth = ri + rj - dist;
+      if (depth > 0.0) {
+        double ux = 1.0, uy = 0.0;
+        if (dist > 0.0) {
+          const double inv = __drcp_rn(dist);  // == 1.0 / dist (both correctly rounded)
+          ux = dx * inv;
+          uy = dy * inv;
+        }
+        const double s = 0.5 * depth;
+        const double mx = ux * s, my = uy * s;
+        xl[i * kDB] = xi - mx;
+        yl[i * kDB] = yi - my;
+        xl[j * kDB] = xj + mx;
+        yl[j * kDB] = yj + my;
+        max_pen = dmax(max_pen, depth);
+        moved = true;
+        // i and j moved: every LATER active pair touching them is re-queued
+        // (re-tested when popped); other pairs' inputs are unchanged.
+        cand.or_above(omask[i], omask[j], pact, p);
+      }
+    }
+    // 5. clamp every object (push_sim.cpp:118 -> :48-54).  clamp(v,-h,h) == v
+    // whenever |v| <= h, so the clamp itself only runs for objects at a wall.
+    bool inside = true;
+    static_for<NMAX>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      if (moved) {
+        x[i] = xl[i * kDB];
+        y[i] = yl[i * kDB];
+      }
+      inside = inside && fabs(x[i]) <= hcl && fabs(y[i]) <= hcl;
+    });
+    if (!inside) {
+      static_for<NMAX>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        const double cx = fclampd(x[i], -hcl, hcl), cy = fclampd(y[i], -hcl, hcl);
+        if (cx != x[i] || cy != y[i]) {
+          x[i] = cx;
+          y[i] = cy;
+          xl[i * kDB] = cx;
+          yl[i * kDB] = cy;
+        }
+      });
+    }
+    if (max_pen <= C.eps_pen || ++iter >= C.max_iters) {
+      ++step;
+      iter = 0;
+    }
+  }
+}
+
+#define PPG_DISC_INST(N) template __global__ void resolve_disc_kernel<N>(const __grid_constant__ SimConst, ResolveArgs, int*);
+PPG_DISC_INST(4)
+PPG_DISC_INST(6)
+PPG_DISC_INST(8)
+PPG_DISC_INST(10)
+PPG_DISC_INST(11)
+PPG_DISC_INST(12)
+PPG_DISC_INST(14)
+PPG_DISC_INST(16)
+#undef PPG_DISC_INST
+
+}  // namespace ppg

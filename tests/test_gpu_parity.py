@@ -180,3 +180,45 @@ def test_run_pmbs_budget_and_errors(ctx):
     c, st = golden_io.cases()[17]
     r = run_pmbs(st, ParallelConfig(budget=Budget.iterations(3), rng_seed=5), ctx=ctx)
     assert r.iterations == 3 and r.stop_reason == "budget"
+
+
+def _generic_ctx():
+    import os
+    from paper_2207_06649_b200 import Context
+    os.environ["PPG_FORCE_GENERIC"] = "1"
+    try:
+        return Context(0, default_params())
+    finally:
+        del os.environ["PPG_FORCE_GENERIC"]
+
+
+@pytest.mark.parametrize("n,motif", [(1, "random"), (3, "random"), (6, "random"), (8, "random"), (9, "random"),
+                                     (11, "random"), (12, "ring"), (14, "ring"), (16, "ring"), (20, "ring")])
+def test_disc_fast_path_matches_generic_and_oracle(ctx, n, motif):
+    """resolve_disc.cu (register-resident persistent kernel, object counts
+    <= 16) against the straight transcription and the CPU oracle, bitwise,
+    on all sampled pushes of several scenes (so start collisions, empty
+    contacts, deep clusters and non-convergence all occur)."""
+    from paper_2207_06649_b200.scenes import _take, generate_cases
+    t, poses, ok = generate_cases(n, np.arange(4000, 4024), 0.0, motif)
+    sel = np.nonzero(ok)[0][:12]
+    t, poses = _take(t, sel), poses[sel]
+    ctx.set_params(P)
+    cand, cnt = ctx.sample_pushes_arrays(poses, t)
+    idx = np.concatenate([np.full(c, k) for k, c in enumerate(cnt)]).astype(np.int64)
+    pushes = np.concatenate([cand[k, :c] for k, c in enumerate(cnt)])
+    # add start-collision pushes (tip placed on each scene's target)
+    bad = np.stack([[p[0, 0], p[0, 1], p[0, 0] + 0.05, p[0, 1]] for p in poses])
+    idx = np.concatenate([idx, np.arange(len(poses))])
+    pushes = np.concatenate([pushes, bad])
+    tt = _take(t, idx)
+    pp = np.ascontiguousarray(poses[idx])
+    out, st, res = ctx.batch_resolve_arrays(tt, pp, pushes)
+    g = _generic_ctx()
+    out2, st2, res2 = g.batch_resolve_arrays(tt, pp, pushes)
+    g.close()
+    o3, s3, r3 = port.batch_resolve(tt, pp, pushes, P)
+    assert np.array_equal(st, s3) and np.array_equal(st2, s3)
+    assert np.all(st[-len(poses):] == 1)
+    assert _bitwise(out, o3).all() and _bitwise(out2, o3).all()
+    assert np.array_equal(res.view(np.uint64), r3.view(np.uint64))
