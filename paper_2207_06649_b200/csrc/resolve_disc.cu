@@ -116,6 +116,8 @@ struct Mask {
   }
 };
 
+constexpr double kNear = 0.002;  // metres, the re-queue filter margin
+
 PPG_DI double fclampd(double v, double lo, double hi) {
   // == std::clamp(v, lo, hi) for non-NaN v (positions are finite)
   return fmin(fmax(v, lo), hi);
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   constexpr int P = NMAX * (NMAX - 1) / 2;
   constexpr int W = (P + 63) / 64;
   extern __shared__ double dsm[];  // [x | y | r][NMAX][kDB]
-  __shared__ uint8_t pi_[P], pj_[P];
+  __shared__ uint16_t pij[P];  // i | j << 8
   __shared__ uint64_t omask[NMAX][W];  // pairs touching object k
 
   const int tid = threadIdx.x;
@@ -139,8 +141,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     int p = 0;
     for (int i = 0; i < NMAX; ++i)
       for (int j = i + 1; j < NMAX; ++j, ++p) {
-        pi_[p] = static_cast<uint8_t>(i);
-        pj_[p] = static_cast<uint8_t>(j);
+        pij[p] = static_cast<uint16_t>(i | (j << 8));
         omask[i][p >> 6] |= 1ull << (p & 63);
         omask[j][p >> 6] |= 1ull << (p & 63);
       }
@@ -234,18 +235,24 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
 
     if (step > C.substeps) {
       // ---- final all-pairs penetration check + output (push_sim.cpp:123-128,
-      // world.cpp:139-152).  Once per environment, from shared memory.
+      // world.cpp:139-152).  Registers hold the final poses (kept in sync by
+      // the clamp step).  max is order-free, so the candidates can be visited
+      // in any order.
+      Mask<W> fin;
+      fin.clear();
+      static_for<P>([&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
+        const double dx = x[i] - x[j], dy = y[i] - y[j];
+        const double rr = r[i] + r[j];
+        if (j < n && !(dx * dx + dy * dy > rr * rr)) fin.w[p >> 6] |= 1ull << (p & 63);
+      });
       double worst = 0.0;
-      for (int i = 0; i + 1 < n; ++i) {
-        const double xi = xl[i * kDB], yi = yl[i * kDB], ri = rl[i * kDB];
-        for (int j = i + 1; j < n; ++j) {
-          const double rj = rl[j * kDB];
-          const double bx = xi - xl[j * kDB], by = yi - yl[j * kDB];
-          const double rr = ri + rj;
-          const double d2 = bx * bx + by * by;
-          if (d2 > rr * rr) continue;
-          worst = dmax(worst, ri + rj - sqrt(d2));  // norm2(pos_j - pos_i) == d2 exactly
-        }
+      while (fin.any()) {
+        const int ij = pij[fin.pop()];
+        const int i = ij & 0xff, j = ij >> 8;
+        const double bx = xl[i * kDB] - xl[j * kDB], by = yl[i * kDB] - yl[j * kDB];
+        worst = dmax(worst, rl[i * kDB] + rl[j * kDB] - sqrt(bx * bx + by * by));  // == norm(pos_j - pos_i)
       }
       const int st = worst > C.eps_pen ? 2 : 0;
       a.status[e] = st;
@@ -304,21 +311,33 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
       });
     }
     // 3-4. object pairs, lexicographic Gauss-Seidel (push_sim.cpp:101-117)
-    Mask<W> cand;
+    // `near` = pairs within reach + kNear: a pair outside it cannot pass the
+    // broad test until the objects have moved by kNear/2 in this pair sweep
+    // (tracked in `swept`), so re-queues after a hit can skip it exactly.
+    Mask<W> cand, near;
     cand.clear();
+    near.clear();
     static_for<P>([&](auto pc) {
       constexpr int p = decltype(pc)::value;
       constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
       const double dx = x[i] - x[j], dy = y[i] - y[j];
       const double rr = r[i] + r[j];
-      if (!(dx * dx + dy * dy > rr * rr)) cand.w[p >> 6] |= 1ull << (p & 63);
+      const double d2 = dx * dx + dy * dy;
+      const double rn = rr + kNear;
+      if (!(d2 > rr * rr)) cand.w[p >> 6] |= 1ull << (p & 63);
+      if (!(d2 > rn * rn)) near.w[p >> 6] |= 1ull << (p & 63);
     });
 #pragma unroll
-    for (int k = 0; k < W; ++k) cand.w[k] &= pact.w[k];
+    for (int k = 0; k < W; ++k) {
+      cand.w[k] &= pact.w[k];
+      near.w[k] &= pact.w[k];
+    }
     bool moved = false;
+    double swept = 0.0;  // sum of the per-hit displacements in this sweep
     while (cand.any()) {
       const int p = cand.pop();
-      const int i = pi_[p], j = pj_[p];
+      const int ij = pij[p];
+      const int i = ij & 0xff, j = ij >> 8;
       const double xi = xl[i * kDB], yi = yl[i * kDB], xj = xl[j * kDB], yj = yl[j * kDB];
       const double ri = rl[i * kDB], rj = rl[j * kDB];
       const double bx = xi - xj, by = yi - yj;
@@ -344,8 +363,12 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         max_pen = dmax(max_pen, depth);
         moved = true;
         // i and j moved: every LATER active pair touching them is re-queued
-        // (re-tested when popped); other pairs' inputs are unchanged.
-        cand.or_above(omask[i], omask[j], pact, p);
+        // (re-tested when popped); other pairs' inputs are unchanged.  While
+        // every object has moved less than kNear/2 since the broad pass (each
+        // hit moves two objects by |u|*s <= s*(1+1e-15)), pairs outside
+        // `near` still fail the broad test, so they are not re-queued.
+        swept += s;
+        cand.or_above(omask[i], omask[j], (2.0 * swept < kNear - 1e-9) ? near : pact, p);
       }
     }
     // 5. clamp every object (push_sim.cpp:118 -> :48-54).  clamp(v,-h,h) == v
