@@ -102,6 +102,7 @@ struct ppg_ctx {
   int disc_blocks_per_sm[kNumDisc] = {};  // resolve_disc_kernel<kDiscSizes[k]>
   bool disc_kernels = false;
   bool force_generic = false;             // PPG_FORCE_GENERIC=1: A/B the generic kernel
+  int disc_bps_override = 0;              // PPG_DISC_BLOCKS_PER_SM: cap resident blocks (experiments)
 };
 
 namespace {
@@ -321,6 +322,8 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
   {
     const char* fg = std::getenv("PPG_FORCE_GENERIC");
     ctx->force_generic = fg && fg[0] == '1';
+    const char* bo = std::getenv("PPG_DISC_BLOCKS_PER_SM");
+    ctx->disc_bps_override = bo ? std::atoi(bo) : 0;
   }
   if (!ok) {
     cudaGetLastError();
@@ -393,7 +396,10 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
     while (kDiscSizes[slot] < S.n) ++slot;
     const int nmax = kDiscSizes[slot];
     const int want = (E + kDiscBlock - 1) / kDiscBlock;
-    const int cap = ctx->disc_blocks_per_sm[slot] * ctx->num_sms;
+    const int bps = ctx->disc_bps_override > 0 && ctx->disc_bps_override < ctx->disc_blocks_per_sm[slot]
+                        ? ctx->disc_bps_override
+                        : ctx->disc_blocks_per_sm[slot];
+    const int cap = bps * ctx->num_sms;
     const int grid = want < cap ? want : cap;
     int* counter = ctx->b_counter.as<int>();
     const size_t sm = disc_smem(nmax);
