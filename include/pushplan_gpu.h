@@ -110,6 +110,10 @@ typedef struct ppg_search_stats {
   int64_t lockstep_rounds;
   uint64_t signature_fnv;       /* FNV-1a-64 of tree_signature() text (mcts.cpp:296-300) */
   int64_t n_nodes;
+  double select_s;              /* host time in select_batch + reset_virtual */
+  double expand_s;              /* batch_expand: device prepare + host attach */
+  double simulate_s;            /* batch_simulate on the device */
+  double backprop_s;            /* host backprop + early-stop bookkeeping */
 } ppg_search_stats;
 
 /* Fills the reference defaults. */

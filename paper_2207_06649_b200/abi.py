@@ -89,6 +89,10 @@ class PpgSearchStats(ctypes.Structure):
         ("lockstep_rounds", c_int64),
         ("signature_fnv", c_uint64),
         ("n_nodes", c_int64),
+        ("select_s", c_double),
+        ("expand_s", c_double),
+        ("simulate_s", c_double),
+        ("backprop_s", c_double),
     ]
 
 

@@ -138,6 +138,7 @@ class SearchResult:  # mcts.hpp:80-91
     signature_fnv: int
     n_nodes: int
     signature: Optional[str] = None
+    phase_s: Optional[dict] = None
 
 
 _ERRS = {abi.PPG_EINVAL: "invalid argument", abi.PPG_ECUDA: "CUDA error",
@@ -273,7 +274,9 @@ class Context:
                         "ppg_run_pmbs")
         return SearchResult(action, st.iterations, st.expansions, st.elapsed_s, abi.STOP_REASONS[st.stop_reason],
                             st.final_tree_depth, st.env_steps, st.rollout_steps, st.lockstep_rounds,
-                            int(st.signature_fnv), st.n_nodes, sig)
+                            int(st.signature_fnv), st.n_nodes, sig,
+                            {"select": st.select_s, "expand": st.expand_s, "simulate": st.simulate_s,
+                             "backprop": st.backprop_s})
 
 
 _DEFAULT_CTX: Optional[Context] = None

@@ -25,6 +25,9 @@ __global__ void expand_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
 __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
+__global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
 template <int NMAX>
 __global__ void resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a, int* next_env);
@@ -97,6 +100,7 @@ struct ppg_ctx {
   DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx;
   DevBuf l_W, l_rew, l_active, l_nactive, l_counters, l_npose, l_nmeta;
   DevBuf b_counter;              // persistent-kernel work counter
+  DevBuf l_push, l_status, l_stepping;
   int32_t* h_nactive = nullptr;  // pinned
   int num_sms = 148;
   int disc_blocks_per_sm[kNumDisc] = {};  // resolve_disc_kernel<kDiscSizes[k]>
@@ -310,6 +314,9 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
   ok = ok && cudaFuncSetAttribute(grasp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(lock_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(lock_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(expand_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(lock_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess;
   ok = ok && for_each_disc_kernel([&](int k, const void* fn) {
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -343,7 +350,7 @@ void ppg_destroy(ppg_ctx* ctx) {
                     &ctx->b_e, &ctx->l_node, &ctx->l_pushes, &ctx->l_done, &ctx->l_byg, &ctx->l_harv,
                     &ctx->l_flag, &ctx->l_reward, &ctx->l_poses, &ctx->l_mt, &ctx->l_mtidx, &ctx->l_W,
                     &ctx->l_rew, &ctx->l_active, &ctx->l_nactive, &ctx->l_counters, &ctx->l_npose,
-                    &ctx->l_nmeta};
+                    &ctx->l_nmeta, &ctx->b_counter, &ctx->l_push, &ctx->l_status, &ctx->l_stepping};
   for (DevBuf* b : bufs) b->release();
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -381,6 +388,40 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
   return PPG_SUCCESS;
 }
 
+// Launches resolve_disc_kernel<N> (N = the smallest instantiated size >= n)
+// as a persistent grid sized for `work` environments.
+static int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st) {
+  CK(ctx->b_counter.ensure(16));
+  CK(cudaMemsetAsync(ctx->b_counter.p, 0, 4, st));
+  int slot = 0;
+  while (kDiscSizes[slot] < n) ++slot;
+  const int nmax = kDiscSizes[slot];
+  const int want = (work + kDiscBlock - 1) / kDiscBlock;
+  const int bps = ctx->disc_bps_override > 0 && ctx->disc_bps_override < ctx->disc_blocks_per_sm[slot]
+                      ? ctx->disc_bps_override
+                      : ctx->disc_blocks_per_sm[slot];
+  const int cap = bps * ctx->num_sms;
+  const int grid = want < 1 ? 1 : (want < cap ? want : cap);
+  int* counter = ctx->b_counter.as<int>();
+  const size_t sm = disc_smem(nmax);
+  switch (nmax) {
+    case 4: resolve_disc_kernel<4><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    case 6: resolve_disc_kernel<6><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    case 8: resolve_disc_kernel<8><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    case 10: resolve_disc_kernel<10><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    case 11: resolve_disc_kernel<11><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    case 12: resolve_disc_kernel<12><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    case 14: resolve_disc_kernel<14><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    default: resolve_disc_kernel<16><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+  }
+  CK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
+static bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
+  return all_discs && n <= 16 && ctx->disc_kernels && !ctx->force_generic;
+}
+
 // Kernel #1 dispatch: all-disc batches (shapes without vertex tables) run the
 // register-resident persistent kernel (resolve_disc.cu) sized to the object
 // count; polygons, n > 16 and the counting variant run the generic kernel.
@@ -389,33 +430,7 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
                           double* d_resid, long long* d_counts, cudaStream_t st) {
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
-  if (!d_counts && all_discs && S.n <= 16 && ctx->disc_kernels && !ctx->force_generic) {
-    CK(ctx->b_counter.ensure(16));
-    CK(cudaMemsetAsync(ctx->b_counter.p, 0, 4, st));
-    int slot = 0;
-    while (kDiscSizes[slot] < S.n) ++slot;
-    const int nmax = kDiscSizes[slot];
-    const int want = (E + kDiscBlock - 1) / kDiscBlock;
-    const int bps = ctx->disc_bps_override > 0 && ctx->disc_bps_override < ctx->disc_blocks_per_sm[slot]
-                        ? ctx->disc_bps_override
-                        : ctx->disc_blocks_per_sm[slot];
-    const int cap = bps * ctx->num_sms;
-    const int grid = want < cap ? want : cap;
-    int* counter = ctx->b_counter.as<int>();
-    const size_t sm = disc_smem(nmax);
-    switch (nmax) {
-      case 4: resolve_disc_kernel<4><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-      case 6: resolve_disc_kernel<6><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-      case 8: resolve_disc_kernel<8><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-      case 10: resolve_disc_kernel<10><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-      case 11: resolve_disc_kernel<11><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-      case 12: resolve_disc_kernel<12><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-      case 14: resolve_disc_kernel<14><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-      default: resolve_disc_kernel<16><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    }
-    CK(cudaGetLastError());
-    return PPG_SUCCESS;
-  }
+  if (!d_counts && use_disc(ctx, all_discs, S.n)) return launch_disc(ctx, C, a, S.n, E, st);
   const int grid = (E + kBlock - 1) / kBlock;
   if (d_counts) resolve_kernel<true><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
   else resolve_kernel<false><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
@@ -597,7 +612,18 @@ int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, 
   const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
   ExpandArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_push.as<double>(), ctx->b_out.as<double>(),
                ctx->b_status.as<int32_t>(), ctx->b_a.as<uint8_t>(), ctx->b_e.as<int32_t>(), ctx->b_b.as<double>(), P};
-  expand_kernel<<<(P + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  if (use_disc(ctx, ctx->scene_all_discs, n)) {
+    // child = parent, resolve in place on the register-resident kernel, then
+    // sample + grasp (or restore the parent for a failed simulation)
+    CK(cudaMemcpyAsync(ctx->b_out.p, ctx->b_in.p, pbytes, cudaMemcpyDeviceToDevice, st));
+    ResolveArgs ra{ctx->scene, ctx->b_out.as<double>(), ctx->b_push.as<double>(), ctx->b_out.as<double>(),
+                   ctx->b_status.as<int32_t>(), nullptr, nullptr, P};
+    const int rc = launch_disc(ctx, C, ra, n, P, st);
+    if (rc != PPG_SUCCESS) return rc;
+    expand_post_kernel<<<(P + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  } else {
+    expand_kernel<<<(P + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(child_poses, ctx->b_out.p, pbytes, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(status, ctx->b_status.p, static_cast<size_t>(P) * 4, cudaMemcpyDeviceToHost, st));
@@ -647,6 +673,9 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   CK(ctx->l_counters.ensure(4 * 8));
   CK(ctx->l_npose.ensure(static_cast<size_t>(n_nodes) * n * 3 * 8));
   CK(ctx->l_nmeta.ensure(static_cast<size_t>(n_nodes) * 3 * 4));
+  CK(ctx->l_push.ensure(static_cast<size_t>(E) * 32));
+  CK(ctx->l_status.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_stepping.ensure(static_cast<size_t>(E) * 4 + 16));
   CK(cudaMemcpyAsync(ctx->l_npose.p, node_poses, static_cast<size_t>(n_nodes) * n * 3 * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ctx->l_nmeta.p, node_meta, static_cast<size_t>(n_nodes) * 3 * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ctx->l_counters.p, 0, 32, st));
@@ -677,6 +706,14 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   a.active = ctx->l_active.as<int32_t>();
   a.n_active = ctx->l_nactive.as<int32_t>();
   a.counters = ctx->l_counters.as<long long>();
+  a.env_push = ctx->l_push.as<double>();
+  a.env_status = ctx->l_status.as<int32_t>();
+  a.n_stepping = ctx->l_stepping.as<int32_t>();
+  a.stepping = ctx->l_stepping.as<int32_t>() + 4;
+  const bool discs = use_disc(ctx, ctx->scene_all_discs, n);
+  ResolveArgs ra{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, 0};
+  ra.idx = a.stepping;
+  ra.E_dev = a.n_stepping;
   const int ginit = ((E > n_nodes ? E : n_nodes) + 255) / 256;
   lock_init_kernel<<<ginit, 256, 0, st>>>(C, a);
   CK(cudaGetLastError());
@@ -687,8 +724,18 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
     CK(cudaStreamSynchronize(st));
     const int act = *ctx->h_nactive;
     if (act == 0) break;
-    lock_step_kernel<<<(act + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
-    CK(cudaGetLastError());
+    const int g = (act + kBlock - 1) / kBlock;
+    if (discs) {  // sample+pick -> register-resident physics (in place) -> grasp + reward
+      lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+      CK(cudaGetLastError());
+      const int rc = launch_disc(ctx, C, ra, n, act, st);
+      if (rc != PPG_SUCCESS) return rc;
+      lock_post_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+      CK(cudaGetLastError());
+    } else {
+      lock_step_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+      CK(cudaGetLastError());
+    }
   }
   CK(cudaMemcpyAsync(rewards_out, a.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
   if (counters) CK(cudaMemcpyAsync(counters, a.counters, 32, cudaMemcpyDeviceToHost, st));

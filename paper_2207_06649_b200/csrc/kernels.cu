@@ -162,6 +162,28 @@ __global__ void __launch_bounds__(128) expand_kernel(const __grid_constant__ Sim
   a.grasp[p] = graspable(P, S, C, a.S.target[0]).graspable ? 1 : 0;
 }
 
+// batch_expand prepare, disc pipeline phase 2 (after resolve_disc_kernel ran
+// in place on the child buffer): dead child on failure, else the child's
+// full untried list and grasp flag (pmbs.cpp:82-93).
+__global__ void __launch_bounds__(128) expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a) {
+  extern __shared__ double smem[];
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.P) return;
+  const int n = C.n;
+  double* child = a.child_poses + static_cast<size_t>(p) * n * 3;
+  if (a.status[p] != 0) {  // dead child: copy of the parent state (mcts.cpp:89-92)
+    const double* parent = a.parent_poses + static_cast<size_t>(p) * n * 3;
+    for (int i = 0; i < n * 3; ++i) child[i] = parent[i];
+    a.grasp[p] = 0;
+    a.n_untried[p] = 0;
+    return;
+  }
+  const PoseView P = stage_poses(smem, n, child);
+  const ShapeView S = a.S.view(0);
+  a.n_untried[p] = sample_all(P, S, C, a.untried + static_cast<size_t>(p) * n * C.na * 4);
+  a.grasp[p] = graspable(P, S, C, a.S.target[0]).graspable ? 1 : 0;
+}
+
 // ---------------- lockstep engine ----------------
 
 // RolloutCursor ctor (mcts.cpp:121-140) for env e at node `node`.
@@ -186,11 +208,8 @@ PPG_DI void cursor_init(const SimConst& C, const LockArgs& a, int e, int node) {
   a.env_reward[e] = reward;
   const int n = C.n;
   const double* src = a.node_poses + static_cast<size_t>(node) * n * 3;
-  for (int i = 0; i < n; ++i) {
-    a.env_poses[(static_cast<size_t>(i)) * a.E + e] = src[i * 3];
-    a.env_poses[(static_cast<size_t>(n + i)) * a.E + e] = src[i * 3 + 1];
-    a.env_poses[(static_cast<size_t>(2 * n + i)) * a.E + e] = src[i * 3 + 2];
-  }
+  double* dst = a.env_poses + static_cast<size_t>(e) * n * 3;
+  for (int i = 0; i < 3 * n; ++i) dst[i] = src[i];
 }
 
 __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
@@ -223,6 +242,7 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
   if (tid == 0) {
     s_active = 0;
     s_rep = 0;
+    *a.n_stepping = 0;
   }
   for (int i = tid; i < a.n_nodes; i += B) a.W[i] = 0;
   __syncthreads();
@@ -298,34 +318,23 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
   }
 }
 
-// RolloutCursor::step (mcts.cpp:142-171) for each active env.
-__global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a) {
-  extern __shared__ double smem[];
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int n_act = *a.n_active;
-  if (gid >= n_act) return;
-  const int e = a.active[gid];
-  const int n = C.n;
-  PoseView P{smem + threadIdx.x, static_cast<int>(blockDim.x), n};
-  for (int i = 0; i < 3 * n; ++i) P.p[i * P.stride] = a.env_poses[static_cast<size_t>(i) * a.E + e];
-  const ShapeView S = a.S.view(0);
-  // sample_pushes: count the valid candidates, remembering which (bitmask).
+// sample_pushes for a lockstep env + the Lemire pick from its MT stream
+// (mcts.cpp:145-152).  Returns false when there is no legal push.
+PPG_DI bool rollout_pick(const PoseView& P, const ShapeView& S, const SimConst& C, const LockArgs& a, int e,
+                         V2& s, V2& t) {
+  // count the valid candidates, remembering which (bitmask)
   uint32_t mask[(kMaxObjects * kMaxNa) / 32];
-  const int total = n * C.na;
+  const int total = P.n * C.na;
   int count = 0;
   for (int c = 0; c < total; ++c) {
     if ((c & 31) == 0) mask[c >> 5] = 0;
-    V2 s, t;
-    if (push_candidate(P, S, C, c / C.na, c % C.na, true, s, t)) {
+    V2 s0, t0;
+    if (push_candidate(P, S, C, c / C.na, c % C.na, true, s0, t0)) {
       mask[c >> 5] |= 1u << (c & 31);
       ++count;
     }
   }
-  if (count == 0) {
-    a.env_done[e] = 1;
-    a.env_reward[e] = 0.0;
-    return;
-  }
+  if (count == 0) return false;
   MtView g{a.mt + e, a.E};
   int idx = a.mt_idx[e];
   const uint64_t k = mt_pick(g, idx, static_cast<uint64_t>(count));
@@ -337,17 +346,13 @@ __global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ 
       ++seen;
     }
   }
-  V2 s, t;
   push_candidate(P, S, C, c / C.na, c % C.na, false, s, t);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
-  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), 1ull);
-  double residual;
-  const int st = resolve_push<false>(P, S, C, s, t, false, &residual, nullptr);
-  if (st != 0) {
-    a.env_done[e] = 1;
-    a.env_reward[e] = 0.0;
-    return;
-  }
+  return true;
+}
+
+// The part of RolloutCursor::step after a successful resolve_push
+// (mcts.cpp:159-170): count the push, grasp check, reward gamma^pushes.
+PPG_DI void rollout_finish_step(const PoseView& P, const ShapeView& S, const SimConst& C, const LockArgs& a, int e) {
   const int pushes = a.env_pushes[e] + 1;
   a.env_pushes[e] = pushes;
   if (graspable(P, S, C, a.S.target[0]).graspable) {
@@ -358,7 +363,83 @@ __global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ 
     a.env_done[e] = 1;
     a.env_reward[e] = 0.0;
   }
-  for (int i = 0; i < 3 * n; ++i) a.env_poses[static_cast<size_t>(i) * a.E + e] = P.p[i * P.stride];
+}
+
+// RolloutCursor::step (mcts.cpp:142-171) for each active env, all in one lane
+// (polygon scenes and n > 16).
+__global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  extern __shared__ double smem[];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_act = *a.n_active;
+  if (gid >= n_act) return;
+  const int e = a.active[gid];
+  const int n = C.n;
+  double* env = a.env_poses + static_cast<size_t>(e) * n * 3;
+  const PoseView P = stage_poses(smem, n, env);
+  const ShapeView S = a.S.view(0);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
+  V2 s, t;
+  if (!rollout_pick(P, S, C, a, e, s, t)) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), 1ull);
+  double residual;
+  const int st = resolve_push<false>(P, S, C, s, t, false, &residual, nullptr);
+  if (st != 0) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  rollout_finish_step(P, S, C, a, e);
+  unstage_poses(P, env);
+}
+
+// Disc scenes, phase 1 of a round: sample + pick for each active env; envs
+// with a legal push are appended to the `stepping` list for the physics
+// kernel (resolve_disc_kernel with env-slot indirection, in place).
+__global__ void __launch_bounds__(128) lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  extern __shared__ double smem[];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_act = *a.n_active;
+  if (gid >= n_act) return;
+  const int e = a.active[gid];
+  const int n = C.n;
+  const PoseView P = stage_poses(smem, n, a.env_poses + static_cast<size_t>(e) * n * 3);
+  const ShapeView S = a.S.view(0);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
+  V2 s, t;
+  if (!rollout_pick(P, S, C, a, e, s, t)) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  double* pu = a.env_push + static_cast<size_t>(e) * 4;
+  pu[0] = s.x;
+  pu[1] = s.y;
+  pu[2] = t.x;
+  pu[3] = t.y;
+  a.stepping[atomicAdd(a.n_stepping, 1)] = e;
+}
+
+// Disc scenes, phase 3: the rest of RolloutCursor::step for the envs the
+// physics kernel resolved.
+__global__ void __launch_bounds__(128) lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  extern __shared__ double smem[];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_st = *a.n_stepping;
+  if (gid == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), static_cast<unsigned long long>(n_st));
+  if (gid >= n_st) return;
+  const int e = a.stepping[gid];
+  if (a.env_status[e] != 0) {  // SimError: reward 0 (mcts.cpp:153-158)
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  const int n = C.n;
+  const PoseView P = stage_poses(smem, n, a.env_poses + static_cast<size_t>(e) * n * 3);
+  rollout_finish_step(P, a.S.view(0), C, a, e);
 }
 
 }  // namespace ppg

@@ -30,6 +30,8 @@ struct ResolveArgs {
   double* residual;        // [E] or null
   long long* counts;       // [E][8] (counting variant)
   int E;
+  const int* idx = nullptr;    // optional env-slot indirection (lockstep / expand)
+  const int* E_dev = nullptr;  // optional device-side count (overrides E)
 };
 
 struct SampleArgs {
@@ -75,7 +77,11 @@ struct LockArgs {
   uint8_t* env_harvested;
   uint8_t* env_flag;
   double* env_reward;
-  double* env_poses;    // [3][n][E] planes, env fastest
+  double* env_poses;    // [E][n][3] (the physics kernels' AoS layout)
+  double* env_push;     // [E][4] this round's push
+  int32_t* env_status;  // [E] this round's resolve status
+  int32_t* stepping;    // [used] envs with a push this round (disc pipeline)
+  int32_t* n_stepping;  // [1]
   uint64_t* mt;         // [312][E]
   int32_t* mt_idx;      // [E]
   int E;                // allocated stride for env arrays

@@ -197,7 +197,10 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
   std::vector<int32_t> status, n_untried, meta;
   std::vector<uint8_t> grasp;
   std::vector<int> children;
+  using clk = std::chrono::steady_clock;
+  const auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
   while (true) {
+    const auto t0 = clk::now();
     // select_batch (pmbs.cpp:52-63)
     sel_node.clear();
     sel_action.clear();
@@ -214,6 +217,8 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
       break;
     }
     for (Node& nd : tree.nodes) nd.vvisits = 0;  // reset_virtual pmbs.cpp:65-68
+    const auto t1 = clk::now();
+    st.select_s += secs(t0, t1);
 
     // batch_expand (pmbs.cpp:70-131): device prepare, host attach in batch order
     const int P = static_cast<int>(sel_node.size());
@@ -265,6 +270,8 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
     }
     st.expansions += P;
     update_es_level(tree);
+    const auto t2 = clk::now();
+    st.expand_s += secs(t1, t2);
 
     // batch_simulate (pmbs.cpp:207-234) on the device
     node_poses.resize(static_cast<size_t>(P) * n * 3);
@@ -282,6 +289,8 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
                            cfg.rng_seed, static_cast<uint64_t>(iter), tree.tree_depth + tree.rollout_depth,
                            rewards.data(), ctr)) != PPG_SUCCESS)
       return rc;
+    const auto t3 = clk::now();
+    st.simulate_s += secs(t2, t3);
     st.rollout_steps += ctr[0];
     st.lockstep_rounds += ctr[1];
     st.env_steps += ctr[3];
@@ -293,7 +302,9 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
         tree.nodes[a].visits += 1;
       }
     ++iter;
-    if (early_stop_satisfied(tree)) {
+    const bool es = early_stop_satisfied(tree);
+    st.backprop_s += secs(t3, clk::now());
+    if (es) {
       stop = 2;
       break;
     }

@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   int step = 0, iter = 0;
   const int total_threads = gridDim.x * kDB;
   int e = blockIdx.x * kDB + tid;
+  int ee = e;
+  const int E = a.E_dev ? *a.E_dev : a.E;
   bool have = false;
   bool need_init = true;
 
@@ -170,9 +172,10 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     if (need_init) {
       need_init = false;
       have = false;
-      while (e < a.E) {
-        const double* src = a.poses_in + static_cast<size_t>(e) * n * 3;
-        const int t = a.S.T == 1 ? 0 : e;
+      while (e < E) {
+        ee = a.idx ? a.idx[e] : e;  // environment slot (indirection for the lockstep engine)
+        const double* src = a.poses_in + static_cast<size_t>(ee) * n * 3;
+        const int t = a.S.T == 1 ? 0 : ee;
         static_for<NMAX>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           const bool real = i < n;
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
           yl[i * kDB] = y[i];
           rl[i * kDB] = r[i];
         });
-        const double* pu = a.pushes + static_cast<size_t>(e) * 4;
+        const double* pu = a.pushes + static_cast<size_t>(ee) * 4;
         start = V2{pu[0], pu[1]};
         const V2 end{pu[2], pu[3]};
         // collides_gripper_start (world.cpp:154-164)
@@ -198,9 +201,9 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
           });
         }
         if (collide) {
-          a.status[e] = 1;
-          if (a.residual) a.residual[e] = 0.0;
-          double* out = a.poses_out + static_cast<size_t>(e) * n * 3;
+          a.status[ee] = 1;
+          if (a.residual) a.residual[ee] = 0.0;
+          double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
           for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
           e = atomicAdd(next_env, 1) + total_threads;
           continue;
@@ -255,14 +258,14 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         worst = dmax(worst, rl[i * kDB] + rl[j * kDB] - sqrt(bx * bx + by * by));  // == norm(pos_j - pos_i)
       }
       const int st = worst > C.eps_pen ? 2 : 0;
-      a.status[e] = st;
-      if (a.residual) a.residual[e] = worst;
-      double* out = a.poses_out + static_cast<size_t>(e) * n * 3;
+      a.status[ee] = st;
+      if (a.residual) a.residual[ee] = worst;
+      double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
       if (st == 0) {
         for (int i = 0; i < n; ++i) {
           out[i * 3] = xl[i * kDB];
           out[i * 3 + 1] = yl[i * kDB];
-          out[i * 3 + 2] = a.poses_in[(static_cast<size_t>(e) * n + i) * 3 + 2];  // discs never rotate
+          out[i * 3 + 2] = a.poses_in[(static_cast<size_t>(ee) * n + i) * 3 + 2];  // discs never rotate (in place: same value)
         }
       } else {
         for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
