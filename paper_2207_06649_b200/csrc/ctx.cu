@@ -27,6 +27,11 @@ __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
+__global__ void resolve_warp_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
+__global__ void expand_warp_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
+__global__ void lock_step_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
+constexpr int kWarpMaxN = 23;
+constexpr int kWarpsPerBlock = 4;
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
 template <int NMAX>
@@ -107,6 +112,7 @@ struct ppg_ctx {
   bool disc_kernels = false;
   bool force_generic = false;             // PPG_FORCE_GENERIC=1: A/B the generic kernel
   int disc_bps_override = 0;              // PPG_DISC_BLOCKS_PER_SM: cap resident blocks (experiments)
+  int warp_max_envs = 4096;               // latency mode (one warp per env) up to this many envs; PPG_WARP_MAX
 };
 
 namespace {
@@ -329,6 +335,8 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
   {
     const char* fg = std::getenv("PPG_FORCE_GENERIC");
     ctx->force_generic = fg && fg[0] == '1';
+    const char* wm = std::getenv("PPG_WARP_MAX");
+    if (wm) ctx->warp_max_envs = std::atoi(wm);
     const char* bo = std::getenv("PPG_DISC_BLOCKS_PER_SM");
     ctx->disc_bps_override = bo ? std::atoi(bo) : 0;
   }
@@ -422,6 +430,11 @@ static bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
   return all_discs && n <= 16 && ctx->disc_kernels && !ctx->force_generic;
 }
 
+// Latency mode: one warp per environment (warp_env.cu) for small batches.
+static bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs) {
+  return all_discs && n <= kWarpMaxN && envs <= ctx->warp_max_envs && !ctx->force_generic;
+}
+
 // Kernel #1 dispatch: all-disc batches (shapes without vertex tables) run the
 // register-resident persistent kernel (resolve_disc.cu) sized to the object
 // count; polygons, n > 16 and the counting variant run the generic kernel.
@@ -430,6 +443,11 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
                           double* d_resid, long long* d_counts, cudaStream_t st) {
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
+  if (!d_counts && use_warp(ctx, all_discs, S.n, E)) {
+    resolve_warp_kernel<<<(E + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
+    CK(cudaGetLastError());
+    return PPG_SUCCESS;
+  }
   if (!d_counts && use_disc(ctx, all_discs, S.n)) return launch_disc(ctx, C, a, S.n, E, st);
   const int grid = (E + kBlock - 1) / kBlock;
   if (d_counts) resolve_kernel<true><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
@@ -612,7 +630,9 @@ int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, 
   const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
   ExpandArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_push.as<double>(), ctx->b_out.as<double>(),
                ctx->b_status.as<int32_t>(), ctx->b_a.as<uint8_t>(), ctx->b_e.as<int32_t>(), ctx->b_b.as<double>(), P};
-  if (use_disc(ctx, ctx->scene_all_discs, n)) {
+  if (use_warp(ctx, ctx->scene_all_discs, n, P)) {
+    expand_warp_kernel<<<(P + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
+  } else if (use_disc(ctx, ctx->scene_all_discs, n)) {
     // child = parent, resolve in place on the register-resident kernel, then
     // sample + grasp (or restore the parent for a failed simulation)
     CK(cudaMemcpyAsync(ctx->b_out.p, ctx->b_in.p, pbytes, cudaMemcpyDeviceToDevice, st));
@@ -725,7 +745,10 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
     const int act = *ctx->h_nactive;
     if (act == 0) break;
     const int g = (act + kBlock - 1) / kBlock;
-    if (discs) {  // sample+pick -> register-resident physics (in place) -> grasp + reward
+    if (use_warp(ctx, ctx->scene_all_discs, n, act)) {  // latency mode: one warp per active env
+      lock_step_warp_kernel<<<(act + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
+      CK(cudaGetLastError());
+    } else if (discs) {  // sample+pick -> register-resident physics (in place) -> grasp + reward
       lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
       CK(cudaGetLastError());
       const int rc = launch_disc(ctx, C, ra, n, act, st);

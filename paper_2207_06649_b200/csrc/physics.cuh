@@ -300,68 +300,76 @@ struct GraspOut {
   int k;  // -1: no feasible pose
 };
 
-// graspable (actions.cpp:113-147) with grasp_fingers (actions.cpp:75-111).
+// One grasp angle k of graspable (actions.cpp:118-140) with grasp_fingers
+// (actions.cpp:75-111).  Returns true when the pose is feasible; *margin is
+// its minimum obstacle clearance and (cx, cy) the grasp centre.
+PPG_DI bool grasp_angle(const PoseView& P, const ShapeView& S, const SimConst& C, int target, int k,
+                        double* margin_out, double* cx, double* cy) {
+  const double ht = C.finger_thickness / 2.0;
+  const double hw = C.finger_width / 2.0;
+  const V2 u{C.g_cos[k], C.g_sin[k]};
+  const V2 v = perp(u);
+  double lo_u, hi_u, lo_v, hi_v;
+  if (S.kind_(target) == 0) {
+    const V2 tp = P.pos(target);
+    const double r = S.rad_(target);
+    const double cu = dot(tp, u);
+    const double cv = dot(tp, v);
+    lo_u = cu - r;
+    hi_u = cu + r;
+    lo_v = cv - r;
+    hi_v = cv + r;
+  } else {
+    Poly tpoly;
+    world_polygon(P, S, target, tpoly);
+    hi_u = support_extent(tpoly, u);
+    lo_u = -support_extent(tpoly, -u);
+    hi_v = support_extent(tpoly, v);
+    lo_v = -support_extent(tpoly, -v);
+  }
+  const double extent = hi_u - lo_u;
+  if (!(extent < C.opening - 2.0 * C.approach_clearance)) return false;
+  const V2 center = u * ((lo_u + hi_u) / 2.0) + v * ((lo_v + hi_v) / 2.0);
+  Poly ra, rb;
+  {
+    const V2 ca = center + u * (-(C.opening / 2.0 + ht));
+    const V2 cb = center + u * (C.opening / 2.0 + ht);
+    ra.n = rb.n = 4;
+    ra.p[0] = ca - u * ht - v * hw;
+    ra.p[1] = ca + u * ht - v * hw;
+    ra.p[2] = ca + u * ht + v * hw;
+    ra.p[3] = ca - u * ht + v * hw;
+    rb.p[0] = cb - u * ht - v * hw;
+    rb.p[1] = cb + u * ht - v * hw;
+    rb.p[2] = cb + u * ht + v * hw;
+    rb.p[3] = cb - u * ht + v * hw;
+  }
+  if (dmin(rect_min_wall_clearance(ra, C.side), rect_min_wall_clearance(rb, C.side)) <= 0.0) return false;
+  double margin = C.side;
+  for (int i = 0; i < S.n; ++i) {
+    if (i == target) continue;
+    const double d = dmin(rect_object_distance(ra, P, S, i), rect_object_distance(rb, P, S, i));
+    if (d <= 0.0) return false;
+    margin = dmin(margin, d);
+  }
+  *margin_out = margin;
+  *cx = center.x;
+  *cy = center.y;
+  return true;
+}
+
+// graspable (actions.cpp:113-147): first strict maximum of the margin over
+// feasible angles in index order.
 PPG_DI GraspOut graspable(const PoseView& P, const ShapeView& S, const SimConst& C, int target) {
   double best_margin = -1.0;
   GraspOut g{false, 0.0, 0.0, 0.0, -1};
-  const double ht = C.finger_thickness / 2.0;
-  const double hw = C.finger_width / 2.0;
-  const bool tdisc = S.kind_(target) == 0;
-  Poly tpoly;
-  if (!tdisc) world_polygon(P, S, target, tpoly);
   for (int k = 0; k < kGraspAngles; ++k) {
-    const V2 u{C.g_cos[k], C.g_sin[k]};
-    const V2 v = perp(u);
-    double lo_u, hi_u, lo_v, hi_v;
-    if (tdisc) {
-      const V2 tp = P.pos(target);
-      const double r = S.rad_(target);
-      const double cu = dot(tp, u);
-      const double cv = dot(tp, v);
-      lo_u = cu - r;
-      hi_u = cu + r;
-      lo_v = cv - r;
-      hi_v = cv + r;
-    } else {
-      hi_u = support_extent(tpoly, u);
-      lo_u = -support_extent(tpoly, -u);
-      hi_v = support_extent(tpoly, v);
-      lo_v = -support_extent(tpoly, -v);
-    }
-    const double extent = hi_u - lo_u;
-    if (!(extent < C.opening - 2.0 * C.approach_clearance)) continue;
-    const V2 center = u * ((lo_u + hi_u) / 2.0) + v * ((lo_v + hi_v) / 2.0);
-    Poly ra, rb;
-    {
-      const V2 ca = center + u * (-(C.opening / 2.0 + ht));
-      const V2 cb = center + u * (C.opening / 2.0 + ht);
-      ra.n = rb.n = 4;
-      ra.p[0] = ca - u * ht - v * hw;
-      ra.p[1] = ca + u * ht - v * hw;
-      ra.p[2] = ca + u * ht + v * hw;
-      ra.p[3] = ca - u * ht + v * hw;
-      rb.p[0] = cb - u * ht - v * hw;
-      rb.p[1] = cb + u * ht - v * hw;
-      rb.p[2] = cb + u * ht + v * hw;
-      rb.p[3] = cb - u * ht + v * hw;
-    }
-    if (dmin(rect_min_wall_clearance(ra, C.side), rect_min_wall_clearance(rb, C.side)) <= 0.0) continue;
-    double margin = C.side;
-    bool feasible = true;
-    for (int i = 0; i < S.n; ++i) {
-      if (i == target) continue;
-      const double d = dmin(rect_object_distance(ra, P, S, i), rect_object_distance(rb, P, S, i));
-      if (d <= 0.0) {
-        feasible = false;
-        break;
-      }
-      margin = dmin(margin, d);
-    }
-    if (feasible && margin > best_margin) {
+    double margin, cx, cy;
+    if (grasp_angle(P, S, C, target, k, &margin, &cx, &cy) && margin > best_margin) {
       best_margin = margin;
       g.k = k;
-      g.x = center.x;
-      g.y = center.y;
+      g.x = cx;
+      g.y = cy;
     }
   }
   if (g.k >= 0) {

@@ -182,14 +182,28 @@ def test_run_pmbs_budget_and_errors(ctx):
     assert r.iterations == 3 and r.stop_reason == "budget"
 
 
-def _generic_ctx():
+def _ctx_with(**env):
+    """A context created under kernel-selection overrides: PPG_FORCE_GENERIC=1
+    (straight transcription), PPG_WARP_MAX=0 (no warp-per-env latency mode)."""
     import os
     from paper_2207_06649_b200 import Context
-    os.environ["PPG_FORCE_GENERIC"] = "1"
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
     try:
         return Context(0, default_params())
     finally:
-        del os.environ["PPG_FORCE_GENERIC"]
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+
+
+def _generic_ctx():
+    return _ctx_with(PPG_FORCE_GENERIC=1)
+
+
+MODES = {"warp": {}, "lane": {"PPG_WARP_MAX": 0}, "generic": {"PPG_FORCE_GENERIC": 1}}
 
 
 @pytest.mark.parametrize("n,motif", [(1, "random"), (3, "random"), (6, "random"), (8, "random"), (9, "random"),
@@ -213,12 +227,65 @@ def test_disc_fast_path_matches_generic_and_oracle(ctx, n, motif):
     pushes = np.concatenate([pushes, bad])
     tt = _take(t, idx)
     pp = np.ascontiguousarray(poses[idx])
-    out, st, res = ctx.batch_resolve_arrays(tt, pp, pushes)
-    g = _generic_ctx()
-    out2, st2, res2 = g.batch_resolve_arrays(tt, pp, pushes)
-    g.close()
     o3, s3, r3 = port.batch_resolve(tt, pp, pushes, P)
-    assert np.array_equal(st, s3) and np.array_equal(st2, s3)
-    assert np.all(st[-len(poses):] == 1)
-    assert _bitwise(out, o3).all() and _bitwise(out2, o3).all()
-    assert np.array_equal(res.view(np.uint64), r3.view(np.uint64))
+    assert np.all(s3[-len(poses):] == 1)
+    for mode, env in MODES.items():
+        c = _ctx_with(**env)
+        out, st, res = c.batch_resolve_arrays(tt, pp, pushes)
+        c.close()
+        assert np.array_equal(st, s3), mode
+        assert _bitwise(out, o3).all(), mode
+        assert np.array_equal(res.view(np.uint64), r3.view(np.uint64)), mode
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_all_kernel_modes_on_golden_resolve_sets(mode):
+    c = _ctx_with(**MODES[mode])
+    for name in ["discs", "ring16", "hard18"]:
+        t, poses, pushes, status, digests, out_ref = golden_io.resolve_set(name)
+        out, st, resid = c.batch_resolve_arrays(t, poses, pushes)
+        assert np.array_equal(st, status), (mode, name)
+        ok = status == 0
+        assert _bitwise(out[ok], out_ref[ok]).all(), (mode, name)
+    c.close()
+
+
+@pytest.mark.parametrize("mode", ["warp", "lane"])
+def test_simulate_and_expand_modes(mode):
+    c = _ctx_with(**MODES[mode])
+    cases = {cc["case_id"]: st for cc, st in golden_io.cases()}
+    for cid, ne, seed, cap, poses, meta, rewards in golden_io.simulate_sets():
+        st = cases[cid]
+        if not np.all(st.kind == 0):
+            continue
+        c.set_params(default_params(n_envs=ne, rng_seed=seed))
+        c.set_scene(st)
+        r, ctr = c.simulate_arrays(poses, meta, ne, True, seed, 0, cap)
+        assert np.array_equal(r, rewards), (mode, cid)
+        ro, co = port.simulate(st, poses, meta, ne, True, seed, 0, cap, default_params(n_envs=ne))
+        assert np.array_equal(ctr, co), (mode, cid)
+    c.set_params(P)
+    for cc, st in golden_io.cases()[10:13]:
+        c.set_scene(st)
+        sp = port.sample_pushes(st, P)
+        parents = np.repeat(st.poses[None], len(sp), 0)
+        child, status, g, nu, un = c.expand_arrays(parents, sp)
+        exp, est, _ = port.batch_resolve(ShapeTable.shared(st), parents, sp, P)
+        assert np.array_equal(status, est), mode
+        for k in range(len(sp)):
+            if est[k] == 0:
+                s2 = st.with_poses(exp[k])
+                sp2 = port.sample_pushes(s2, P)
+                assert nu[k] == len(sp2) and _bitwise(un[k, :nu[k]][None], sp2[None]).all(), mode
+                assert bool(g[k]) == port.graspable(s2, P)[0], mode
+    c.close()
+
+
+@pytest.mark.parametrize("idx", [12, 17, 19])
+def test_fingerprints_lane_mode(idx):
+    c = _ctx_with(PPG_WARP_MAX=0)
+    cc, st = golden_io.cases()[idx]
+    d = cc["decision"]
+    r = run_pmbs(st, ParallelConfig(rng_seed=int(cc["seed"])), ctx=c)
+    assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
+    c.close()
