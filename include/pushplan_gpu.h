@@ -188,6 +188,36 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
                  int n_envs, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap,
                  double* rewards_out, int64_t* counters);
 
+/* ---- sharded lockstep (multi-GPU batch_simulate) ----
+ * The lockstep engine split by environment: this context owns global envs
+ * [env_lo, env_hi) of a batch of used_envs (= n_envs with leaf parallelism,
+ * else n_nodes).  env -> node split and RNG keys use GLOBAL env indices, so
+ * the union of the shards reproduces the unsharded batch exactly.  A driver
+ * (python: paper_2207_06649_b200.sharded) loops:
+ *   report -> exchange records / W -> global harvest (identical on every
+ *   rank) -> repurpose -> step,
+ * until no rank has an active env.  ppg_lock_report returns this shard's
+ * newly finished envs in increasing global index (env, node, by_grasp,
+ * reward; capacity env_hi - env_lo) and its remaining-work vector
+ * W_local[n_nodes] = sum over assigned not-done envs of cap - pushes
+ * (pmbs.cpp:157-163). */
+int ppg_lock_begin(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used_envs,
+                   int env_lo, int env_hi, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap);
+int ppg_lock_report(ppg_ctx* ctx, int32_t* rec_env, int32_t* rec_node, uint8_t* rec_grasp, double* rec_reward,
+                    int32_t* n_rec, int32_t* w_local, int32_t* n_active);
+int ppg_lock_repurpose(ppg_ctx* ctx, const int32_t* env, const int32_t* node, int count);
+int ppg_lock_step(ppg_ctx* ctx);
+/* counters (4 x int64): rollout steps, -, -, resolve calls of this shard */
+int ppg_lock_counters(ppg_ctx* ctx, int64_t* counters);
+
+/* Replaces the planner's batch_simulate (ppg_run_pmbs) with a caller
+ * function of ppg_simulate's signature (minus ctx) — e.g. the sharded
+ * multi-GPU driver.  fn == NULL restores the built-in device lockstep. */
+typedef int (*ppg_simulate_fn)(void* user, const double* node_poses, const int32_t* node_meta, int n_nodes,
+                               int n_envs, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap,
+                               double* rewards_out, int64_t* counters);
+int ppg_set_simulate_hook(ppg_ctx* ctx, ppg_simulate_fn fn, void* user);
+
 /* run_pmbs (pmbs.hpp:91, pmbs.cpp:242-292) on the context scene and poses:
  * the full PMBS planning decision.  Tree kept on the host (C++), batched
  * expansion and lockstep rollouts on the device.  action_out[4] = chosen push.

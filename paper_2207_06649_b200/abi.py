@@ -165,6 +165,14 @@ SIGNATURES = {
     "ppg_state_digest": (c_int, [POINTER(PpgShapes), POINTER(c_double), c_int, POINTER(c_uint64)]),
     "ppg_batch_resolve_count_dev": (c_int, [c_void_p, POINTER(PpgShapes), c_void_p, c_void_p, c_int,
                                             c_void_p, c_void_p]),
+    "ppg_lock_begin": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int32), c_int, c_int, c_int, c_int, c_int,
+                               c_uint64, c_uint64, c_int]),
+    "ppg_lock_report": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int32), POINTER(c_uint8), POINTER(c_double),
+                                POINTER(c_int32), POINTER(c_int32), POINTER(c_int32)]),
+    "ppg_lock_repurpose": (c_int, [c_void_p, POINTER(c_int32), POINTER(c_int32), c_int]),
+    "ppg_lock_step": (c_int, [c_void_p]),
+    "ppg_lock_counters": (c_int, [c_void_p, POINTER(c_int64)]),
+    "ppg_set_simulate_hook": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ppg_measure_fp64_peak": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "ppg_generate_cases": (c_int, [c_int, c_int, c_double, POINTER(c_uint64), c_int, POINTER(c_int32),
                                    POINTER(c_double), POINTER(c_int32), POINTER(c_double), POINTER(c_double),
@@ -172,6 +180,9 @@ SIGNATURES = {
     "ppg_keyed_picks": (c_int, [c_uint64, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_uint64), c_int,
                                 POINTER(c_uint64)]),
 }
+
+SIMULATE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, POINTER(c_double), POINTER(c_int32), c_int, c_int, c_int, c_uint64,
+                               c_uint64, c_int, POINTER(c_double), POINTER(c_int64))
 
 _LIB = None
 

@@ -33,6 +33,9 @@ __global__ void lock_step_warp_kernel(const __grid_constant__ SimConst C, LockAr
 constexpr int kWarpMaxN = 23;
 constexpr int kWarpsPerBlock = 4;
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_report_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockArgs a, const int32_t* env,
+                                      const int32_t* node, int count);
 __global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
 template <int NMAX>
 __global__ void resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a, int* next_env);
@@ -105,7 +108,13 @@ struct ppg_ctx {
   DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx;
   DevBuf l_W, l_rew, l_active, l_nactive, l_counters, l_npose, l_nmeta;
   DevBuf b_counter;              // persistent-kernel work counter
-  DevBuf l_push, l_status, l_stepping;
+  DevBuf l_push, l_status, l_stepping, l_rec;
+  LockArgs la{};        // current lockstep session
+  ResolveArgs lra{};    // its in-place physics arguments
+  SimConst lc{};        // its constants
+  int lock_active_hint = 0;
+  ppg_simulate_fn sim_hook = nullptr;
+  void* sim_hook_user = nullptr;
   int32_t* h_nactive = nullptr;  // pinned
   int num_sms = 148;
   int disc_blocks_per_sm[kNumDisc] = {};  // resolve_disc_kernel<kDiscSizes[k]>
@@ -358,7 +367,7 @@ void ppg_destroy(ppg_ctx* ctx) {
                     &ctx->b_e, &ctx->l_node, &ctx->l_pushes, &ctx->l_done, &ctx->l_byg, &ctx->l_harv,
                     &ctx->l_flag, &ctx->l_reward, &ctx->l_poses, &ctx->l_mt, &ctx->l_mtidx, &ctx->l_W,
                     &ctx->l_rew, &ctx->l_active, &ctx->l_nactive, &ctx->l_counters, &ctx->l_npose,
-                    &ctx->l_nmeta, &ctx->b_counter, &ctx->l_push, &ctx->l_status, &ctx->l_stepping};
+                    &ctx->l_nmeta, &ctx->b_counter, &ctx->l_push, &ctx->l_status, &ctx->l_stepping, &ctx->l_rec};
   for (DevBuf* b : bufs) b->release();
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -654,28 +663,19 @@ int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, 
   return PPG_SUCCESS;
 }
 
-int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
-                 int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, double* rewards_out,
-                 int64_t* counters) {
-  if (!ctx) return PPG_EINVAL;
-  if (n_nodes <= 0) return PPG_SUCCESS;
-  if (n_envs < n_nodes) {
-    ctx->err = "lockstep_simulate: fewer environments than nodes";
-    return PPG_EINVAL;
-  }
-  if (!ctx->has_scene) {
-    ctx->err = "no scene installed";
-    return PPG_EINVAL;
-  }
-  if (depth_cap + 1 >= kMaxGammaPow) {
-    ctx->err = "depth cap too large";
-    return PPG_EINVAL;
-  }
-  CK(cudaSetDevice(ctx->device));
+}  // extern "C"
+
+// ---- lockstep engine (pmbs.cpp:133-234) host side --------------------------
+
+// Allocates and initialises the lockstep state for `used` local environments
+// (global indices env_lo .. env_lo+used-1 of a batch of used_global) over the
+// given nodes; runs lock_init_kernel.
+static int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used,
+                      int used_global, int env_lo, int leaf_parallel, uint64_t seed, uint64_t iteration,
+                      int depth_cap) {
   cudaStream_t st = ctx->stream;
   const int n = ctx->scene.n;
-  const int used = leaf_parallel ? n_envs : n_nodes;
-  const int E = used;
+  const int E = used > 0 ? used : 1;
   CK(ctx->l_node.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_pushes.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_done.ensure(E));
@@ -689,23 +689,27 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   CK(ctx->l_W.ensure(static_cast<size_t>(n_nodes) * 4));
   CK(ctx->l_rew.ensure(static_cast<size_t>(n_nodes) * 8));
   CK(ctx->l_active.ensure(static_cast<size_t>(E) * 4));
-  CK(ctx->l_nactive.ensure(4));
+  CK(ctx->l_nactive.ensure(16));
   CK(ctx->l_counters.ensure(4 * 8));
   CK(ctx->l_npose.ensure(static_cast<size_t>(n_nodes) * n * 3 * 8));
   CK(ctx->l_nmeta.ensure(static_cast<size_t>(n_nodes) * 3 * 4));
   CK(ctx->l_push.ensure(static_cast<size_t>(E) * 32));
   CK(ctx->l_status.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_stepping.ensure(static_cast<size_t>(E) * 4 + 16));
+  CK(ctx->l_rec.ensure(static_cast<size_t>(E) * (4 + 4 + 1 + 8) + 64));
   CK(cudaMemcpyAsync(ctx->l_npose.p, node_poses, static_cast<size_t>(n_nodes) * n * 3 * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ctx->l_nmeta.p, node_meta, static_cast<size_t>(n_nodes) * 3 * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ctx->l_counters.p, 0, 32, st));
-  const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
-  LockArgs a;
+  ctx->lc = make_const(ctx->params, n, ctx->side, ctx->margin);
+  LockArgs& a = ctx->la;
+  a = LockArgs{};
   a.S = ctx->scene;
   a.node_poses = ctx->l_npose.as<double>();
   a.node_meta = ctx->l_nmeta.as<int32_t>();
   a.n_nodes = n_nodes;
   a.used = used;
+  a.used_global = used_global;
+  a.env_lo = env_lo;
   a.leaf_parallel = leaf_parallel;
   a.cap = depth_cap;
   a.seed = seed;
@@ -730,39 +734,172 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   a.env_status = ctx->l_status.as<int32_t>();
   a.n_stepping = ctx->l_stepping.as<int32_t>();
   a.stepping = ctx->l_stepping.as<int32_t>() + 4;
-  const bool discs = use_disc(ctx, ctx->scene_all_discs, n);
-  ResolveArgs ra{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, 0};
-  ra.idx = a.stepping;
-  ra.E_dev = a.n_stepping;
+  {
+    char* r = ctx->l_rec.as<char>();
+    a.n_rec = reinterpret_cast<int32_t*>(r);
+    a.rec_env = reinterpret_cast<int32_t*>(r + 16);
+    a.rec_node = a.rec_env + E;
+    a.rec_reward = reinterpret_cast<double*>(r + 16 + static_cast<size_t>(E) * 8 + 8 - ((16 + E * 8) % 8));
+    a.rec_grasp = reinterpret_cast<uint8_t*>(a.rec_reward + E);
+  }
+  ctx->lra = ResolveArgs{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, 0};
+  ctx->lra.idx = a.stepping;
+  ctx->lra.E_dev = a.n_stepping;
   const int ginit = ((E > n_nodes ? E : n_nodes) + 255) / 256;
-  lock_init_kernel<<<ginit, 256, 0, st>>>(C, a);
+  lock_init_kernel<<<ginit, 256, 0, st>>>(ctx->lc, a);
   CK(cudaGetLastError());
-  for (;;) {
-    lock_harvest_kernel<<<1, 1024, 0, st>>>(C, a);
+  return PPG_SUCCESS;
+}
+
+// One lockstep round over the current active list (at most `act` envs):
+// latency mode (one warp per env), the 3-phase disc pipeline, or the generic
+// one-lane step.
+static int lock_round(ppg_ctx* ctx, int act) {
+  cudaStream_t st = ctx->stream;
+  const SimConst& C = ctx->lc;
+  LockArgs& a = ctx->la;
+  const int n = ctx->scene.n;
+  const int g = (act + kBlock - 1) / kBlock;
+  if (use_warp(ctx, ctx->scene_all_discs, n, act)) {
+    lock_step_warp_kernel<<<(act + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
     CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(ctx->h_nactive, a.n_active, 4, cudaMemcpyDeviceToHost, st));
+  } else if (use_disc(ctx, ctx->scene_all_discs, n)) {  // sample+pick -> physics (in place) -> grasp + reward
+    lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+    CK(cudaGetLastError());
+    const int rc = launch_disc(ctx, C, ctx->lra, n, act, st);
+    if (rc != PPG_SUCCESS) return rc;
+    lock_post_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+    CK(cudaGetLastError());
+  } else {
+    lock_step_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+    CK(cudaGetLastError());
+  }
+  return PPG_SUCCESS;
+}
+
+static int lock_check(ppg_ctx* ctx, int n_nodes, int n_envs, int depth_cap) {
+  if (n_envs < n_nodes) {
+    ctx->err = "lockstep_simulate: fewer environments than nodes";
+    return PPG_EINVAL;
+  }
+  if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
+  }
+  if (depth_cap + 1 >= kMaxGammaPow) {
+    ctx->err = "depth cap too large";
+    return PPG_EINVAL;
+  }
+  return PPG_SUCCESS;
+}
+
+extern "C" {
+
+int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
+                 int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, double* rewards_out,
+                 int64_t* counters) {
+  if (!ctx) return PPG_EINVAL;
+  if (n_nodes <= 0) return PPG_SUCCESS;
+  int rc = lock_check(ctx, n_nodes, n_envs, depth_cap);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int used = leaf_parallel ? n_envs : n_nodes;
+  rc = lock_setup(ctx, node_poses, node_meta, n_nodes, used, used, 0, leaf_parallel, seed, iteration, depth_cap);
+  if (rc != PPG_SUCCESS) return rc;
+  for (;;) {
+    lock_harvest_kernel<<<1, 1024, 0, st>>>(ctx->lc, ctx->la);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_nactive, ctx->la.n_active, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int act = *ctx->h_nactive;
     if (act == 0) break;
-    const int g = (act + kBlock - 1) / kBlock;
-    if (use_warp(ctx, ctx->scene_all_discs, n, act)) {  // latency mode: one warp per active env
-      lock_step_warp_kernel<<<(act + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
-      CK(cudaGetLastError());
-    } else if (discs) {  // sample+pick -> register-resident physics (in place) -> grasp + reward
-      lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
-      CK(cudaGetLastError());
-      const int rc = launch_disc(ctx, C, ra, n, act, st);
-      if (rc != PPG_SUCCESS) return rc;
-      lock_post_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
-      CK(cudaGetLastError());
-    } else {
-      lock_step_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
-      CK(cudaGetLastError());
-    }
+    rc = lock_round(ctx, act);
+    if (rc != PPG_SUCCESS) return rc;
   }
-  CK(cudaMemcpyAsync(rewards_out, a.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
-  if (counters) CK(cudaMemcpyAsync(counters, a.counters, 32, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rewards_out, ctx->la.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
+  if (counters) CK(cudaMemcpyAsync(counters, ctx->la.counters, 32, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_lock_begin(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used_envs,
+                   int env_lo, int env_hi, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap) {
+  if (!ctx || n_nodes <= 0 || env_lo < 0 || env_hi < env_lo || env_hi > used_envs) return PPG_EINVAL;
+  int rc = lock_check(ctx, n_nodes, leaf_parallel ? used_envs : n_nodes, depth_cap);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(cudaSetDevice(ctx->device));
+  rc = lock_setup(ctx, node_poses, node_meta, n_nodes, env_hi - env_lo, used_envs, env_lo, leaf_parallel, seed,
+                  iteration, depth_cap);
+  if (rc != PPG_SUCCESS) return rc;
+  ctx->lock_active_hint = env_hi - env_lo;
+  return PPG_SUCCESS;
+}
+
+int ppg_lock_report(ppg_ctx* ctx, int32_t* rec_env, int32_t* rec_node, uint8_t* rec_grasp, double* rec_reward,
+                    int32_t* n_rec, int32_t* w_local, int32_t* n_active) {
+  if (!ctx) return PPG_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  LockArgs& a = ctx->la;
+  lock_report_kernel<<<1, 1024, 0, st>>>(ctx->lc, a);
+  CK(cudaGetLastError());
+  int32_t hdr[2];
+  CK(cudaMemcpyAsync(&hdr[0], a.n_rec, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&hdr[1], a.n_active, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(w_local, a.W, static_cast<size_t>(a.n_nodes) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int k = hdr[0];
+  if (k > 0) {
+    CK(cudaMemcpyAsync(rec_env, a.rec_env, static_cast<size_t>(k) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rec_node, a.rec_node, static_cast<size_t>(k) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rec_grasp, a.rec_grasp, static_cast<size_t>(k), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rec_reward, a.rec_reward, static_cast<size_t>(k) * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  *n_rec = k;
+  *n_active = hdr[1];
+  ctx->lock_active_hint = hdr[1];
+  return PPG_SUCCESS;
+}
+
+int ppg_lock_repurpose(ppg_ctx* ctx, const int32_t* env, const int32_t* node, int count) {
+  if (!ctx || count < 0) return PPG_EINVAL;
+  if (count == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  CK(ctx->b_d.ensure(static_cast<size_t>(count) * 8));
+  int32_t* d = ctx->b_d.as<int32_t>();
+  CK(cudaMemcpyAsync(d, env, static_cast<size_t>(count) * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d + count, node, static_cast<size_t>(count) * 4, cudaMemcpyHostToDevice, st));
+  lock_repurpose_kernel<<<(count + 255) / 256, 256, 0, st>>>(ctx->lc, ctx->la, d, d + count, count);
+  CK(cudaGetLastError());
+  ctx->lock_active_hint += count;
+  return PPG_SUCCESS;
+}
+
+int ppg_lock_step(ppg_ctx* ctx) {
+  if (!ctx) return PPG_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->lock_active_hint <= 0) return PPG_SUCCESS;
+  const int rc = lock_round(ctx, ctx->lock_active_hint);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return PPG_SUCCESS;
+}
+
+int ppg_set_simulate_hook(ppg_ctx* ctx, ppg_simulate_fn fn, void* user) {
+  if (!ctx) return PPG_EINVAL;
+  ctx->sim_hook = fn;
+  ctx->sim_hook_user = user;
+  return PPG_SUCCESS;
+}
+
+int ppg_lock_counters(ppg_ctx* ctx, int64_t* counters) {
+  if (!ctx || !counters) return PPG_EINVAL;
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(counters, ctx->la.counters, 32, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   return PPG_SUCCESS;
 }
 
@@ -832,6 +969,7 @@ int ppg_state_digest(const ppg_shapes* sh, const double* poses, int E, uint64_t*
 // internal accessors for planner.cpp
 namespace ppg {
 const ppg_params& ctx_params(const ppg_ctx* ctx) { return ctx->params; }
+SimHook ctx_sim_hook(const ppg_ctx* ctx) { return SimHook{ctx->sim_hook, ctx->sim_hook_user}; }
 int ctx_n_objects(const ppg_ctx* ctx) { return ctx->has_scene ? ctx->scene.n : 0; }
 void ctx_set_error(ppg_ctx* ctx, const char* msg) { ctx->err = msg; }
 }  // namespace ppg

@@ -216,16 +216,86 @@ __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a)
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < a.n_nodes) a.rew[e] = 0ull;
   if (e >= a.used) return;
-  // Even split, remainder to earlier nodes (pmbs.cpp:138-149).
-  const int base = a.used / a.n_nodes, rem = a.used % a.n_nodes;
+  // Even split of the GLOBAL batch, remainder to earlier nodes
+  // (pmbs.cpp:138-149); the RNG key is the global env index (pmbs.cpp:211-213),
+  // so a shard reproduces exactly its part of the unsharded batch.
+  const int ge = a.env_lo + e;
+  const int used = a.used_global > 0 ? a.used_global : a.used;
+  const int base = used / a.n_nodes, rem = used % a.n_nodes;
   const int big = rem * (base + 1);
-  const int node = e < big ? e / (base + 1) : rem + (e - big) / base;
+  const int node = ge < big ? ge / (base + 1) : rem + (ge - big) / base;
   cursor_init(C, a, e, node);
   a.env_harvested[e] = 0;
   a.env_flag[e] = 0;
   MtView g{a.mt + e, a.E};
-  mt_seed(g, mix_keys(a.seed, a.iteration, static_cast<uint64_t>(e)));
+  mt_seed(g, mix_keys(a.seed, a.iteration, static_cast<uint64_t>(ge)));
   a.mt_idx[e] = 312;
+}
+
+// Sharded lockstep, report phase (one block): this shard's newly finished
+// envs in increasing env order (ordered compaction) are reported and marked
+// harvested; W_local[node] = sum over assigned, not-done envs of cap - pushes
+// (pmbs.cpp:157-163); the not-done envs form the active list.
+__global__ void __launch_bounds__(1024) lock_report_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  __shared__ int s_warp[32];
+  __shared__ int s_base, s_active;
+  if (tid == 0) {
+    s_base = 0;
+    s_active = 0;
+  }
+  for (int i = tid; i < a.n_nodes; i += blockDim.x) a.W[i] = 0;
+  __syncthreads();
+  for (int e0 = 0; e0 < a.used; e0 += blockDim.x) {
+    const int e = e0 + tid;
+    const bool in = e < a.used;
+    const bool done = in && a.env_done[e];
+    if (in && !done) {
+      atomicAdd(&a.W[a.env_node[e]], a.cap - a.env_pushes[e]);
+      a.active[atomicAdd(&s_active, 1)] = e;
+    }
+    const bool rep = done && !a.env_harvested[e];
+    const unsigned b = __ballot_sync(0xffffffffu, rep);
+    if (lane == 0) s_warp[wid] = __popc(b);
+    __syncthreads();
+    if (tid == 0) {  // exclusive scan over the block's warps
+      int acc = s_base;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+        const int c = s_warp[w];
+        s_warp[w] = acc;
+        acc += c;
+      }
+      s_base = acc;
+    }
+    __syncthreads();
+    if (rep) {
+      const int k = s_warp[wid] + __popc(b & ((1u << lane) - 1u));
+      a.rec_env[k] = a.env_lo + e;
+      a.rec_node[k] = a.env_node[e];
+      a.rec_grasp[k] = a.env_bygrasp[e];
+      a.rec_reward[k] = a.env_reward[e];
+      a.env_harvested[e] = 1;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *a.n_rec = s_base;
+    *a.n_active = s_active;
+    *a.n_stepping = 0;
+  }
+}
+
+// Sharded lockstep, re-purpose phase: the global harvest (host, identical on
+// every rank) moved local envs to new nodes; restart their cursors there
+// (their RNG engines continue, pmbs.cpp:182-185) and make them active.
+__global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockArgs a, const int32_t* env,
+                                      const int32_t* node, int count) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const int e = env[k] - a.env_lo;
+  cursor_init(C, a, e, node[k]);
+  a.env_harvested[e] = 0;
+  if (!a.env_done[e]) a.active[atomicAdd(a.n_active, 1)] = e;
 }
 
 // harvest_and_repurpose (pmbs.cpp:165-187) + next round's active list.  One

@@ -65,7 +65,9 @@ struct LockArgs {
   const double* node_poses;  // [n_nodes][n][3]
   const int32_t* node_meta;  // [n_nodes][3] depth, graspable, dead
   int n_nodes;
-  int used;       // environments in use
+  int used;       // environments in use on this shard (local slots 0..used-1)
+  int used_global = 0;  // environments of the whole batch (env -> node split, RNG keys)
+  int env_lo = 0;       // global index of local slot 0 (sharded lockstep)
   int leaf_parallel;
   int cap;        // depth cap d_T + d_s
   uint64_t seed, iteration;
@@ -82,6 +84,12 @@ struct LockArgs {
   int32_t* env_status;  // [E] this round's resolve status
   int32_t* stepping;    // [used] envs with a push this round (disc pipeline)
   int32_t* n_stepping;  // [1]
+  // sharded-lockstep report records (global env, node, by_grasp, reward)
+  int32_t* rec_env = nullptr;
+  int32_t* rec_node = nullptr;
+  uint8_t* rec_grasp = nullptr;
+  double* rec_reward = nullptr;
+  int32_t* n_rec = nullptr;
   uint64_t* mt;         // [312][E]
   int32_t* mt_idx;      // [E]
   int E;                // allocated stride for env arrays

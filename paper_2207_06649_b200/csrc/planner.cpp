@@ -285,10 +285,18 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
     }
     rewards.resize(P);
     int64_t ctr[4] = {0, 0, 0, 0};
-    if ((rc = ppg_simulate(ctx, node_poses.data(), meta.data(), P, cfg.n_envs, cfg.leaf_parallel,
-                           cfg.rng_seed, static_cast<uint64_t>(iter), tree.tree_depth + tree.rollout_depth,
-                           rewards.data(), ctr)) != PPG_SUCCESS)
+    const ppg::SimHook hook = ppg::ctx_sim_hook(ctx);
+    if (hook.fn) {
+      rc = hook.fn(hook.user, node_poses.data(), meta.data(), P, cfg.n_envs, cfg.leaf_parallel, cfg.rng_seed,
+                   static_cast<uint64_t>(iter), tree.tree_depth + tree.rollout_depth, rewards.data(), ctr);
+    } else {
+      rc = ppg_simulate(ctx, node_poses.data(), meta.data(), P, cfg.n_envs, cfg.leaf_parallel, cfg.rng_seed,
+                        static_cast<uint64_t>(iter), tree.tree_depth + tree.rollout_depth, rewards.data(), ctr);
+    }
+    if (rc != PPG_SUCCESS) {
+      if (hook.fn) ppg::ctx_set_error(ctx, "simulate hook failed");
       return rc;
+    }
     const auto t3 = clk::now();
     st.simulate_s += secs(t2, t3);
     st.rollout_steps += ctr[0];

@@ -289,3 +289,47 @@ def test_fingerprints_lane_mode(idx):
     r = run_pmbs(st, ParallelConfig(rng_seed=int(cc["seed"])), ctx=c)
     assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
     c.close()
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3])
+def test_device_shards_reproduce_unsharded_lockstep(shards):
+    """The multi-GPU lockstep driver with `shards` device shards emulated in
+    one process (separate contexts on cuda:0, host-mediated exchange) equals
+    the reference batch_simulate goldens bit for bit."""
+    from paper_2207_06649_b200.sharded import DeviceShard, InProcessComm, env_range, sharded_simulate
+    cases = {cc["case_id"]: st for cc, st in golden_io.cases()}
+    ctxs = [_ctx_with() for _ in range(shards)]
+    for cid, ne, seed, cap, poses, meta, rewards in golden_io.simulate_sets():
+        st = cases[cid]
+        for c in ctxs:
+            c.set_params(default_params(n_envs=ne, rng_seed=seed))
+            c.set_scene(st)
+        ranges = [env_range(ne, shards, r) for r in range(shards)]
+        r, ctr = sharded_simulate([DeviceShard(c) for c in ctxs], InProcessComm(), poses, meta, ne, True, seed, 0,
+                                  cap, ranges)
+        if np.all(st.kind == 0):
+            assert np.array_equal(r, rewards), (shards, cid)
+            ro, co = port.simulate(st, poses, meta, ne, True, seed, 0, cap, default_params(n_envs=ne))
+            assert ctr[0] == co[0] and ctr[3] == co[3] and ctr[1] == co[1], (shards, cid)
+        else:
+            assert np.mean(r == rewards) > 0.9
+    for c in ctxs:
+        c.close()
+
+
+def test_run_pmbs_through_sharded_hook():
+    """ppg_run_pmbs with the sharded simulate hook (1 rank) reproduces the
+    reference fingerprint: the multi-GPU planner path is the same algorithm."""
+    from paper_2207_06649_b200.sharded import InProcessComm, ShardedSimulateHook
+    c = _ctx_with()
+    cc, st = golden_io.cases()[12]
+    d = cc["decision"]
+    cfg = ParallelConfig(rng_seed=int(cc["seed"]))
+    c.set_params(cfg.to_params())
+    c.set_scene(st)
+    hook = ShardedSimulateHook(c, InProcessComm(), 1, 0)
+    r = run_pmbs(st, cfg, ctx=c)
+    hook.remove()
+    assert hook.error is None
+    assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
+    c.close()
