@@ -241,6 +241,10 @@ int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev,
                                 const double* poses_in, const double* pushes, int E,
                                 int64_t* counts_dev, void* stream);
 
+/* Test helper: the device port of glibc sincos (the reference's libm,
+ * __sincos_fma) on n arguments |x| < 105414350; bit-identical to the host. */
+int ppg_debug_sincos(ppg_ctx* ctx, const double* x, int n, double* s, double* c);
+
 /* Measurement helper (not on the hot path): the FP64 CUDA-core pipe peak in
  * DFMA instructions per second, from a dependent-chain microbenchmark on the
  * context's device — the roofline denominator of the FP64 kernels. */

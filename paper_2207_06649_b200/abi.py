@@ -173,6 +173,7 @@ SIGNATURES = {
     "ppg_lock_step": (c_int, [c_void_p]),
     "ppg_lock_counters": (c_int, [c_void_p, POINTER(c_int64)]),
     "ppg_set_simulate_hook": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ppg_debug_sincos": (c_int, [c_void_p, POINTER(c_double), c_int, POINTER(c_double), POINTER(c_double)]),
     "ppg_measure_fp64_peak": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "ppg_generate_cases": (c_int, [c_int, c_int, c_double, POINTER(c_uint64), c_int, POINTER(c_int32),
                                    POINTER(c_double), POINTER(c_int32), POINTER(c_double), POINTER(c_double),

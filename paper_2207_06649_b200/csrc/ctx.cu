@@ -37,6 +37,7 @@ __global__ void lock_report_kernel(const __grid_constant__ SimConst C, LockArgs 
 __global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockArgs a, const int32_t* env,
                                       const int32_t* node, int count);
 __global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
+__global__ void debug_sincos_kernel(const double* x, int n, double* s, double* c);
 template <int NMAX>
 __global__ void resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a, int* next_env);
 
@@ -900,6 +901,25 @@ int ppg_lock_counters(ppg_ctx* ctx, int64_t* counters) {
   CK(cudaSetDevice(ctx->device));
   CK(cudaMemcpyAsync(counters, ctx->la.counters, 32, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  return PPG_SUCCESS;
+}
+
+int ppg_debug_sincos(ppg_ctx* ctx, const double* x, int n, double* s, double* c) {
+  if (!ctx || n < 0) return PPG_EINVAL;
+  if (n == 0) return PPG_SUCCESS;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t b = static_cast<size_t>(n) * 8;
+  CK(ctx->b_a.ensure(b));
+  CK(ctx->b_b.ensure(b));
+  CK(ctx->b_c.ensure(b));
+  CK(cudaMemcpyAsync(ctx->b_a.p, x, b, cudaMemcpyHostToDevice, st));
+  debug_sincos_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx->b_a.as<double>(), n, ctx->b_b.as<double>(),
+                                                       ctx->b_c.as<double>());
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(s, ctx->b_b.p, b, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c, ctx->b_c.p, b, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return PPG_SUCCESS;
 }
 

@@ -516,6 +516,12 @@ __global__ void __launch_bounds__(128) lock_post_kernel(const __grid_constant__ 
 
 namespace ppg {
 
+// Test hook: the device glibc sincos on an array (parity with host libm).
+__global__ void debug_sincos_kernel(const double* x, int n, double* s, double* c) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) glibc_sincos(x[i], s + i, c + i);
+}
+
 // Measurement only (not on the hot path): the FP64 CUDA-core pipe peak, as
 // the denominator of the roofline.  8 independent DFMA chains per thread.
 __global__ void __launch_bounds__(256) fp64_peak_kernel(double* out, int iters, double b, double c) {

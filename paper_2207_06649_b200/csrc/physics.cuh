@@ -12,6 +12,7 @@
 #pragma once
 
 #include "geom.cuh"
+#include "glibc_sincos.cuh"
 
 namespace ppg {
 
@@ -71,7 +72,7 @@ struct PoseView {
 PPG_DI void world_polygon(const PoseView& P, const ShapeView& S, int i, Poly& out) {
   const double th = P.th(i);
   double s, c;
-  sincos(th, &s, &c);
+  glibc_sincos(th, &s, &c);  // bit-identical to the reference's libm sincos
   const V2 pos = P.pos(i);
   out.n = S.nv_(i);
   for (int k = 0; k < out.n; ++k) {
@@ -233,7 +234,7 @@ PPG_DI int resolve_push(const PoseView& P, const ShapeView& S, const SimConst& C
 PPG_DI double contour_radius(const PoseView& P, const ShapeView& S, int i, V2 d) {
   if (S.kind_(i) == 0) return S.rad_(i);
   double s, c;
-  sincos(-P.th(i), &s, &c);
+  glibc_sincos(-P.th(i), &s, &c);
   const V2 dl{c * d.x - s * d.y, s * d.x + c * d.y};
   double best = 0.0;
   const int nv = S.nv_(i);
