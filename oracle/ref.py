@@ -58,7 +58,8 @@ def lib():
         L.ref_first_iteration.argtypes = [c_void_p, c_int, POINTER(PpgParams), c_uint64, POINTER(c_double),
                                           POINTER(c_int32), POINTER(c_double), POINTER(c_int32)]
         L.ref_run_episode.argtypes = [c_void_p, c_int, c_char_p, c_int, POINTER(PpgParams), c_int, c_uint64,
-                                      c_int, POINTER(c_int32), POINTER(c_double)]
+                                      c_int, POINTER(c_int32), POINTER(c_double), c_char_p]
+        L.ref_replay_log.argtypes = [c_char_p, c_char_p, c_int]
         _LIB = L
     return _LIB
 
@@ -234,10 +235,18 @@ def first_iteration(st: WorldState, params: PpgParams, iteration: int = 0):
 
 
 def run_episode(st: WorldState, case_id: str, trial: int, params: PpgParams, threads: int = 1,
-                seed_base: int = 0, action_cap: int = 16):
+                seed_base: int = 0, action_cap: int = 16, log_path: str = ""):
+    """bench::run_episode (bench.cpp:54-126), optionally writing its JSONL log."""
     h = state_handle(st)
     comp = c_int32()
     ps = c_double()
     used = lib().ref_run_episode(h.ptr, 0, case_id.encode(), trial, ctypes.byref(params), threads,
-                                 seed_base, action_cap, ctypes.byref(comp), ctypes.byref(ps))
+                                 seed_base, action_cap, ctypes.byref(comp), ctypes.byref(ps), log_path.encode())
     return {"actions_used": used, "completed": bool(comp.value), "planning_s": ps.value}
+
+
+def replay_log(path: str):
+    """bench::replay_log (bench.cpp:319-377): (ok, report)."""
+    buf = ctypes.create_string_buffer(4096)
+    ok = lib().ref_replay_log(path.encode(), buf, 4096)
+    return bool(ok), buf.value.decode()

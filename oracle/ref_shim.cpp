@@ -8,6 +8,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <memory>
 #include <random>
 #include <string>
@@ -380,7 +382,7 @@ int ref_first_iteration(void* h, int i, const ppg_params* p, uint64_t iteration,
 // used, sets completed and planning seconds.
 int ref_run_episode(void* h, int i, const char* case_id, int trial, const ppg_params* p,
                     int threads, uint64_t seed_base, int action_cap, int32_t* completed,
-                    double* planning_s) {
+                    double* planning_s, const char* log_path) {
   const WorldState& w = static_cast<States*>(h)->v.at(i);
   bench::BenchmarkConfig cfg;
   cfg.search = to_cfg(p);
@@ -388,10 +390,28 @@ int ref_run_episode(void* h, int i, const char* case_id, int trial, const ppg_pa
   cfg.action_cap = action_cap;
   cfg.seed_base = seed_base;
   const uint64_t seed = bench::episode_seed(seed_base, case_id, trial);
-  const bench::EpisodeResult r = bench::run_episode(w, case_id, trial, cfg, seed, nullptr);
+  std::ofstream log_file;
+  if (log_path && log_path[0]) log_file.open(log_path);
+  const bench::EpisodeResult r =
+      bench::run_episode(w, case_id, trial, cfg, seed, log_file.is_open() ? &log_file : nullptr);
   *completed = r.completed ? 1 : 0;
   *planning_s = r.planning_time_s;
   return r.actions_used;
+}
+
+// bench::replay_log (bench.cpp:319-377): 1 when the JSONL episode log's
+// recorded actions re-fold through the reference simulator with matching
+// state digests.
+int ref_replay_log(const char* path, char* report, int cap) {
+  std::ostringstream out;
+  const bool ok = bench::replay_log(path, out);
+  const std::string s = out.str();
+  if (report && cap > 0) {
+    const size_t m = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(report, s.data(), m);
+    report[m] = '\0';
+  }
+  return ok ? 1 : 0;
 }
 
 }  // extern "C"
