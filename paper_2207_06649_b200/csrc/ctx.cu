@@ -45,7 +45,7 @@ constexpr int kBlock = 128;
 constexpr int kDiscBlock = 128;  // resolve_disc.cu kDB
 constexpr int kNumDisc = 8;
 constexpr int kDiscSizes[kNumDisc] = {4, 6, 8, 10, 11, 12, 14, 16};
-constexpr size_t kMaxSmem = 3 * kMaxObjects * kBlock * sizeof(double);
+constexpr size_t kMaxSmem = kPosePlanes * kMaxObjects * kBlock * sizeof(double);
 
 }  // namespace ppg
 
@@ -258,7 +258,7 @@ bool for_each_disc_kernel(F&& f) {
 
 size_t disc_smem(int nmax) { return static_cast<size_t>(3) * nmax * kDiscBlock * sizeof(double); }
 
-size_t smem_for(int n) { return static_cast<size_t>(3) * n * kBlock * sizeof(double); }
+size_t smem_for(int n) { return static_cast<size_t>(kPosePlanes) * n * kBlock * sizeof(double); }
 
 }  // namespace
 

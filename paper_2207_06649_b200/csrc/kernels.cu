@@ -50,13 +50,14 @@ __global__ void shape_prep_kernel(ShapesDev S, const int* kind, const double* ra
 }
 
 // Stages environment e's AoS poses into this lane's shared-memory column.
-PPG_DI PoseView stage_poses(double* smem, int n, const double* src) {
+PPG_DI PoseView stage_poses(double* smem, int n, const double* src, const ShapeView& S) {
   PoseView P{smem + threadIdx.x, static_cast<int>(blockDim.x), n};
   for (int i = 0; i < n; ++i) {
     P.x(i) = src[i * 3];
     P.y(i) = src[i * 3 + 1];
     P.th(i) = src[i * 3 + 2];
   }
+  refresh_all_trig(P, S);
   return P;
 }
 
@@ -74,8 +75,8 @@ __global__ void __launch_bounds__(128) resolve_kernel(const __grid_constant__ Si
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= a.E) return;
   const int n = C.n;
-  const PoseView P = stage_poses(smem, n, a.poses_in + static_cast<size_t>(e) * n * 3);
   const ShapeView S = a.S.view(a.S.T == 1 ? 0 : e);
+  const PoseView P = stage_poses(smem, n, a.poses_in + static_cast<size_t>(e) * n * 3, S);
   const double* pu = a.pushes + static_cast<size_t>(e) * 4;
   double residual = 0.0;
   Counts cnt{0, 0, 0, 0, 0, 0, 0, 0};
@@ -117,8 +118,8 @@ __global__ void __launch_bounds__(128) sample_kernel(const __grid_constant__ Sim
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= a.E) return;
   const int n = C.n;
-  const PoseView P = stage_poses(smem, n, a.poses + static_cast<size_t>(e) * n * 3);
   const ShapeView S = a.S.view(a.S.T == 1 ? 0 : e);
+  const PoseView P = stage_poses(smem, n, a.poses + static_cast<size_t>(e) * n * 3, S);
   a.count[e] = sample_all(P, S, C, a.out + static_cast<size_t>(e) * n * C.na * 4);
 }
 
@@ -127,9 +128,9 @@ __global__ void __launch_bounds__(128) grasp_kernel(const __grid_constant__ SimC
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= a.E) return;
   const int n = C.n;
-  const PoseView P = stage_poses(smem, n, a.poses + static_cast<size_t>(e) * n * 3);
   const int t = a.S.T == 1 ? 0 : e;
   const ShapeView S = a.S.view(t);
+  const PoseView P = stage_poses(smem, n, a.poses + static_cast<size_t>(e) * n * 3, S);
   const GraspOut g = graspable(P, S, C, a.S.target[t]);
   a.grasp[e] = g.graspable ? 1 : 0;
   a.margin[e] = g.margin;
@@ -144,8 +145,8 @@ __global__ void __launch_bounds__(128) expand_kernel(const __grid_constant__ Sim
   if (p >= a.P) return;
   const int n = C.n;
   const double* parent = a.parent_poses + static_cast<size_t>(p) * n * 3;
-  const PoseView P = stage_poses(smem, n, parent);
   const ShapeView S = a.S.view(0);
+  const PoseView P = stage_poses(smem, n, parent, S);
   const double* act = a.actions + static_cast<size_t>(p) * 4;
   double residual;
   const int st = resolve_push<false>(P, S, C, V2{act[0], act[1]}, V2{act[2], act[3]}, true, &residual, nullptr);
@@ -178,8 +179,8 @@ __global__ void __launch_bounds__(128) expand_post_kernel(const __grid_constant_
     a.n_untried[p] = 0;
     return;
   }
-  const PoseView P = stage_poses(smem, n, child);
   const ShapeView S = a.S.view(0);
+  const PoseView P = stage_poses(smem, n, child, S);
   a.n_untried[p] = sample_all(P, S, C, a.untried + static_cast<size_t>(p) * n * C.na * 4);
   a.grasp[p] = graspable(P, S, C, a.S.target[0]).graspable ? 1 : 0;
 }
@@ -445,8 +446,8 @@ __global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ 
   const int e = a.active[gid];
   const int n = C.n;
   double* env = a.env_poses + static_cast<size_t>(e) * n * 3;
-  const PoseView P = stage_poses(smem, n, env);
   const ShapeView S = a.S.view(0);
+  const PoseView P = stage_poses(smem, n, env, S);
   atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
   V2 s, t;
   if (!rollout_pick(P, S, C, a, e, s, t)) {
@@ -476,8 +477,8 @@ __global__ void __launch_bounds__(128) lock_sample_kernel(const __grid_constant_
   if (gid >= n_act) return;
   const int e = a.active[gid];
   const int n = C.n;
-  const PoseView P = stage_poses(smem, n, a.env_poses + static_cast<size_t>(e) * n * 3);
   const ShapeView S = a.S.view(0);
+  const PoseView P = stage_poses(smem, n, a.env_poses + static_cast<size_t>(e) * n * 3, S);
   atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
   V2 s, t;
   if (!rollout_pick(P, S, C, a, e, s, t)) {
@@ -508,8 +509,9 @@ __global__ void __launch_bounds__(128) lock_post_kernel(const __grid_constant__ 
     return;
   }
   const int n = C.n;
-  const PoseView P = stage_poses(smem, n, a.env_poses + static_cast<size_t>(e) * n * 3);
-  rollout_finish_step(P, a.S.view(0), C, a, e);
+  const ShapeView S = a.S.view(0);
+  const PoseView P = stage_poses(smem, n, a.env_poses + static_cast<size_t>(e) * n * 3, S);
+  rollout_finish_step(P, S, C, a, e);
 }
 
 }  // namespace ppg

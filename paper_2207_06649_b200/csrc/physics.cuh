@@ -58,6 +58,9 @@ struct ShapeView {
   }
 };
 
+// Planes x | y | theta | cos(theta) | sin(theta) (the last two cached for
+// polygons: world_polygon is a pure function of the pose, so computing the
+// glibc sincos once per rotation instead of in every narrow test is exact).
 struct PoseView {
   double* p;
   int stride;
@@ -65,14 +68,29 @@ struct PoseView {
   PPG_DI double& x(int i) const { return p[i * stride]; }
   PPG_DI double& y(int i) const { return p[(n + i) * stride]; }
   PPG_DI double& th(int i) const { return p[(2 * n + i) * stride]; }
+  PPG_DI double& c(int i) const { return p[(3 * n + i) * stride]; }
+  PPG_DI double& s(int i) const { return p[(4 * n + i) * stride]; }
   PPG_DI V2 pos(int i) const { return V2{x(i), y(i)}; }
 };
+constexpr int kPosePlanes = 5;
 
-// world.cpp:57-62 (Vec2::rotated geometry.hpp:29-32)
-PPG_DI void world_polygon(const PoseView& P, const ShapeView& S, int i, Poly& out) {
-  const double th = P.th(i);
+// Refreshes the cached rotation of polygon i (after its theta changed).
+PPG_DI void refresh_trig(const PoseView& P, int i) {
   double s, c;
-  glibc_sincos(th, &s, &c);  // bit-identical to the reference's libm sincos
+  glibc_sincos(P.th(i), &s, &c);  // bit-identical to the reference's libm sincos
+  P.s(i) = s;
+  P.c(i) = c;
+}
+
+PPG_DI void refresh_all_trig(const PoseView& P, const ShapeView& S) {
+  for (int i = 0; i < P.n; ++i)
+    if (S.kind_(i) != 0) refresh_trig(P, i);
+}
+
+// world.cpp:57-62 (Vec2::rotated geometry.hpp:29-32), with the rotation's
+// sincos from the cache.
+PPG_DI void world_polygon(const PoseView& P, const ShapeView& S, int i, Poly& out) {
+  const double s = P.s(i), c = P.c(i);
   const V2 pos = P.pos(i);
   out.n = S.nv_(i);
   for (int k = 0; k < out.n; ++k) {
@@ -139,6 +157,7 @@ PPG_DI void apply_contact_motion(const PoseView& P, const ShapeView& S, int i, V
   double dtheta = gain * cross(lever, t) / lever2;
   dtheta = dclamp(dtheta, -0.2, 0.2);
   P.th(i) = wrap_angle(P.th(i) + dtheta);
+  refresh_trig(P, i);
 }
 
 // world.cpp:139-152

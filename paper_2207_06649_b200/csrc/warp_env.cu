@@ -41,8 +41,10 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-// Per-warp shared block: x[n] | y[n] | theta[n] contiguous (a stride-1
-// PoseView, so the lane-level physics.cuh helpers apply), radii at [96, 128).
+// Per-warp shared block: x[n] | y[n] | theta[n] | cos | sin contiguous (a
+// stride-1 PoseView, so the lane-level physics.cuh helpers apply), radii at
+// [128, 160).  Latency mode runs disc scenes only, so the trig planes stay
+// unused.
 struct WarpEnv {
   double* x;
   double* y;
@@ -50,7 +52,7 @@ struct WarpEnv {
   double* r;
   int n;
   int lane;
-  PPG_DI WarpEnv(double* blk, int n_, int lane_) : x(blk), y(blk + n_), th(blk + 2 * n_), r(blk + 96), n(n_), lane(lane_) {}
+  PPG_DI WarpEnv(double* blk, int n_, int lane_) : x(blk), y(blk + n_), th(blk + 2 * n_), r(blk + 128), n(n_), lane(lane_) {}
   PPG_DI PoseView view() const { return PoseView{x, 1, n}; }
 };
 
@@ -382,7 +384,7 @@ PPG_DI GraspOut warp_graspable(const WarpEnv& W, const ShapeView& S, const SimCo
 // batch_resolve, one warp per environment (small batches).
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) resolve_warp_kernel(const __grid_constant__ SimConst C,
                                                                           ResolveArgs a) {
-  __shared__ double blk[kWarpsPerBlock][128];
+  __shared__ double blk[kWarpsPerBlock][160];
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
   build_pairs(pij, C.n);
   const int wib = threadIdx.x >> 5;
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) resolve_warp_kernel(const
 // batch_expand prepare (pmbs.cpp:82-93), one warp per (node, action) pair.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const __grid_constant__ SimConst C,
                                                                          ExpandArgs a) {
-  __shared__ double blk[kWarpsPerBlock][128];
+  __shared__ double blk[kWarpsPerBlock][160];
   __shared__ unsigned valid[kWarpsPerBlock][32];
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
   build_pairs(pij, C.n);
@@ -469,7 +471,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
 // RolloutCursor::step (mcts.cpp:142-171), one warp per active environment.
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(const __grid_constant__ SimConst C,
                                                                             LockArgs a) {
-  __shared__ double blk[kWarpsPerBlock][128];
+  __shared__ double blk[kWarpsPerBlock][160];
   __shared__ unsigned valid[kWarpsPerBlock][32];
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
   build_pairs(pij, C.n);
