@@ -205,6 +205,37 @@ def run_reference(args, world, rank):
     print(json.dumps(line))
 
 
+def pmbs_decisions(ctx, with_reference: bool):
+    """BASELINE's second metric, PMBS planning s/decision: the first decision
+    of proj/cases case_18 (10 discs, the deepest first decision: 51 iterations
+    at the reference default N_e = 64) at N_e = 64 / 1000 / 4096 on this GPU
+    vs the unmodified reference run_pmbs with WorkerPool(nproc) on this box's
+    host cores.  Same seed; the GPU decision and tree signature equal the
+    reference's (tests/test_gpu_parity.py)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_io
+    from paper_2207_06649_b200 import Budget, ParallelConfig, run_pmbs
+    c, st = {cc["case_id"]: (cc, s) for cc, s in golden_io.cases()}["case_18"]
+    out = {"scene": "proj/cases/case_18 (first decision)", "unit": "s/decision", "reference_threads": os.cpu_count()}
+    for ne in (64, 1000, 4096):
+        cfg = ParallelConfig(rng_seed=int(c["seed"]), n_envs=ne, budget=Budget.seconds(60.0))
+        run_pmbs(st, cfg, ctx=ctx)  # warm-up
+        t0 = time.perf_counter()
+        r = run_pmbs(st, cfg, ctx=ctx)
+        dt = time.perf_counter() - t0
+        row = {"gpu_s": dt, "iterations": r.iterations, "env_steps": r.env_steps,
+               "gpu_env_steps_per_s": r.env_steps / dt}
+        if with_reference:
+            from oracle import ref
+            if ref.available():
+                t0 = time.perf_counter()
+                q = ref.run_search(st, cfg.to_params(), threads=os.cpu_count() or 1)
+                row["reference_s"] = time.perf_counter() - t0
+                row["same_decision"] = bool(list(q["action"]) == list(r.action) and q["sig_fnv"] == r.signature_fnv)
+        out[f"n_envs_{ne}"] = row
+    return out
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_2207_06649_b200 import Context, abi
@@ -356,6 +387,8 @@ def run_ours(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_sample(table, poses, pushes, params, min(args.ref_sample, E),
                                                     args.cpu_seconds, os.cpu_count() or 1)
+    if rank == 0 and world == 1 and not args.no_pmbs:
+        line["pmbs_decision"] = pmbs_decisions(ctx, not args.no_cpu_baseline)
     if rank == 0:
         print(json.dumps(line))
     ctx.close()
@@ -371,6 +404,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pmbs", action="store_true", help="skip the PMBS s/decision block")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
