@@ -97,56 +97,69 @@ PPG_DI void warp_store(const WarpEnv& W, double* poses) {
 // resolve_push (push_sim.cpp:58-130) for a disc scene, one warp.  Returns
 // 0 ok, 1 start collision, 2 not converged (uniform); *residual = final max
 // pairwise penetration.
+//
+// Register-centric: lane l OWNS object l (x, y, r in registers); every lane
+// keeps register copies of the positions of its pairs (p = 32w + l) and their
+// squared reach, refreshed by shuffles from the owners after the tip phase
+// and patched in place after each pair hit (the moved positions are
+// warp-uniform values).  No shared memory and no __syncwarp inside the
+// iteration: shuffles and ballots are the only cross-lane traffic.  The
+// block's shared pose copy is written back at the end for the sampler /
+// grasp helpers.
 PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 start, V2 end, bool check_start,
                         double* residual) {
   const int n = W.n, l = W.lane;
-  double* const x = W.x;
-  double* const y = W.y;
-  double* const r = W.r;
   __syncwarp();
+  const bool real = l < n;
+  double xo = real ? W.x[l] : 0.0, yo = real ? W.y[l] : 0.0;
+  const double ro = real ? W.r[l] : 0.0;
   if (check_start) {  // collides_gripper_start (world.cpp:154-164)
     const double rr = C.tip_r + C.tip_clear;
     const double h = C.side / 2.0;
     const bool wall = start.x - rr < -h || start.x + rr > h || start.y - rr < -h || start.y + rr > h;
-    const bool col = l < n && dmax(0.0, norm(start - V2{x[l], y[l]}) - r[l]) < rr;
+    const bool col = real && dmax(0.0, norm(start - V2{xo, yo}) - ro) < rr;
     if (wall || __any_sync(kFull, col)) {
       *residual = 0.0;
       return 1;
     }
   }
   const V2 delta = (end - start) * (1.0 / C.substeps);
-  const double max_diam = warp_max(l < n ? 2.0 * r[l] : 0.0);
+  const double max_diam = warp_max(real ? 2.0 * ro : 0.0);
   const double reach = (C.push_distance + C.tip_r) + 2.0 * max_diam;
-  const unsigned active =
-      __ballot_sync(kFull, l < n && dist_point_segment(V2{x[l], y[l]}, start, end) <= reach + r[l]);
+  const unsigned active = __ballot_sync(kFull, real && dist_point_segment(V2{xo, yo}, start, end) <= reach + ro);
   const int P = n * (n - 1) / 2;
   const int nw = (P + 31) >> 5;
-  // this lane's pairs (p = 32w + l)
+  // this lane's pairs (p = 32w + l), their squared reach and position caches
   int pi[kWarpWords], pj[kWarpWords];
   unsigned pact[kWarpWords];  // warp-uniform: active pairs per word
+  double rs[kWarpWords], rr2[kWarpWords], ax[kWarpWords], ay[kWarpWords], bx[kWarpWords], by[kWarpWords];
 #pragma unroll
   for (int w = 0; w < kWarpWords; ++w) {
     const int p = 32 * w + l;
-    const int ij = (w < nw && p < P) ? pij[p] : 0;
+    const bool valid = w < nw && p < P;
+    const int ij = valid ? pij[p] : 0;
     pi[w] = ij & 0xff;
     pj[w] = ij >> 8;
-    pact[w] = __ballot_sync(kFull, w < nw && p < P && (active >> pi[w] & 1u) && (active >> pj[w] & 1u));
+    pact[w] = __ballot_sync(kFull, valid && (active >> pi[w] & 1u) && (active >> pj[w] & 1u));
+    rs[w] = __shfl_sync(kFull, ro, pi[w]) + __shfl_sync(kFull, ro, pj[w]);  // br_a + br_b
+    rr2[w] = rs[w] * rs[w];
+    ax[w] = ay[w] = bx[w] = by[w] = 0.0;
   }
   const double hcl = C.side / 2.0 - C.margin - 1e-9;
-  const bool mine = l < n && (active >> l & 1u);
+  const bool mine = real && (active >> l & 1u);
+  const double tr = C.tip_r;
   for (int step = 1; step <= C.substeps; ++step) {
     const V2 tc = start + delta * static_cast<double>(step);
     for (int iter = 0; iter < C.max_iters; ++iter) {
       double mp = 0.0;
-      // tip vs own object
+      // tip vs own object (push_sim.cpp:90-100)
       if (mine) {
-        const double xi = x[l], yi = y[l], ri = r[l];
-        const double dx = xi - tc.x, dy = yi - tc.y;
+        const double dx = xo - tc.x, dy = yo - tc.y;
         const double d2 = dx * dx + dy * dy;
-        const double rt = C.tip_r + ri;
+        const double rt = tr + ro;
         if (!(d2 > rt * rt)) {
           const double dist = sqrt(d2);
-          const double depth = C.tip_r + ri - dist;
+          const double depth = tr + ro - dist;
           if (depth > 0.0) {
             double ux = 1.0, uy = 0.0;
             if (dist > 0.0) {
@@ -154,29 +167,28 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
               ux = dx * inv;
               uy = dy * inv;
             }
-            x[l] = xi + ux * depth;
-            y[l] = yi + uy * depth;
+            xo = xo + ux * depth;
+            yo = yo + uy * depth;
             mp = depth;
           }
         }
       }
-      __syncwarp();
-      // pair broad phase -> warp-uniform candidate words
+      // pair broad phase (push_sim.cpp:107-108) on refreshed caches
       unsigned cand[kWarpWords];
 #pragma unroll
       for (int w = 0; w < kWarpWords; ++w) {
         cand[w] = 0u;
         if (w < nw) {  // warp-uniform
-          bool pass = false;
-          if (pact[w] >> l & 1u) {
-            const double bx = x[pi[w]] - x[pj[w]], by = y[pi[w]] - y[pj[w]];
-            const double rr = r[pi[w]] + r[pj[w]];
-            pass = !(bx * bx + by * by > rr * rr);
-          }
-          cand[w] = __ballot_sync(kFull, pass);
+          ax[w] = __shfl_sync(kFull, xo, pi[w]);
+          ay[w] = __shfl_sync(kFull, yo, pi[w]);
+          bx[w] = __shfl_sync(kFull, xo, pj[w]);
+          by[w] = __shfl_sync(kFull, yo, pj[w]);
+          const double ex = ax[w] - bx[w], ey = ay[w] - by[w];
+          cand[w] = __ballot_sync(kFull, (pact[w] >> l & 1u) && !(ex * ex + ey * ey > rr2[w]));
         }
       }
-      // lexicographic candidate sweep (uniform)
+      // lexicographic candidate sweep (uniform); each set bit passes the
+      // broad test on the current poses
 #pragma unroll
       for (int w = 0; w < kWarpWords; ++w) {
         while (w < nw && cand[w]) {
@@ -185,10 +197,11 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
           const int p = 32 * w + b;
           const int ij = pij[p];
           const int i = ij & 0xff, j = ij >> 8;
-          const double xi = x[i], yi = y[i], xj = x[j], yj = y[j];
-          const double ri = r[i], rj = r[j];
-          const double bx = xi - xj, by = yi - yj;
-          const double d2 = bx * bx + by * by;
+          const double xi = __shfl_sync(kFull, xo, i), yi = __shfl_sync(kFull, yo, i);
+          const double xj = __shfl_sync(kFull, xo, j), yj = __shfl_sync(kFull, yo, j);
+          const double ri = __shfl_sync(kFull, ro, i), rj = __shfl_sync(kFull, ro, j);
+          const double ex = xi - xj, ey = yi - yj;
+          const double d2 = ex * ex + ey * ey;
           const double dist = sqrt(d2);  // == norm(pos_j - pos_i)
           const double depth = ri + rj - dist;
           if (depth > 0.0) {
@@ -200,28 +213,39 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
             }
             const double s = 0.5 * depth;
             const double mx = ux * s, my = uy * s;
-            __syncwarp();
-            if (l == 0) {
-              x[i] = xi - mx;
-              y[i] = yi - my;
-              x[j] = xj + mx;
-              y[j] = yj + my;
+            const double nxi = xi - mx, nyi = yi - my, nxj = xj + mx, nyj = yj + my;
+            if (l == i) {
+              xo = nxi;
+              yo = nyi;
             }
-            __syncwarp();
+            if (l == j) {
+              xo = nxj;
+              yo = nyj;
+            }
             mp = dmax(mp, depth);
-            // re-test the later active pairs touching i or j on the new poses
+            // patch the caches and re-test the later active pairs touching i or j
 #pragma unroll
             for (int v = 0; v < kWarpWords; ++v) {
               if (v < w || v >= nw) continue;  // warp-uniform: only words holding pairs after p
+              if (pi[v] == i) {
+                ax[v] = nxi;
+                ay[v] = nyi;
+              } else if (pi[v] == j) {
+                ax[v] = nxj;
+                ay[v] = nyj;
+              }
+              if (pj[v] == i) {
+                bx[v] = nxi;
+                by[v] = nyi;
+              } else if (pj[v] == j) {
+                bx[v] = nxj;
+                by[v] = nyj;
+              }
               const int q = 32 * v + l;
               const bool touch = q > p && (pact[v] >> l & 1u) &&
                                  (pi[v] == i || pi[v] == j || pj[v] == i || pj[v] == j);
-              bool pass = false;
-              if (touch) {
-                const double ex = x[pi[v]] - x[pj[v]], ey = y[pi[v]] - y[pj[v]];
-                const double er = r[pi[v]] + r[pj[v]];
-                pass = !(ex * ex + ey * ey > er * er);
-              }
+              const double fx = ax[v] - bx[v], fy = ay[v] - by[v];
+              const bool pass = touch && !(fx * fx + fy * fy > rr2[v]);
               const unsigned tm = __ballot_sync(kFull, touch);
               const unsigned pm = __ballot_sync(kFull, pass);
               cand[v] = (cand[v] & ~tm) | pm;
@@ -230,27 +254,30 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
         }
       }
       // clamp every object (push_sim.cpp:118 -> :48-54)
-      if (l < n) {
-        const double cx = x[l], cy = y[l];
-        if (!(fabs(cx) <= hcl)) x[l] = fmin(fmax(cx, -hcl), hcl);
-        if (!(fabs(cy) <= hcl)) y[l] = fmin(fmax(cy, -hcl), hcl);
+      if (real) {
+        if (!(fabs(xo) <= hcl)) xo = fmin(fmax(xo, -hcl), hcl);
+        if (!(fabs(yo) <= hcl)) yo = fmin(fmax(yo, -hcl), hcl);
       }
-      __syncwarp();
       if (!__any_sync(kFull, mp > C.eps_pen)) break;  // max_pen <= eps_pen
     }
   }
   // final all-pairs check (world.cpp:139-152), order-free max
   double worst = 0.0;
-  for (int w = 0; w < nw; ++w) {
-    const int p = 32 * w + l;
-    if (p < P) {
-      const double bx = x[pi[w]] - x[pj[w]], by = y[pi[w]] - y[pj[w]];
-      const double rr = r[pi[w]] + r[pj[w]];
-      const double d2 = bx * bx + by * by;
-      if (!(d2 > rr * rr)) worst = dmax(worst, rr - sqrt(d2));
+#pragma unroll
+  for (int w = 0; w < kWarpWords; ++w) {
+    if (w < nw) {
+      const double fx = __shfl_sync(kFull, xo, pi[w]) - __shfl_sync(kFull, xo, pj[w]);
+      const double fy = __shfl_sync(kFull, yo, pi[w]) - __shfl_sync(kFull, yo, pj[w]);
+      const double d2 = fx * fx + fy * fy;
+      if (32 * w + l < P && !(d2 > rr2[w])) worst = dmax(worst, rs[w] - sqrt(d2));  // (ra + rb) - dist
     }
   }
   worst = warp_max(worst);
+  if (real) {
+    W.x[l] = xo;
+    W.y[l] = yo;
+  }
+  __syncwarp();
   *residual = worst;
   return worst > C.eps_pen ? 2 : 0;
 }
