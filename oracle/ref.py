@@ -40,6 +40,8 @@ def lib():
         L.ref_load_scene.argtypes = [c_char_p]
         L.ref_fixture.restype = c_void_p
         L.ref_fixture.argtypes = [c_char_p, c_double, c_int]
+        L.ref_deep_search_case.restype = c_void_p
+        L.ref_deep_search_case.argtypes = [c_uint64, c_int]
         L.ref_state_digest.restype = c_uint64
         L.ref_state_digest.argtypes = [c_void_p, c_int]
         L.ref_batch_resolve.argtypes = [c_void_p, POINTER(c_double), POINTER(PpgParams), c_int, POINTER(c_double)]
@@ -117,6 +119,12 @@ def load_scene(path: str) -> WorldState:
 def fixture(name: str, arg: float = 0.0, iarg: int = 0) -> WorldState:
     """tests/support/scenes.cpp fixtures."""
     h = Handle(lib().ref_fixture(name.encode(), arg, iarg))
+    return h.export(0)
+
+
+def deep_search_case(seed: int, n_objects: int) -> WorldState:
+    """acceptance.cpp:124-134."""
+    h = Handle(lib().ref_deep_search_case(seed, n_objects))
     return h.export(0)
 
 

@@ -193,6 +193,22 @@ void* ref_fixture(const char* name, double arg, int iarg) {
   return st;
 }
 
+// acceptance.cpp:124-134 deep_search_case: a random scene that is not
+// graspable, has legal pushes and no winning first push.
+void* ref_deep_search_case(uint64_t seed, int n_objects) {
+  mcts::SearchConfig probe;
+  for (uint64_t k = 0; k < 2000; ++k) {
+    const WorldState s = testing::random_scene(mix_keys(seed, k), n_objects);
+    if (graspable(s, probe.grasp, probe.margin_threshold).graspable) continue;
+    if (sample_pushes(s, probe.pushes_per_object, probe.tip).empty()) continue;
+    if (!testing::winning_first_pushes(s, probe, 1).empty()) continue;
+    auto* st = new States;
+    st->v.push_back(s);
+    return st;
+  }
+  return nullptr;
+}
+
 uint64_t ref_state_digest(void* h, int i) {
   return state_digest(static_cast<States*>(h)->v.at(i));
 }

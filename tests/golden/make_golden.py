@@ -171,7 +171,36 @@ def rng():
         json.dump(out, fh)
 
 
+def acceptance():
+    """Reference acceptance criteria C1 (acceptance.cpp:184-211: N_e = 1 PMBS
+    == serial MCTS on 25 deep cases x 500 iterations) and C4 (:283-305:
+    N_e = 16, 200 iterations, identical across pool sizes) — the expected
+    trees (FNV of tree_signature) and actions from the reference."""
+    out = {"c1": [], "c4": []}
+    for i in range(25):
+        st = ref.deep_search_case(1000 + i, 8 + i % 5)
+        p = default_params(budget_iterations=1, max_iterations=500, rng_seed=4000 + i)
+        r = ref.run_search(st, p, threads=1, serial=True)
+        q = ref.run_search(st, default_params(budget_iterations=1, max_iterations=500, rng_seed=4000 + i, n_envs=1,
+                                              leaf_parallel=0), threads=1)
+        assert q["sig_fnv"] == r["sig_fnv"]
+        out["c1"].append({"state": state_json(st), "seed": 4000 + i, "sig_fnv": str(r["sig_fnv"]),
+                          "action": r["action"].tolist(), "iterations": r["iterations"], "stop": r["stop"]})
+    for i in range(10):
+        st = ref.deep_search_case(2000 + i, 8 + i % 5)
+        p = default_params(budget_iterations=1, max_iterations=200, rng_seed=500 + i, n_envs=16)
+        r = ref.run_search(st, p, threads=8)
+        out["c4"].append({"state": state_json(st), "seed": 500 + i, "sig_fnv": str(r["sig_fnv"]),
+                          "action": r["action"].tolist(), "iterations": r["iterations"], "stop": r["stop"]})
+    with open(os.path.join(HERE, "acceptance.json"), "w") as fh:
+        json.dump(out, fh)
+    print("acceptance c1/c4", len(out["c1"]), len(out["c4"]), flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        globals()[sys.argv[1]]()
+        sys.exit(0)
     rng()
     cases()
     resolve_set("discs", 0.0, 384, 1000)

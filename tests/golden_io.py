@@ -58,3 +58,16 @@ def fnv_bytes(b: bytes) -> int:
         h ^= c
         h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
     return h
+
+
+def _state(s):
+    return WorldState(np.array(s["kind"], np.int32), np.array(s["radius"], np.float64),
+                      np.array(s["n_vertices"], np.int32), np.array(s["vertices"], np.float64),
+                      np.array(s["poses"], np.float64), s["target_index"], s["side_length"], s["boundary_margin"])
+
+
+def acceptance():
+    """Reference acceptance C1 / C4 fixtures (tests/golden/make_golden.py acceptance)."""
+    with open(os.path.join(GOLDEN, "acceptance.json")) as f:
+        d = json.load(f)
+    return {k: [(x, _state(x["state"])) for x in v] for k, v in d.items()}
