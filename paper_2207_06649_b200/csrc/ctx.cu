@@ -27,11 +27,27 @@ __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
+template <int NW>
 __global__ void resolve_warp_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
+template <int NW>
 __global__ void expand_warp_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
+template <int NW>
 __global__ void lock_step_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
 constexpr int kWarpMaxN = 23;
 constexpr int kWarpsPerBlock = 4;
+// pair-mask words of the latency-mode kernels (warp_env.cuh warp_words_for)
+constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 : 8; }
+// Launches KERNEL<NW> (one warp per item, `items` items) for n objects.
+#define PPG_WARP_LAUNCH(KERNEL, n, items, st, ...)                                          \
+  do {                                                                                      \
+    const int g_ = ((items) + kWarpsPerBlock - 1) / kWarpsPerBlock;                         \
+    switch (warp_words(n)) {                                                                \
+      case 1: KERNEL<1><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
+      case 2: KERNEL<2><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
+      case 4: KERNEL<4><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
+      default: KERNEL<8><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;           \
+    }                                                                                       \
+  } while (0)
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_report_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockArgs a, const int32_t* env,
@@ -454,7 +470,7 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
   if (!d_counts && use_warp(ctx, all_discs, S.n, E)) {
-    resolve_warp_kernel<<<(E + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
+    PPG_WARP_LAUNCH(resolve_warp_kernel, S.n, E, st, C, a);
     CK(cudaGetLastError());
     return PPG_SUCCESS;
   }
@@ -641,7 +657,7 @@ int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, 
   ExpandArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_push.as<double>(), ctx->b_out.as<double>(),
                ctx->b_status.as<int32_t>(), ctx->b_a.as<uint8_t>(), ctx->b_e.as<int32_t>(), ctx->b_b.as<double>(), P};
   if (use_warp(ctx, ctx->scene_all_discs, n, P)) {
-    expand_warp_kernel<<<(P + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
+    PPG_WARP_LAUNCH(expand_warp_kernel, n, P, st, C, a);
   } else if (use_disc(ctx, ctx->scene_all_discs, n)) {
     // child = parent, resolve in place on the register-resident kernel, then
     // sample + grasp (or restore the parent for a failed simulation)
@@ -762,7 +778,7 @@ static int lock_round(ppg_ctx* ctx, int act) {
   const int n = ctx->scene.n;
   const int g = (act + kBlock - 1) / kBlock;
   if (use_warp(ctx, ctx->scene_all_discs, n, act)) {
-    lock_step_warp_kernel<<<(act + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(C, a);
+    PPG_WARP_LAUNCH(lock_step_warp_kernel, n, act, st, C, a);
     CK(cudaGetLastError());
   } else if (use_disc(ctx, ctx->scene_all_discs, n)) {  // sample+pick -> physics (in place) -> grasp + reward
     lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
