@@ -218,12 +218,29 @@ typedef int (*ppg_simulate_fn)(void* user, const double* node_poses, const int32
                                double* rewards_out, int64_t* counters);
 int ppg_set_simulate_hook(ppg_ctx* ctx, ppg_simulate_fn fn, void* user);
 
+/* Planner selection for ppg_run_pmbs (also env PPG_PLANNER=host|device):
+ * AUTO = the device-resident tree unless a simulate hook is installed (the
+ * sharded multi-GPU driver needs the host tree); HOST = tree on the host
+ * (planner.cpp); DEVICE = tree on the device (dtree.cu). */
+#define PPG_PLANNER_AUTO 0
+#define PPG_PLANNER_HOST 1
+#define PPG_PLANNER_DEVICE 2
+int ppg_set_planner(ppg_ctx* ctx, int mode);
+
 /* run_pmbs (pmbs.hpp:91, pmbs.cpp:242-292) on the context scene and poses:
- * the full PMBS planning decision.  Tree kept on the host (C++), batched
- * expansion and lockstep rollouts on the device.  action_out[4] = chosen push.
+ * the full PMBS planning decision, batched expansion and lockstep rollouts
+ * on the device, the tree per ppg_set_planner.  action_out[4] = chosen push.
  * Returns PPG_ENOLEGAL when the root has no legal push. */
 int ppg_run_pmbs(ppg_ctx* ctx, const double* root_poses, double* action_out,
                  ppg_search_stats* stats);
+
+/* run_pmbs with the search tree resident on the device: batched UCT leaf
+ * selection with virtual visits (pmbs.cpp:12-63), expansion + attach
+ * (:70-131), lockstep rollouts (:133-234) and backprop (:236-240) are one
+ * CUDA-graph launch per PMBS iteration.  Same results as the host tree;
+ * writes the tree signature like ppg_run_pmbs_sig (sig_buf may be NULL). */
+int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_out,
+                        ppg_search_stats* stats, char* sig_buf, int64_t sig_cap, int64_t* sig_len);
 
 /* Same, and also writes the tree_signature text (mcts.cpp:284-300) into
  * sig_buf (NUL-terminated, truncated to sig_cap); *sig_len = full length. */

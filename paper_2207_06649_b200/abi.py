@@ -19,6 +19,7 @@ PPG_MAX_OBJECTS = 32
 PPG_MAX_VERTICES = 8
 
 PPG_SUCCESS = 0
+PPG_PLANNER_AUTO, PPG_PLANNER_HOST, PPG_PLANNER_DEVICE = 0, 1, 2
 PPG_EINVAL = -1
 PPG_ECUDA = -2
 PPG_ENOLEGAL = -3
@@ -173,6 +174,9 @@ SIGNATURES = {
     "ppg_lock_step": (c_int, [c_void_p]),
     "ppg_lock_counters": (c_int, [c_void_p, POINTER(c_int64)]),
     "ppg_set_simulate_hook": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "ppg_set_planner": (c_int, [c_void_p, c_int]),
+    "ppg_run_pmbs_device": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(PpgSearchStats),
+                                    c_char_p, c_int64, POINTER(c_int64)]),
     "ppg_debug_sincos": (c_int, [c_void_p, POINTER(c_double), c_int, POINTER(c_double), POINTER(c_double)]),
     "ppg_measure_fp64_peak": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "ppg_generate_cases": (c_int, [c_int, c_int, c_double, POINTER(c_uint64), c_int, POINTER(c_int32),

@@ -177,6 +177,12 @@ class Context:
             raise ValueError(f"{what}: {msg}")
         raise DeviceError(f"{what}: {msg}")
 
+    def set_planner(self, mode: str):
+        """"auto" (device tree unless a simulate hook is installed), "host"
+        (planner.cpp) or "device" (dtree.cu) for run_pmbs."""
+        code = {"auto": abi.PPG_PLANNER_AUTO, "host": abi.PPG_PLANNER_HOST, "device": abi.PPG_PLANNER_DEVICE}[mode]
+        self._check(self.lib.ppg_set_planner(self.ptr, code), "ppg_set_planner")
+
     def set_params(self, params: PpgParams):
         self.params = params
         self._check(self.lib.ppg_set_params(self.ptr, ctypes.byref(params)), "ppg_set_params")

@@ -13,135 +13,7 @@
 #include "ctx.h"
 #include "kernels.cuh"
 
-namespace ppg {
-
-template <bool kCount>
-__global__ void resolve_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
-__global__ void shape_prep_kernel(ShapesDev S, const int* kind, const double* radius, const int* nv,
-                                  const double* verts, const int* target);
-__global__ void sample_kernel(const __grid_constant__ SimConst C, SampleArgs a);
-__global__ void grasp_kernel(const __grid_constant__ SimConst C, SampleArgs a);
-__global__ void expand_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
-__global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
-__global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
-__global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
-__global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
-__global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
-template <int NW>
-__global__ void resolve_warp_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
-template <int NW>
-__global__ void expand_warp_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
-template <int NW>
-__global__ void lock_step_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
-constexpr int kWarpMaxN = 23;
-constexpr int kWarpsPerBlock = 4;
-// pair-mask words of the latency-mode kernels (warp_env.cuh warp_words_for)
-constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 : 8; }
-// Launches KERNEL<NW> (one warp per item, `items` items) for n objects.
-#define PPG_WARP_LAUNCH(KERNEL, n, items, st, ...)                                          \
-  do {                                                                                      \
-    const int g_ = ((items) + kWarpsPerBlock - 1) / kWarpsPerBlock;                         \
-    switch (warp_words(n)) {                                                                \
-      case 1: KERNEL<1><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
-      case 2: KERNEL<2><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
-      case 4: KERNEL<4><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
-      default: KERNEL<8><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;           \
-    }                                                                                       \
-  } while (0)
-__global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
-__global__ void lock_report_kernel(const __grid_constant__ SimConst C, LockArgs a);
-__global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockArgs a, const int32_t* env,
-                                      const int32_t* node, int count);
-__global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
-__global__ void debug_sincos_kernel(const double* x, int n, double* s, double* c);
-template <int NMAX>
-__global__ void resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a, int* next_env);
-
-constexpr int kBlock = 128;
-constexpr int kDiscBlock = 128;  // resolve_disc.cu kDB
-constexpr int kNumDisc = 8;
-constexpr int kDiscSizes[kNumDisc] = {4, 6, 8, 10, 11, 12, 14, 16};
-constexpr size_t kMaxSmem = kPosePlanes * kMaxObjects * kBlock * sizeof(double);
-
-}  // namespace ppg
-
-using namespace ppg;
-
-#define CK(call)                                                                         \
-  do {                                                                                   \
-    cudaError_t e_ = (call);                                                             \
-    if (e_ != cudaSuccess) {                                                             \
-      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                     \
-      return PPG_ECUDA;                                                                  \
-    }                                                                                    \
-  } while (0)
-
-namespace {
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-    size_t want = bytes < 256 ? 256 : bytes;
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) cap = want;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
-}  // namespace
-
-struct ppg_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  ppg_params params{};
-  std::string err;
-  // shared scene (ppg_set_scene)
-  bool has_scene = false;
-  bool scene_all_discs = false;
-  ShapesDev scene;
-  std::vector<int32_t> h_kind, h_nv, h_target;
-  std::vector<double> h_radius, h_verts;
-  double side = 0.288, margin = 0.0;
-  DevBuf scene_buf, scene_in;
-  // per-call shape tables (batch_resolve with per-env shapes)
-  DevBuf shape_buf, shape_in;
-  // I/O scratch
-  DevBuf b_in, b_push, b_out, b_status, b_resid, b_a, b_b, b_c, b_d, b_e;
-  // lockstep state
-  DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx;
-  DevBuf l_W, l_rew, l_active, l_nactive, l_counters, l_npose, l_nmeta;
-  DevBuf b_counter;              // persistent-kernel work counter
-  DevBuf l_push, l_status, l_stepping, l_rec;
-  LockArgs la{};        // current lockstep session
-  ResolveArgs lra{};    // its in-place physics arguments
-  SimConst lc{};        // its constants
-  int lock_active_hint = 0;
-  ppg_simulate_fn sim_hook = nullptr;
-  void* sim_hook_user = nullptr;
-  int32_t* h_nactive = nullptr;  // pinned
-  int num_sms = 148;
-  int disc_blocks_per_sm[kNumDisc] = {};  // resolve_disc_kernel<kDiscSizes[k]>
-  bool disc_kernels = false;
-  bool force_generic = false;             // PPG_FORCE_GENERIC=1: A/B the generic kernel
-  int disc_bps_override = 0;              // PPG_DISC_BLOCKS_PER_SM: cap resident blocks (experiments)
-  int warp_max_envs = 4096;               // latency mode (one warp per env) up to this many envs; PPG_WARP_MAX
-};
-
-namespace {
+#include "ctx_impl.cuh"
 
 SimConst make_const(const ppg_params& p, int n, double side, double margin) {
   SimConst C;
@@ -276,8 +148,6 @@ size_t disc_smem(int nmax) { return static_cast<size_t>(3) * nmax * kDiscBlock *
 
 size_t smem_for(int n) { return static_cast<size_t>(kPosePlanes) * n * kBlock * sizeof(double); }
 
-}  // namespace
-
 // ---------------------------------------------------------------------------
 
 extern "C" {
@@ -363,6 +233,8 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
     ctx->force_generic = fg && fg[0] == '1';
     const char* wm = std::getenv("PPG_WARP_MAX");
     if (wm) ctx->warp_max_envs = std::atoi(wm);
+    const char* pl = std::getenv("PPG_PLANNER");
+    if (pl) ctx->planner = !std::strcmp(pl, "host") ? PPG_PLANNER_HOST : !std::strcmp(pl, "device") ? PPG_PLANNER_DEVICE : 0;
     const char* bo = std::getenv("PPG_DISC_BLOCKS_PER_SM");
     ctx->disc_bps_override = bo ? std::atoi(bo) : 0;
   }
@@ -386,6 +258,7 @@ void ppg_destroy(ppg_ctx* ctx) {
                     &ctx->l_rew, &ctx->l_active, &ctx->l_nactive, &ctx->l_counters, &ctx->l_npose,
                     &ctx->l_nmeta, &ctx->b_counter, &ctx->l_push, &ctx->l_status, &ctx->l_stepping, &ctx->l_rec};
   for (DevBuf* b : bufs) b->release();
+  dtree_release(ctx);
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -422,11 +295,15 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
   return PPG_SUCCESS;
 }
 
+}  // extern "C"
+
 // Launches resolve_disc_kernel<N> (N = the smallest instantiated size >= n)
-// as a persistent grid sized for `work` environments.
-static int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st) {
+// as a persistent grid sized for `work` environments.  The work counter
+// (ctx->b_counter) is zeroed here unless the caller's graph zeroes it.
+int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st,
+                bool zero_counter) {
   CK(ctx->b_counter.ensure(16));
-  CK(cudaMemsetAsync(ctx->b_counter.p, 0, 4, st));
+  if (zero_counter) CK(cudaMemsetAsync(ctx->b_counter.p, 0, 4, st));
   int slot = 0;
   while (kDiscSizes[slot] < n) ++slot;
   const int nmax = kDiscSizes[slot];
@@ -452,12 +329,12 @@ static int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, in
   return PPG_SUCCESS;
 }
 
-static bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
+bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
   return all_discs && n <= 16 && ctx->disc_kernels && !ctx->force_generic;
 }
 
 // Latency mode: one warp per environment (warp_env.cu) for small batches.
-static bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs) {
+bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs) {
   return all_discs && n <= kWarpMaxN && envs <= ctx->warp_max_envs && !ctx->force_generic;
 }
 
@@ -483,6 +360,8 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
 }
 
 
+
+extern "C" {
 
 int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in, const double* pushes,
                       int E, double* poses_out, int32_t* status, double* residual) {
@@ -905,6 +784,12 @@ int ppg_lock_step(ppg_ctx* ctx) {
   return PPG_SUCCESS;
 }
 
+int ppg_set_planner(ppg_ctx* ctx, int mode) {
+  if (!ctx || mode < PPG_PLANNER_AUTO || mode > PPG_PLANNER_DEVICE) return PPG_EINVAL;
+  ctx->planner = mode;
+  return PPG_SUCCESS;
+}
+
 int ppg_set_simulate_hook(ppg_ctx* ctx, ppg_simulate_fn fn, void* user) {
   if (!ctx) return PPG_EINVAL;
   ctx->sim_hook = fn;
@@ -1006,6 +891,7 @@ int ppg_state_digest(const ppg_shapes* sh, const double* poses, int E, uint64_t*
 namespace ppg {
 const ppg_params& ctx_params(const ppg_ctx* ctx) { return ctx->params; }
 SimHook ctx_sim_hook(const ppg_ctx* ctx) { return SimHook{ctx->sim_hook, ctx->sim_hook_user}; }
+int ctx_planner(const ppg_ctx* ctx) { return ctx->planner; }
 int ctx_n_objects(const ppg_ctx* ctx) { return ctx->has_scene ? ctx->scene.n : 0; }
 void ctx_set_error(ppg_ctx* ctx, const char* msg) { ctx->err = msg; }
 }  // namespace ppg

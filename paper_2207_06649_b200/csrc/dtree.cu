@@ -1,0 +1,1081 @@
+// dtree.cu — the device-resident PMBS search tree (north star
+// item 3): batched UCT leaf selection with virtual loss, batched expansion,
+// lockstep rollouts and batched backpropagation all run on the device, and
+// ONE CUDA-graph launch executes one whole PMBS iteration (Algorithm 1 of
+// arxiv 2207.06649; run_pmbs, pmbs.cpp:242-292).  The lockstep rounds run
+// inside the graph under a conditional WHILE node whose condition the
+// harvest kernel sets (n_active > 0), so the host only reads a few status
+// words per iteration (stop flag, sizes) to decide whether to launch again.
+//
+// Decision-for-decision identical to the host planner (planner.cpp) and so
+// to the reference:
+//   select_batch / descend_virtual / ucb_virtual / pop_untried (pmbs.cpp:12-63,
+//     mcts.cpp:13-16) -> dt_select_kernel: one warp, children scanned 32 at a
+//     time, first maximum in insertion order; UCB with the host's glibc log
+//     table and IEEE sqrt / division; subtree_selectable (pmbs.cpp:21-28) is
+//     kept INCREMENTALLY as a per-node count of selectable children (selc)
+//     instead of a recursive scan;
+//   reset_virtual (pmbs.cpp:65-68) -> dt_gather_kernel;
+//   batch_expand attach (pmbs.cpp:95-131, mcts.cpp:77-105) -> dt_attach_kernel
+//     (child slot == popped untried index, so the batch-order append is a
+//     parallel scatter) + dt_copy_kernel; d_T shrink (pmbs.cpp:119-127) and
+//     update_es_level / level_settled (mcts.cpp:187-209) from per-level
+//     counts of unsettled nodes;
+//   batch_simulate (pmbs.cpp:207-234) -> the lockstep kernels with their
+//     per-iteration values read on the device (LockArgs.dyn);
+//   backprop_max -> backprop_mean (pmbs.cpp:236-240, mcts.cpp:180-185) ->
+//     dt_backprop_kernel: lane d folds the rewards into the depth-d ancestor
+//     in batch order (exact FP64 summation order);
+//   early_stop_satisfied + budget (mcts.cpp:211-216, pmbs.cpp:282-290) ->
+//     dt_stop_kernel.
+// The final tree is read back once for best_root_child (mcts.cpp:218-235)
+// and the tree signature (mcts.cpp:284-300).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "ctx_impl.cuh"
+
+namespace ppg {
+
+constexpr int kMaxTreeDepth = 32;  // ancestor row stride; node depths <= tree_depth < 32
+
+struct DTScal {
+  int n_nodes;
+  int n_pairs;          // this iteration's selections
+  int dT, dS;           // tree_depth, rollout_depth
+  int es_level;
+  int min_grasp_depth;  // over attached graspable children (INT_MAX: none)
+  int levels;           // max depth + 1
+  int stop;             // -1 running, 0 budget, 1 explored, 2 early stop, 3 internal error
+  int iteration;
+  int recompute;        // d_T shrank this iteration: recount the selectable children
+  int lock_dyn[4];      // LockArgs.dyn: n_nodes, used envs, depth cap, iteration
+  long long a_used;     // action-pool entries in use
+  long long expansions;
+  int unsettled[kMaxTreeDepth];  // non-terminal nodes with untried actions, per depth
+  int err[4];                    // first invariant violation seen on the device (debug)
+};
+
+struct DTree {
+  // node arrays [cap_nodes]
+  int32_t* parent;
+  int32_t* depth;
+  double* q;
+  long long* visits;
+  int32_t* vv;        // virtual visits
+  uint8_t* flags;     // bit0 graspable, bit1 dead (terminal == flags != 0)
+  long long* u_off;   // untried actions (apool) and children (cpool) share this offset
+  int32_t* u_n;
+  int32_t* u_head;
+  int32_t* c_n;
+  int32_t* selc;      // selectable children
+  double* action;     // [cap][4]
+  double* poses;      // [cap][n][3]
+  int32_t* anc;       // [cap][kMaxTreeDepth]: ancestor at each depth (self at its own)
+  double* apool;      // [cap_actions][4]
+  int32_t* cpool;     // [cap_actions]
+  // per-iteration batch [n_envs]
+  int32_t* sel_node;
+  long long* sel_act;
+  double* gp;         // parent poses [P][n][3]
+  double* ga;         // actions [P][4]
+  double* cp;         // child poses [P][n][3] (the new nodes' poses, in batch order)
+  int32_t* st;
+  uint8_t* gr;
+  int32_t* nu;
+  double* un;         // [P][n*na][4]
+  int32_t* meta;      // [P][3] depth, graspable, dead
+  const unsigned long long* rew;  // lockstep per-new-node max reward bits
+  const double* logtab;           // logtab[k] == glibc log((double)k)
+  DTScal* sc;
+  int n_envs, n, na, leaf_parallel, max_iters;
+  double c_explore;
+};
+
+namespace {
+
+__device__ __forceinline__ bool dt_self(const DTree& t, int x, int dT) {
+  return t.flags[x] == 0 && t.depth[x] < dT && t.u_head[x] < t.u_n[x];
+}
+
+// subtree_selectable (pmbs.cpp:21-28) under the selc invariant.
+__device__ __forceinline__ bool dt_selectable(const DTree& t, int x, int dT) {
+  return t.flags[x] == 0 && ((t.depth[x] < dT && t.u_head[x] < t.u_n[x]) || t.selc[x] > 0);
+}
+
+constexpr unsigned kAll = 0xffffffffu;
+
+// select_batch (pmbs.cpp:52-63): up to n_envs descents with virtual visits.
+__global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
+  DTScal* sc = t.sc;
+  const int l = threadIdx.x;
+  const int dT = sc->dT;
+  int draws = 0;
+  bool bad = false;
+  if (sc->stop < 0) {
+    for (; draws < t.n_envs; ++draws) {
+      if (!dt_selectable(t, 0, dT)) break;
+      int x = 0;
+      while (!dt_self(t, x, dT)) {  // descend_virtual (pmbs.cpp:30-48)
+        const long long co = t.u_off[x];
+        const int cn = t.c_n[x];
+        const double lg = t.logtab[t.visits[x] + t.vv[x]];  // log(n_parent)
+        double bs = -INFINITY;
+        int bk = INT_MAX;
+        for (int k = l; k < cn; k += 32) {
+          const int ch = t.cpool[co + k];
+          if (!dt_selectable(t, ch, dT)) continue;
+          const long long nci = t.visits[ch] + t.vv[ch];
+          double s = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
+          if (nci != 0) {
+            const double nc = static_cast<double>(nci);
+            s = t.q[ch] / nc + t.c_explore * sqrt(2.0 * lg / nc);
+          }
+          if (s > bs) {
+            bs = s;
+            bk = k;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // first maximum in insertion order
+          const double os = __shfl_xor_sync(kAll, bs, o);
+          const int ok = __shfl_xor_sync(kAll, bk, o);
+          if (os > bs || (os == bs && ok < bk)) {
+            bs = os;
+            bk = ok;
+          }
+        }
+        if (bk == INT_MAX) {  // impossible under the selc invariant
+          bad = true;
+          break;
+        }
+        x = t.cpool[co + bk];
+      }
+      if (bad) break;
+      if (l == 0) {  // pop_untried (mcts.cpp:13-16) + virtual visit up the path
+        const int h = t.u_head[x];
+        t.sel_node[draws] = x;
+        t.sel_act[draws] = t.u_off[x] + h;
+        t.u_head[x] = h + 1;
+        for (int a = x; a >= 0; a = t.parent[a]) t.vv[a] += 1;
+        if (h + 1 == t.u_n[x]) {  // now fully expanded
+          sc->unsettled[t.depth[x]] -= 1;
+          if (t.selc[x] == 0)  // x left the selectable set: update its ancestors
+            for (int p = t.parent[x]; p >= 0; p = t.parent[p]) {
+              t.selc[p] -= 1;
+              if (dt_selectable(t, p, dT)) break;
+            }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (l == 0) {
+    sc->n_pairs = draws;
+    if (bad) sc->stop = 3;
+    else if (draws == 0 && sc->stop < 0) sc->stop = 1;  // TreeExhausted: explored
+  }
+}
+
+// reset_virtual (pmbs.cpp:65-68) + gather of the batch's parent poses and
+// actions (and the child-pose buffer the in-place disc kernel resolves).
+__global__ void dt_gather_kernel(DTree t, bool copy_child) {
+  const int P = t.sc->n_pairs, N = t.sc->n_nodes, n3 = t.n * 3;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x, G = gridDim.x * blockDim.x;
+  for (int i = g; i < N; i += G) t.vv[i] = 0;
+  for (int i = g; i < P * n3; i += G) {
+    const int k = i / n3, r = i - k * n3;
+    const double v = t.poses[static_cast<size_t>(t.sel_node[k]) * n3 + r];
+    t.gp[i] = v;
+    if (copy_child) t.cp[i] = v;
+  }
+  for (int i = g; i < P * 4; i += G) t.ga[i] = t.apool[t.sel_act[i >> 2] * 4 + (i & 3)];
+}
+
+// batch_expand attach (pmbs.cpp:95-131) for the whole batch at once.  One
+// block.  Every pop produced exactly one child, so the child created from
+// untried index h of node p sits in children slot h: the batch-order append
+// is a scatter.  Untried lists are appended to the pool in batch order (block
+// scan).  Selectable-children counts are updated with atomics ("first
+// incrementer propagates"); if d_T shrinks they are recounted instead.
+__global__ void __launch_bounds__(1024) dt_attach_kernel(DTree t) {
+  DTScal* sc = t.sc;
+  const int P = sc->n_pairs;
+  const int tid = threadIdx.x, B = blockDim.x;
+  __shared__ long long s_part[1024];
+  __shared__ int s_mind, s_maxd;
+  if (P == 0) {
+    if (tid == 0) {
+      sc->lock_dyn[0] = 0;
+      sc->lock_dyn[1] = 0;
+      sc->lock_dyn[2] = sc->dT + sc->dS;
+      sc->lock_dyn[3] = sc->iteration;
+    }
+    return;
+  }
+  const int base = sc->n_nodes, dT0 = sc->dT;
+  const long long a0 = sc->a_used;
+  if (tid == 0) {
+    s_mind = INT_MAX;
+    s_maxd = 0;
+  }
+  // exclusive scan of the untried counts of the live children, batch order
+  const int chunk = (P + B - 1) / B;
+  const int k0 = tid * chunk, k1 = min(P, k0 + chunk);
+  long long loc = 0;
+  for (int k = k0; k < k1; ++k) loc += t.st[k] == 0 ? t.nu[k] : 0;
+  s_part[tid] = loc;
+  __syncthreads();
+  for (int off = 1; off < B; off <<= 1) {  // Hillis-Steele inclusive scan
+    const long long v = tid >= off ? s_part[tid - off] : 0;
+    __syncthreads();
+    s_part[tid] += v;
+    __syncthreads();
+  }
+  long long run = a0 + s_part[tid] - loc;
+  for (int k = k0; k < k1; ++k) {
+    const int id = base + k, p = t.sel_node[k], d = t.depth[p] + 1;
+    const bool alive = t.st[k] == 0;  // a failed simulation yields a dead child (pmbs.cpp:105-107)
+    const bool g = alive && t.gr[k] != 0;
+    const int un = alive ? t.nu[k] : 0;
+    const bool dead = !g && un == 0;
+    t.parent[id] = p;
+    t.depth[id] = d;
+    t.q[id] = 0.0;
+    t.visits[id] = 0;
+    t.vv[id] = 0;
+    t.flags[id] = static_cast<uint8_t>((g ? 1 : 0) | (dead ? 2 : 0));
+    t.u_off[id] = run;
+    run += un;
+    t.u_n[id] = un;
+    t.u_head[id] = 0;
+    t.c_n[id] = 0;
+    t.selc[id] = 0;
+    const long long h = t.sel_act[k] - t.u_off[p];
+    t.cpool[t.u_off[p] + h] = id;
+    t.c_n[p] = t.u_head[p];  // every pop so far has its child now (same value from every writer)
+    t.meta[k * 3] = d;
+    t.meta[k * 3 + 1] = g ? 1 : 0;
+    t.meta[k * 3 + 2] = dead ? 1 : 0;
+    if (!g && !dead) atomicAdd(&sc->unsettled[d], 1);  // non-terminal with untried actions
+    if (g) atomicMin(&s_mind, d);
+    atomicMax(&s_maxd, d);
+    if (!g && !dead && d < dT0) {  // a selectable child: p (and maybe ancestors) become selectable
+      for (int x = p; x >= 0; x = t.parent[x]) {
+        const int old = atomicAdd(&t.selc[x], 1);
+        if (old > 0 || dt_self(t, x, dT0)) break;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    sc->n_nodes = base + P;
+    sc->a_used = a0 + s_part[B - 1];
+    sc->levels = max(sc->levels, s_maxd + 1);
+    sc->recompute = 0;
+    if (s_mind < INT_MAX) {
+      sc->min_grasp_depth = min(sc->min_grasp_depth, s_mind);
+      if (s_mind < sc->dT) {  // shallower graspable child (pmbs.cpp:119-127)
+        sc->dT = s_mind;
+        sc->dS = 0;
+        sc->recompute = 1;
+      }
+    }
+    // update_es_level (mcts.cpp:202-209) with level_settled (:189-198)
+    if (sc->es_level <= sc->dT) {
+      const int L = sc->es_level - 1;
+      const bool settled = L < 0 || L >= sc->levels || L >= sc->dT || sc->unsettled[L] == 0;
+      if (settled) sc->es_level += 1;
+    }
+    sc->lock_dyn[0] = P;
+    sc->lock_dyn[1] = t.leaf_parallel ? t.n_envs : P;
+    sc->lock_dyn[2] = sc->dT + sc->dS;
+    sc->lock_dyn[3] = sc->iteration;
+  }
+}
+
+// Recount selc bottom-up after d_T shrank (selectability of every node may
+// have changed).  One block, one pass per depth level.
+__global__ void __launch_bounds__(1024) dt_recount_kernel(DTree t) {
+  const DTScal* sc = t.sc;
+  if (!sc->recompute) return;
+  const int N = sc->n_nodes, dT = sc->dT;
+  for (int L = sc->levels - 1; L >= 0; --L) {
+    for (int x = threadIdx.x; x < N; x += blockDim.x) {
+      if (t.depth[x] != L) continue;
+      int c = 0;
+      const long long co = t.u_off[x];
+      for (int k = 0; k < t.c_n[x]; ++k) c += dt_selectable(t, t.cpool[co + k], dT) ? 1 : 0;
+      t.selc[x] = c;
+    }
+    __syncthreads();
+  }
+}
+
+// The new nodes' poses, actions, untried lists and ancestor rows.
+__global__ void dt_copy_kernel(DTree t) {
+  const DTScal* sc = t.sc;
+  const int P = sc->n_pairs, base = sc->n_nodes - P, n3 = t.n * 3, cap = t.n * t.na * 4;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x, G = gridDim.x * blockDim.x;
+  for (int i = g; i < P * n3; i += G) t.poses[static_cast<size_t>(base) * n3 + i] = t.cp[i];
+  for (int i = g; i < P * 4; i += G) t.action[static_cast<size_t>(base) * 4 + i] = t.ga[i];
+  for (int i = g; i < P * kMaxTreeDepth; i += G) {
+    const int k = i / kMaxTreeDepth, d = i - k * kMaxTreeDepth, id = base + k;
+    const int dd = t.depth[id];
+    if (d < dd) t.anc[static_cast<size_t>(id) * kMaxTreeDepth + d] = t.anc[static_cast<size_t>(t.sel_node[k]) * kMaxTreeDepth + d];
+    else if (d == dd) t.anc[static_cast<size_t>(id) * kMaxTreeDepth + d] = id;
+  }
+  for (int k = blockIdx.x; k < P; k += gridDim.x) {
+    const int id = base + k, un = t.u_n[id];
+    const double* src = t.un + static_cast<size_t>(k) * cap;
+    double* dst = t.apool + t.u_off[id] * 4;
+    for (int i = threadIdx.x; i < un * 4; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+// backprop_max -> backprop_mean (pmbs.cpp:236-240, mcts.cpp:180-185): for
+// each new node in batch order, q_sum += r and visits += 1 on every node of
+// its root path.  Lane d owns depth d, so each node's additions happen in
+// batch order (the FP64 sum is the reference's).
+__global__ void __launch_bounds__(32) dt_backprop_kernel(DTree t) {
+  const DTScal* sc = t.sc;
+  const int P = sc->n_pairs, base = sc->n_nodes - P, d = threadIdx.x;
+  int cur = -1;
+  double cq = 0.0;
+  long long cv = 0;
+  for (int k = 0; k < P; ++k) {
+    const int id = base + k, D = t.depth[id];
+    const double r = __longlong_as_double(static_cast<long long>(t.rew[k]));
+    if (d == D) {
+      t.q[id] = 0.0 + r;
+      t.visits[id] = 1;
+    } else if (d < D) {
+      const int a = t.anc[static_cast<size_t>(id) * kMaxTreeDepth + d];
+      if (a < 0 || a >= sc->n_nodes) {  // corrupt ancestor row: report, do not touch memory
+        if (atomicCAS(const_cast<int*>(&sc->err[0]), 0, 1) == 0) {
+          const_cast<DTScal*>(sc)->err[1] = id;
+          const_cast<DTScal*>(sc)->err[2] = d;
+          const_cast<DTScal*>(sc)->err[3] = a;
+        }
+        continue;
+      }
+      if (a != cur) {
+        if (cur >= 0) {
+          t.q[cur] = cq;
+          t.visits[cur] = cv;
+        }
+        cur = a;
+        cq = t.q[a];
+        cv = t.visits[a];
+      }
+      cq += r;
+      cv += 1;
+    }
+  }
+  if (cur >= 0) {
+    t.q[cur] = cq;
+    t.visits[cur] = cv;
+  }
+}
+
+// End of an iteration: early stop (mcts.cpp:211-216) then the iteration
+// budget (pmbs.cpp:282-290).
+__global__ void dt_stop_kernel(DTree t) {
+  DTScal* sc = t.sc;
+  const int P = sc->n_pairs;
+  if (P == 0) return;
+  sc->iteration += 1;
+  sc->expansions += P;
+  if (sc->stop >= 0) return;
+  if (sc->min_grasp_depth <= sc->es_level) sc->stop = 2;
+  else if (t.max_iters > 0 && sc->iteration >= t.max_iters) sc->stop = 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct DTreeState {
+  // tree
+  DevBuf parent, depth, q, visits, vv, flags, u_off, u_n, u_head, c_n, selc, action, poses, anc, apool, cpool;
+  // batch
+  DevBuf sel_node, sel_act, gp, ga, cp, st, gr, nu, un, meta, logtab, sc;
+  // lockstep state
+  DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx, l_W, l_rew, l_active,
+      l_nactive, l_counters, l_push, l_status, l_stepping;
+  int cap_nodes = 0;
+  long long cap_actions = 0;
+  int n_envs = 0, n = 0, na = 0;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaStream_t st2 = nullptr;
+  DTree t{};
+  LockArgs la{};
+  ResolveArgs lra{};
+  SimConst C{};
+  std::string key;  // configuration the graph was captured for
+
+  void release_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+  }
+  void release() {
+    release_graph();
+    if (st2) cudaStreamDestroy(st2);
+    st2 = nullptr;
+    DevBuf* bufs[] = {&parent, &depth, &q, &visits, &vv, &flags, &u_off, &u_n, &u_head, &c_n, &selc, &action,
+                      &poses, &anc, &apool, &cpool, &sel_node, &sel_act, &gp, &ga, &cp, &st, &gr, &nu, &un,
+                      &meta, &logtab, &sc, &l_node, &l_pushes, &l_done, &l_byg, &l_harv, &l_flag, &l_reward,
+                      &l_poses, &l_mt, &l_mtidx, &l_W, &l_rew, &l_active, &l_nactive, &l_counters, &l_push,
+                      &l_status, &l_stepping};
+    for (DevBuf* b : bufs) b->release();
+  }
+};
+
+void dtree_release(ppg_ctx* ctx) {
+  if (ctx->dtree) {
+    ctx->dtree->release();
+    delete ctx->dtree;
+    ctx->dtree = nullptr;
+  }
+}
+
+namespace {
+
+// Grows a node- or action-indexed buffer to `want` elements of `esz` bytes,
+// preserving the first `used` elements.
+cudaError_t grow(DevBuf& b, size_t want, size_t used, size_t esz, cudaStream_t st) {
+  if (want * esz <= b.cap) return cudaSuccess;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, want * esz);
+  if (e != cudaSuccess) return e;
+  if (b.p && used) e = cudaMemcpyAsync(p, b.p, used * esz, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  if (b.p) {
+    cudaStreamSynchronize(st);
+    cudaFree(b.p);
+  }
+  b.p = p;
+  b.cap = want * esz;
+  return cudaSuccess;
+}
+
+double ucb_score_host(double q, long vis_child, long vis_parent, double c) {  // mcts.cpp:41-46
+  if (vis_child == 0) return std::numeric_limits<double>::infinity();
+  const double mean = q / static_cast<double>(vis_child);
+  return mean + c * std::sqrt(2.0 * std::log(static_cast<double>(vis_parent)) / static_cast<double>(vis_child));
+}
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char ch : s) {
+    h ^= ch;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+}  // namespace
+
+}  // namespace ppg
+
+using namespace ppg;
+
+#define DCK(call)                                                                        \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                     \
+      return PPG_ECUDA;                                                                  \
+    }                                                                                    \
+  } while (0)
+
+namespace {
+
+// Ensures tree capacity for `nodes` nodes and `actions` pool entries.
+int dt_reserve(ppg_ctx* ctx, DTreeState& S, int used_nodes, long long used_actions, int nodes, long long actions) {
+  cudaStream_t st = ctx->stream;
+  const int n = S.n;
+  if (nodes > S.cap_nodes) {
+    const size_t want = static_cast<size_t>(nodes), u = static_cast<size_t>(used_nodes);
+    DCK(grow(S.parent, want, u, 4, st));
+    DCK(grow(S.depth, want, u, 4, st));
+    DCK(grow(S.q, want, u, 8, st));
+    DCK(grow(S.visits, want, u, 8, st));
+    DCK(grow(S.vv, want, u, 4, st));
+    DCK(grow(S.flags, want, u, 1, st));
+    DCK(grow(S.u_off, want, u, 8, st));
+    DCK(grow(S.u_n, want, u, 4, st));
+    DCK(grow(S.u_head, want, u, 4, st));
+    DCK(grow(S.c_n, want, u, 4, st));
+    DCK(grow(S.selc, want, u, 4, st));
+    DCK(grow(S.action, want, u, 32, st));
+    DCK(grow(S.poses, want, u, static_cast<size_t>(n) * 24, st));
+    DCK(grow(S.anc, want, u, kMaxTreeDepth * 4, st));
+    // log table: index visits + virtual visits <= nodes + n_envs
+    const size_t lt = want + static_cast<size_t>(S.n_envs) + 2;
+    std::vector<double> tab(lt);
+    for (size_t k = 0; k < lt; ++k) tab[k] = std::log(static_cast<double>(k));
+    DCK(S.logtab.ensure(lt * 8));
+    DCK(cudaMemcpyAsync(S.logtab.p, tab.data(), lt * 8, cudaMemcpyHostToDevice, st));
+    DCK(cudaStreamSynchronize(st));
+    S.cap_nodes = nodes;
+    S.release_graph();
+  }
+  if (actions > S.cap_actions) {
+    DCK(grow(S.apool, static_cast<size_t>(actions), static_cast<size_t>(used_actions), 32, st));
+    DCK(grow(S.cpool, static_cast<size_t>(actions), static_cast<size_t>(used_actions), 4, st));
+    S.cap_actions = actions;
+    S.release_graph();
+  }
+  return PPG_SUCCESS;
+}
+
+// Per-search batch + lockstep buffers (sized by n_envs).
+int dt_batch(ppg_ctx* ctx, DTreeState& S) {
+  const int E = S.n_envs, n = S.n, na = S.na;
+  DCK(S.sel_node.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.sel_act.ensure(static_cast<size_t>(E) * 8));
+  DCK(S.gp.ensure(static_cast<size_t>(E) * n * 24));
+  DCK(S.ga.ensure(static_cast<size_t>(E) * 32));
+  DCK(S.cp.ensure(static_cast<size_t>(E) * n * 24));
+  DCK(S.st.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.gr.ensure(static_cast<size_t>(E)));
+  DCK(S.nu.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.un.ensure(static_cast<size_t>(E) * n * na * 32));
+  DCK(S.meta.ensure(static_cast<size_t>(E) * 12));
+  DCK(S.sc.ensure(sizeof(DTScal)));
+  DCK(S.l_node.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_pushes.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_done.ensure(E));
+  DCK(S.l_byg.ensure(E));
+  DCK(S.l_harv.ensure(E));
+  DCK(S.l_flag.ensure(E));
+  DCK(S.l_reward.ensure(static_cast<size_t>(E) * 8));
+  DCK(S.l_poses.ensure(static_cast<size_t>(E) * n * 24));
+  DCK(S.l_mt.ensure(static_cast<size_t>(E) * 312 * 8));
+  DCK(S.l_mtidx.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_W.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_rew.ensure(static_cast<size_t>(E) * 8));
+  DCK(S.l_active.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_nactive.ensure(16));
+  DCK(S.l_counters.ensure(32));
+  DCK(S.l_push.ensure(static_cast<size_t>(E) * 32));
+  DCK(S.l_status.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_stepping.ensure(static_cast<size_t>(E) * 4 + 16));
+  DCK(ctx->b_counter.ensure(16));  // launch_disc's work counter (no allocation during capture)
+  return PPG_SUCCESS;
+}
+
+void dt_views(ppg_ctx* ctx, DTreeState& S) {
+  DTree& t = S.t;
+  t.parent = S.parent.as<int32_t>();
+  t.depth = S.depth.as<int32_t>();
+  t.q = S.q.as<double>();
+  t.visits = S.visits.as<long long>();
+  t.vv = S.vv.as<int32_t>();
+  t.flags = S.flags.as<uint8_t>();
+  t.u_off = S.u_off.as<long long>();
+  t.u_n = S.u_n.as<int32_t>();
+  t.u_head = S.u_head.as<int32_t>();
+  t.c_n = S.c_n.as<int32_t>();
+  t.selc = S.selc.as<int32_t>();
+  t.action = S.action.as<double>();
+  t.poses = S.poses.as<double>();
+  t.anc = S.anc.as<int32_t>();
+  t.apool = S.apool.as<double>();
+  t.cpool = S.cpool.as<int32_t>();
+  t.sel_node = S.sel_node.as<int32_t>();
+  t.sel_act = S.sel_act.as<long long>();
+  t.gp = S.gp.as<double>();
+  t.ga = S.ga.as<double>();
+  t.cp = S.cp.as<double>();
+  t.st = S.st.as<int32_t>();
+  t.gr = S.gr.as<uint8_t>();
+  t.nu = S.nu.as<int32_t>();
+  t.un = S.un.as<double>();
+  t.meta = S.meta.as<int32_t>();
+  t.rew = S.l_rew.as<unsigned long long>();
+  t.logtab = S.logtab.as<double>();
+  t.sc = S.sc.as<DTScal>();
+  const ppg_params& p = ctx->params;
+  t.n_envs = S.n_envs;
+  t.n = S.n;
+  t.na = S.na;
+  t.leaf_parallel = p.leaf_parallel;
+  t.max_iters = p.budget_iterations ? static_cast<int>(p.max_iterations) : 0;
+  t.c_explore = p.c_explore;
+
+  LockArgs& a = S.la;
+  a = LockArgs{};
+  a.S = ctx->scene;
+  a.node_poses = t.cp;
+  a.node_meta = t.meta;
+  a.n_nodes = S.n_envs;
+  a.used = S.n_envs;
+  a.used_global = S.n_envs;
+  a.env_lo = 0;
+  a.leaf_parallel = p.leaf_parallel;
+  a.cap = 0;
+  a.seed = p.rng_seed;
+  a.iteration = 0;
+  a.env_node = S.l_node.as<int32_t>();
+  a.env_pushes = S.l_pushes.as<int32_t>();
+  a.env_done = S.l_done.as<uint8_t>();
+  a.env_bygrasp = S.l_byg.as<uint8_t>();
+  a.env_harvested = S.l_harv.as<uint8_t>();
+  a.env_flag = S.l_flag.as<uint8_t>();
+  a.env_reward = S.l_reward.as<double>();
+  a.env_poses = S.l_poses.as<double>();
+  a.env_push = S.l_push.as<double>();
+  a.env_status = S.l_status.as<int32_t>();
+  a.n_stepping = S.l_stepping.as<int32_t>();
+  a.stepping = S.l_stepping.as<int32_t>() + 4;
+  a.mt = S.l_mt.as<uint64_t>();
+  a.mt_idx = S.l_mtidx.as<int32_t>();
+  a.E = S.n_envs;
+  a.W = S.l_W.as<int32_t>();
+  a.rew = S.l_rew.as<unsigned long long>();
+  a.active = S.l_active.as<int32_t>();
+  a.n_active = S.l_nactive.as<int32_t>();
+  a.counters = S.l_counters.as<long long>();
+  a.dyn = t.sc->lock_dyn;
+  S.lra = ResolveArgs{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, S.n_envs};
+  S.lra.idx = a.stepping;
+  S.lra.E_dev = a.n_stepping;
+  S.C = make_const(ctx->params, S.n, ctx->side, ctx->margin);
+}
+
+// One lockstep round (captured into the WHILE body).
+int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, bool warp, bool disc) {
+  const int E = S.n_envs, n = S.n;
+  const int g = (E + kBlock - 1) / kBlock;
+  if (warp) {
+    PPG_WARP_LAUNCH(lock_step_warp_kernel, n, E, st, S.C, S.la);
+  } else if (disc) {
+    lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(S.C, S.la);
+    DCK(cudaGetLastError());
+    const int rc = launch_disc(ctx, S.C, S.lra, n, E, st);
+    if (rc != PPG_SUCCESS) return rc;
+    lock_post_kernel<<<g, kBlock, smem_for(n), st>>>(S.C, S.la);
+  } else {
+    lock_step_kernel<<<g, kBlock, smem_for(n), st>>>(S.C, S.la);
+  }
+  DCK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
+// Captures one PMBS iteration as a graph (select -> expand -> attach ->
+// lockstep WHILE -> backprop -> stop).
+int dt_capture(ppg_ctx* ctx, DTreeState& S) {
+  cudaStream_t st = ctx->stream;
+  const int E = S.n_envs, n = S.n;
+  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E);
+  const bool disc = !warp && use_disc(ctx, ctx->scene_all_discs, n);
+  const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
+  if (!S.st2) DCK(cudaStreamCreateWithFlags(&S.st2, cudaStreamNonBlocking));
+  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  DCK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphConditionalHandle cond;
+  DCK(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
+  S.la.cond = cond;
+  const DTree& t = S.t;
+  dt_select_kernel<<<1, 32, 0, st>>>(t);
+  dt_gather_kernel<<<gg, 256, 0, st>>>(t, disc);
+  {
+    ExpandArgs a{ctx->scene, t.gp, t.ga, t.cp, t.st, t.gr, t.nu, t.un, E};
+    a.P_dev = &t.sc->n_pairs;
+    if (warp) {
+      PPG_WARP_LAUNCH(expand_warp_kernel, n, E, st, S.C, a);
+    } else if (disc) {
+      ResolveArgs ra{ctx->scene, t.cp, t.ga, t.cp, t.st, nullptr, nullptr, E};
+      ra.E_dev = &t.sc->n_pairs;
+      const int rc = launch_disc(ctx, S.C, ra, n, E, st);
+      if (rc != PPG_SUCCESS) return rc;
+      expand_post_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(S.C, a);
+    } else {
+      expand_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(S.C, a);
+    }
+    DCK(cudaGetLastError());
+  }
+  dt_attach_kernel<<<1, 1024, 0, st>>>(t);
+  dt_recount_kernel<<<1, 1024, 0, st>>>(t);
+  dt_copy_kernel<<<gg, 256, 0, st>>>(t);
+  lock_init_kernel<<<(E + 255) / 256, 256, 0, st>>>(S.C, S.la);
+  lock_harvest_kernel<<<1, 1024, 0, st>>>(S.C, S.la);
+  DCK(cudaGetLastError());
+  // lockstep rounds: WHILE (n_active > 0) { round; harvest }
+  DCK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = cond;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  DCK(cudaGraphAddNode(&wnode, g, deps, nd, &cp));
+  DCK(cudaStreamUpdateCaptureDependencies(st, &wnode, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  DCK(cudaStreamBeginCaptureToGraph(S.st2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  int rc = dt_round(ctx, S, S.st2, warp, disc);
+  lock_harvest_kernel<<<1, 1024, 0, S.st2>>>(S.C, S.la);
+  cudaGraph_t body_out = nullptr;
+  const cudaError_t e2 = cudaStreamEndCapture(S.st2, &body_out);
+  if (rc != PPG_SUCCESS) return rc;
+  DCK(e2);
+  dt_backprop_kernel<<<1, 32, 0, st>>>(t);
+  dt_stop_kernel<<<1, 1, 0, st>>>(t);
+  DCK(cudaGetLastError());
+  DCK(cudaStreamEndCapture(st, &S.graph));
+  DCK(cudaGraphInstantiate(&S.exec, S.graph, 0));
+  return PPG_SUCCESS;
+}
+
+// Debug path (PPG_DTREE_DEBUG=1): the same iteration launched kernel by
+// kernel with a synchronize + error check after each, the lockstep loop
+// driven from the host.
+int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
+  cudaStream_t st = ctx->stream;
+  const int E = S.n_envs, n = S.n;
+  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E);
+  const bool disc = !warp && use_disc(ctx, ctx->scene_all_discs, n);
+  const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
+  const DTree& t = S.t;
+  S.la.cond = 0;
+#define DSTEP(name, launch)                                                              \
+  do {                                                                                   \
+    launch;                                                                              \
+    cudaError_t e_ = cudaStreamSynchronize(st);                                          \
+    if (e_ == cudaSuccess) e_ = cudaGetLastError();                                      \
+    if (e_ != cudaSuccess) {                                                             \
+      ctx->err = std::string("dtree debug: ") + name + ": " + cudaGetErrorString(e_);    \
+      return PPG_ECUDA;                                                                  \
+    }                                                                                    \
+  } while (0)
+  DSTEP("select", (dt_select_kernel<<<1, 32, 0, st>>>(t)));
+  DSTEP("gather", (dt_gather_kernel<<<gg, 256, 0, st>>>(t, disc)));
+  {
+    ExpandArgs a{ctx->scene, t.gp, t.ga, t.cp, t.st, t.gr, t.nu, t.un, E};
+    a.P_dev = &t.sc->n_pairs;
+    if (warp) {
+      DSTEP("expand_warp", PPG_WARP_LAUNCH(expand_warp_kernel, n, E, st, S.C, a));
+    } else if (disc) {
+      ResolveArgs ra{ctx->scene, t.cp, t.ga, t.cp, t.st, nullptr, nullptr, E};
+      ra.E_dev = &t.sc->n_pairs;
+      DSTEP("expand_disc", launch_disc(ctx, S.C, ra, n, E, st));
+      DSTEP("expand_post", (expand_post_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(S.C, a)));
+    } else {
+      DSTEP("expand", (expand_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(S.C, a)));
+    }
+  }
+  DSTEP("attach", (dt_attach_kernel<<<1, 1024, 0, st>>>(t)));
+  DSTEP("recount", (dt_recount_kernel<<<1, 1024, 0, st>>>(t)));
+  DSTEP("copy", (dt_copy_kernel<<<gg, 256, 0, st>>>(t)));
+  DSTEP("lock_init", (lock_init_kernel<<<(E + 255) / 256, 256, 0, st>>>(S.C, S.la)));
+  for (;;) {
+    DSTEP("harvest", (lock_harvest_kernel<<<1, 1024, 0, st>>>(S.C, S.la)));
+    int act = 0;
+    DCK(cudaMemcpy(&act, S.la.n_active, 4, cudaMemcpyDeviceToHost));
+    if (act == 0) break;
+    DSTEP("round", dt_round(ctx, S, st, warp, disc));
+  }
+  DSTEP("backprop", (dt_backprop_kernel<<<1, 32, 0, st>>>(t)));
+  DSTEP("stop", (dt_stop_kernel<<<1, 1, 0, st>>>(t)));
+#undef DSTEP
+  return PPG_SUCCESS;
+}
+
+std::string signature(const std::vector<int32_t>& depth, const std::vector<double>& action,
+                      const std::vector<long long>& visits, const std::vector<double>& q,
+                      const std::vector<uint8_t>& flags, const std::vector<long long>& u_off,
+                      const std::vector<int32_t>& c_n, const std::vector<int32_t>& cpool) {
+  // pre-order, children in insertion order (mcts.cpp:284-300)
+  std::string out;
+  std::vector<std::pair<int, int>> stack{{0, -1}};
+  char buf[256];
+  while (!stack.empty()) {
+    auto& [x, k] = stack.back();
+    if (k < 0) {
+      std::snprintf(buf, sizeof buf, "%d|%.17g,%.17g,%.17g,%.17g|%ld|%.17g|%c%c\n", depth[x], action[x * 4],
+                    action[x * 4 + 1], action[x * 4 + 2], action[x * 4 + 3], static_cast<long>(visits[x]), q[x],
+                    (flags[x] & 1) ? 'g' : '.', (flags[x] & 2) ? 'd' : '.');
+      out += buf;
+      k = 0;
+    }
+    if (k < c_n[x]) {
+      const int ch = cpool[u_off[x] + k];
+      ++k;
+      stack.push_back({ch, -1});
+    } else {
+      stack.pop_back();
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats,
+                        char* sig_buf, int64_t sig_cap, int64_t* sig_len) {
+  if (!ctx || !root_poses || !action_out) return PPG_EINVAL;
+  if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
+  }
+  const auto t_start = std::chrono::steady_clock::now();
+  const auto elapsed = [&t_start] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  const ppg_params& p = ctx->params;
+  if (p.n_envs < 1) {
+    ctx->err = "n_envs must be >= 1";
+    return PPG_EINVAL;
+  }
+  if (p.tree_depth + 1 >= kMaxTreeDepth || p.tree_depth + p.rollout_depth + 1 >= kMaxGammaPow) {
+    ctx->err = "device tree: tree_depth too large";
+    return PPG_EINVAL;
+  }
+  DCK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int n = ctx->scene.n, na = p.pushes_per_object;
+  // root: sample_pushes + graspable (SearchTree::create, mcts.cpp:28-39)
+  std::vector<double> root_untried(static_cast<size_t>(n) * na * 4);
+  int32_t cnt = 0;
+  int rc = ppg_sample_pushes(ctx, nullptr, root_poses, 1, root_untried.data(), &cnt);
+  if (rc != PPG_SUCCESS) return rc;
+  uint8_t rg = 0;
+  rc = ppg_graspable(ctx, root_poses, 1, &rg, nullptr, nullptr, nullptr, nullptr);
+  if (rc != PPG_SUCCESS) return rc;
+  if (cnt == 0) {
+    ctx->err = "no legal push action at the root";
+    return PPG_ENOLEGAL;
+  }
+  if (!ctx->dtree) ctx->dtree = new DTreeState;
+  DTreeState& S = *ctx->dtree;
+  {
+    // everything baked into the captured graph: parameters, scene tables
+    std::string key(reinterpret_cast<const char*>(&p), sizeof p);
+    key.append(reinterpret_cast<const char*>(&ctx->scene), sizeof ctx->scene);
+    key.append(reinterpret_cast<const char*>(&ctx->side), sizeof ctx->side);
+    key.append(reinterpret_cast<const char*>(&ctx->margin), sizeof ctx->margin);
+    if (S.key != key) S.release_graph();
+    S.key = key;
+  }
+  if (S.n != n) {  // per-node pose rows change size: start the tree buffers afresh
+    DevBuf* node_bufs[] = {&S.parent, &S.depth, &S.q, &S.visits, &S.vv, &S.flags, &S.u_off, &S.u_n, &S.u_head,
+                           &S.c_n, &S.selc, &S.action, &S.poses, &S.anc, &S.apool, &S.cpool};
+    DCK(cudaStreamSynchronize(st));
+    for (DevBuf* b : node_bufs) b->release();
+    S.cap_nodes = 0;
+    S.cap_actions = 0;
+    S.release_graph();
+  }
+  S.n_envs = p.n_envs;
+  S.n = n;
+  S.na = na;
+  const long long per_iter_actions = static_cast<long long>(p.n_envs) * n * na;
+  if (S.logtab.cap < (static_cast<size_t>(S.cap_nodes) + p.n_envs + 2) * 8) {  // log table covers visits + n_envs
+    S.cap_nodes = 0;  // forces dt_reserve to re-grow (contents preserved up to used = 0: fresh search)
+  }
+  {
+    int want = 1 + p.n_envs * (p.budget_iterations ? std::min<long long>(p.max_iterations, 64) : 8);
+    if (const char* cn = std::getenv("PPG_DTREE_NODES")) want = std::max(want, std::atoi(cn));
+    want = std::max(want, 1 + 2 * p.n_envs);
+    if ((rc = dt_reserve(ctx, S, 0, 0, want, static_cast<long long>(want) * n * na)) != PPG_SUCCESS) return rc;
+  }
+  if ((rc = dt_batch(ctx, S)) != PPG_SUCCESS) return rc;
+  dt_views(ctx, S);
+  // root node + scalars
+  {
+    const int32_t zero = 0, m1 = -1;
+    const long long zl = 0;
+    const double zd = 0.0;
+    const uint8_t rf = static_cast<uint8_t>(rg ? 1 : 0);  // dead needs untried.empty(): cnt > 0 here
+    DCK(cudaMemcpyAsync(S.t.parent, &m1, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.depth, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.q, &zd, 8, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.visits, &zl, 8, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.vv, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.flags, &rf, 1, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.u_off, &zl, 8, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.u_n, &cnt, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.u_head, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.c_n, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.selc, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemsetAsync(S.t.action, 0, 32, st));
+    DCK(cudaMemcpyAsync(S.t.poses, root_poses, static_cast<size_t>(n) * 24, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.anc, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.apool, root_untried.data(), static_cast<size_t>(cnt) * 32, cudaMemcpyHostToDevice, st));
+    DTScal h;
+    std::memset(&h, 0, sizeof h);
+    h.n_nodes = 1;
+    h.dT = p.tree_depth;
+    h.dS = p.rollout_depth;
+    h.es_level = 1;
+    h.min_grasp_depth = INT_MAX;
+    h.levels = 1;
+    h.stop = -1;
+    h.a_used = cnt;
+    h.unsettled[0] = rg ? 0 : 1;  // root: non-terminal with untried actions unless graspable
+    DCK(cudaMemcpyAsync(S.t.sc, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemsetAsync(S.la.counters, 0, 32, st));
+  }
+  DTScal h;
+  std::memset(&h, 0, sizeof h);
+  int stop = -1;
+  const char* dbg = std::getenv("PPG_DTREE_DEBUG");
+  const bool debug = dbg && dbg[0] == '1';
+  const bool gdebug = dbg && dbg[0] == '2';  // graph mode, synchronize + check every launch
+  bool regrown = false;
+  const auto t_loop = std::chrono::steady_clock::now();
+  for (;;) {
+    // capacity for one more iteration (the host learns the sizes after each)
+    {
+      const int prev_it = h.iteration, prev_nodes = h.n_nodes;
+      cudaError_t e = cudaMemcpyAsync(&h, S.t.sc, sizeof h, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) {
+        char m[256];
+        std::snprintf(m, sizeof m, "dtree: iteration after %d (nodes %d, cap %d, regrown %d): %s", prev_it,
+                      prev_nodes, S.cap_nodes, regrown ? 1 : 0, cudaGetErrorString(e));
+        ctx->err = m;
+        return PPG_ECUDA;
+      }
+    }
+    if (h.err[0]) {
+      char m[256];
+      std::snprintf(m, sizeof m, "dtree: corrupt ancestor row: node %d depth %d ancestor %d (iteration %d, nodes %d)",
+                    h.err[1], h.err[2], h.err[3], h.iteration, h.n_nodes);
+      ctx->err = m;
+      return PPG_EINVAL;
+    }
+    if (h.stop >= 0) {
+      stop = h.stop;
+      break;
+    }
+    if (!p.budget_iterations && h.iteration > 0 && elapsed() >= p.max_seconds) {
+      stop = 0;
+      break;
+    }
+    if (h.n_nodes + p.n_envs > S.cap_nodes || h.a_used + per_iter_actions > S.cap_actions) {
+      const int want = std::max(2 * S.cap_nodes, h.n_nodes + p.n_envs);
+      const long long wa = std::max(2 * S.cap_actions, h.a_used + per_iter_actions);
+      if ((rc = dt_reserve(ctx, S, h.n_nodes, h.a_used, want, wa)) != PPG_SUCCESS) return rc;
+      dt_views(ctx, S);
+      regrown = true;
+    }
+    if (debug) {
+      if ((rc = dt_iteration_debug(ctx, S)) != PPG_SUCCESS) return rc;
+      continue;
+    }
+    if (!S.exec && (rc = dt_capture(ctx, S)) != PPG_SUCCESS) {
+      cudaStreamCaptureStatus cs;
+      if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t junk;
+        cudaStreamEndCapture(st, &junk);
+        if (junk) cudaGraphDestroy(junk);
+      }
+      cudaGetLastError();
+      S.release_graph();
+      return rc;
+    }
+    DCK(cudaGraphLaunch(S.exec, st));
+    if (gdebug) {
+      const cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) {
+        char m[256];
+        std::snprintf(m, sizeof m, "dtree graph debug: iteration %d (nodes %d, cap %d, regrown %d): %s", h.iteration,
+                      h.n_nodes, S.cap_nodes, regrown ? 1 : 0, cudaGetErrorString(e));
+        ctx->err = m;
+        return PPG_ECUDA;
+      }
+    }
+  }
+  const double loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_loop).count();
+  if (stop == 3) {
+    ctx->err = "device tree: selection invariant violated";
+    return PPG_EINVAL;
+  }
+  // read the tree back once
+  const int N = h.n_nodes;
+  std::vector<int32_t> depth(N), c_n(N), parent(N);
+  std::vector<double> q(N), action(static_cast<size_t>(N) * 4);
+  std::vector<long long> visits(N), u_off(N);
+  std::vector<uint8_t> flags(N);
+  std::vector<int32_t> cpool(static_cast<size_t>(h.a_used));
+  int64_t ctr[4];
+  DCK(cudaMemcpyAsync(depth.data(), S.t.depth, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(c_n.data(), S.t.c_n, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(q.data(), S.t.q, N * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(action.data(), S.t.action, N * 32ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(visits.data(), S.t.visits, N * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(u_off.data(), S.t.u_off, N * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(flags.data(), S.t.flags, N, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(cpool.data(), S.t.cpool, static_cast<size_t>(h.a_used) * 4, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(ctr, S.la.counters, 32, cudaMemcpyDeviceToHost, st));
+  DCK(cudaStreamSynchronize(st));
+  // best_root_child (mcts.cpp:218-235)
+  int best = -1;
+  double best_score = -std::numeric_limits<double>::infinity();
+  long long best_visits = -1;
+  for (int k = 0; k < c_n[0]; ++k) {
+    const int ch = cpool[u_off[0] + k];
+    if (visits[ch] == 0) continue;
+    const double score = p.rank_by_ucb ? ucb_score_host(q[ch], static_cast<long>(visits[ch]), static_cast<long>(visits[0]),
+                                                        p.c_explore)
+                                       : q[ch] / static_cast<double>(visits[ch]);
+    if (score > best_score || (score == best_score && visits[ch] > best_visits)) {
+      best_score = score;
+      best_visits = visits[ch];
+      best = ch;
+    }
+  }
+  if (best < 0) {
+    ctx->err = "search produced no evaluated root child";
+    return PPG_EINVAL;
+  }
+  std::memcpy(action_out, &action[static_cast<size_t>(best) * 4], 32);
+  const std::string sig = signature(depth, action, visits, q, flags, u_off, c_n, cpool);
+  if (stats) {
+    ppg_search_stats s;
+    std::memset(&s, 0, sizeof s);
+    s.iterations = h.iteration;
+    s.expansions = h.expansions;
+    s.elapsed_s = elapsed();
+    s.stop_reason = stop;
+    s.final_tree_depth = h.dT;
+    s.env_steps = ctr[3] + h.expansions;
+    s.rollout_steps = ctr[0];
+    s.lockstep_rounds = ctr[1];
+    s.signature_fnv = fnv1a(sig);
+    s.n_nodes = N;
+    s.simulate_s = loop_s;  // one graph per iteration: the phases are not timed separately
+    *stats = s;
+  }
+  if (sig_len) *sig_len = static_cast<int64_t>(sig.size());
+  if (sig_buf && sig_cap > 0) {
+    const size_t m = sig.size() < static_cast<size_t>(sig_cap - 1) ? sig.size() : static_cast<size_t>(sig_cap - 1);
+    std::memcpy(sig_buf, sig.data(), m);
+    sig_buf[m] = '\0';
+  }
+  return PPG_SUCCESS;
+}
+
+}  // extern "C"

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(128) grasp_kernel(const __grid_constant__ SimC
 __global__ void __launch_bounds__(128) expand_kernel(const __grid_constant__ SimConst C, ExpandArgs a) {
   extern __shared__ double smem[];
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.P) return;
+  if (p >= (a.P_dev ? *a.P_dev : a.P)) return;
   const int n = C.n;
   const double* parent = a.parent_poses + static_cast<size_t>(p) * n * 3;
   const ShapeView S = a.S.view(0);
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(128) expand_kernel(const __grid_constant__ Sim
 __global__ void __launch_bounds__(128) expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a) {
   extern __shared__ double smem[];
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.P) return;
+  if (p >= (a.P_dev ? *a.P_dev : a.P)) return;
   const int n = C.n;
   double* child = a.child_poses + static_cast<size_t>(p) * n * 3;
   if (a.status[p] != 0) {  // dead child: copy of the parent state (mcts.cpp:89-92)
@@ -214,6 +214,7 @@ PPG_DI void cursor_init(const SimConst& C, const LockArgs& a, int e, int node) {
 }
 
 __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < a.n_nodes) a.rew[e] = 0ull;
   if (e >= a.used) return;
@@ -306,6 +307,7 @@ __global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockAr
 // node on ties), then W[best] += cap - depth(best).  This reproduces the
 // reference's O(E*N*E) rescan exactly in O(E + repurposes * N / 32).
 __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
   const int tid = threadIdx.x;
   const int B = blockDim.x;
   __shared__ int s_active;
@@ -386,6 +388,8 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     *a.n_active = s_active;
     a.counters[2] += s_rep;
     if (s_active > 0) a.counters[1] += 1;
+    // device tree graph: the lockstep WHILE node runs another round iff envs remain
+    if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), s_active > 0 ? 1u : 0u);
   }
 }
 
@@ -439,6 +443,7 @@ PPG_DI void rollout_finish_step(const PoseView& P, const ShapeView& S, const Sim
 // RolloutCursor::step (mcts.cpp:142-171) for each active env, all in one lane
 // (polygon scenes and n > 16).
 __global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
   extern __shared__ double smem[];
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_act = *a.n_active;
@@ -471,6 +476,7 @@ __global__ void __launch_bounds__(128) lock_step_kernel(const __grid_constant__ 
 // with a legal push are appended to the `stepping` list for the physics
 // kernel (resolve_disc_kernel with env-slot indirection, in place).
 __global__ void __launch_bounds__(128) lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
   extern __shared__ double smem[];
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_act = *a.n_active;
@@ -497,6 +503,7 @@ __global__ void __launch_bounds__(128) lock_sample_kernel(const __grid_constant_
 // Disc scenes, phase 3: the rest of RolloutCursor::step for the envs the
 // physics kernel resolved.
 __global__ void __launch_bounds__(128) lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
   extern __shared__ double smem[];
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_st = *a.n_stepping;

@@ -57,6 +57,7 @@ struct ExpandArgs {
   int32_t* n_untried;          // [P]
   double* untried;             // [P][n*na][4]
   int P;
+  const int* P_dev = nullptr;  // optional device-side count (overrides P; device tree)
 };
 
 // Lockstep engine state (pmbs.cpp:133-205), all in HBM.
@@ -100,6 +101,21 @@ struct LockArgs {
   int32_t* active;           // [used]
   int32_t* n_active;         // [1]
   long long* counters;       // [4] steps, rounds, repurposes, resolve calls
+  // device tree (dtree.cu): per-iteration values read on the device, so one
+  // captured graph serves every PMBS iteration
+  const int32_t* dyn = nullptr;        // [4] n_nodes, used, depth cap, iteration (overrides)
+  unsigned long long cond = 0;         // graph WHILE handle: harvest sets it to (n_active > 0)
 };
+
+// Applies the device-side per-iteration overrides (device tree mode).
+__device__ __forceinline__ void lock_dyn(LockArgs& a) {
+  if (a.dyn) {
+    a.n_nodes = a.dyn[0];
+    a.used = a.dyn[1];
+    a.used_global = a.dyn[1];
+    a.cap = a.dyn[2];
+    a.iteration = static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[3]));
+  }
+}
 
 }  // namespace ppg

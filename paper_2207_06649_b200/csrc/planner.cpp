@@ -360,14 +360,24 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
 
 extern "C" {
 
+// AUTO: the device tree unless a simulate hook (sharded driver) is installed.
+static bool use_device_tree(const ppg_ctx* ctx) {
+  const int mode = ppg::ctx_planner(ctx);
+  if (mode == PPG_PLANNER_HOST) return false;
+  if (mode == PPG_PLANNER_DEVICE) return true;
+  return ppg::ctx_sim_hook(ctx).fn == nullptr;
+}
+
 int ppg_run_pmbs(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats) {
   if (!ctx || !root_poses || !action_out) return PPG_EINVAL;
+  if (use_device_tree(ctx)) return ppg_run_pmbs_device(ctx, root_poses, action_out, stats, nullptr, 0, nullptr);
   return run(ctx, root_poses, action_out, stats, nullptr);
 }
 
 int ppg_run_pmbs_sig(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats,
                      char* sig_buf, int64_t sig_cap, int64_t* sig_len) {
   if (!ctx || !root_poses || !action_out) return PPG_EINVAL;
+  if (use_device_tree(ctx)) return ppg_run_pmbs_device(ctx, root_poses, action_out, stats, sig_buf, sig_cap, sig_len);
   std::string s;
   const int rc = run(ctx, root_poses, action_out, stats, &s);
   if (rc != PPG_SUCCESS) return rc;

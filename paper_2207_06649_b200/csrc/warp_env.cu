@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
   build_pairs(pij, C.n);
   const int wib = threadIdx.x >> 5;
   const int p = blockIdx.x * kWarpsPerBlock + wib;
-  if (p >= a.P) return;
+  if (p >= (a.P_dev ? *a.P_dev : a.P)) return;
   const int n = C.n, l = threadIdx.x & 31;
   WarpEnv W(blk[wib], n, l);
   const ShapeView S = a.S.view(0);
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
 template <int NW>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(const __grid_constant__ SimConst C,
                                                                             LockArgs a) {
+  lock_dyn(a);
   __shared__ double blk[kWarpsPerBlock][160];
   __shared__ unsigned valid[kWarpsPerBlock][32];
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];

@@ -1,0 +1,75 @@
+"""Device-resident PMBS tree (csrc/dtree.cu): one CUDA-graph
+launch per PMBS iteration (selection with virtual visits, expansion +
+attach, lockstep rollouts under a conditional WHILE node, backprop).  It must
+reproduce the reference decision, tree signature and statistics exactly —
+the same bar as the host tree (planner.cpp), which is run beside it."""
+import pytest
+
+import golden_io
+from paper_2207_06649_b200 import Budget, ParallelConfig, run_pmbs
+from paper_2207_06649_b200.scenes import generate_case
+
+pytestmark = pytest.mark.gpu
+
+
+def _both(ctx, st, cfg):
+    out = {}
+    for mode in ("host", "device"):
+        ctx.set_planner(mode)
+        out[mode] = run_pmbs(st, cfg, ctx=ctx, want_signature=True)
+    ctx.set_planner("auto")
+    return out["host"], out["device"]
+
+
+def _same(h, d):
+    assert d.signature == h.signature
+    assert list(d.action) == list(h.action)
+    assert (d.iterations, d.expansions, d.stop_reason, d.final_tree_depth, d.n_nodes) == \
+        (h.iterations, h.expansions, h.stop_reason, h.final_tree_depth, h.n_nodes)
+    assert (d.env_steps, d.rollout_steps, d.lockstep_rounds) == (h.env_steps, h.rollout_steps, h.lockstep_rounds)
+
+
+@pytest.mark.parametrize("idx", list(range(20)))
+def test_device_tree_first_decisions(ctx, idx):
+    """All 20 proj/cases first decisions (N_e = 64): device tree == host tree
+    == the reference fingerprint."""
+    c, st = golden_io.cases()[idx]
+    d = c["decision"]
+    h, dv = _both(ctx, st, ParallelConfig(rng_seed=int(c["seed"])))
+    _same(h, dv)
+    assert dv.signature_fnv == int(d["sig_fnv"]) and list(dv.action) == d["action"]
+
+
+@pytest.mark.parametrize("n_envs,iters,leaf", [(1, 60, False), (7, 25, True), (300, 6, True), (300, 6, False),
+                                               (5000, 3, True)])
+def test_device_tree_budgets_and_widths(ctx, n_envs, iters, leaf):
+    """Iteration budgets, narrow / wide batches (capacity growth, the lane-
+    per-env kernels past the latency-mode limit) and no leaf parallelism."""
+    c, st = golden_io.cases()[17]
+    cfg = ParallelConfig(rng_seed=11, n_envs=n_envs, leaf_parallel=leaf, budget=Budget.iterations(iters))
+    h, dv = _both(ctx, st, cfg)
+    _same(h, dv)
+
+
+@pytest.mark.parametrize("seed", [3, 8])
+def test_device_tree_dense_deep(ctx, seed):
+    """C4-like: dense ring motif (16 discs), deeper tree, wider action set."""
+    st = generate_case(16, 0.0, seed, "ring")
+    cfg = ParallelConfig(rng_seed=seed, n_envs=256, tree_depth=9, pushes_per_object=24,
+                         budget=Budget.iterations(8))
+    h, dv = _both(ctx, st, cfg)
+    _same(h, dv)
+
+
+def test_device_tree_acceptance_c1(ctx):
+    """Reference acceptance C1 (N_e = 1, no leaf parallelism == serial MCTS)
+    through the device tree, on the first 6 deep cases."""
+    ctx.set_planner("device")
+    try:
+        for rec, st in golden_io.acceptance()["c1"][:6]:
+            cfg = ParallelConfig(budget=Budget.iterations(500), rng_seed=rec["seed"], n_envs=1, leaf_parallel=False)
+            r = run_pmbs(st, cfg, ctx=ctx)
+            assert r.signature_fnv == int(rec["sig_fnv"]), rec["seed"]
+            assert list(r.action) == rec["action"] and r.iterations == rec["iterations"]
+    finally:
+        ctx.set_planner("auto")
