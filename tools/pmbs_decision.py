@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--tree-depth", type=int, default=7)
     ap.add_argument("--repeat", type=int, default=2)
+    ap.add_argument("--planner", default="auto", choices=["auto", "host", "device"])
     args = ap.parse_args()
 
     import torch
@@ -57,6 +58,7 @@ def main():
         seed = int(c["seed"])
         name = args.case
     ctx = Context(local)
+    ctx.set_planner(args.planner)
     cfg = ParallelConfig(rng_seed=seed, n_envs=args.n_envs, tree_depth=args.tree_depth,
                          budget=Budget.iterations(args.iters))
     ctx.set_params(cfg.to_params())
@@ -77,7 +79,7 @@ def main():
     if hook and hook.error:
         raise hook.error
     if rank == 0:
-        print(json.dumps({"scene": name, "n_gpus": world, "n_envs": args.n_envs, "iterations": r.iterations,
+        print(json.dumps({"scene": name, "planner": args.planner, "n_gpus": world, "n_envs": args.n_envs, "iterations": r.iterations,
                           "expansions": r.expansions, "stop": r.stop_reason, "env_steps": r.env_steps,
                           "lockstep_rounds": r.lockstep_rounds, "s_per_decision": best,
                           "env_steps_per_s": r.env_steps / best, "action": list(r.action),
