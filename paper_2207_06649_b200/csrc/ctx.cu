@@ -233,6 +233,8 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
     ctx->force_generic = fg && fg[0] == '1';
     const char* wm = std::getenv("PPG_WARP_MAX");
     if (wm) ctx->warp_max_envs = std::atoi(wm);
+    const char* wp = std::getenv("PPG_WARP_POLY");
+    if (wp) ctx->warp_poly = wp[0] != '0';
     const char* pl = std::getenv("PPG_PLANNER");
     if (pl) ctx->planner = !std::strcmp(pl, "host") ? PPG_PLANNER_HOST : !std::strcmp(pl, "device") ? PPG_PLANNER_DEVICE : 0;
     const char* bo = std::getenv("PPG_DISC_BLOCKS_PER_SM");
@@ -335,7 +337,8 @@ bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
 
 // Latency mode: one warp per environment (warp_env.cu) for small batches.
 bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs) {
-  return all_discs && n <= kWarpMaxN && envs <= ctx->warp_max_envs && !ctx->force_generic;
+  const bool shape_ok = all_discs ? n <= kWarpMaxN : (ctx->warp_poly && n <= kPolyMaxN);
+  return shape_ok && envs <= ctx->warp_max_envs && !ctx->force_generic;
 }
 
 // Kernel #1 dispatch: all-disc batches (shapes without vertex tables) run the
@@ -347,7 +350,7 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
   if (!d_counts && use_warp(ctx, all_discs, S.n, E)) {
-    PPG_WARP_LAUNCH(resolve_warp_kernel, S.n, E, st, C, a);
+    PPG_WARP_LAUNCH(resolve_warp_kernel, !all_discs, S.n, E, st, C, a);
     CK(cudaGetLastError());
     return PPG_SUCCESS;
   }
@@ -536,7 +539,7 @@ int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, 
   ExpandArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_push.as<double>(), ctx->b_out.as<double>(),
                ctx->b_status.as<int32_t>(), ctx->b_a.as<uint8_t>(), ctx->b_e.as<int32_t>(), ctx->b_b.as<double>(), P};
   if (use_warp(ctx, ctx->scene_all_discs, n, P)) {
-    PPG_WARP_LAUNCH(expand_warp_kernel, n, P, st, C, a);
+    PPG_WARP_LAUNCH(expand_warp_kernel, !ctx->scene_all_discs, n, P, st, C, a);
   } else if (use_disc(ctx, ctx->scene_all_discs, n)) {
     // child = parent, resolve in place on the register-resident kernel, then
     // sample + grasp (or restore the parent for a failed simulation)
@@ -657,7 +660,7 @@ static int lock_round(ppg_ctx* ctx, int act) {
   const int n = ctx->scene.n;
   const int g = (act + kBlock - 1) / kBlock;
   if (use_warp(ctx, ctx->scene_all_discs, n, act)) {
-    PPG_WARP_LAUNCH(lock_step_warp_kernel, n, act, st, C, a);
+    PPG_WARP_LAUNCH(lock_step_warp_kernel, !ctx->scene_all_discs, n, act, st, C, a);
     CK(cudaGetLastError());
   } else if (use_disc(ctx, ctx->scene_all_discs, n)) {  // sample+pick -> physics (in place) -> grasp + reward
     lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);

@@ -25,25 +25,35 @@ __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
-template <int NW>
+template <int NW, bool kPoly>
 __global__ void resolve_warp_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
-template <int NW>
+template <int NW, bool kPoly>
 __global__ void expand_warp_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
-template <int NW>
+template <int NW, bool kPoly>
 __global__ void lock_step_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
 constexpr int kWarpMaxN = 23;
+constexpr int kPolyMaxN = 16;  // warp_poly.cuh
 constexpr int kWarpsPerBlock = 4;
 // pair-mask words of the latency-mode kernels (warp_env.cuh warp_words_for)
 constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 : 8; }
-// Launches KERNEL<NW> (one warp per item, `items` items) for n objects.
-#define PPG_WARP_LAUNCH(KERNEL, n, items, st, ...)                                          \
+// Launches KERNEL<NW, poly> (one warp per item, `items` items) for n objects;
+// poly: the scene has polygons (warp_poly.cuh, n <= kPolyMaxN).
+#define PPG_WARP_LAUNCH(KERNEL, poly, n, items, st, ...)                                    \
   do {                                                                                      \
     const int g_ = ((items) + kWarpsPerBlock - 1) / kWarpsPerBlock;                         \
-    switch (warp_words(n)) {                                                                \
-      case 1: KERNEL<1><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
-      case 2: KERNEL<2><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
-      case 4: KERNEL<4><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;            \
-      default: KERNEL<8><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__); break;           \
+    const int w_ = warp_words(n);                                                           \
+    if (poly) {                                                                             \
+      if (w_ == 1) KERNEL<1, true><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__);        \
+      else if (w_ == 2) KERNEL<2, true><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__);   \
+      else KERNEL<4, true><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__);                \
+    } else if (w_ == 1) {                                                                   \
+      KERNEL<1, false><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__);                    \
+    } else if (w_ == 2) {                                                                   \
+      KERNEL<2, false><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__);                    \
+    } else if (w_ == 4) {                                                                   \
+      KERNEL<4, false><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__);                    \
+    } else {                                                                                \
+      KERNEL<8, false><<<g_, kWarpsPerBlock * 32, 0, st>>>(__VA_ARGS__);                    \
     }                                                                                       \
   } while (0)
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
@@ -143,7 +153,8 @@ struct ppg_ctx {
   int disc_bps_override = 0;              // PPG_DISC_BLOCKS_PER_SM: cap resident blocks (experiments)
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
-  int warp_max_envs = 4096;               // latency mode (one warp per env) up to this many envs; PPG_WARP_MAX
+  int warp_max_envs = 4096;
+  bool warp_poly = true;                  // polygon scenes in latency mode; PPG_WARP_POLY=0 disables               // latency mode (one warp per env) up to this many envs; PPG_WARP_MAX
 };
 
 SimConst make_const(const ppg_params& p, int n, double side, double margin);

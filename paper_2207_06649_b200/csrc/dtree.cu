@@ -663,7 +663,7 @@ int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, bool warp, bool disc)
   const int E = S.n_envs, n = S.n;
   const int g = (E + kBlock - 1) / kBlock;
   if (warp) {
-    PPG_WARP_LAUNCH(lock_step_warp_kernel, n, E, st, S.C, S.la);
+    PPG_WARP_LAUNCH(lock_step_warp_kernel, !ctx->scene_all_discs, n, E, st, S.C, S.la);
   } else if (disc) {
     lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(S.C, S.la);
     DCK(cudaGetLastError());
@@ -702,7 +702,7 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
     ExpandArgs a{ctx->scene, t.gp, t.ga, t.cp, t.st, t.gr, t.nu, t.un, E};
     a.P_dev = &t.sc->n_pairs;
     if (warp) {
-      PPG_WARP_LAUNCH(expand_warp_kernel, n, E, st, S.C, a);
+      PPG_WARP_LAUNCH(expand_warp_kernel, !ctx->scene_all_discs, n, E, st, S.C, a);
     } else if (disc) {
       ResolveArgs ra{ctx->scene, t.cp, t.ga, t.cp, t.st, nullptr, nullptr, E};
       ra.E_dev = &t.sc->n_pairs;
@@ -773,7 +773,7 @@ int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
     ExpandArgs a{ctx->scene, t.gp, t.ga, t.cp, t.st, t.gr, t.nu, t.un, E};
     a.P_dev = &t.sc->n_pairs;
     if (warp) {
-      DSTEP("expand_warp", PPG_WARP_LAUNCH(expand_warp_kernel, n, E, st, S.C, a));
+      DSTEP("expand_warp", PPG_WARP_LAUNCH(expand_warp_kernel, !ctx->scene_all_discs, n, E, st, S.C, a));
     } else if (disc) {
       ResolveArgs ra{ctx->scene, t.cp, t.ga, t.cp, t.st, nullptr, nullptr, E};
       ra.E_dev = &t.sc->n_pairs;

@@ -30,16 +30,46 @@
 #include <cuda_runtime.h>
 
 #include "warp_env.cuh"
+#include "warp_poly.cuh"
 
 namespace ppg {
 
 // ---------------------------------------------------------------------------
 
 // batch_resolve, one warp per environment (small batches).
-template <int NW>
+// Polygon caches of the latency-mode kernels (kPoly instantiations only).
+#define PPG_POLY_SMEM                                      \
+  __shared__ V2 poly_wv[kPoly ? kWarpsPerBlock : 1][kPoly ? kPolyMaxN * kMaxV : 1]; \
+  __shared__ V2 poly_cen[kPoly ? kWarpsPerBlock : 1][kPoly ? kPolyMaxN : 1];
+
+// resolve with the variant for the scene's object kinds (warp_poly.cuh for
+// scenes with polygons)
+template <int NW, bool kPoly>
+PPG_DI int warp_resolve_any(WarpEnv& W, const WarpPoly& G, const PolyShape& O, const ShapeView& S, const SimConst& C,
+                            const uint16_t* pij, V2 start, V2 end, bool check_start, double* residual) {
+  if constexpr (kPoly) {
+    return warp_resolve_poly<NW>(W, G, O, S, C, pij, start, end, check_start, residual);
+  } else {
+    return warp_resolve<NW>(W, C, pij, start, end, check_start, residual);
+  }
+}
+
+// Pose load of the latency-mode kernels: for polygon scenes also the trig
+// planes and the world-polygon caches, which the sampler / graspable helpers
+// (world_polygon on the PoseView) and warp_resolve_poly read.
+template <bool kPoly>
+PPG_DI PolyShape warp_load_any(WarpEnv& W, const WarpPoly& G, const double* poses, const ShapeView& S) {
+  warp_load(W, poses, S);
+  PolyShape O{0, 0, 0.0, 0.0};
+  if constexpr (kPoly) O = warp_poly_load(W, G, S);
+  return O;
+}
+
+template <int NW, bool kPoly>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) resolve_warp_kernel(const __grid_constant__ SimConst C,
                                                                           ResolveArgs a) {
   __shared__ double blk[kWarpsPerBlock][160];
+  PPG_POLY_SMEM
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
   build_pairs(pij, C.n);
   const int wib = threadIdx.x >> 5;
@@ -50,10 +80,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) resolve_warp_kernel(const
   WarpEnv W(blk[wib], C.n, static_cast<int>(threadIdx.x & 31));
   const ShapeView S = a.S.view(a.S.T == 1 ? 0 : ee);
   const int n = C.n;
-  warp_load(W, a.poses_in + static_cast<size_t>(ee) * n * 3, S);
+  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  const PolyShape O = warp_load_any<kPoly>(W, G, a.poses_in + static_cast<size_t>(ee) * n * 3, S);
   const double* pu = a.pushes + static_cast<size_t>(ee) * 4;
   double residual = 0.0;
-  const int st = warp_resolve<NW>(W, C, pij, V2{pu[0], pu[1]}, V2{pu[2], pu[3]}, true, &residual);
+  const int st = warp_resolve_any<NW, kPoly>(W, G, O, S, C, pij, V2{pu[0], pu[1]}, V2{pu[2], pu[3]}, true,
+                                             &residual);
   if (W.lane == 0) {
     a.status[ee] = st;
     if (a.residual) a.residual[ee] = residual;
@@ -67,10 +99,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) resolve_warp_kernel(const
 }
 
 // batch_expand prepare (pmbs.cpp:82-93), one warp per (node, action) pair.
-template <int NW>
+template <int NW, bool kPoly>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const __grid_constant__ SimConst C,
                                                                          ExpandArgs a) {
   __shared__ double blk[kWarpsPerBlock][160];
+  PPG_POLY_SMEM
   __shared__ unsigned valid[kWarpsPerBlock][32];
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
   build_pairs(pij, C.n);
@@ -81,10 +114,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
   WarpEnv W(blk[wib], n, l);
   const ShapeView S = a.S.view(0);
   const double* parent = a.parent_poses + static_cast<size_t>(p) * n * 3;
-  warp_load(W, parent, S);
+  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  const PolyShape O = warp_load_any<kPoly>(W, G, parent, S);
   const double* act = a.actions + static_cast<size_t>(p) * 4;
   double residual;
-  const int st = warp_resolve<NW>(W, C, pij, V2{act[0], act[1]}, V2{act[2], act[3]}, true, &residual);
+  const int st = warp_resolve_any<NW, kPoly>(W, G, O, S, C, pij, V2{act[0], act[1]}, V2{act[2], act[3]}, true,
+                                             &residual);
   double* child = a.child_poses + static_cast<size_t>(p) * n * 3;
   if (l == 0) a.status[p] = st;
   if (st != 0) {  // dead child: copy of the parent state (mcts.cpp:89-92)
@@ -125,9 +160,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
 }
 
 // RolloutCursor::step (mcts.cpp:142-171), one warp per active environment.
-template <int NW>
+template <int NW, bool kPoly>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(const __grid_constant__ SimConst C,
                                                                             LockArgs a) {
+  PPG_POLY_SMEM
   lock_dyn(a);
   __shared__ double blk[kWarpsPerBlock][160];
   __shared__ unsigned valid[kWarpsPerBlock][32];
@@ -141,7 +177,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(con
   WarpEnv W(blk[wib], n, l);
   const ShapeView S = a.S.view(0);
   double* env = a.env_poses + static_cast<size_t>(e) * n * 3;
-  warp_load(W, env, S);
+  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  const PolyShape O = warp_load_any<kPoly>(W, G, env, S);
   if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
   const int count = warp_sample_mask(W, S, C, valid[wib]);
   if (count == 0) {  // no legal push: reward 0 (mcts.cpp:146-150)
@@ -165,7 +202,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(con
   push_candidate(W.view(), S, C, c / C.na, c % C.na, false, s, t);
   if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), 1ull);
   double residual;
-  const int st = warp_resolve<NW>(W, C, pij, s, t, false, &residual);
+  const int st = warp_resolve_any<NW, kPoly>(W, G, O, S, C, pij, s, t, false, &residual);
   if (st != 0) {  // SimError: reward 0 (mcts.cpp:153-158)
     if (l == 0) {
       a.env_done[e] = 1;
@@ -189,14 +226,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(con
   warp_store(W, env);
 }
 
-#define PPG_WARP_INST(NW)                                                                           \
-  template __global__ void resolve_warp_kernel<NW>(const __grid_constant__ SimConst, ResolveArgs);  \
-  template __global__ void expand_warp_kernel<NW>(const __grid_constant__ SimConst, ExpandArgs);    \
-  template __global__ void lock_step_warp_kernel<NW>(const __grid_constant__ SimConst, LockArgs);
-PPG_WARP_INST(1)
-PPG_WARP_INST(2)
-PPG_WARP_INST(4)
-PPG_WARP_INST(8)
+#define PPG_WARP_INST(NW, P)                                                                            \
+  template __global__ void resolve_warp_kernel<NW, P>(const __grid_constant__ SimConst, ResolveArgs);  \
+  template __global__ void expand_warp_kernel<NW, P>(const __grid_constant__ SimConst, ExpandArgs);    \
+  template __global__ void lock_step_warp_kernel<NW, P>(const __grid_constant__ SimConst, LockArgs);
+PPG_WARP_INST(1, false)
+PPG_WARP_INST(2, false)
+PPG_WARP_INST(4, false)
+PPG_WARP_INST(8, false)
+PPG_WARP_INST(1, true)
+PPG_WARP_INST(2, true)
+PPG_WARP_INST(4, true)
 #undef PPG_WARP_INST
 
 }  // namespace ppg

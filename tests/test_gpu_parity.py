@@ -350,3 +350,60 @@ def test_device_sincos_matches_glibc(ctx):
         hs[i], hc[i] = a.value, b.value
     bad = np.nonzero((s.view(np.uint64) != hs.view(np.uint64)) | (c.view(np.uint64) != hc.view(np.uint64)))[0]
     assert len(bad) == 0, [(float(x[i]), float(s[i]), float(hs[i]), float(c[i]), float(hc[i])) for i in bad[:5]]
+
+
+@pytest.mark.parametrize("n,pf,motif", [(3, 1.0, "random"), (6, 0.5, "random"), (9, 0.35, "random"),
+                                        (10, 1.0, "random"), (12, 0.5, "wall"), (16, 0.35, "ring"),
+                                        (16, 1.0, "random")])
+def test_polygon_latency_mode_matches_generic_and_oracle(ctx, n, pf, motif):
+    """warp_poly.cuh (one warp per env, SAT axes / closest-point edges /
+    vertex updates spread over lanes, cached world polygons) against the
+    straight one-lane transcription and the CPU oracle, bitwise, on every
+    sampled push of several polygon scenes plus start-collision pushes."""
+    from paper_2207_06649_b200.scenes import _take, generate_cases
+    t, poses, ok = generate_cases(n, np.arange(7000, 7030), pf, motif)
+    sel = np.nonzero(ok)[0][:10]
+    if len(sel) == 0:
+        pytest.skip("generator rejected every seed")
+    t, poses = _take(t, sel), poses[sel]
+    ctx.set_params(P)
+    cand, cnt = ctx.sample_pushes_arrays(poses, t)
+    idx = np.concatenate([np.full(c, k) for k, c in enumerate(cnt)]).astype(np.int64)
+    pushes = np.concatenate([cand[k, :c] for k, c in enumerate(cnt)])
+    bad = np.stack([[p[0, 0], p[0, 1], p[0, 0] + 0.05, p[0, 1]] for p in poses])
+    idx = np.concatenate([idx, np.arange(len(poses))])
+    pushes = np.concatenate([pushes, bad])
+    tt = _take(t, idx)
+    pp = np.ascontiguousarray(poses[idx])
+    o3, s3, r3 = port.batch_resolve(tt, pp, pushes, P)
+    for mode, env in [("warp", {}), ("generic", {"PPG_FORCE_GENERIC": 1})]:
+        c = _ctx_with(**env)
+        out, st, res = c.batch_resolve_arrays(tt, pp, pushes)
+        c.close()
+        assert np.array_equal(st, s3), mode
+        assert _bitwise(out, o3).all(), mode
+        assert np.array_equal(res.view(np.uint64), r3.view(np.uint64)), mode
+
+
+@pytest.mark.parametrize("mode", ["warp", "generic"])
+def test_polygon_golden_resolve_set_all_modes(mode):
+    c = _ctx_with(**({"PPG_FORCE_GENERIC": 1} if mode == "generic" else {}))
+    t, poses, pushes, status, digests, out_ref = golden_io.resolve_set("polygons")
+    out, st, resid = c.batch_resolve_arrays(t, poses, pushes)
+    assert np.array_equal(st, status)
+    ok = status == 0
+    assert _bitwise(out[ok], out_ref[ok]).all()
+    c.close()
+
+
+@pytest.mark.parametrize("idx", [8, 9, 15, 16])
+def test_polygon_fingerprints_generic_vs_latency(idx):
+    """The polygon proj/cases first decisions with the polygon latency mode
+    switched off (PPG_WARP_POLY=0 -> one-lane kernels) match the fingerprint
+    too, so both paths are pinned to the reference tree."""
+    c = _ctx_with(PPG_WARP_POLY=0)
+    cc, st = golden_io.cases()[idx]
+    d = cc["decision"]
+    r = run_pmbs(st, ParallelConfig(rng_seed=int(cc["seed"])), ctx=c)
+    assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
+    c.close()
