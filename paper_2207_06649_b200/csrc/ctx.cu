@@ -232,7 +232,10 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
     const char* fg = std::getenv("PPG_FORCE_GENERIC");
     ctx->force_generic = fg && fg[0] == '1';
     const char* wm = std::getenv("PPG_WARP_MAX");
-    if (wm) ctx->warp_max_envs = std::atoi(wm);
+    if (wm) {
+      ctx->warp_max_envs = std::atoi(wm);
+      ctx->warp_max_explicit = true;
+    }
     const char* wp = std::getenv("PPG_WARP_POLY");
     if (wp) ctx->warp_poly = wp[0] != '0';
     const char* pl = std::getenv("PPG_PLANNER");
@@ -336,9 +339,15 @@ bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
 }
 
 // Latency mode: one warp per environment (warp_env.cu) for small batches.
+// Below the batch size where the lane-per-env disc kernel takes over (or
+// always, where the only alternative is the one-lane generic kernel: discs
+// with n > 16, polygon scenes), unless PPG_WARP_MAX caps it explicitly.
 bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs) {
+  if (ctx->force_generic) return false;
   const bool shape_ok = all_discs ? n <= kWarpMaxN : (ctx->warp_poly && n <= kPolyMaxN);
-  return shape_ok && envs <= ctx->warp_max_envs && !ctx->force_generic;
+  if (!shape_ok) return false;
+  if (ctx->warp_max_explicit || (all_discs && n <= 16 && ctx->disc_kernels)) return envs <= ctx->warp_max_envs;
+  return true;
 }
 
 // Kernel #1 dispatch: all-disc batches (shapes without vertex tables) run the
