@@ -233,7 +233,66 @@ def pmbs_decisions(ctx, with_reference: bool):
                 row["reference_s"] = time.perf_counter() - t0
                 row["same_decision"] = bool(list(q["action"]) == list(r.action) and q["sig_fnv"] == r.signature_fnv)
         out[f"n_envs_{ne}"] = row
+    out["c4"] = c4_decision(ctx, with_reference)
+    out["c3"] = c3_episodes(ctx, with_reference)
     return out
+
+
+def c4_decision(ctx, with_reference: bool):
+    """BASELINE config 4: a dense 18-disc ring motif (generate_case_motif(Ring,
+    18), seed 19), d_T = 9, N_a = 24, N_e = 4096, iteration budget 10 — GPU
+    (device tree) vs the reference run_pmbs with WorkerPool(nproc)."""
+    from paper_2207_06649_b200 import Budget, ParallelConfig, run_pmbs
+    from paper_2207_06649_b200.scenes import generate_case
+    st = generate_case(18, 0.0, 19, "ring")
+    cfg = ParallelConfig(rng_seed=19, n_envs=4096, tree_depth=9, pushes_per_object=24,
+                         budget=Budget.iterations(10))
+    run_pmbs(st, cfg, ctx=ctx)
+    t0 = time.perf_counter()
+    r = run_pmbs(st, cfg, ctx=ctx)
+    row = {"scene": "ring18 seed 19", "n_envs": 4096, "tree_depth": 9, "pushes_per_object": 24,
+           "gpu_s": time.perf_counter() - t0, "iterations": r.iterations, "env_steps": r.env_steps}
+    if with_reference:
+        from oracle import ref
+        if ref.available():
+            t0 = time.perf_counter()
+            q = ref.run_search(st, cfg.to_params(), threads=os.cpu_count() or 1)
+            row["reference_s"] = time.perf_counter() - t0
+            row["same_decision"] = bool(list(q["action"]) == list(r.action) and q["sig_fnv"] == r.signature_fnv)
+    return row
+
+
+def c3_episodes(ctx, with_reference: bool):
+    """BASELINE config 3: full object-retrieval episodes (bench::run_episode)
+    on the 11 ten-object proj/cases scenes, trial 0, N_e = 1000 (the paper's
+    setting), default budget — mean s/decision on the GPU vs the reference
+    run_episode with WorkerPool(nproc); outcomes compared episode by episode."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_io
+    from paper_2207_06649_b200 import ParallelConfig
+    from paper_2207_06649_b200.episode import episode_seed, run_episode
+    cases = {c["case_id"]: st for c, st in golden_io.cases()}
+    ids = ["case_03", "case_07", "case_08", "case_10", "case_12", "case_15", "case_16", "case_17", "case_18",
+           "case_19", "case_20"]
+    gpu_t = gpu_d = ref_t = ref_d = 0.0
+    same = True
+    for cid in ids:
+        cfg = ParallelConfig(n_envs=1000)
+        seed = episode_seed(0, cid, 0)
+        r = run_episode(cases[cid], cid, 0, cfg, seed, ctx=ctx)
+        gpu_t += r.planning_time_s
+        gpu_d += r.decisions
+        if with_reference:
+            from oracle import ref
+            if ref.available():
+                q = ref.run_episode(cases[cid], cid, 0, cfg.to_params(), threads=os.cpu_count() or 1)
+                ref_t += q["planning_s"]
+                ref_d += r.decisions  # same outcome => the same decisions (checked below)
+                same = same and q["actions_used"] == r.actions_used and q["completed"] == r.completed
+    row = {"cases": len(ids), "n_envs": 1000, "decisions": int(gpu_d), "gpu_s_per_decision": gpu_t / max(1, gpu_d)}
+    if ref_d:
+        row.update({"reference_s_per_decision": ref_t / ref_d, "same_outcomes": bool(same)})
+    return row
 
 
 def run_ours(args, world, rank, local):

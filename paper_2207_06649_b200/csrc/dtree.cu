@@ -58,7 +58,11 @@ struct DTScal {
   int stop;             // -1 running, 0 budget, 1 explored, 2 early stop, 3 internal error
   int iteration;
   int recompute;        // d_T shrank this iteration: recount the selectable children
-  int lock_dyn[4];      // LockArgs.dyn: n_nodes, used envs, depth cap, iteration
+  int lock_dyn[6];      // LockArgs.dyn: n_nodes, used envs, depth cap, iteration, seed lo / hi
+  int max_iters;        // iteration budget (0: seconds budget, checked by the host)
+  double c_explore;     // UCB exploration constant
+  // (the per-search values live here, not in the captured kernel arguments,
+  // so one captured graph serves every search with the same shapes)
   long long a_used;     // action-pool entries in use
   long long expansions;
   int unsettled[kMaxTreeDepth];  // non-terminal nodes with untried actions, per depth
@@ -97,8 +101,7 @@ struct DTree {
   const unsigned long long* rew;  // lockstep per-new-node max reward bits
   const double* logtab;           // logtab[k] == glibc log((double)k)
   DTScal* sc;
-  int n_envs, n, na, leaf_parallel, max_iters;
-  double c_explore;
+  int n_envs, n, na, leaf_parallel;
 };
 
 namespace {
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
   DTScal* sc = t.sc;
   const int l = threadIdx.x;
   const int dT = sc->dT;
+  const double cexp = sc->c_explore;
   int draws = 0;
   bool bad = false;
   if (sc->stop < 0) {
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
           double s = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
           if (nci != 0) {
             const double nc = static_cast<double>(nci);
-            s = t.q[ch] / nc + t.c_explore * sqrt(2.0 * lg / nc);
+            s = t.q[ch] / nc + cexp * sqrt(2.0 * lg / nc);
           }
           if (s > bs) {
             bs = s;
@@ -397,7 +401,7 @@ __global__ void dt_stop_kernel(DTree t) {
   sc->expansions += P;
   if (sc->stop >= 0) return;
   if (sc->min_grasp_depth <= sc->es_level) sc->stop = 2;
-  else if (t.max_iters > 0 && sc->iteration >= t.max_iters) sc->stop = 0;
+  else if (sc->max_iters > 0 && sc->iteration >= sc->max_iters) sc->stop = 0;
 }
 
 }  // namespace
@@ -615,8 +619,6 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
   t.n = S.n;
   t.na = S.na;
   t.leaf_parallel = p.leaf_parallel;
-  t.max_iters = p.budget_iterations ? static_cast<int>(p.max_iterations) : 0;
-  t.c_explore = p.c_explore;
 
   LockArgs& a = S.la;
   a = LockArgs{};
@@ -870,11 +872,22 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
   if (!ctx->dtree) ctx->dtree = new DTreeState;
   DTreeState& S = *ctx->dtree;
   {
-    // everything baked into the captured graph: parameters, scene tables
-    std::string key(reinterpret_cast<const char*>(&p), sizeof p);
+    // everything baked into the captured graph: parameters (minus the
+    // per-search values kept in DTScal), scene tables
+    ppg_params kp = p;
+    kp.rng_seed = 0;
+    kp.c_explore = 0.0;
+    kp.budget_iterations = 0;
+    kp.max_iterations = 0;
+    kp.max_seconds = 0.0;
+    std::string key(reinterpret_cast<const char*>(&kp), sizeof kp);
     key.append(reinterpret_cast<const char*>(&ctx->scene), sizeof ctx->scene);
     key.append(reinterpret_cast<const char*>(&ctx->side), sizeof ctx->side);
     key.append(reinterpret_cast<const char*>(&ctx->margin), sizeof ctx->margin);
+    // kernel-mode inputs (which kernels the graph holds)
+    const int modes[6] = {ctx->scene_all_discs ? 1 : 0, ctx->force_generic ? 1 : 0, ctx->warp_poly ? 1 : 0,
+                          ctx->warp_max_envs, ctx->warp_max_explicit ? 1 : 0, ctx->disc_kernels ? 1 : 0};
+    key.append(reinterpret_cast<const char*>(modes), sizeof modes);
     if (S.key != key) S.release_graph();
     S.key = key;
   }
@@ -934,6 +947,10 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     h.stop = -1;
     h.a_used = cnt;
     h.unsettled[0] = rg ? 0 : 1;  // root: non-terminal with untried actions unless graspable
+    h.max_iters = p.budget_iterations ? static_cast<int>(p.max_iterations) : 0;
+    h.c_explore = p.c_explore;
+    h.lock_dyn[4] = static_cast<int>(static_cast<uint32_t>(p.rng_seed));
+    h.lock_dyn[5] = static_cast<int>(static_cast<uint32_t>(p.rng_seed >> 32));
     DCK(cudaMemcpyAsync(S.t.sc, &h, sizeof h, cudaMemcpyHostToDevice, st));
     DCK(cudaMemsetAsync(S.la.counters, 0, 32, st));
   }

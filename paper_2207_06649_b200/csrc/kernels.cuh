@@ -103,7 +103,7 @@ struct LockArgs {
   long long* counters;       // [4] steps, rounds, repurposes, resolve calls
   // device tree (dtree.cu): per-iteration values read on the device, so one
   // captured graph serves every PMBS iteration
-  const int32_t* dyn = nullptr;        // [4] n_nodes, used, depth cap, iteration (overrides)
+  const int32_t* dyn = nullptr;        // [6] n_nodes, used, depth cap, iteration, seed lo, seed hi (overrides)
   unsigned long long cond = 0;         // graph WHILE handle: harvest sets it to (n_active > 0)
 };
 
@@ -115,6 +115,8 @@ __device__ __forceinline__ void lock_dyn(LockArgs& a) {
     a.used_global = a.dyn[1];
     a.cap = a.dyn[2];
     a.iteration = static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[3]));
+    a.seed = static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[4])) |
+             static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[5])) << 32;
   }
 }
 
