@@ -264,6 +264,11 @@ void ppg_destroy(ppg_ctx* ctx) {
                     &ctx->l_nmeta, &ctx->b_counter, &ctx->l_push, &ctx->l_status, &ctx->l_stepping, &ctx->l_rec};
   for (DevBuf* b : bufs) b->release();
   dtree_release(ctx);
+  for (int k = 0; k < kChunks; ++k) {
+    ctx->chunk_in[k].release();
+    ctx->chunk_buf[k].release();
+    if (ctx->chunk_stream[k]) cudaStreamDestroy(ctx->chunk_stream[k]);
+  }
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -306,9 +311,10 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
 // as a persistent grid sized for `work` environments.  The work counter
 // (ctx->b_counter) is zeroed here unless the caller's graph zeroes it.
 int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st,
-                bool zero_counter) {
-  CK(ctx->b_counter.ensure(16));
-  if (zero_counter) CK(cudaMemsetAsync(ctx->b_counter.p, 0, 4, st));
+                bool zero_counter, int slot_counter) {
+  CK(ctx->b_counter.ensure(64));
+  int* counter = ctx->b_counter.as<int>() + 4 * slot_counter;  // one counter per concurrent launch
+  if (zero_counter) CK(cudaMemsetAsync(counter, 0, 4, st));
   int slot = 0;
   while (kDiscSizes[slot] < n) ++slot;
   const int nmax = kDiscSizes[slot];
@@ -318,7 +324,6 @@ int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, in
                       : ctx->disc_blocks_per_sm[slot];
   const int cap = bps * ctx->num_sms;
   const int grid = want < 1 ? 1 : (want < cap ? want : cap);
-  int* counter = ctx->b_counter.as<int>();
   const size_t sm = disc_smem(nmax);
   switch (nmax) {
     case 4: resolve_disc_kernel<4><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
@@ -355,7 +360,7 @@ bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs) {
 // count; polygons, n > 16 and the counting variant run the generic kernel.
 static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, double side, double margin,
                           const double* d_in, const double* d_push, int E, double* d_out, int32_t* d_status,
-                          double* d_resid, long long* d_counts, cudaStream_t st) {
+                          double* d_resid, long long* d_counts, cudaStream_t st, int slot = 0) {
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
   if (!d_counts && use_warp(ctx, all_discs, S.n, E)) {
@@ -363,7 +368,7 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
     CK(cudaGetLastError());
     return PPG_SUCCESS;
   }
-  if (!d_counts && use_disc(ctx, all_discs, S.n)) return launch_disc(ctx, C, a, S.n, E, st);
+  if (!d_counts && use_disc(ctx, all_discs, S.n)) return launch_disc(ctx, C, a, S.n, E, st, true, slot);
   const int grid = (E + kBlock - 1) / kBlock;
   if (d_counts) resolve_kernel<true><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
   else resolve_kernel<false><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
@@ -375,48 +380,101 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
 
 extern "C" {
 
+// Large host-buffer batches are split into kChunks slices processed on
+// separate streams, so the host<->device copies of one slice overlap the
+// physics of the others (the element-wise results are independent of the
+// split).  Below this size one launch on the context stream.
+constexpr int kPipelineMinEnvs = 32768;
+
+static int batch_resolve_chunk(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in,
+                               const double* pushes, int e0, int e1, double* poses_out, int32_t* status,
+                               double* residual, cudaStream_t st, int slot) {
+  const int Ek = e1 - e0;
+  ShapesDev S;
+  double side, margin;
+  bool discs;
+  if (shapes) {
+    ppg_shapes sub = *shapes;
+    if (shapes->n_tables != 1) {  // this slice's tables
+      const size_t n = static_cast<size_t>(shapes->n_objects);
+      sub.n_tables = Ek;
+      sub.kind = shapes->kind + e0 * n;
+      sub.radius = shapes->radius + e0 * n;
+      sub.n_vertices = shapes->n_vertices ? shapes->n_vertices + e0 * n : nullptr;
+      sub.vertices = shapes->vertices ? shapes->vertices + e0 * n * kMaxV * 2 : nullptr;
+      sub.target_index = shapes->target_index + e0;
+    }
+    const int rc = upload_shapes(ctx, &sub, false, ctx->chunk_in[slot], ctx->chunk_buf[slot], S, st);
+    if (rc != PPG_SUCCESS) return rc;
+    side = shapes->side_length;
+    margin = shapes->boundary_margin;
+    discs = host_all_discs(&sub);
+  } else {
+    S = ctx->scene;
+    side = ctx->side;
+    margin = ctx->margin;
+    discs = ctx->scene_all_discs;
+  }
+  const size_t row = static_cast<size_t>(S.n) * 3;
+  double* d_in = ctx->b_in.as<double>() + e0 * row;
+  double* d_out = ctx->b_out.as<double>() + e0 * row;
+  double* d_push = ctx->b_push.as<double>() + e0 * 4ull;
+  int32_t* d_st = ctx->b_status.as<int32_t>() + e0;
+  double* d_res = ctx->b_resid.as<double>() + e0;
+  CK(cudaMemcpyAsync(d_in, poses_in + e0 * row, Ek * row * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_push, pushes + e0 * 4ull, Ek * 32ull, cudaMemcpyHostToDevice, st));
+  const int rc = launch_resolve(ctx, S, discs, side, margin, d_in, d_push, Ek, d_out, d_st, d_res, nullptr, st, slot);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(cudaMemcpyAsync(poses_out + e0 * row, d_out, Ek * row * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(status + e0, d_st, Ek * 4ull, cudaMemcpyDeviceToHost, st));
+  if (residual) CK(cudaMemcpyAsync(residual + e0, d_res, Ek * 8ull, cudaMemcpyDeviceToHost, st));
+  return PPG_SUCCESS;
+}
+
 int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in, const double* pushes,
                       int E, double* poses_out, int32_t* status, double* residual) {
   if (!ctx || E < 0) return PPG_EINVAL;
   if (E == 0) return PPG_SUCCESS;
   CK(cudaSetDevice(ctx->device));
-  cudaStream_t st = ctx->stream;
-  ShapesDev S;
-  double side, margin;
   if (shapes) {
     if (shapes->n_tables != 1 && shapes->n_tables != E) {
       ctx->err = "batch_resolve: states and shape tables must have equal length";
       return PPG_EINVAL;
     }
-    const int rc = upload_shapes(ctx, shapes, false, ctx->shape_in, ctx->shape_buf, S, st);
-    if (rc != PPG_SUCCESS) return rc;
-    side = shapes->side_length;
-    margin = shapes->boundary_margin;
-  } else {
-    if (!ctx->has_scene) {
-      ctx->err = "no scene installed";
+    if (shapes->n_objects < 1 || shapes->n_objects > kMaxObjects) {
+      ctx->err = "n_objects must be in [1, 32] and n_tables >= 1";
       return PPG_EINVAL;
     }
-    S = ctx->scene;
-    side = ctx->side;
-    margin = ctx->margin;
+  } else if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
   }
-  const size_t pbytes = static_cast<size_t>(E) * S.n * 3 * sizeof(double);
+  const int n = shapes ? shapes->n_objects : ctx->scene.n;
+  const size_t pbytes = static_cast<size_t>(E) * n * 3 * sizeof(double);
   CK(ctx->b_in.ensure(pbytes));
   CK(ctx->b_out.ensure(pbytes));
   CK(ctx->b_push.ensure(static_cast<size_t>(E) * 4 * sizeof(double)));
   CK(ctx->b_status.ensure(static_cast<size_t>(E) * sizeof(int32_t)));
   CK(ctx->b_resid.ensure(static_cast<size_t>(E) * sizeof(double)));
-  CK(cudaMemcpyAsync(ctx->b_in.p, poses_in, pbytes, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(ctx->b_push.p, pushes, static_cast<size_t>(E) * 32, cudaMemcpyHostToDevice, st));
-  const bool discs = shapes ? host_all_discs(shapes) : ctx->scene_all_discs;
-  int rc = launch_resolve(ctx, S, discs, side, margin, ctx->b_in.as<double>(), ctx->b_push.as<double>(), E,
-                          ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(), ctx->b_resid.as<double>(), nullptr, st);
-  if (rc != PPG_SUCCESS) return rc;
-  CK(cudaMemcpyAsync(poses_out, ctx->b_out.p, pbytes, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(status, ctx->b_status.p, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToHost, st));
-  if (residual) CK(cudaMemcpyAsync(residual, ctx->b_resid.p, static_cast<size_t>(E) * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK(ctx->b_counter.ensure(64));
+  const int chunks = E >= kPipelineMinEnvs ? kChunks : 1;
+  if (chunks == 1) {
+    int rc = batch_resolve_chunk(ctx, shapes, poses_in, pushes, 0, E, poses_out, status, residual, ctx->stream, 0);
+    if (rc != PPG_SUCCESS) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return PPG_SUCCESS;
+  }
+  for (int k = 0; k < chunks; ++k)
+    if (!ctx->chunk_stream[k]) CK(cudaStreamCreateWithFlags(&ctx->chunk_stream[k], cudaStreamNonBlocking));
+  CK(cudaStreamSynchronize(ctx->stream));  // earlier work on the context stream
+  for (int k = 0; k < chunks; ++k) {
+    const int e0 = static_cast<int>(static_cast<long long>(E) * k / chunks);
+    const int e1 = static_cast<int>(static_cast<long long>(E) * (k + 1) / chunks);
+    const int rc = batch_resolve_chunk(ctx, shapes, poses_in, pushes, e0, e1, poses_out, status, residual,
+                                       ctx->chunk_stream[k], k);
+    if (rc != PPG_SUCCESS) return rc;
+  }
+  for (int k = 0; k < chunks; ++k) CK(cudaStreamSynchronize(ctx->chunk_stream[k]));
   return PPG_SUCCESS;
 }
 

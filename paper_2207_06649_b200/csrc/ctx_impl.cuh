@@ -33,6 +33,7 @@ template <int NW, bool kPoly>
 __global__ void lock_step_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
 constexpr int kWarpMaxN = 23;
 constexpr int kPolyMaxN = 16;  // warp_poly.cuh
+constexpr int kChunks = 4;     // slices of a pipelined host-buffer batch_resolve
 constexpr int kWarpsPerBlock = 4;
 // pair-mask words of the latency-mode kernels (warp_env.cuh warp_words_for)
 constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 : 8; }
@@ -151,6 +152,9 @@ struct ppg_ctx {
   bool disc_kernels = false;
   bool force_generic = false;             // PPG_FORCE_GENERIC=1: A/B the generic kernel
   int disc_bps_override = 0;              // PPG_DISC_BLOCKS_PER_SM: cap resident blocks (experiments)
+  // pipelined batch_resolve (host buffers): per-slice streams and shape tables
+  cudaStream_t chunk_stream[ppg::kChunks] = {};
+  DevBuf chunk_in[ppg::kChunks], chunk_buf[ppg::kChunks];
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
   int warp_max_envs = 4096;
@@ -162,6 +166,6 @@ SimConst make_const(const ppg_params& p, int n, double side, double margin);
 size_t disc_smem(int nmax);
 size_t smem_for(int n);
 int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st,
-                bool zero_counter = true);
+                bool zero_counter = true, int slot_counter = 0);
 bool use_disc(const ppg_ctx* ctx, bool all_discs, int n);
 bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs);

@@ -407,3 +407,22 @@ def test_polygon_fingerprints_generic_vs_latency(idx):
     r = run_pmbs(st, ParallelConfig(rng_seed=int(cc["seed"])), ctx=c)
     assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
     c.close()
+
+
+def test_pipelined_host_batch_resolve(ctx):
+    """ppg_batch_resolve with host buffers at E >= 32K runs as 4 slices on
+    separate streams (copies overlap physics); results are element-wise, so
+    they must equal the oracle bit for bit (checked on a 4K subsample spread
+    over all slices) and be identical run to run."""
+    from paper_2207_06649_b200.scenes import _take, c2_workload
+    ctx.set_params(P)
+    table, poses, pushes, _ = c2_workload(ctx, 40000)
+    out, st, res = ctx.batch_resolve_arrays(table, poses, pushes)
+    out2, st2, res2 = ctx.batch_resolve_arrays(table, poses, pushes)
+    assert _bitwise(out, out2).all() and np.array_equal(st, st2)
+    idx = np.linspace(0, 39999, 4000).astype(np.int64)
+    o3, s3, r3 = port.batch_resolve(_take(table, idx), np.ascontiguousarray(poses[idx]),
+                                    np.ascontiguousarray(pushes[idx]), P)
+    assert np.array_equal(st[idx], s3)
+    assert _bitwise(out[idx], o3).all()
+    assert np.array_equal(res[idx].view(np.uint64), r3.view(np.uint64))
