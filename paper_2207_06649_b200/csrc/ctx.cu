@@ -344,14 +344,20 @@ bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
 }
 
 // Latency mode: one warp per environment (warp_env.cu) for small batches.
-// Below the batch size where the lane-per-env disc kernel takes over (or
-// always, where the only alternative is the one-lane generic kernel: discs
-// with n > 16, polygon scenes), unless PPG_WARP_MAX caps it explicitly.
-bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs) {
+// Latency mode (one warp per env) vs the lane-per-env kernels.  For PMBS
+// work (expansion, lockstep rounds: sample + pick + resolve + graspable per
+// env-step) latency mode always wins — its sampler and graspable run across
+// the lanes, and a round costs its slowest env-step (measured: case_18 at
+// N_e = 16K, 1.02 s -> 0.44 s).  For plain batch_resolve throughput the
+// lane-per-env disc kernel wins above 4,096 envs (discs, n <= 16); scenes
+// without it (discs with n > 16, polygons) stay in latency mode.
+// PPG_WARP_MAX, if set, caps latency mode everywhere.
+bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs) {
   if (ctx->force_generic) return false;
   const bool shape_ok = all_discs ? n <= kWarpMaxN : (ctx->warp_poly && n <= kPolyMaxN);
   if (!shape_ok) return false;
-  if (ctx->warp_max_explicit || (all_discs && n <= 16 && ctx->disc_kernels)) return envs <= ctx->warp_max_envs;
+  if (ctx->warp_max_explicit) return envs <= ctx->warp_max_envs;
+  if (!pmbs && all_discs && n <= 16 && ctx->disc_kernels) return envs <= ctx->warp_max_envs;
   return true;
 }
 
@@ -363,7 +369,7 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
                           double* d_resid, long long* d_counts, cudaStream_t st, int slot = 0) {
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
-  if (!d_counts && use_warp(ctx, all_discs, S.n, E)) {
+  if (!d_counts && use_warp(ctx, all_discs, S.n, E, false)) {
     PPG_WARP_LAUNCH(resolve_warp_kernel, !all_discs, S.n, E, st, C, a);
     CK(cudaGetLastError());
     return PPG_SUCCESS;
@@ -605,7 +611,7 @@ int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, 
   const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
   ExpandArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_push.as<double>(), ctx->b_out.as<double>(),
                ctx->b_status.as<int32_t>(), ctx->b_a.as<uint8_t>(), ctx->b_e.as<int32_t>(), ctx->b_b.as<double>(), P};
-  if (use_warp(ctx, ctx->scene_all_discs, n, P)) {
+  if (use_warp(ctx, ctx->scene_all_discs, n, P, true)) {
     PPG_WARP_LAUNCH(expand_warp_kernel, !ctx->scene_all_discs, n, P, st, C, a);
   } else if (use_disc(ctx, ctx->scene_all_discs, n)) {
     // child = parent, resolve in place on the register-resident kernel, then
@@ -726,7 +732,7 @@ static int lock_round(ppg_ctx* ctx, int act) {
   LockArgs& a = ctx->la;
   const int n = ctx->scene.n;
   const int g = (act + kBlock - 1) / kBlock;
-  if (use_warp(ctx, ctx->scene_all_discs, n, act)) {
+  if (use_warp(ctx, ctx->scene_all_discs, n, act, true)) {
     PPG_WARP_LAUNCH(lock_step_warp_kernel, !ctx->scene_all_discs, n, act, st, C, a);
     CK(cudaGetLastError());
   } else if (use_disc(ctx, ctx->scene_all_discs, n)) {  // sample+pick -> physics (in place) -> grasp + reward

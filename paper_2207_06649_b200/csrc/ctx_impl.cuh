@@ -168,4 +168,4 @@ size_t smem_for(int n);
 int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st,
                 bool zero_counter = true, int slot_counter = 0);
 bool use_disc(const ppg_ctx* ctx, bool all_discs, int n);
-bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs);
+bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs);

@@ -684,7 +684,7 @@ int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, bool warp, bool disc)
 int dt_capture(ppg_ctx* ctx, DTreeState& S) {
   cudaStream_t st = ctx->stream;
   const int E = S.n_envs, n = S.n;
-  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E);
+  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E, true);
   const bool disc = !warp && use_disc(ctx, ctx->scene_all_discs, n);
   const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
   if (!S.st2) DCK(cudaStreamCreateWithFlags(&S.st2, cudaStreamNonBlocking));
@@ -754,7 +754,7 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
 int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
   cudaStream_t st = ctx->stream;
   const int E = S.n_envs, n = S.n;
-  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E);
+  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E, true);
   const bool disc = !warp && use_disc(ctx, ctx->scene_all_discs, n);
   const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
   const DTree& t = S.t;
