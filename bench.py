@@ -369,7 +369,12 @@ def run_ours(args, world, rank, local):
     launch_s = sum(step_ms) * 1e-3 / args.steps
     achieved = ops_total / launch_s
     roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
-            "frac": achieved / peak.value, "traffic": None,
+            "frac": achieved / peak.value,
+            # DRAM bytes per launch of resolve_disc_kernel<10> at E = 65,536 from one
+            # `ncu --set full` capture (dram__bytes_read.sum 23.22 MB + dram__bytes_write.sum
+            # 78 KB; profiles/README.md): the inputs read once, outputs stay in L2
+            "traffic": 23.30e6 if E == E_DEFAULT and n == 10 else None,
+            "traffic_unit": "bytes per launch (ncu)",
             "note": "algorithmic FP64 ops (+,-,*,/,sqrt = 1 each, SURVEY 8d formula, counted on this workload) per "
                     "step / step time; peak = measured DFMA instr/s (= FP64 FLOP/s / 2) on this GPU; HBM is not "
                     "the bound (" + f"{(E * (n * 3 * 8 * 2 + 32 + 4 + 8 + n * 12)) / launch_s / 1e9:.1f}" +
