@@ -135,18 +135,38 @@ __global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
         const double lg = t.logtab[t.visits[x] + t.vv[x]];  // log(n_parent)
         double bs = -INFINITY;
         int bk = INT_MAX;
-        for (int k = l; k < cn; k += 32) {
-          const int ch = t.cpool[co + k];
-          if (!dt_selectable(t, ch, dT)) continue;
-          const long long nci = t.visits[ch] + t.vv[ch];
-          double s = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
-          if (nci != 0) {
-            const double nc = static_cast<double>(nci);
-            s = t.q[ch] / nc + cexp * sqrt(2.0 * lg / nc);
+        // children k = l, l + 32, ... in chunks of kScanU per lane: all loads
+        // of a chunk are issued before any score is formed (memory-level
+        // parallelism); per lane the children stay in increasing order
+        constexpr int kScanU = 4;
+        for (int k0 = 0; k0 < cn; k0 += 32 * kScanU) {
+          int ch[kScanU];
+#pragma unroll
+          for (int u = 0; u < kScanU; ++u) {
+            const int k = k0 + 32 * u + l;
+            ch[u] = k < cn ? t.cpool[co + k] : -1;
           }
-          if (s > bs) {
-            bs = s;
-            bk = k;
+          bool sel[kScanU];
+          long long nci[kScanU];
+          double qc[kScanU];
+#pragma unroll
+          for (int u = 0; u < kScanU; ++u) {
+            sel[u] = ch[u] >= 0 && dt_selectable(t, ch[u], dT);
+            nci[u] = ch[u] >= 0 ? t.visits[ch[u]] + t.vv[ch[u]] : 0;
+            qc[u] = ch[u] >= 0 ? t.q[ch[u]] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kScanU; ++u) {
+            if (!sel[u]) continue;
+            double s = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
+            if (nci[u] != 0) {
+              const double nc = static_cast<double>(nci[u]);
+              s = qc[u] / nc + cexp * sqrt(2.0 * lg / nc);
+            }
+            if (s > bs) {
+              bs = s;
+              bk = k0 + 32 * u + l;
+            }
           }
         }
 #pragma unroll
