@@ -302,10 +302,9 @@ __global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockAr
 
 // harvest_and_repurpose (pmbs.cpp:165-187) + next round's active list.  One
 // block.  Rewards are order-free (max of non-negative doubles via their bit
-// patterns); the re-purposing decisions are sequential in env order and run
-// in warp 0: argmax of per-node remaining work W (strict >, W > 0, lowest
-// node on ties), then W[best] += cap - depth(best).  This reproduces the
-// reference's O(E*N*E) rescan exactly in O(E + repurposes * N / 32).
+// patterns); per-node remaining work W by atomics; the re-purposing target is
+// one block-wide argmax of W (see below).  This reproduces the reference's
+// O(E*N*E) sequential rescan exactly in O(E + N).
 __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
   lock_dyn(a);
   const int tid = threadIdx.x;
@@ -332,42 +331,66 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     }
   }
   __syncthreads();
-  if (a.leaf_parallel && tid < 32) {
-    const int lane = tid;
-    for (int base = 0; base < a.used; base += 32) {
-      const int e = base + lane;
-      unsigned m = __ballot_sync(0xffffffffu, e < a.used && a.env_flag[e] == 1);
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const int ce = base + src;
-        int bw = 0, bi = -1;
-        for (int i = lane; i < a.n_nodes; i += 32) {
-          const int w = a.W[i];
-          if (w > bw) {
-            bw = w;
-            bi = i;
-          }
-        }
-        for (int off = 16; off > 0; off >>= 1) {
-          const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
-            bw = ow;
-            bi = oi;
-          }
-        }
-        if (bi >= 0) {
-          if (lane == 0) {
-            a.W[bi] += a.cap - a.node_meta[bi * 3];
-            a.env_flag[ce] = 2;
-            a.env_node[ce] = bi;
-            ++s_rep;
-          }
-        }
-        __syncwarp();
+  if (a.leaf_parallel) {
+    // Re-purposing (pmbs.cpp:171-185): each by-grasp env of the pass goes to
+    // argmax_i remaining_work(i) (strict >, W > 0, lowest node on ties), and
+    // the only change to W during the pass is W[best] += the new cursor's
+    // remaining work (>= 0): best stays the argmax, so every re-purposed env
+    // of the pass goes to the SAME node, found by one block-wide argmax.
+    __shared__ int s_bw[32], s_bi[32];
+    __shared__ int s_best;
+    int bw = 0, bi = -1;
+    for (int i = tid; i < a.n_nodes; i += B) {
+      const int w = a.W[i];
+      if (w > bw) {
+        bw = w;
+        bi = i;
       }
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
+        bw = ow;
+        bi = oi;
+      }
+    }
+    if ((tid & 31) == 0) {
+      s_bw[tid >> 5] = bw;
+      s_bi[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int nw = B >> 5;
+      bw = tid < nw ? s_bw[tid] : 0;
+      bi = tid < nw ? s_bi[tid] : -1;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
+          bw = ow;
+          bi = oi;
+        }
+      }
+      if (tid == 0) s_best = bi;
+    }
+    __syncthreads();
+    const int best = s_best;
+    int rep = 0;
+    for (int e = tid; e < a.used; e += B) {
+      if (a.env_flag[e] == 1) {
+        if (best >= 0) {
+          a.env_flag[e] = 2;
+          a.env_node[e] = best;
+          ++rep;
+        } else {
+          a.env_flag[e] = 0;
+        }
+      }
+    }
+    if (rep) atomicAdd(reinterpret_cast<unsigned long long*>(&s_rep), static_cast<unsigned long long>(rep));
   }
   __syncthreads();
   for (int e = tid; e < a.used; e += B) {
