@@ -66,6 +66,7 @@ def harvest(rec: Records, W: np.ndarray, node_depth: np.ndarray, cap: int, leaf_
     round in global env order.  Updates `rewards` (max) and W in place and
     returns the re-purposing assignments (env, node)."""
     out_env, out_node = [], []
+    best = None
     for k in range(len(rec.env)):
         nd = int(rec.node[k])
         r = float(rec.reward[k])
@@ -73,7 +74,10 @@ def harvest(rec: Records, W: np.ndarray, node_depth: np.ndarray, cap: int, leaf_
             rewards[nd] = r
         if not leaf_parallel or not rec.grasp[k]:
             continue
-        best = int(np.argmax(W)) if len(W) else -1  # first maximum == lowest node on ties
+        if best is None:
+            # argmax W, first maximum == lowest node on ties.  Within a pass W
+            # only grows at the chosen node, so the target never changes.
+            best = int(np.argmax(W)) if len(W) else -1
         if best >= 0 and W[best] > 0:
             W[best] += cap - int(node_depth[best])
             out_env.append(int(rec.env[k]))
