@@ -236,6 +236,8 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
       ctx->warp_max_envs = std::atoi(wm);
       ctx->warp_max_explicit = true;
     }
+    const char* hm = std::getenv("PPG_HYBRID_MIN");
+    if (hm) ctx->hybrid_min_envs = std::atoi(hm);
     const char* wp = std::getenv("PPG_WARP_POLY");
     if (wp) ctx->warp_poly = wp[0] != '0';
     const char* pl = std::getenv("PPG_PLANNER");
@@ -359,6 +361,60 @@ bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs) {
   if (ctx->warp_max_explicit) return envs <= ctx->warp_max_envs;
   if (!pmbs && all_discs && n <= 16 && ctx->disc_kernels) return envs <= ctx->warp_max_envs;
   return true;
+}
+
+RoundMode round_mode(const ppg_ctx* ctx, int n, int envs) {
+  if (use_warp(ctx, ctx->scene_all_discs, n, envs, true)) {
+    const bool hybrid_ok = ctx->scene_all_discs && n <= 16 && ctx->disc_kernels && !ctx->warp_max_explicit;
+    return hybrid_ok && envs >= ctx->hybrid_min_envs ? RoundMode::kHybrid : RoundMode::kWarp;
+  }
+  if (use_disc(ctx, ctx->scene_all_discs, n)) return RoundMode::kLaneDisc;
+  return RoundMode::kGeneric;
+}
+
+// One lockstep round (RolloutCursor::step for every active env) over the
+// `work` envs the grids are sized for:
+//  kWarp     one warp per env: sample + pick + resolve + graspable;
+//  kHybrid   large disc batches: sample + pick one warp per env ->
+//            resolve_disc lane kernel (in place) -> graspable one warp per env;
+//  kLaneDisc the same three phases one lane per env;
+//  kAdaptive kWarp and kHybrid kernels both launched, the harvest's
+//            round_mode flag (n_active >= hybrid_min) selects one per round;
+//  kGeneric  the straight one-lane transcription.
+int lock_round_on(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const ResolveArgs& ra, int work,
+                  RoundMode mode, cudaStream_t st) {
+  const int n = ctx->scene.n;
+  const int g = (work + kBlock - 1) / kBlock;
+  const int gw = (work + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  switch (mode) {
+    case RoundMode::kWarp:
+      PPG_WARP_LAUNCH(lock_step_warp_kernel, !ctx->scene_all_discs, n, work, st, C, a);
+      break;
+    case RoundMode::kAdaptive:  // both; the harvest's round_mode flag picks (device tree)
+      PPG_WARP_LAUNCH(lock_step_warp_kernel, false, n, work, st, C, a);
+      CK(cudaGetLastError());
+      [[fallthrough]];
+    case RoundMode::kHybrid: {
+      lock_sample_warp_kernel<<<gw, kWarpsPerBlock * 32, 0, st>>>(C, a);
+      CK(cudaGetLastError());
+      const int rc = launch_disc(ctx, C, ra, n, work, st);
+      if (rc != PPG_SUCCESS) return rc;
+      lock_post_warp_kernel<<<gw, kWarpsPerBlock * 32, 0, st>>>(C, a);
+      break;
+    }
+    case RoundMode::kLaneDisc: {
+      lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+      CK(cudaGetLastError());
+      const int rc = launch_disc(ctx, C, ra, n, work, st);
+      if (rc != PPG_SUCCESS) return rc;
+      lock_post_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+      break;
+    }
+    default:
+      lock_step_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
+  }
+  CK(cudaGetLastError());
+  return PPG_SUCCESS;
 }
 
 // Kernel #1 dispatch: all-disc batches (shapes without vertex tables) run the
@@ -727,26 +783,7 @@ static int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* nod
 // latency mode (one warp per env), the 3-phase disc pipeline, or the generic
 // one-lane step.
 static int lock_round(ppg_ctx* ctx, int act) {
-  cudaStream_t st = ctx->stream;
-  const SimConst& C = ctx->lc;
-  LockArgs& a = ctx->la;
-  const int n = ctx->scene.n;
-  const int g = (act + kBlock - 1) / kBlock;
-  if (use_warp(ctx, ctx->scene_all_discs, n, act, true)) {
-    PPG_WARP_LAUNCH(lock_step_warp_kernel, !ctx->scene_all_discs, n, act, st, C, a);
-    CK(cudaGetLastError());
-  } else if (use_disc(ctx, ctx->scene_all_discs, n)) {  // sample+pick -> physics (in place) -> grasp + reward
-    lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
-    CK(cudaGetLastError());
-    const int rc = launch_disc(ctx, C, ctx->lra, n, act, st);
-    if (rc != PPG_SUCCESS) return rc;
-    lock_post_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
-    CK(cudaGetLastError());
-  } else {
-    lock_step_kernel<<<g, kBlock, smem_for(n), st>>>(C, a);
-    CK(cudaGetLastError());
-  }
-  return PPG_SUCCESS;
+  return lock_round_on(ctx, ctx->lc, ctx->la, ctx->lra, act, round_mode(ctx, ctx->scene.n, act), ctx->stream);
 }
 
 static int lock_check(ppg_ctx* ctx, int n_nodes, int n_envs, int depth_cap) {

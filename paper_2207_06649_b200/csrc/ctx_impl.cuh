@@ -58,6 +58,8 @@ constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 
     }                                                                                       \
   } while (0)
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_sample_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_post_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_report_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockArgs a, const int32_t* env,
                                       const int32_t* node, int count);
@@ -158,6 +160,8 @@ struct ppg_ctx {
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
   int warp_max_envs = 4096;
+  int hybrid_min_envs = 24576;           // lockstep rounds with >= this many active envs (discs, n <= 16)
+                                          // run the hybrid warp-sampler / lane-physics round; PPG_HYBRID_MIN
   bool warp_max_explicit = false;        // PPG_WARP_MAX given: a hard cap for every scene type
   bool warp_poly = true;                  // polygon scenes in latency mode; PPG_WARP_POLY=0 disables               // latency mode (one warp per env) up to this many envs; PPG_WARP_MAX
 };
@@ -169,3 +173,7 @@ int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, in
                 bool zero_counter = true, int slot_counter = 0);
 bool use_disc(const ppg_ctx* ctx, bool all_discs, int n);
 bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs);
+enum class RoundMode { kWarp, kHybrid, kLaneDisc, kGeneric, kAdaptive };
+RoundMode round_mode(const ppg_ctx* ctx, int n, int envs);
+int lock_round_on(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const ResolveArgs& ra, int work,
+                  RoundMode mode, cudaStream_t st);

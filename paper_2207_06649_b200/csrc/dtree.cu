@@ -67,6 +67,7 @@ struct DTScal {
   long long expansions;
   int unsettled[kMaxTreeDepth];  // non-terminal nodes with untried actions, per depth
   int err[4];                    // first invariant violation seen on the device (debug)
+  int round_mode;                // adaptive lockstep rounds (LockArgs.round_mode)
 };
 
 struct DTree {
@@ -674,6 +675,8 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
   a.n_active = S.l_nactive.as<int32_t>();
   a.counters = S.l_counters.as<long long>();
   a.dyn = t.sc->lock_dyn;
+  a.round_mode = &t.sc->round_mode;
+  a.hybrid_min = ctx->hybrid_min_envs;
   S.lra = ResolveArgs{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, S.n_envs};
   S.lra.idx = a.stepping;
   S.lra.E_dev = a.n_stepping;
@@ -681,22 +684,11 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
 }
 
 // One lockstep round (captured into the WHILE body).
-int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, bool warp, bool disc) {
-  const int E = S.n_envs, n = S.n;
-  const int g = (E + kBlock - 1) / kBlock;
-  if (warp) {
-    PPG_WARP_LAUNCH(lock_step_warp_kernel, !ctx->scene_all_discs, n, E, st, S.C, S.la);
-  } else if (disc) {
-    lock_sample_kernel<<<g, kBlock, smem_for(n), st>>>(S.C, S.la);
-    DCK(cudaGetLastError());
-    const int rc = launch_disc(ctx, S.C, S.lra, n, E, st);
-    if (rc != PPG_SUCCESS) return rc;
-    lock_post_kernel<<<g, kBlock, smem_for(n), st>>>(S.C, S.la);
-  } else {
-    lock_step_kernel<<<g, kBlock, smem_for(n), st>>>(S.C, S.la);
-  }
-  DCK(cudaGetLastError());
-  return PPG_SUCCESS;
+int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st) {
+  // hybrid-capable batches decide per round on the device (harvest flag)
+  RoundMode m = round_mode(ctx, S.n, S.n_envs);
+  if (m == RoundMode::kHybrid && ctx->hybrid_min_envs > 0) m = RoundMode::kAdaptive;
+  return lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, m, st);
 }
 
 // Captures one PMBS iteration as a graph (select -> expand -> attach ->
@@ -754,7 +746,7 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
   DCK(cudaStreamUpdateCaptureDependencies(st, &wnode, 1, cudaStreamSetCaptureDependencies));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   DCK(cudaStreamBeginCaptureToGraph(S.st2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  int rc = dt_round(ctx, S, S.st2, warp, disc);
+  int rc = dt_round(ctx, S, S.st2);
   lock_harvest_kernel<<<1, 1024, 0, S.st2>>>(S.C, S.la);
   cudaGraph_t body_out = nullptr;
   const cudaError_t e2 = cudaStreamEndCapture(S.st2, &body_out);
@@ -814,7 +806,7 @@ int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
     int act = 0;
     DCK(cudaMemcpy(&act, S.la.n_active, 4, cudaMemcpyDeviceToHost));
     if (act == 0) break;
-    DSTEP("round", dt_round(ctx, S, st, warp, disc));
+    DSTEP("round", dt_round(ctx, S, st));
   }
   DSTEP("backprop", (dt_backprop_kernel<<<1, 32, 0, st>>>(t)));
   DSTEP("stop", (dt_stop_kernel<<<1, 1, 0, st>>>(t)));
@@ -905,8 +897,9 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     key.append(reinterpret_cast<const char*>(&ctx->side), sizeof ctx->side);
     key.append(reinterpret_cast<const char*>(&ctx->margin), sizeof ctx->margin);
     // kernel-mode inputs (which kernels the graph holds)
-    const int modes[6] = {ctx->scene_all_discs ? 1 : 0, ctx->force_generic ? 1 : 0, ctx->warp_poly ? 1 : 0,
-                          ctx->warp_max_envs, ctx->warp_max_explicit ? 1 : 0, ctx->disc_kernels ? 1 : 0};
+    const int modes[7] = {ctx->scene_all_discs ? 1 : 0, ctx->force_generic ? 1 : 0, ctx->warp_poly ? 1 : 0,
+                          ctx->warp_max_envs, ctx->warp_max_explicit ? 1 : 0, ctx->disc_kernels ? 1 : 0,
+                          ctx->hybrid_min_envs};
     key.append(reinterpret_cast<const char*>(modes), sizeof modes);
     if (S.key != key) S.release_graph();
     S.key = key;

@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     *a.n_active = s_active;
     a.counters[2] += s_rep;
     if (s_active > 0) a.counters[1] += 1;
+    if (a.round_mode) *a.round_mode = s_active >= a.hybrid_min ? 1 : 0;
     // device tree graph: the lockstep WHILE node runs another round iff envs remain
     if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), s_active > 0 ? 1u : 0u);
   }

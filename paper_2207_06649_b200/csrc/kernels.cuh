@@ -105,6 +105,11 @@ struct LockArgs {
   // captured graph serves every PMBS iteration
   const int32_t* dyn = nullptr;        // [6] n_nodes, used, depth cap, iteration, seed lo, seed hi (overrides)
   unsigned long long cond = 0;         // graph WHILE handle: harvest sets it to (n_active > 0)
+  // adaptive rounds (device tree): harvest writes *round_mode = 1 (hybrid:
+  // warp sampler + lane physics) when n_active >= hybrid_min, else 0 (one
+  // warp per env); the kernels of the other mode return at once
+  int* round_mode = nullptr;
+  int hybrid_min = 0;
 };
 
 // Applies the device-side per-iteration overrides (device tree mode).

@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(con
                                                                             LockArgs a) {
   PPG_POLY_SMEM
   lock_dyn(a);
+  if (a.round_mode && *a.round_mode != 0) return;  // adaptive: a hybrid round
   __shared__ double blk[kWarpsPerBlock][160];
   __shared__ unsigned valid[kWarpsPerBlock][32];
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
@@ -224,6 +225,95 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(con
     }
   }
   warp_store(W, env);
+}
+
+// Hybrid lockstep round for large disc batches: the sampler + pick and the
+// graspable check of RolloutCursor::step (mcts.cpp:142-171) one warp per env
+// (their candidate / angle loops spread over the lanes), the physics in
+// between on the lane-per-env disc kernel (resolve_disc.cu, in place through
+// the `stepping` list).  Phase 1: sample + pick.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_sample_warp_kernel(const __grid_constant__ SimConst C,
+                                                                              LockArgs a) {
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode == 0) return;  // adaptive: a one-warp-per-env round
+  __shared__ double blk[kWarpsPerBlock][160];
+  __shared__ unsigned valid[kWarpsPerBlock][32];
+  const int wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  if (gw >= *a.n_active) return;
+  const int e = a.active[gw];
+  const int n = C.n, l = threadIdx.x & 31;
+  WarpEnv W(blk[wib], n, l);
+  const ShapeView S = a.S.view(0);
+  warp_load(W, a.env_poses + static_cast<size_t>(e) * n * 3, S);
+  if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
+  const int count = warp_sample_mask(W, S, C, valid[wib]);
+  if (count == 0) {  // no legal push: reward 0 (mcts.cpp:146-150)
+    if (l == 0) {
+      a.env_done[e] = 1;
+      a.env_reward[e] = 0.0;
+    }
+    return;
+  }
+  const MtView g{a.mt + e, a.E};
+  int idx = a.mt_idx[e];
+  const uint64_t k = warp_mt_pick(g, idx, static_cast<uint64_t>(count), l);
+  if (l == 0) a.mt_idx[e] = idx;
+  int w = 0, seen = 0;
+  while (seen + __popc(valid[wib][w]) <= static_cast<int>(k)) seen += __popc(valid[wib][w++]);
+  unsigned bits = valid[wib][w];
+  for (int drop = static_cast<int>(k) - seen; drop > 0; --drop) bits &= bits - 1;
+  const int c = 32 * w + __ffs(bits) - 1;
+  if (l == 0) {
+    V2 s, t;
+    push_candidate(W.view(), S, C, c / C.na, c % C.na, false, s, t);
+    double* pu = a.env_push + static_cast<size_t>(e) * 4;
+    pu[0] = s.x;
+    pu[1] = s.y;
+    pu[2] = t.x;
+    pu[3] = t.y;
+    a.stepping[atomicAdd(a.n_stepping, 1)] = e;
+  }
+}
+
+// Phase 3: the rest of RolloutCursor::step for the envs the physics kernel
+// resolved (SimError -> reward 0; else count the push, graspable, reward).
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_post_warp_kernel(const __grid_constant__ SimConst C,
+                                                                            LockArgs a) {
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode == 0) return;  // adaptive: a one-warp-per-env round
+  __shared__ double blk[kWarpsPerBlock][160];
+  const int wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  const int n_st = *a.n_stepping;
+  if (gw == 0 && (threadIdx.x & 31) == 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), static_cast<unsigned long long>(n_st));
+  if (gw >= n_st) return;
+  const int e = a.stepping[gw];
+  const int n = C.n, l = threadIdx.x & 31;
+  if (a.env_status[e] != 0) {  // SimError (mcts.cpp:153-158)
+    if (l == 0) {
+      a.env_done[e] = 1;
+      a.env_reward[e] = 0.0;
+    }
+    return;
+  }
+  WarpEnv W(blk[wib], n, l);
+  const ShapeView S = a.S.view(0);
+  warp_load(W, a.env_poses + static_cast<size_t>(e) * n * 3, S);
+  const GraspOut gr = warp_graspable(W, S, C, a.S.target[0]);
+  if (l == 0) {
+    const int pushes = a.env_pushes[e] + 1;
+    a.env_pushes[e] = pushes;
+    if (gr.graspable) {
+      a.env_done[e] = 1;
+      a.env_bygrasp[e] = 1;
+      a.env_reward[e] = C.gamma_pow[pushes];
+    } else if (pushes >= a.cap) {
+      a.env_done[e] = 1;
+      a.env_reward[e] = 0.0;
+    }
+  }
 }
 
 #define PPG_WARP_INST(NW, P)                                                                            \

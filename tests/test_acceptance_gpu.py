@@ -19,7 +19,7 @@ def test_c1_single_env_pmbs_equals_serial_mcts(ctx):
         assert list(r.action) == rec["action"] and r.iterations == rec["iterations"] and r.stop_reason == rec["stop"]
 
 
-@pytest.mark.parametrize("mode", [{}, {"PPG_WARP_MAX": 0}, {"PPG_FORCE_GENERIC": 1}])
+@pytest.mark.parametrize("mode", [{}, {"PPG_WARP_MAX": 0}, {"PPG_FORCE_GENERIC": 1}, {"PPG_HYBRID_MIN": 0}])
 def test_c4_scheduling_independence(mode):
     from test_gpu_parity import _ctx_with
     c = _ctx_with(**mode)

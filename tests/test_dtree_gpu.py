@@ -73,3 +73,20 @@ def test_device_tree_acceptance_c1(ctx):
             assert list(r.action) == rec["action"] and r.iterations == rec["iterations"]
     finally:
         ctx.set_planner("auto")
+
+
+def test_device_tree_hybrid_rounds():
+    """Large-batch lockstep rounds (warp sampler / graspable + lane physics)
+    forced on (PPG_HYBRID_MIN=0) inside the device-tree graph: same trees."""
+    from test_gpu_parity import _ctx_with
+    c = _ctx_with(PPG_HYBRID_MIN=0)
+    for idx in (12, 17):
+        cc, st = golden_io.cases()[idx]
+        d = cc["decision"]
+        r = run_pmbs(st, ParallelConfig(rng_seed=int(cc["seed"])), ctx=c)
+        assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
+    _, st = golden_io.cases()[17]
+    cfg = ParallelConfig(rng_seed=11, n_envs=300, budget=Budget.iterations(6))
+    h, dv = _both(c, st, cfg)
+    _same(h, dv)
+    c.close()

@@ -192,7 +192,8 @@ def _generic_ctx():
     return _ctx_with(PPG_FORCE_GENERIC=1)
 
 
-MODES = {"warp": {}, "lane": {"PPG_WARP_MAX": 0}, "generic": {"PPG_FORCE_GENERIC": 1}}
+MODES = {"warp": {}, "lane": {"PPG_WARP_MAX": 0}, "generic": {"PPG_FORCE_GENERIC": 1},
+         "hybrid": {"PPG_HYBRID_MIN": 0}}  # hybrid: warp sampler / grasp + lane physics lockstep rounds
 
 
 @pytest.mark.parametrize("n,motif", [(1, "random"), (3, "random"), (6, "random"), (8, "random"), (9, "random"),
@@ -239,7 +240,7 @@ def test_all_kernel_modes_on_golden_resolve_sets(mode):
     c.close()
 
 
-@pytest.mark.parametrize("mode", ["warp", "lane"])
+@pytest.mark.parametrize("mode", ["warp", "lane", "hybrid"])
 def test_simulate_and_expand_modes(mode):
     c = _ctx_with(**MODES[mode])
     cases = {cc["case_id"]: st for cc, st in golden_io.cases()}
@@ -270,9 +271,10 @@ def test_simulate_and_expand_modes(mode):
     c.close()
 
 
+@pytest.mark.parametrize("env", [{"PPG_WARP_MAX": 0}, {"PPG_HYBRID_MIN": 0}])
 @pytest.mark.parametrize("idx", [12, 17, 19])
-def test_fingerprints_lane_mode(idx):
-    c = _ctx_with(PPG_WARP_MAX=0)
+def test_fingerprints_lane_mode(idx, env):
+    c = _ctx_with(**env)
     cc, st = golden_io.cases()[idx]
     d = cc["decision"]
     r = run_pmbs(st, ParallelConfig(rng_seed=int(cc["seed"])), ctx=c)
