@@ -68,6 +68,7 @@ struct DTScal {
   int unsettled[kMaxTreeDepth];  // non-terminal nodes with untried actions, per depth
   int err[4];                    // first invariant violation seen on the device (debug)
   int round_mode;                // adaptive lockstep rounds (LockArgs.round_mode)
+  int round_guard;               // rounds of this iteration's lockstep (< 0: limit hit)
 };
 
 struct DTree {
@@ -675,7 +676,8 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
   a.n_active = S.l_nactive.as<int32_t>();
   a.counters = S.l_counters.as<long long>();
   a.dyn = t.sc->lock_dyn;
-  a.round_mode = &t.sc->round_mode;
+  a.round_mode = nullptr;  // set by dt_mode for adaptive graphs
+  a.round_guard = &t.sc->round_guard;
   a.hybrid_min = ctx->hybrid_min_envs;
   S.lra = ResolveArgs{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, S.n_envs};
   S.lra.idx = a.stepping;
@@ -684,10 +686,17 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
 }
 
 // One lockstep round (captured into the WHILE body).
-int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st) {
-  // hybrid-capable batches decide per round on the device (harvest flag)
+// Round mode of the device-tree graph: hybrid-capable batches decide per
+// round on the device (the harvest's round_mode flag); every other batch
+// has one fixed mode and no flag (so the harvest never writes one).
+RoundMode dt_mode(ppg_ctx* ctx, DTreeState& S) {
   RoundMode m = round_mode(ctx, S.n, S.n_envs);
   if (m == RoundMode::kHybrid && ctx->hybrid_min_envs > 0) m = RoundMode::kAdaptive;
+  S.la.round_mode = m == RoundMode::kAdaptive ? &S.t.sc->round_mode : nullptr;
+  return m;
+}
+
+int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, RoundMode m) {
   return lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, m, st);
 }
 
@@ -709,6 +718,7 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
   cudaGraphConditionalHandle cond;
   DCK(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
   S.la.cond = cond;
+  const RoundMode mode = dt_mode(ctx, S);
   const DTree& t = S.t;
   dt_select_kernel<<<1, 32, 0, st>>>(t);
   dt_gather_kernel<<<gg, 256, 0, st>>>(t, disc);
@@ -746,7 +756,7 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
   DCK(cudaStreamUpdateCaptureDependencies(st, &wnode, 1, cudaStreamSetCaptureDependencies));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   DCK(cudaStreamBeginCaptureToGraph(S.st2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  int rc = dt_round(ctx, S, S.st2);
+  int rc = dt_round(ctx, S, S.st2, mode);
   lock_harvest_kernel<<<1, 1024, 0, S.st2>>>(S.C, S.la);
   cudaGraph_t body_out = nullptr;
   const cudaError_t e2 = cudaStreamEndCapture(S.st2, &body_out);
@@ -771,6 +781,7 @@ int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
   const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
   const DTree& t = S.t;
   S.la.cond = 0;
+  const RoundMode mode = dt_mode(ctx, S);
 #define DSTEP(name, launch)                                                              \
   do {                                                                                   \
     launch;                                                                              \
@@ -806,7 +817,7 @@ int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
     int act = 0;
     DCK(cudaMemcpy(&act, S.la.n_active, 4, cudaMemcpyDeviceToHost));
     if (act == 0) break;
-    DSTEP("round", dt_round(ctx, S, st));
+    DSTEP("round", dt_round(ctx, S, st, mode));
   }
   DSTEP("backprop", (dt_backprop_kernel<<<1, 32, 0, st>>>(t)));
   DSTEP("stop", (dt_stop_kernel<<<1, 1, 0, st>>>(t)));
@@ -988,6 +999,10 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
         ctx->err = m;
         return PPG_ECUDA;
       }
+    }
+    if (h.round_guard < 0) {
+      ctx->err = "device tree: lockstep rounds exceeded the safety limit";
+      return PPG_EINVAL;
     }
     if (h.err[0]) {
       char m[256];

@@ -216,6 +216,7 @@ PPG_DI void cursor_init(const SimConst& C, const LockArgs& a, int e, int node) {
 __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
   lock_dyn(a);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e == 0 && a.round_guard) *a.round_guard = 0;
   if (e < a.n_nodes) a.rew[e] = 0ull;
   if (e >= a.used) return;
   // Even split of the GLOBAL batch, remainder to earlier nodes
@@ -412,8 +413,13 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     a.counters[2] += s_rep;
     if (s_active > 0) a.counters[1] += 1;
     if (a.round_mode) *a.round_mode = s_active >= a.hybrid_min ? 1 : 0;
+    bool go = s_active > 0;
+    if (a.round_guard && go && ++*a.round_guard > kLockRoundLimit) {
+      *a.round_guard = -1;  // non-terminating lockstep: reported by the host
+      go = false;
+    }
     // device tree graph: the lockstep WHILE node runs another round iff envs remain
-    if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), s_active > 0 ? 1u : 0u);
+    if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), go ? 1u : 0u);
   }
 }
 

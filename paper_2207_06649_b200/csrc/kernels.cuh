@@ -110,7 +110,13 @@ struct LockArgs {
   // warp per env); the kernels of the other mode return at once
   int* round_mode = nullptr;
   int hybrid_min = 0;
+  // device tree: rounds of the current lockstep call; the harvest stops the
+  // WHILE loop (and marks the counter negative) past kLockRoundLimit, so a
+  // bug surfaces as an error instead of a hung graph
+  int* round_guard = nullptr;
 };
+
+constexpr int kLockRoundLimit = 1 << 20;
 
 // Applies the device-side per-iteration overrides (device tree mode).
 __device__ __forceinline__ void lock_dyn(LockArgs& a) {

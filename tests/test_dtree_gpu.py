@@ -90,3 +90,23 @@ def test_device_tree_hybrid_rounds():
     h, dv = _both(c, st, cfg)
     _same(h, dv)
     c.close()
+
+
+@pytest.mark.parametrize("scene", ["case_18", "case_16", "ring18"])
+def test_device_tree_adaptive_rounds(scene):
+    """PPG_HYBRID_MIN=64: rounds with >= 64 active envs are hybrid, the rest
+    one warp per env, switched per round on the device (disc scenes with the
+    lane kernel); scenes without it (polygons: case_16, 18 discs) keep one
+    fixed mode.  Must finish and equal the host tree."""
+    from paper_2207_06649_b200.scenes import generate_case
+    from test_gpu_parity import _ctx_with
+    c = _ctx_with(PPG_HYBRID_MIN=64)
+    if scene == "ring18":
+        st = generate_case(18, 0.0, 5, "ring")
+        cfg = ParallelConfig(rng_seed=5, n_envs=512, budget=Budget.iterations(3))
+    else:
+        cc, st = {x["case_id"]: (x, s) for x, s in golden_io.cases()}[scene]
+        cfg = ParallelConfig(rng_seed=int(cc["seed"]), n_envs=512, budget=Budget.iterations(4))
+    h, dv = _both(c, st, cfg)
+    _same(h, dv)
+    c.close()
