@@ -160,7 +160,7 @@ struct ppg_ctx {
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
   int warp_max_envs = 4096;
-  int hybrid_min_envs = 24576;           // lockstep rounds with >= this many active envs (discs, n <= 16)
+  int hybrid_min_envs = 8192;            // lockstep rounds with >= this many active envs (discs, n <= 16)
                                           // run the hybrid warp-sampler / lane-physics round; PPG_HYBRID_MIN
   bool warp_max_explicit = false;        // PPG_WARP_MAX given: a hard cap for every scene type
   bool warp_poly = true;                  // polygon scenes in latency mode; PPG_WARP_POLY=0 disables               // latency mode (one warp per env) up to this many envs; PPG_WARP_MAX
