@@ -119,17 +119,27 @@ __device__ __forceinline__ bool dt_selectable(const DTree& t, int x, int dT) {
 
 constexpr unsigned kAll = 0xffffffffu;
 
-// select_batch (pmbs.cpp:52-63): up to n_envs descents with virtual visits.
-__global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
+// select_batch (pmbs.cpp:52-63): up to n_envs descents with virtual visits,
+// one block.  At every level the block scores the node's children in
+// parallel (kSelThreads per round, loads of a round issued before scoring),
+// reduces to the FIRST maximum in insertion order, and descends; thread 0
+// pops the untried action and updates virtual visits / selectable counts.
+constexpr int kSelThreads = 256;
+
+__global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
+  constexpr int kWarps = kSelThreads / 32;
+  __shared__ double s_bs[kWarps];
+  __shared__ int s_bk[kWarps];
+  __shared__ int s_x;
   DTScal* sc = t.sc;
-  const int l = threadIdx.x;
+  const int tid = threadIdx.x, l = tid & 31, wid = tid >> 5;
   const int dT = sc->dT;
   const double cexp = sc->c_explore;
   int draws = 0;
   bool bad = false;
   if (sc->stop < 0) {
     for (; draws < t.n_envs; ++draws) {
-      if (!dt_selectable(t, 0, dT)) break;
+      if (!dt_selectable(t, 0, dT)) break;  // every thread reads the same state
       int x = 0;
       while (!dt_self(t, x, dT)) {  // descend_virtual (pmbs.cpp:30-48)
         const long long co = t.u_off[x];
@@ -137,15 +147,12 @@ __global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
         const double lg = t.logtab[t.visits[x] + t.vv[x]];  // log(n_parent)
         double bs = -INFINITY;
         int bk = INT_MAX;
-        // children k = l, l + 32, ... in chunks of kScanU per lane: all loads
-        // of a chunk are issued before any score is formed (memory-level
-        // parallelism); per lane the children stay in increasing order
-        constexpr int kScanU = 4;
-        for (int k0 = 0; k0 < cn; k0 += 32 * kScanU) {
+        constexpr int kScanU = 2;
+        for (int k0 = 0; k0 < cn; k0 += kSelThreads * kScanU) {
           int ch[kScanU];
 #pragma unroll
           for (int u = 0; u < kScanU; ++u) {
-            const int k = k0 + 32 * u + l;
+            const int k = k0 + kSelThreads * u + tid;
             ch[u] = k < cn ? t.cpool[co + k] : -1;
           }
           bool sel[kScanU];
@@ -160,14 +167,14 @@ __global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
 #pragma unroll
           for (int u = 0; u < kScanU; ++u) {
             if (!sel[u]) continue;
-            double s = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
+            double sv = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
             if (nci[u] != 0) {
               const double nc = static_cast<double>(nci[u]);
-              s = qc[u] / nc + cexp * sqrt(2.0 * lg / nc);
+              sv = qc[u] / nc + cexp * sqrt(2.0 * lg / nc);
             }
-            if (s > bs) {
-              bs = s;
-              bk = k0 + 32 * u + l;
+            if (sv > bs) {
+              bs = sv;
+              bk = k0 + kSelThreads * u + tid;
             }
           }
         }
@@ -180,14 +187,34 @@ __global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
             bk = ok;
           }
         }
-        if (bk == INT_MAX) {  // impossible under the selc invariant
+        if (l == 0) {
+          s_bs[wid] = bs;
+          s_bk[wid] = bk;
+        }
+        __syncthreads();
+        if (wid == 0) {
+          bs = l < kWarps ? s_bs[l] : -INFINITY;
+          bk = l < kWarps ? s_bk[l] : INT_MAX;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double os = __shfl_xor_sync(kAll, bs, o);
+            const int ok = __shfl_xor_sync(kAll, bk, o);
+            if (os > bs || (os == bs && ok < bk)) {
+              bs = os;
+              bk = ok;
+            }
+          }
+          if (l == 0) s_x = bk == INT_MAX ? -1 : t.cpool[co + bk];  // -1: impossible under the selc invariant
+        }
+        __syncthreads();
+        x = s_x;
+        if (x < 0) {
           bad = true;
           break;
         }
-        x = t.cpool[co + bk];
       }
       if (bad) break;
-      if (l == 0) {  // pop_untried (mcts.cpp:13-16) + virtual visit up the path
+      if (tid == 0) {  // pop_untried (mcts.cpp:13-16) + virtual visit up the path
         const int h = t.u_head[x];
         t.sel_node[draws] = x;
         t.sel_act[draws] = t.u_off[x] + h;
@@ -202,10 +229,10 @@ __global__ void __launch_bounds__(32) dt_select_kernel(DTree t) {
             }
         }
       }
-      __syncwarp();
+      __syncthreads();
     }
   }
-  if (l == 0) {
+  if (tid == 0) {
     sc->n_pairs = draws;
     if (bad) sc->stop = 3;
     else if (draws == 0 && sc->stop < 0) sc->stop = 1;  // TreeExhausted: explored
@@ -720,7 +747,7 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
   S.la.cond = cond;
   const RoundMode mode = dt_mode(ctx, S);
   const DTree& t = S.t;
-  dt_select_kernel<<<1, 32, 0, st>>>(t);
+  dt_select_kernel<<<1, kSelThreads, 0, st>>>(t);
   dt_gather_kernel<<<gg, 256, 0, st>>>(t, disc);
   {
     ExpandArgs a{ctx->scene, t.gp, t.ga, t.cp, t.st, t.gr, t.nu, t.un, E};
@@ -792,7 +819,7 @@ int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
       return PPG_ECUDA;                                                                  \
     }                                                                                    \
   } while (0)
-  DSTEP("select", (dt_select_kernel<<<1, 32, 0, st>>>(t)));
+  DSTEP("select", (dt_select_kernel<<<1, kSelThreads, 0, st>>>(t)));
   DSTEP("gather", (dt_gather_kernel<<<gg, 256, 0, st>>>(t, disc)));
   {
     ExpandArgs a{ctx->scene, t.gp, t.ga, t.cp, t.st, t.gr, t.nu, t.un, E};
