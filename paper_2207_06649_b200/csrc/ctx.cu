@@ -325,7 +325,9 @@ int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, in
                       ? ctx->disc_bps_override
                       : ctx->disc_blocks_per_sm[slot];
   const int cap = bps * ctx->num_sms;
-  const int grid = want < 1 ? 1 : (want < cap ? want : cap);
+  // a batch that fills at least half the resident lanes gets one full wave
+  // (every SM the same number of blocks; the kernel spreads the envs evenly)
+  const int grid = want * 2 >= cap ? cap : (want < 1 ? 1 : want);
   const size_t sm = disc_smem(nmax);
   switch (nmax) {
     case 4: resolve_disc_kernel<4><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;

@@ -29,6 +29,7 @@
 // warps stay full until the batch drains (no per-warp max-iteration tail).
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <utility>
 
 #include "kernels.cuh"
@@ -160,10 +161,14 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   Mask<W> pact;  // pairs with both objects active
   V2 start{0.0, 0.0}, delta{0.0, 0.0};
   int step = 0, iter = 0;
-  const int total_threads = gridDim.x * kDB;
-  int e = blockIdx.x * kDB + tid;
-  int ee = e;
   const int E = a.E_dev ? *a.E_dev : a.E;
+  // First environments: an even share per block (`per` <= kDB), so a full
+  // wave of blocks (the launch fills every SM equally) gives every SM the
+  // same number of environments; the rest are fetched with one atomic each.
+  const int per = min(kDB, (E + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x));
+  const int total_threads = gridDim.x * per;
+  int e = tid < per ? blockIdx.x * per + tid : INT_MAX;
+  int ee = e;
   bool have = false;
   bool need_init = true;
 
