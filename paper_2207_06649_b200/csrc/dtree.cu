@@ -405,33 +405,49 @@ __global__ void __launch_bounds__(32) dt_backprop_kernel(DTree t) {
   int cur = -1;
   double cq = 0.0;
   long long cv = 0;
-  for (int k = 0; k < P; ++k) {
-    const int id = base + k, D = t.depth[id];
-    const double r = __longlong_as_double(static_cast<long long>(t.rew[k]));
-    if (d == D) {
-      t.q[id] = 0.0 + r;
-      t.visits[id] = 1;
-    } else if (d < D) {
-      const int a = t.anc[static_cast<size_t>(id) * kMaxTreeDepth + d];
-      if (a < 0 || a >= sc->n_nodes) {  // corrupt ancestor row: report, do not touch memory
-        if (atomicCAS(const_cast<int*>(&sc->err[0]), 0, 1) == 0) {
-          const_cast<DTScal*>(sc)->err[1] = id;
-          const_cast<DTScal*>(sc)->err[2] = d;
-          const_cast<DTScal*>(sc)->err[3] = a;
+  // 32 new nodes at a time: lane j fetches node k0 + j's depth and reward,
+  // every lane fetches its depth's ancestor of all 32 (independent loads),
+  // then the batch-order fold runs on shuffled values
+  for (int k0 = 0; k0 < P; k0 += 32) {
+    const int kj = k0 + d;
+    const int Dj = kj < P ? t.depth[base + kj] : -1;
+    const double rj = kj < P ? __longlong_as_double(static_cast<long long>(t.rew[kj])) : 0.0;
+    int anc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      anc[j] = k0 + j < P ? t.anc[static_cast<size_t>(base + k0 + j) * kMaxTreeDepth + d] : -1;
+    const int m = P - k0 < 32 ? P - k0 : 32;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j >= m) break;
+      const int id = base + k0 + j;
+      const int D = __shfl_sync(kAll, Dj, j);
+      const double r = __shfl_sync(kAll, rj, j);
+      if (d == D) {
+        t.q[id] = 0.0 + r;
+        t.visits[id] = 1;
+      } else if (d < D) {
+        const int a = anc[j];
+        if (a < 0 || a >= sc->n_nodes) {  // corrupt ancestor row: report, do not touch memory
+          if (atomicCAS(const_cast<int*>(&sc->err[0]), 0, 1) == 0) {
+            const_cast<DTScal*>(sc)->err[1] = id;
+            const_cast<DTScal*>(sc)->err[2] = d;
+            const_cast<DTScal*>(sc)->err[3] = a;
+          }
+          continue;
         }
-        continue;
-      }
-      if (a != cur) {
-        if (cur >= 0) {
-          t.q[cur] = cq;
-          t.visits[cur] = cv;
+        if (a != cur) {
+          if (cur >= 0) {
+            t.q[cur] = cq;
+            t.visits[cur] = cv;
+          }
+          cur = a;
+          cq = t.q[a];
+          cv = t.visits[a];
         }
-        cur = a;
-        cq = t.q[a];
-        cv = t.visits[a];
+        cq += r;
+        cv += 1;
       }
-      cq += r;
-      cv += 1;
     }
   }
   if (cur >= 0) {
