@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
   __shared__ double s_bs[kWarps];
   __shared__ int s_bk[kWarps];
   __shared__ int s_x;
+  __shared__ int s_path[kMaxTreeDepth];  // the draw's root path (node at each depth)
   DTScal* sc = t.sc;
   const int tid = threadIdx.x, l = tid & 31, wid = tid >> 5;
   const int dT = sc->dT;
@@ -140,7 +141,8 @@ __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
   if (sc->stop < 0) {
     for (; draws < t.n_envs; ++draws) {
       if (!dt_selectable(t, 0, dT)) break;  // every thread reads the same state
-      int x = 0;
+      int x = 0, lvl = 0;
+      if (tid == 0) s_path[0] = 0;
       while (!dt_self(t, x, dT)) {  // descend_virtual (pmbs.cpp:30-48)
         const long long co = t.u_off[x];
         const int cn = t.c_n[x];
@@ -204,22 +206,26 @@ __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
               bk = ok;
             }
           }
-          if (l == 0) s_x = bk == INT_MAX ? -1 : t.cpool[co + bk];  // -1: impossible under the selc invariant
+          if (l == 0) {
+            s_x = bk == INT_MAX ? -1 : t.cpool[co + bk];  // -1: impossible under the selc invariant
+            if (lvl + 1 < kMaxTreeDepth) s_path[lvl + 1] = s_x;
+          }
         }
         __syncthreads();
         x = s_x;
+        ++lvl;
         if (x < 0) {
           bad = true;
           break;
         }
       }
       if (bad) break;
-      if (tid == 0) {  // pop_untried (mcts.cpp:13-16) + virtual visit up the path
+      if (tid <= lvl) t.vv[s_path[tid]] += 1;  // virtual visit on the root path (one node per thread)
+      if (tid == 0) {  // pop_untried (mcts.cpp:13-16)
         const int h = t.u_head[x];
         t.sel_node[draws] = x;
         t.sel_act[draws] = t.u_off[x] + h;
         t.u_head[x] = h + 1;
-        for (int a = x; a >= 0; a = t.parent[a]) t.vv[a] += 1;
         if (h + 1 == t.u_n[x]) {  // now fully expanded
           sc->unsettled[t.depth[x]] -= 1;
           if (t.selc[x] == 0)  // x left the selectable set: update its ancestors
