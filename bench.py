@@ -235,7 +235,33 @@ def pmbs_decisions(ctx, with_reference: bool):
         out[f"n_envs_{ne}"] = row
     out["c4"] = c4_decision(ctx, with_reference)
     out["c3"] = c3_episodes(ctx, with_reference)
+    out["c2_polygons"] = c2_polygons(ctx, with_reference)
     return out
+
+
+def c2_polygons(ctx, with_reference: bool):
+    """BASELINE config 2's polygon variant: generate_case(10, ShapeMix{0.35})
+    scenes, one sampled push each, 16,384 envs through ppg_batch_resolve (host
+    buffers, end to end) vs the reference batch_resolve with WorkerPool(nproc)
+    on a 1,024-env sample."""
+    from paper_2207_06649_b200.abi import default_params
+    from paper_2207_06649_b200.scenes import c2_workload
+    params = default_params()
+    ctx.set_params(params)
+    E = 16384
+    table, poses, pushes, _ = c2_workload(ctx, E, N_OBJ, 0.35)
+    ctx.batch_resolve_arrays(table, poses, pushes)  # warm-up
+    best = None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ctx.batch_resolve_arrays(table, poses, pushes)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    row = {"workload": f"E={E} generate_case(10, ShapeMix{{0.35}}) scenes, 1 push/env", "unit": UNIT,
+           "gpu_e2e": E / best}
+    if with_reference:
+        row["reference"] = cpu_reference_sample(table, poses, pushes, params, 1024, 3.0, os.cpu_count() or 1)
+    return row
 
 
 def c4_decision(ctx, with_reference: bool):
