@@ -10,8 +10,8 @@
 // Decision-for-decision identical to the host planner (planner.cpp) and so
 // to the reference:
 //   select_batch / descend_virtual / ucb_virtual / pop_untried (pmbs.cpp:12-63,
-//     mcts.cpp:13-16) -> dt_select_kernel: one warp, children scanned 32 at a
-//     time, first maximum in insertion order; UCB with the host's glibc log
+//     mcts.cpp:13-16) -> dt_select_kernel: one block scores a node's
+//     children in parallel, first maximum in insertion order; UCB with the host's glibc log
 //     table and IEEE sqrt / division; subtree_selectable (pmbs.cpp:21-28) is
 //     kept INCREMENTALLY as a per-node count of selectable children (selc)
 //     instead of a recursive scan;
