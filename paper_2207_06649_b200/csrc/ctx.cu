@@ -270,6 +270,7 @@ void ppg_destroy(ppg_ctx* ctx) {
     ctx->chunk_in[k].release();
     ctx->chunk_buf[k].release();
     if (ctx->chunk_stream[k]) cudaStreamDestroy(ctx->chunk_stream[k]);
+    if (ctx->chunk_ev[k]) cudaEventDestroy(ctx->chunk_ev[k]);
   }
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -452,8 +453,12 @@ constexpr int kPipelineMinEnvs = 32768;
 
 static int batch_resolve_chunk(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in,
                                const double* pushes, int e0, int e1, double* poses_out, int32_t* status,
-                               double* residual, cudaStream_t st, int slot) {
+                               double* residual, cudaStream_t st, int slot, cudaEvent_t after = nullptr,
+                               cudaEvent_t h2d_done = nullptr) {
   const int Ek = e1 - e0;
+  // host->device copies in slice order (slice k's physics overlaps slice
+  // k+1's copies instead of every slice waiting for interleaved copies)
+  if (after) CK(cudaStreamWaitEvent(st, after, 0));
   ShapesDev S;
   double side, margin;
   bool discs;
@@ -487,6 +492,7 @@ static int batch_resolve_chunk(ppg_ctx* ctx, const ppg_shapes* shapes, const dou
   double* d_res = ctx->b_resid.as<double>() + e0;
   CK(cudaMemcpyAsync(d_in, poses_in + e0 * row, Ek * row * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_push, pushes + e0 * 4ull, Ek * 32ull, cudaMemcpyHostToDevice, st));
+  if (h2d_done) CK(cudaEventRecord(h2d_done, st));
   const int rc = launch_resolve(ctx, S, discs, side, margin, d_in, d_push, Ek, d_out, d_st, d_res, nullptr, st, slot);
   if (rc != PPG_SUCCESS) return rc;
   CK(cudaMemcpyAsync(poses_out + e0 * row, d_out, Ek * row * 8, cudaMemcpyDeviceToHost, st));
@@ -528,14 +534,17 @@ int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* pose
     CK(cudaStreamSynchronize(ctx->stream));
     return PPG_SUCCESS;
   }
-  for (int k = 0; k < chunks; ++k)
+  for (int k = 0; k < chunks; ++k) {
     if (!ctx->chunk_stream[k]) CK(cudaStreamCreateWithFlags(&ctx->chunk_stream[k], cudaStreamNonBlocking));
+    if (!ctx->chunk_ev[k]) CK(cudaEventCreateWithFlags(&ctx->chunk_ev[k], cudaEventDisableTiming));
+  }
   CK(cudaStreamSynchronize(ctx->stream));  // earlier work on the context stream
   for (int k = 0; k < chunks; ++k) {
     const int e0 = static_cast<int>(static_cast<long long>(E) * k / chunks);
     const int e1 = static_cast<int>(static_cast<long long>(E) * (k + 1) / chunks);
     const int rc = batch_resolve_chunk(ctx, shapes, poses_in, pushes, e0, e1, poses_out, status, residual,
-                                       ctx->chunk_stream[k], k);
+                                       ctx->chunk_stream[k], k, k ? ctx->chunk_ev[k - 1] : nullptr,
+                                       ctx->chunk_ev[k]);
     if (rc != PPG_SUCCESS) return rc;
   }
   for (int k = 0; k < chunks; ++k) CK(cudaStreamSynchronize(ctx->chunk_stream[k]));

@@ -156,6 +156,7 @@ struct ppg_ctx {
   int disc_bps_override = 0;              // PPG_DISC_BLOCKS_PER_SM: cap resident blocks (experiments)
   // pipelined batch_resolve (host buffers): per-slice streams and shape tables
   cudaStream_t chunk_stream[ppg::kChunks] = {};
+  cudaEvent_t chunk_ev[ppg::kChunks] = {};  // slice k's host->device copies done
   DevBuf chunk_in[ppg::kChunks], chunk_buf[ppg::kChunks];
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
