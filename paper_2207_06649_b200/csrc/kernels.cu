@@ -402,10 +402,14 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     }
   }
   __syncthreads();
-  for (int e0 = 0; e0 < a.used; e0 += B) {
+  for (int e0 = 0; e0 < a.used; e0 += B) {  // active list: one shared atomic per warp
     const int e = e0 + tid;
     const bool act = e < a.used && !a.env_done[e];
-    if (act) a.active[atomicAdd(&s_active, 1)] = e;
+    const unsigned m = __ballot_sync(0xffffffffu, act);
+    int base = 0;
+    if ((tid & 31) == 0 && m) base = atomicAdd(&s_active, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (act) a.active[base + __popc(m & ((1u << (tid & 31)) - 1u))] = e;
   }
   __syncthreads();
   if (tid == 0) {
