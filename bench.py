@@ -236,7 +236,30 @@ def pmbs_decisions(ctx, with_reference: bool):
     out["c4"] = c4_decision(ctx, with_reference)
     out["c3"] = c3_episodes(ctx, with_reference)
     out["c2_polygons"] = c2_polygons(ctx, with_reference)
+    out["rollouts"] = rollout_throughput(ctx)
     return out
+
+
+def rollout_throughput(ctx):
+    """SURVEY §8d's second C2 metric, rollout env-steps/s (the fused
+    RolloutCursor::step: sample + pick + resolve + graspable): one lockstep
+    batch_simulate of 65,536 envs from case_18's root (cap d_T + d_s = 10,
+    leaf parallel, re-purposing on), through ppg_simulate."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_io
+    from paper_2207_06649_b200.abi import default_params
+    c, st = {cc["case_id"]: (cc, s) for cc, s in golden_io.cases()}["case_18"]
+    ne = 65536
+    ctx.set_params(default_params(n_envs=ne, rng_seed=int(c["seed"])))
+    ctx.set_scene(st)
+    meta = np.zeros((1, 3), np.int32)
+    ctx.simulate_arrays(st.poses[None], meta, ne, True, int(c["seed"]), 0, 10)  # warm-up
+    t0 = time.perf_counter()
+    _, ctr = ctx.simulate_arrays(st.poses[None], meta, ne, True, int(c["seed"]), 1, 10)
+    dt = time.perf_counter() - t0
+    return {"workload": "ppg_simulate: 65,536 envs from proj/cases/case_18's root, cap 10", "unit": UNIT,
+            "rollout_steps": int(ctr[0]), "resolve_calls": int(ctr[3]), "rounds": int(ctr[1]),
+            "repurposes": int(ctr[2]), "seconds": dt, "rollout_env_steps_per_s": int(ctr[0]) / dt}
 
 
 def c2_polygons(ctx, with_reference: bool):
