@@ -13,7 +13,8 @@ from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpmbs_b200.so")
+# PPG_LIB: load another build of the library (A/B experiments); default in-tree
+LIB_PATH = os.environ.get("PPG_LIB") or os.path.join(HERE, "libpmbs_b200.so")
 
 PPG_MAX_OBJECTS = 32
 PPG_MAX_VERTICES = 8

@@ -34,6 +34,11 @@ SimConst make_const(const ppg_params& p, int n, double side, double margin) {
   C.margin_threshold = p.margin_threshold;
   C.na = p.pushes_per_object;
   C.n = n;
+  static const bool no_fix = [] {
+    const char* v = std::getenv("PPG_NO_FIXPOINT");
+    return v && v[0] == '1';
+  }();
+  C.fixpoint = no_fix ? 0 : 1;
   // Same expressions and the same glibc as the reference (actions.cpp:59-60,
   // :77-78; mcts.cpp:132 std::pow(double, int) == pow(double, double)).
   const int n_per_object = p.pushes_per_object;
@@ -134,13 +139,16 @@ bool host_all_discs(const ppg_shapes* sh) {
 
 template <class F>
 bool for_each_disc_kernel(F&& f) {
-  const void* fns[kNumDisc] = {
-      reinterpret_cast<const void*>(&resolve_disc_kernel<4>), reinterpret_cast<const void*>(&resolve_disc_kernel<6>),
-      reinterpret_cast<const void*>(&resolve_disc_kernel<8>), reinterpret_cast<const void*>(&resolve_disc_kernel<10>),
-      reinterpret_cast<const void*>(&resolve_disc_kernel<11>), reinterpret_cast<const void*>(&resolve_disc_kernel<12>),
-      reinterpret_cast<const void*>(&resolve_disc_kernel<14>), reinterpret_cast<const void*>(&resolve_disc_kernel<16>)};
-  for (int k = 0; k < kNumDisc; ++k)
-    if (!f(k, fns[k])) return false;
+#define PPG_DISC_FN(N, X) reinterpret_cast<const void*>(&resolve_disc_kernel<N, X>)
+  const void* fns[2][kNumDisc] = {
+      {PPG_DISC_FN(4, false), PPG_DISC_FN(6, false), PPG_DISC_FN(8, false), PPG_DISC_FN(10, false),
+       PPG_DISC_FN(11, false), PPG_DISC_FN(12, false), PPG_DISC_FN(14, false), PPG_DISC_FN(16, false)},
+      {PPG_DISC_FN(4, true), PPG_DISC_FN(6, true), PPG_DISC_FN(8, true), PPG_DISC_FN(10, true),
+       PPG_DISC_FN(11, true), PPG_DISC_FN(12, true), PPG_DISC_FN(14, true), PPG_DISC_FN(16, true)}};
+#undef PPG_DISC_FN
+  for (int v = 1; v >= 0; --v)  // occupancy is taken from the last call: the plain variant
+    for (int k = 0; k < kNumDisc; ++k)
+      if (!f(k, fns[v][k])) return false;
   return true;
 }
 
@@ -314,7 +322,7 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
 // as a persistent grid sized for `work` environments.  The work counter
 // (ctx->b_counter) is zeroed here unless the caller's graph zeroes it.
 int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st,
-                bool zero_counter, int slot_counter) {
+                bool zero_counter, int slot_counter, bool fixpoint) {
   CK(ctx->b_counter.ensure(64));
   int* counter = ctx->b_counter.as<int>() + 4 * slot_counter;  // one counter per concurrent launch
   if (zero_counter) CK(cudaMemsetAsync(counter, 0, 4, st));
@@ -330,16 +338,20 @@ int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, in
   // (every SM the same number of blocks; the kernel spreads the envs evenly)
   const int grid = want * 2 >= cap ? cap : (want < 1 ? 1 : want);
   const size_t sm = disc_smem(nmax);
+#define PPG_DISC_LAUNCH(N)                                                              \
+  (fixpoint ? resolve_disc_kernel<N, true><<<grid, kDiscBlock, sm, st>>>(C, a, counter)  \
+            : resolve_disc_kernel<N, false><<<grid, kDiscBlock, sm, st>>>(C, a, counter))
   switch (nmax) {
-    case 4: resolve_disc_kernel<4><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    case 6: resolve_disc_kernel<6><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    case 8: resolve_disc_kernel<8><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    case 10: resolve_disc_kernel<10><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    case 11: resolve_disc_kernel<11><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    case 12: resolve_disc_kernel<12><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    case 14: resolve_disc_kernel<14><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
-    default: resolve_disc_kernel<16><<<grid, kDiscBlock, sm, st>>>(C, a, counter); break;
+    case 4: PPG_DISC_LAUNCH(4); break;
+    case 6: PPG_DISC_LAUNCH(6); break;
+    case 8: PPG_DISC_LAUNCH(8); break;
+    case 10: PPG_DISC_LAUNCH(10); break;
+    case 11: PPG_DISC_LAUNCH(11); break;
+    case 12: PPG_DISC_LAUNCH(12); break;
+    case 14: PPG_DISC_LAUNCH(14); break;
+    default: PPG_DISC_LAUNCH(16); break;
   }
+#undef PPG_DISC_LAUNCH
   CK(cudaGetLastError());
   return PPG_SUCCESS;
 }
@@ -433,7 +445,7 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
     CK(cudaGetLastError());
     return PPG_SUCCESS;
   }
-  if (!d_counts && use_disc(ctx, all_discs, S.n)) return launch_disc(ctx, C, a, S.n, E, st, true, slot);
+  if (!d_counts && use_disc(ctx, all_discs, S.n)) return launch_disc(ctx, C, a, S.n, E, st, true, slot, false);
   const int grid = (E + kBlock - 1) / kBlock;
   if (d_counts) resolve_kernel<true><<<grid, kBlock, smem_for(S.n), st>>>(C, a);
   else resolve_kernel<false><<<grid, kBlock, smem_for(S.n), st>>>(C, a);

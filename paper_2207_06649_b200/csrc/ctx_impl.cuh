@@ -65,7 +65,7 @@ __global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockAr
                                       const int32_t* node, int count);
 __global__ void fp64_peak_kernel(double* out, int iters, double b, double c);
 __global__ void debug_sincos_kernel(const double* x, int n, double* s, double* c);
-template <int NMAX>
+template <int NMAX, bool kFix>
 __global__ void resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a, int* next_env);
 
 constexpr int kBlock = 128;
@@ -170,8 +170,10 @@ struct ppg_ctx {
 SimConst make_const(const ppg_params& p, int n, double side, double margin);
 size_t disc_smem(int nmax);
 size_t smem_for(int n);
+// fixpoint: the variant that ends a substep at a bit-identical fixed point
+// (jammed pushes, frequent in rollouts); batch_resolve uses the plain one
 int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int work, cudaStream_t st,
-                bool zero_counter = true, int slot_counter = 0);
+                bool zero_counter = true, int slot_counter = 0, bool fixpoint = true);
 bool use_disc(const ppg_ctx* ctx, bool all_discs, int n);
 bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs);
 enum class RoundMode { kWarp, kHybrid, kLaneDisc, kGeneric, kAdaptive };

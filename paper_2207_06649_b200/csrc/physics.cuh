@@ -34,6 +34,7 @@ struct SimConst {
   double margin_threshold;
   int na;  // pushes_per_object
   int n;   // objects per environment
+  int fixpoint;  // skip the rest of a substep at a bit-identical fixed point (PPG_NO_FIXPOINT=1: off)
   double dir_cos[kMaxNa], dir_sin[kMaxNa];
   double g_cos[kGraspAngles], g_sin[kGraspAngles];
   double gamma_pow[kMaxGammaPow];
@@ -206,6 +207,16 @@ PPG_DI int resolve_push(const PoseView& P, const ShapeView& S, const SimConst& C
     if (kCount) cnt->s++;
     for (int iter = 0; iter < C.max_iters; ++iter) {
       double max_pen = 0.0;
+      // fixed-point check (not in the work-counting variant, which must count
+      // every reference iteration): iteration-start poses of a long substep
+      double sx[kMaxObjects], sy[kMaxObjects], st[kMaxObjects];
+      const bool fixcheck = !kCount && C.fixpoint && iter >= 6;
+      if (fixcheck)
+        for (int i = 0; i < n; ++i) {
+          sx[i] = P.x(i);
+          sy[i] = P.y(i);
+          st[i] = P.th(i);
+        }
       for (int i = 0; i < n; ++i) {
         if (!(active >> i & 1u)) continue;
         const double reach = C.tip_r + S.br_(i);
@@ -242,6 +253,14 @@ PPG_DI int resolve_push(const PoseView& P, const ShapeView& S, const SimConst& C
         P.y(i) = dclamp(P.y(i), -h, h);
       }
       if (max_pen <= C.eps_pen) break;
+      if (fixcheck) {  // every pose bit-identical: the rest of the substep repeats this iteration
+        bool same = true;
+        for (int i = 0; i < n; ++i)
+          same = same && __double_as_longlong(P.x(i)) == __double_as_longlong(sx[i]) &&
+                 __double_as_longlong(P.y(i)) == __double_as_longlong(sy[i]) &&
+                 __double_as_longlong(P.th(i)) == __double_as_longlong(st[i]);
+        if (same) break;
+      }
     }
   }
   const double final_pen = max_pairwise_penetration<kCount>(P, S, kCount ? &cnt->pfinal : nullptr);

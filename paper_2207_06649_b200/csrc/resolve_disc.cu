@@ -118,6 +118,7 @@ struct Mask {
 };
 
 constexpr double kNear = 0.002;  // metres, the re-queue filter margin
+constexpr int kFixK = 6;         // check for a fixed point from this iteration of a substep on
 
 PPG_DI double fclampd(double v, double lo, double hi) {
   // == std::clamp(v, lo, hi) for non-NaN v (positions are finite)
@@ -126,7 +127,7 @@ PPG_DI double fclampd(double v, double lo, double hi) {
 
 }  // namespace
 
-template <int NMAX>
+template <int NMAX, bool kFix>
 __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a,
                                                                int* next_env) {
   constexpr int P = NMAX * (NMAX - 1) / 2;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   double* const rl = dsm + 2 * NMAX * kDB + tid;
 
   double x[NMAX], y[NMAX], r[NMAX];
+  double fx0[NMAX], fy0[NMAX];  // fixed-point check copies (local memory)
   uint32_t active = 0;
   Mask<W> pact;  // pairs with both objects active
   V2 start{0.0, 0.0}, delta{0.0, 0.0};
@@ -284,6 +286,15 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     // ---- one projection iteration of substep `step` (push_sim.cpp:87-120)
     const V2 tc = start + delta * static_cast<double>(step);
     double max_pen = 0.0;
+    // fixed-point check for long substeps (jams): the iteration-start state,
+    // in local memory (runtime-indexed, so it never costs registers)
+    if (kFix && C.fixpoint && iter >= kFixK) {
+#pragma unroll 1
+      for (int k = 0; k < n; ++k) {
+        fx0[k] = xl[k * kDB];
+        fy0[k] = yl[k * kDB];
+      }
+    }
     // 1-2. tip vs objects (push_sim.cpp:90-100)
     uint32_t tcand = 0;
     static_for<NMAX>([&](auto ic) {
@@ -402,14 +413,27 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         }
       });
     }
-    if (max_pen <= C.eps_pen || ++iter >= C.max_iters) {
+    // Fixed point: the iteration left every position bit-identical, so each
+    // remaining iteration of the substep repeats it exactly (max_pen > eps
+    // each time) up to max_iters: the substep ends with this state.
+    bool fixed = false;
+    if (kFix && C.fixpoint && iter >= kFixK && !(max_pen <= C.eps_pen)) {
+      fixed = true;
+#pragma unroll 1
+      for (int k = 0; k < n; ++k)
+        fixed = fixed && __double_as_longlong(xl[k * kDB]) == __double_as_longlong(fx0[k]) &&
+                __double_as_longlong(yl[k * kDB]) == __double_as_longlong(fy0[k]);
+    }
+    if (max_pen <= C.eps_pen || fixed || ++iter >= C.max_iters) {
       ++step;
       iter = 0;
     }
   }
 }
 
-#define PPG_DISC_INST(N) template __global__ void resolve_disc_kernel<N>(const __grid_constant__ SimConst, ResolveArgs, int*);
+#define PPG_DISC_INST(N)                                                                                       \
+  template __global__ void resolve_disc_kernel<N, false>(const __grid_constant__ SimConst, ResolveArgs, int*); \
+  template __global__ void resolve_disc_kernel<N, true>(const __grid_constant__ SimConst, ResolveArgs, int*);
 PPG_DISC_INST(4)
 PPG_DISC_INST(6)
 PPG_DISC_INST(8)

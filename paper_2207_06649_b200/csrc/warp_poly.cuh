@@ -327,6 +327,7 @@ PPG_DI int warp_resolve_poly(WarpEnv& W, const WarpPoly& G, const PolyShape& O, 
     const V2 tc = start + delta * static_cast<double>(step);
     for (int iter = 0; iter < C.max_iters; ++iter) {
       double mp = 0.0;
+      const double xs = real ? X[l] : 0.0, ys = real ? Y[l] : 0.0, ts = real ? P.th(l) : 0.0;  // iteration start
       // tip vs own object (push_sim.cpp:90-100), lane per object
       if (mine) {
         const V2 pos{X[l], Y[l]};
@@ -441,6 +442,12 @@ PPG_DI int warp_resolve_poly(WarpEnv& W, const WarpPoly& G, const PolyShape& O, 
         if (moved && O.kind != 0) lane_refresh(W, G, S, l, O.nv);
       }
       if (!__any_sync(kFull, mp > C.eps_pen)) break;  // max_pen <= eps_pen
+      // fixed point (see warp_resolve): every pose bit-identical to the
+      // iteration start -> the remaining iterations of the substep repeat it
+      const bool same = !real || (__double_as_longlong(X[l]) == __double_as_longlong(xs) &&
+                                  __double_as_longlong(Y[l]) == __double_as_longlong(ys) &&
+                                  __double_as_longlong(P.th(l)) == __double_as_longlong(ts));
+      if (C.fixpoint && __all_sync(kFull, same)) break;
       __syncwarp();
     }
   }

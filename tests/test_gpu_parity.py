@@ -193,7 +193,8 @@ def _generic_ctx():
 
 
 MODES = {"warp": {}, "lane": {"PPG_WARP_MAX": 0}, "generic": {"PPG_FORCE_GENERIC": 1},
-         "hybrid": {"PPG_HYBRID_MIN": 0}}  # hybrid: warp sampler / grasp + lane physics lockstep rounds
+         "hybrid": {"PPG_HYBRID_MIN": 0},  # hybrid: warp sampler / grasp + lane physics lockstep rounds
+         "nofix": {"PPG_NO_FIXPOINT": 1}}  # no fixed-point substep skipping (must not change a bit)
 
 
 @pytest.mark.parametrize("n,motif", [(1, "random"), (3, "random"), (6, "random"), (8, "random"), (9, "random"),
@@ -240,7 +241,7 @@ def test_all_kernel_modes_on_golden_resolve_sets(mode):
     c.close()
 
 
-@pytest.mark.parametrize("mode", ["warp", "lane", "hybrid"])
+@pytest.mark.parametrize("mode", ["warp", "lane", "hybrid", "nofix"])
 def test_simulate_and_expand_modes(mode):
     c = _ctx_with(**MODES[mode])
     cases = {cc["case_id"]: st for cc, st in golden_io.cases()}
