@@ -257,11 +257,18 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
 #pragma unroll
             for (int v = w; v < NW; ++v) {
               const bool touch = (om[v] & hm) != 0u && (v > w || l > b);
-              const unsigned tm = __ballot_sync(kFull, touch);
-              if (tm) {
+              if (v == w) {  // the hit's own word nearly always holds later touched pairs: no vote
                 bool h = false;
                 if (touch) h = pair_eval(X, Y, pa[v], pb[v], rr2[v], rs[v], nxa[v], nya[v], nxb[v], nyb[v], dep[v]);
+                const unsigned tm = __ballot_sync(kFull, touch);
                 hit[v] = (hit[v] & ~tm) | __ballot_sync(kFull, h);
+              } else {
+                const unsigned tm = __ballot_sync(kFull, touch);
+                if (tm) {
+                  bool h = false;
+                  if (touch) h = pair_eval(X, Y, pa[v], pb[v], rr2[v], rs[v], nxa[v], nya[v], nxb[v], nyb[v], dep[v]);
+                  hit[v] = (hit[v] & ~tm) | __ballot_sync(kFull, h);
+                }
               }
             }
           }
@@ -312,7 +319,7 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
               for (int v = w; v < NW; ++v) {
                 const bool touch = (om[v] & hm) != 0u && 32 * v + l > p;
                 const unsigned tm = __ballot_sync(kFull, touch);
-                if (tm) {
+                if (v == w || tm) {  // the hit's own word: no branch on the vote
                   bool pass = false;
                   if (touch) {
                     const double fx = X[pa[v]] - X[pb[v]], fy = Y[pa[v]] - Y[pb[v]];
