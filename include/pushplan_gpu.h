@@ -219,9 +219,10 @@ typedef int (*ppg_simulate_fn)(void* user, const double* node_poses, const int32
 int ppg_set_simulate_hook(ppg_ctx* ctx, ppg_simulate_fn fn, void* user);
 
 /* Planner selection for ppg_run_pmbs (also env PPG_PLANNER=host|device):
- * AUTO = the device-resident tree unless a simulate hook is installed (the
- * sharded multi-GPU driver needs the host tree); HOST = tree on the host
- * (planner.cpp); DEVICE = tree on the device (dtree.cu). */
+ * AUTO = DEVICE = the device-resident tree (dtree.cu; with a simulate hook
+ * installed — the sharded multi-GPU driver — each iteration runs its rollouts
+ * through the hook between two graph launches); HOST = tree on the host
+ * (planner.cpp). */
 #define PPG_PLANNER_AUTO 0
 #define PPG_PLANNER_HOST 1
 #define PPG_PLANNER_DEVICE 2

@@ -491,8 +491,10 @@ struct DTreeState {
   int cap_nodes = 0;
   long long cap_actions = 0;
   int n_envs = 0, n = 0, na = 0;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec = nullptr;  // the iteration (or its pre part when hooked)
   cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec_post = nullptr;  // hooked: backprop + stop
+  cudaGraph_t graph_post = nullptr;
   cudaStream_t st2 = nullptr;
   DTree t{};
   LockArgs la{};
@@ -503,8 +505,10 @@ struct DTreeState {
   void release_graph() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
-    exec = nullptr;
-    graph = nullptr;
+    if (exec_post) cudaGraphExecDestroy(exec_post);
+    if (graph_post) cudaGraphDestroy(graph_post);
+    exec = exec_post = nullptr;
+    graph = graph_post = nullptr;
   }
   void release() {
     release_graph();
@@ -749,25 +753,13 @@ int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, RoundMode m) {
   return lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, m, st);
 }
 
-// Captures one PMBS iteration as a graph (select -> expand -> attach ->
-// lockstep WHILE -> backprop -> stop).
-int dt_capture(ppg_ctx* ctx, DTreeState& S) {
-  cudaStream_t st = ctx->stream;
+// select -> gather -> expand -> attach -> recount -> copy: the part of an
+// iteration before batch_simulate (launched into a capturing stream).
+int dt_launch_pre(ppg_ctx* ctx, DTreeState& S, cudaStream_t st) {
   const int E = S.n_envs, n = S.n;
   const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E, true);
   const bool disc = !warp && use_disc(ctx, ctx->scene_all_discs, n);
   const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
-  if (!S.st2) DCK(cudaStreamCreateWithFlags(&S.st2, cudaStreamNonBlocking));
-  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  cudaStreamCaptureStatus cs;
-  cudaGraph_t g = nullptr;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t nd = 0;
-  DCK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
-  cudaGraphConditionalHandle cond;
-  DCK(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
-  S.la.cond = cond;
-  const RoundMode mode = dt_mode(ctx, S);
   const DTree& t = S.t;
   dt_select_kernel<<<1, kSelThreads, 0, st>>>(t);
   dt_gather_kernel<<<gg, 256, 0, st>>>(t, disc);
@@ -790,6 +782,56 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
   dt_attach_kernel<<<1, 1024, 0, st>>>(t);
   dt_recount_kernel<<<1, 1024, 0, st>>>(t);
   dt_copy_kernel<<<gg, 256, 0, st>>>(t);
+  DCK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
+// With a simulate hook installed (the sharded multi-GPU driver) an iteration
+// is two graphs around the host call: pre (above) and post (backprop, stop).
+int dt_capture_hooked(ppg_ctx* ctx, DTreeState& S) {
+  cudaStream_t st = ctx->stream;
+  S.la.cond = 0;
+  S.la.round_mode = nullptr;
+  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  int rc = dt_launch_pre(ctx, S, st);
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(st, &g);
+  if (rc != PPG_SUCCESS) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  DCK(e);
+  S.graph = g;
+  DCK(cudaGraphInstantiate(&S.exec, S.graph, 0));
+  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  dt_backprop_kernel<<<1, 32, 0, st>>>(S.t);
+  dt_stop_kernel<<<1, 1, 0, st>>>(S.t);
+  DCK(cudaStreamEndCapture(st, &S.graph_post));
+  DCK(cudaGraphInstantiate(&S.exec_post, S.graph_post, 0));
+  return PPG_SUCCESS;
+}
+
+// Captures one PMBS iteration as a graph (select -> expand -> attach ->
+// lockstep WHILE -> backprop -> stop).
+int dt_capture(ppg_ctx* ctx, DTreeState& S) {
+  cudaStream_t st = ctx->stream;
+  const int E = S.n_envs;
+  if (!S.st2) DCK(cudaStreamCreateWithFlags(&S.st2, cudaStreamNonBlocking));
+  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  DCK(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphConditionalHandle cond;
+  DCK(cudaGraphConditionalHandleCreate(&cond, g, 0, 0));
+  S.la.cond = cond;
+  const RoundMode mode = dt_mode(ctx, S);
+  const DTree& t = S.t;
+  {
+    const int rc = dt_launch_pre(ctx, S, st);
+    if (rc != PPG_SUCCESS) return rc;
+  }
   lock_init_kernel<<<(E + 255) / 256, 256, 0, st>>>(S.C, S.la);
   lock_harvest_kernel<<<1, 1024, 0, st>>>(S.C, S.la);
   DCK(cudaGetLastError());
@@ -957,9 +999,9 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     key.append(reinterpret_cast<const char*>(&ctx->side), sizeof ctx->side);
     key.append(reinterpret_cast<const char*>(&ctx->margin), sizeof ctx->margin);
     // kernel-mode inputs (which kernels the graph holds)
-    const int modes[7] = {ctx->scene_all_discs ? 1 : 0, ctx->force_generic ? 1 : 0, ctx->warp_poly ? 1 : 0,
+    const int modes[8] = {ctx->scene_all_discs ? 1 : 0, ctx->force_generic ? 1 : 0, ctx->warp_poly ? 1 : 0,
                           ctx->warp_max_envs, ctx->warp_max_explicit ? 1 : 0, ctx->disc_kernels ? 1 : 0,
-                          ctx->hybrid_min_envs};
+                          ctx->hybrid_min_envs, ctx->sim_hook ? 1 : 0};
     key.append(reinterpret_cast<const char*>(modes), sizeof modes);
     if (S.key != key) S.release_graph();
     S.key = key;
@@ -1034,6 +1076,12 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
   const bool debug = dbg && dbg[0] == '1';
   const bool gdebug = dbg && dbg[0] == '2';  // graph mode, synchronize + check every launch
   bool regrown = false;
+  // simulate hook (sharded driver): rollouts by the caller between the two
+  // graphs of an iteration, per-pair rewards copied back as the harvest's bits
+  const bool hooked = ctx->sim_hook != nullptr;
+  int64_t hook_ctr[4] = {0, 0, 0, 0};
+  std::vector<double> h_cp, h_rew;
+  std::vector<int32_t> h_meta;
   const auto t_loop = std::chrono::steady_clock::now();
   for (;;) {
     // capacity for one more iteration (the host learns the sizes after each)
@@ -1075,11 +1123,11 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
       dt_views(ctx, S);
       regrown = true;
     }
-    if (debug) {
+    if (debug && !hooked) {
       if ((rc = dt_iteration_debug(ctx, S)) != PPG_SUCCESS) return rc;
       continue;
     }
-    if (!S.exec && (rc = dt_capture(ctx, S)) != PPG_SUCCESS) {
+    if (!S.exec && (rc = hooked ? dt_capture_hooked(ctx, S) : dt_capture(ctx, S)) != PPG_SUCCESS) {
       cudaStreamCaptureStatus cs;
       if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
         cudaGraph_t junk;
@@ -1091,6 +1139,31 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
       return rc;
     }
     DCK(cudaGraphLaunch(S.exec, st));
+    if (hooked) {
+      DTScal hs;
+      DCK(cudaMemcpyAsync(&hs, S.t.sc, sizeof hs, cudaMemcpyDeviceToHost, st));
+      DCK(cudaStreamSynchronize(st));
+      const int P = hs.n_pairs;
+      if (P > 0) {
+        h_cp.resize(static_cast<size_t>(P) * n * 3);
+        h_meta.resize(static_cast<size_t>(P) * 3);
+        h_rew.assign(P, 0.0);
+        DCK(cudaMemcpyAsync(h_cp.data(), S.t.cp, h_cp.size() * 8, cudaMemcpyDeviceToHost, st));
+        DCK(cudaMemcpyAsync(h_meta.data(), S.t.meta, h_meta.size() * 4, cudaMemcpyDeviceToHost, st));
+        DCK(cudaStreamSynchronize(st));
+        int64_t c4[4] = {0, 0, 0, 0};
+        rc = ctx->sim_hook(ctx->sim_hook_user, h_cp.data(), h_meta.data(), P, p.n_envs, p.leaf_parallel, p.rng_seed,
+                           static_cast<uint64_t>(hs.lock_dyn[3]), hs.lock_dyn[2], h_rew.data(), c4);
+        if (rc != PPG_SUCCESS) {
+          ctx->err = "simulate hook failed";
+          return rc;
+        }
+        for (int k = 0; k < 4; ++k) hook_ctr[k] += c4[k];
+        // backprop reads the rewards as the harvest's atomicMax bits
+        DCK(cudaMemcpyAsync(S.la.rew, h_rew.data(), static_cast<size_t>(P) * 8, cudaMemcpyHostToDevice, st));
+      }
+      DCK(cudaGraphLaunch(S.exec_post, st));
+    }
     if (gdebug) {
       const cudaError_t e = cudaStreamSynchronize(st);
       if (e != cudaSuccess) {
@@ -1125,6 +1198,7 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
   DCK(cudaMemcpyAsync(cpool.data(), S.t.cpool, static_cast<size_t>(h.a_used) * 4, cudaMemcpyDeviceToHost, st));
   DCK(cudaMemcpyAsync(ctr, S.la.counters, 32, cudaMemcpyDeviceToHost, st));
   DCK(cudaStreamSynchronize(st));
+  for (int k = 0; k < 4; ++k) ctr[k] += hook_ctr[k];
   // best_root_child (mcts.cpp:218-235)
   int best = -1;
   double best_score = -std::numeric_limits<double>::infinity();

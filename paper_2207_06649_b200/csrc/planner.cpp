@@ -360,13 +360,9 @@ int run(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_s
 
 extern "C" {
 
-// AUTO: the device tree unless a simulate hook (sharded driver) is installed.
-static bool use_device_tree(const ppg_ctx* ctx) {
-  const int mode = ppg::ctx_planner(ctx);
-  if (mode == PPG_PLANNER_HOST) return false;
-  if (mode == PPG_PLANNER_DEVICE) return true;
-  return ppg::ctx_sim_hook(ctx).fn == nullptr;
-}
+// AUTO and DEVICE: the device tree (with a simulate hook installed its
+// rollouts go through the hook); HOST: this file's tree.
+static bool use_device_tree(const ppg_ctx* ctx) { return ppg::ctx_planner(ctx) != PPG_PLANNER_HOST; }
 
 int ppg_run_pmbs(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats) {
   if (!ctx || !root_poses || !action_out) return PPG_EINVAL;

@@ -228,12 +228,16 @@ def sharded_simulate(shards, comm, node_poses, node_meta, n_envs: int, leaf_para
 
 class ShardedSimulateHook:
     """Installs sharded_simulate as the planner's batch_simulate
-    (ppg_set_simulate_hook), so ppg_run_pmbs on every rank runs the same host
-    tree with the rollout batch sharded across ranks."""
+    (ppg_set_simulate_hook), so ppg_run_pmbs on every rank runs the same tree
+    (device-resident by default, dtree.cu) with the rollout batch sharded
+    across ranks.  `extra_ctxs`: further local contexts that act as ranks
+    rank+1, rank+2, ... (in-process emulation of a wider world on one GPU;
+    their scene and parameters must match ctx's)."""
 
-    def __init__(self, ctx, comm, world: int, rank: int):
+    def __init__(self, ctx, comm, world: int, rank: int, extra_ctxs=()):
         self.ctx, self.comm, self.world, self.rank = ctx, comm, world, rank
         self.shard = DeviceShard(ctx)
+        self.shards = [self.shard] + [DeviceShard(c) for c in extra_ctxs]
         self.error = None
 
         def fn(user, node_poses, node_meta, n_nodes, n_envs, leaf_parallel, seed, iteration, depth_cap, rewards_out,
@@ -243,8 +247,8 @@ class ShardedSimulateHook:
                 poses = np.ctypeslib.as_array(node_poses, shape=(n_nodes, n, 3)).copy()
                 meta = np.ctypeslib.as_array(node_meta, shape=(n_nodes, 3)).copy()
                 used = n_envs if leaf_parallel else n_nodes
-                rng = [env_range(used, self.world, self.rank)]
-                r, c = sharded_simulate([self.shard], self.comm, poses, meta, n_envs, bool(leaf_parallel), seed,
+                rng = [env_range(used, self.world, self.rank + i) for i in range(len(self.shards))]
+                r, c = sharded_simulate(self.shards, self.comm, poses, meta, n_envs, bool(leaf_parallel), seed,
                                         iteration, depth_cap, rng)
                 np.ctypeslib.as_array(rewards_out, shape=(n_nodes,))[:] = r
                 if counters:

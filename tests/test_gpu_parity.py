@@ -306,22 +306,54 @@ def test_device_shards_reproduce_unsharded_lockstep(shards):
         c.close()
 
 
-def test_run_pmbs_through_sharded_hook():
-    """ppg_run_pmbs with the sharded simulate hook (1 rank) reproduces the
-    reference fingerprint: the multi-GPU planner path is the same algorithm."""
+@pytest.mark.parametrize("planner,shards", [("host", 1), ("device", 1), ("device", 3), ("host", 2)])
+def test_run_pmbs_through_sharded_hook(planner, shards):
+    """ppg_run_pmbs with the sharded simulate hook (`shards` ranks emulated in
+    one process) reproduces the reference fingerprint, with the tree on the
+    host or on the device: the multi-GPU planner path is the same algorithm."""
     from paper_2207_06649_b200.sharded import InProcessComm, ShardedSimulateHook
-    c = _ctx_with()
+    ctxs = [_ctx_with() for _ in range(shards)]
     cc, st = golden_io.cases()[12]
     d = cc["decision"]
     cfg = ParallelConfig(rng_seed=int(cc["seed"]))
-    c.set_params(cfg.to_params())
-    c.set_scene(st)
-    hook = ShardedSimulateHook(c, InProcessComm(), 1, 0)
-    r = run_pmbs(st, cfg, ctx=c)
+    for c in ctxs:
+        c.set_params(cfg.to_params())
+        c.set_scene(st)
+    c = ctxs[0]
+    c.set_planner(planner)
+    hook = ShardedSimulateHook(c, InProcessComm(), shards, 0, extra_ctxs=ctxs[1:])
+    r = run_pmbs(st, cfg, ctx=c, want_signature=True)
     hook.remove()
     assert hook.error is None
     assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
-    c.close()
+    r2 = run_pmbs(st, cfg, ctx=c, want_signature=True)  # the hook removed: built-in lockstep, same tree
+    assert r2.signature == r.signature
+    assert (r2.env_steps, r2.rollout_steps, r2.lockstep_rounds) == (r.env_steps, r.rollout_steps, r.lockstep_rounds)
+    for x in ctxs:
+        x.close()
+
+
+def test_device_tree_sharded_hook_wide():
+    """Device tree + 2 emulated shards on a wide batch (N_e = 2,000, dense
+    ring): same tree and counters as the unsharded device tree."""
+    from paper_2207_06649_b200.scenes import generate_case
+    from paper_2207_06649_b200.sharded import InProcessComm, ShardedSimulateHook
+    st = generate_case(16, 0.0, 3, "ring")
+    cfg = ParallelConfig(rng_seed=3, n_envs=2000, budget=Budget.iterations(3))
+    ctxs = [_ctx_with() for _ in range(2)]
+    for c in ctxs:
+        c.set_params(cfg.to_params())
+        c.set_scene(st)
+    base = run_pmbs(st, cfg, ctx=ctxs[0], want_signature=True)
+    hook = ShardedSimulateHook(ctxs[0], InProcessComm(), 2, 0, extra_ctxs=ctxs[1:])
+    r = run_pmbs(st, cfg, ctx=ctxs[0], want_signature=True)
+    hook.remove()
+    assert hook.error is None
+    assert r.signature == base.signature and list(r.action) == list(base.action)
+    assert (r.env_steps, r.rollout_steps, r.lockstep_rounds) == (base.env_steps, base.rollout_steps,
+                                                                 base.lockstep_rounds)
+    for c in ctxs:
+        c.close()
 
 
 def test_device_sincos_matches_glibc(ctx):
