@@ -66,7 +66,7 @@ PPG_DI PolyShape warp_load_any(WarpEnv& W, const WarpPoly& G, const double* pose
 }
 
 template <int NW, bool kPoly>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) resolve_warp_kernel(const __grid_constant__ SimConst C,
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kPoly ? 4 : 1) resolve_warp_kernel(const __grid_constant__ SimConst C,
                                                                           ResolveArgs a) {
   __shared__ double blk[kWarpsPerBlock][160];
   PPG_POLY_SMEM

@@ -37,6 +37,15 @@ constexpr int kPolyMaxN = 16;  // polygon latency mode: objects per scene
 
 namespace {
 
+// Code size matters here: with the narrow-phase body inlined once per
+// pair-mask word (and the contact motion, which holds a sincos, twice per
+// hit) the kernels grew past 500 KB of SASS and stalled on instruction fetch
+// (ncu: "no_instruction" 59 % of the cycles between issues, polygon
+// batch_resolve at 0.73 M env-steps/s).  The candidate sweep and the motion
+// are now loops emitting each body once (2.1 M env-steps/s); the final check
+// is out of line.
+#define PPG_NI __device__ __noinline__
+
 // Per-warp polygon caches (shared memory).
 struct WarpPoly {
   V2* wv;   // [kPolyMaxN][kMaxV] world vertices
@@ -242,9 +251,48 @@ PPG_DI void warp_apply_motion(const WarpEnv& W, const WarpPoly& G, const ShapeVi
   }
 }
 
+// Narrow test of candidate pair ij (object_pair_overlap, push_sim.cpp:20-32)
+// and, on a hit, the half-depth contact motion of both objects
+// (push_sim.cpp:109-116); uniform over the warp.  Returns the hit's object
+// mask (0: no hit) and raises *mp to the depth.
+PPG_DI unsigned warp_pair_poly(const WarpEnv& W, const WarpPoly& G, const PolyShape& O, const ShapeView& S,
+                               const SimConst& C, int ij, int l, double* mp) {
+  const int i = ij & 0xff, j = ij >> 8;
+  const int ki = __shfl_sync(kFull, O.kind, i), kj = __shfl_sync(kFull, O.kind, j);
+  const int ni = __shfl_sync(kFull, O.nv, i), nj = __shfl_sync(kFull, O.nv, j);
+  const double ri = __shfl_sync(kFull, O.r, i), rj = __shfl_sync(kFull, O.r, j);
+  const V2 pi_{W.x[i], W.y[i]}, pj_{W.x[j], W.y[j]};
+  Overlap o;
+  bool hit;
+  if (ki == 0 && kj == 0) {
+    o = disc_disc_overlap(pi_, ri, pj_, rj);
+    hit = o.depth > 0.0;
+  } else if (ki == 0) {
+    o = warp_disc_poly(G, j, nj, pi_, ri, l);
+    hit = o.depth > 0.0;
+  } else if (kj == 0) {
+    o = warp_disc_poly(G, i, ni, pj_, rj, l);
+    o.dir = -o.dir;
+    hit = o.depth > 0.0;
+  } else {
+    o = warp_poly_poly(G, i, ni, j, nj, l, &hit);
+    hit = hit && o.depth > 0.0;
+  }
+  if (!hit) return 0u;
+  // i then j (one copy of the motion code: it holds a sincos)
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const bool si = side == 0;
+    const V2 t = o.dir * (si ? -(0.5 * o.depth) : 0.5 * o.depth);
+    warp_apply_motion(W, G, S, si ? i : j, si ? ki : kj, si ? ni : nj, t, o.contact, C.gain, l);
+  }
+  *mp = dmax(*mp, o.depth);
+  return (1u << i) | (1u << j);
+}
+
 // Scalar object_pair_overlap depth (push_sim.cpp:20-32) on the caches, for
 // the final penetration check (one pair per lane).
-PPG_DI double lane_pair_depth(const WarpEnv& W, const WarpPoly& G, int a, int ka, int na, double ra, int b, int kb,
+PPG_NI double lane_pair_depth(const WarpEnv& W, const WarpPoly& G, int a, int ka, int na, double ra, int b, int kb,
                               int nb, double rb) {
   const V2 pa{W.x[a], W.y[a]}, pb{W.x[b], W.y[b]};
   if (ka == 0 && kb == 0) return disc_disc_overlap(pa, ra, pb, rb).depth;
@@ -375,53 +423,39 @@ PPG_DI int warp_resolve_poly(WarpEnv& W, const WarpPoly& G, const PolyShape& O, 
         const double ex = X[pa[w]] - X[pb[w]], ey = Y[pa[w]] - Y[pb[w]];
         cand[w] = __ballot_sync(kFull, om[w] != 0u && !(ex * ex + ey * ey > rr2[w]));
       }
-      // uniform lexicographic candidate sweep, narrow tests spread over lanes
+      // uniform lexicographic candidate sweep, narrow tests spread over lanes;
+      // the word loop is not unrolled (the narrow-phase body is emitted once,
+      // the per-word registers are picked by compare-select)
+      int w = 0;
+#pragma unroll 1
+      while (w < NW) {
+        unsigned cw = 0u;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        while (cand[w]) {
-          const int b = __ffs(cand[w]) - 1;
-          cand[w] &= cand[w] - 1;
-          const int p = 32 * w + b;
-          const int ij = pij[p];
-          const int i = ij & 0xff, j = ij >> 8;
-          const int ki = __shfl_sync(kFull, O.kind, i), kj = __shfl_sync(kFull, O.kind, j);
-          const int ni = __shfl_sync(kFull, O.nv, i), nj = __shfl_sync(kFull, O.nv, j);
-          const double ri = __shfl_sync(kFull, O.r, i), rj = __shfl_sync(kFull, O.r, j);
-          const V2 pi_{X[i], Y[i]}, pj_{X[j], Y[j]};
-          Overlap o;
-          bool hit;
-          if (ki == 0 && kj == 0) {
-            o = disc_disc_overlap(pi_, ri, pj_, rj);
-            hit = o.depth > 0.0;
-          } else if (ki == 0) {
-            o = warp_disc_poly(G, j, nj, pi_, ri, l);
-            hit = o.depth > 0.0;
-          } else if (kj == 0) {
-            o = warp_disc_poly(G, i, ni, pj_, rj, l);
-            o.dir = -o.dir;
-            hit = o.depth > 0.0;
-          } else {
-            o = warp_poly_poly(G, i, ni, j, nj, l, &hit);
-            hit = hit && o.depth > 0.0;
-          }
-          if (hit) {
-            warp_apply_motion(W, G, S, i, ki, ni, -o.dir * (0.5 * o.depth), o.contact, C.gain, l);
-            warp_apply_motion(W, G, S, j, kj, nj, o.dir * (0.5 * o.depth), o.contact, C.gain, l);
-            mp = dmax(mp, o.depth);
-            // re-test the later active pairs touching i or j
-            const unsigned hm = (1u << i) | (1u << j);
+        for (int v = 0; v < NW; ++v)
+          if (v == w) cw = cand[v];
+        if (!cw) {
+          ++w;
+          continue;
+        }
+        const int b = __ffs(cw) - 1;
 #pragma unroll
-            for (int v = w; v < NW; ++v) {
-              const bool touch = (om[v] & hm) != 0u && 32 * v + l > p;
-              const unsigned tm = __ballot_sync(kFull, touch);
-              if (tm) {
-                bool pass = false;
-                if (touch) {
-                  const double fx = X[pa[v]] - X[pb[v]], fy = Y[pa[v]] - Y[pb[v]];
-                  pass = !(fx * fx + fy * fy > rr2[v]);
-                }
-                cand[v] = (cand[v] & ~tm) | __ballot_sync(kFull, pass);
+        for (int v = 0; v < NW; ++v)
+          if (v == w) cand[v] = cw & (cw - 1);
+        const int p = 32 * w + b;
+        const unsigned hm = warp_pair_poly(W, G, O, S, C, pij[p], l, &mp);
+        if (hm) {
+          // re-test the later active pairs touching i or j
+#pragma unroll
+          for (int v = 0; v < NW; ++v) {
+            const bool touch = v >= w && (om[v] & hm) != 0u && 32 * v + l > p;
+            const unsigned tm = __ballot_sync(kFull, touch);
+            if (tm) {
+              bool pass = false;
+              if (touch) {
+                const double fx = X[pa[v]] - X[pb[v]], fy = Y[pa[v]] - Y[pb[v]];
+                pass = !(fx * fx + fy * fy > rr2[v]);
               }
+              cand[v] = (cand[v] & ~tm) | __ballot_sync(kFull, pass);
             }
           }
         }
