@@ -432,6 +432,39 @@ int lock_round_on(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const Reso
   return PPG_SUCCESS;
 }
 
+// Polygon batches (one warp per env): past one resident wave the grid is
+// persistent, warps taking envs from a counter (per-env cost varies by an
+// order of magnitude; fixed 4-warp blocks idled on their slowest env).
+template <int NW>
+static int launch_resolve_poly_t(ppg_ctx* ctx, const SimConst& C, ResolveArgs a, int E, cudaStream_t st, int slot) {
+  static int bps = -1;  // resident blocks per SM (a property of the kernel on this device)
+  if (bps < 0) {
+    int b = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, resolve_warp_kernel<NW, true>, kWarpsPerBlock * 32, 0));
+    bps = b > 0 ? b : 1;
+  }
+  const int want = (E + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int cap = bps * ctx->num_sms;
+  int grid = want;
+  if (want > cap) {
+    CK(ctx->b_counter.ensure(64));
+    a.work_counter = ctx->b_counter.as<int>() + 4 * slot;
+    CK(cudaMemsetAsync(a.work_counter, 0, 4, st));
+    grid = cap;
+  }
+  resolve_warp_kernel<NW, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(C, a);
+  CK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
+static int launch_resolve_poly(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, int E, cudaStream_t st,
+                               int slot) {
+  const int w = warp_words(n);
+  if (w == 1) return launch_resolve_poly_t<1>(ctx, C, a, E, st, slot);
+  if (w == 2) return launch_resolve_poly_t<2>(ctx, C, a, E, st, slot);
+  return launch_resolve_poly_t<4>(ctx, C, a, E, st, slot);
+}
+
 // Kernel #1 dispatch: all-disc batches (shapes without vertex tables) run the
 // register-resident persistent kernel (resolve_disc.cu) sized to the object
 // count; polygons, n > 16 and the counting variant run the generic kernel.
@@ -441,7 +474,8 @@ static int launch_resolve(ppg_ctx* ctx, const ShapesDev& S, bool all_discs, doub
   const SimConst C = make_const(ctx->params, S.n, side, margin);
   ResolveArgs a{S, d_in, d_push, d_out, d_status, d_resid, d_counts, E};
   if (!d_counts && use_warp(ctx, all_discs, S.n, E, false)) {
-    PPG_WARP_LAUNCH(resolve_warp_kernel, !all_discs, S.n, E, st, C, a);
+    if (!all_discs) return launch_resolve_poly(ctx, C, a, S.n, E, st, slot);
+    PPG_WARP_LAUNCH(resolve_warp_kernel, false, S.n, E, st, C, a);
     CK(cudaGetLastError());
     return PPG_SUCCESS;
   }

@@ -20,9 +20,11 @@ namespace ppg {
 #ifdef __CUDACC__
 #define PPG_DI __device__ __forceinline__
 #define PPG_HD __host__ __device__ __forceinline__
+#define PPG_ROLLED _Pragma("unroll 1")
 #else
 #define PPG_DI inline
 #define PPG_HD inline
+#define PPG_ROLLED
 #endif
 
 PPG_HD double inf_d() { return __builtin_huge_val(); }
@@ -89,32 +91,47 @@ constexpr int kMaxV = 8;
 struct Poly {
   int n;
   V2 p[kMaxV];
+  PPG_HD V2 v(int i) const { return p[i]; }
+};
+
+// The same polygon held elsewhere: the per-warp shared-memory vertex cache of
+// warp_poly.cuh.  The polygon functions below take either; their edge loops
+// stay rolled (each unrolled copy carried a division, and the inlined copies
+// made the polygon kernels overflow the instruction cache).
+struct PolyRef {
+  const V2* p;
+  int n;
+  PPG_HD V2 v(int i) const { return p[i]; }
 };
 
 // geometry.cpp:56-64
-PPG_HD bool point_in_convex(V2 p, const Poly& poly) {
+template <class PG>
+PPG_HD bool point_in_convex(V2 p, const PG& poly) {
+  PPG_ROLLED
   for (int i = 0; i < poly.n; ++i) {
-    const V2 a = poly.p[i];
-    const V2 b = poly.p[i + 1 == poly.n ? 0 : i + 1];
+    const V2 a = poly.v(i);
+    const V2 b = poly.v(i + 1 == poly.n ? 0 : i + 1);
     if (cross(b - a, p - a) < 0.0) return false;
   }
   return true;
 }
 
 // geometry.cpp:66-79
-PPG_HD V2 polygon_centroid(const Poly& poly) {
+template <class PG>
+PPG_HD V2 polygon_centroid(const PG& poly) {
   double area2 = 0.0;
   V2 c{0.0, 0.0};
+  PPG_ROLLED
   for (int i = 0; i < poly.n; ++i) {
-    const V2 a = poly.p[i];
-    const V2 b = poly.p[i + 1 == poly.n ? 0 : i + 1];
+    const V2 a = poly.v(i);
+    const V2 b = poly.v(i + 1 == poly.n ? 0 : i + 1);
     const double w = cross(a, b);
     area2 += w;
     const V2 t = (a + b) * w;
     c.x += t.x;
     c.y += t.y;
   }
-  if (area2 == 0.0) return poly.n == 0 ? V2{0.0, 0.0} : poly.p[0];
+  if (area2 == 0.0) return poly.n == 0 ? V2{0.0, 0.0} : poly.v(0);
   return c * (1.0 / (3.0 * area2));
 }
 
@@ -126,11 +143,13 @@ PPG_HD double support_extent(const Poly& poly, V2 dir) {
 }
 
 // geometry.cpp:87-100
-PPG_HD V2 closest_point_on_polygon(V2 p, const Poly& poly) {
+template <class PG>
+PPG_HD V2 closest_point_on_polygon(V2 p, const PG& poly) {
   V2 best{0.0, 0.0};
   double best_d = inf_d();
+  PPG_ROLLED
   for (int i = 0; i < poly.n; ++i) {
-    const V2 q = closest_point_on_segment(p, poly.p[i], poly.p[i + 1 == poly.n ? 0 : i + 1]);
+    const V2 q = closest_point_on_segment(p, poly.v(i), poly.v(i + 1 == poly.n ? 0 : i + 1));
     const double d = norm2(p - q);
     if (d < best_d) {
       best_d = d;
@@ -141,7 +160,8 @@ PPG_HD V2 closest_point_on_polygon(V2 p, const Poly& poly) {
 }
 
 // geometry.cpp:102-105
-PPG_HD double signed_dist_point_polygon(V2 p, const Poly& poly) {
+template <class PG>
+PPG_HD double signed_dist_point_polygon(V2 p, const PG& poly) {
   const double d = norm(p - closest_point_on_polygon(p, poly));
   return point_in_convex(p, poly) ? -d : d;
 }
@@ -164,7 +184,8 @@ PPG_HD Overlap disc_disc_overlap(V2 ca, double ra, V2 cb, double rb) {
 }
 
 // geometry.cpp:117-132
-PPG_HD Overlap disc_polygon_overlap(V2 c, double r, const Poly& poly) {
+template <class PG>
+PPG_HD Overlap disc_polygon_overlap(V2 c, double r, const PG& poly) {
   Overlap o;
   const V2 q = closest_point_on_polygon(c, poly);
   const V2 d = q - c;

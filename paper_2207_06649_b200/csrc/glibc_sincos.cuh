@@ -107,38 +107,46 @@ PPG_DI int reduce(double x, double& a, double& da) {
   return n;
 }
 
-PPG_DI double do_sincos(double a, double da, int n) {
-  const double r = (n & 1) ? do_cos(a, da) : do_sin(a, da);
-  return (n & 2) ? -r : r;
-}
 
 }  // namespace gsc
 
-// sincos (s_sincos.c) for |x| < 105414350.
+// sincos (s_sincos.c) for |x| < 105414350.  Every branch of the library
+// ends in do_sin and do_cos of one reduced argument (a, da); they are
+// evaluated once here and the quadrant picks and signs them, so the body
+// holds one copy of each (code size: this is inlined into every polygon
+// kernel).
 PPG_DI void glibc_sincos(double x, double* sinx, double* cosx) {
   const int k = __double2hiint(x) & 0x7fffffff;
-  if (k < 0x400368fd) {
-    if (k < 0x3e400000) {  // |x| < 2^-27
-      *sinx = x;
-      *cosx = 1.0;
-      return;
-    }
-    if (k < 0x3feb6000) {  // |x| < 0.855469
-      *sinx = gsc::do_sin(x, 0.0);
-      *cosx = gsc::do_cos(x, 0.0);
-      return;
-    }
-    const double y = gsc::hp0() - fabs(x);  // |x| < 2.426265
-    const double a = y + gsc::hp1();
-    const double da = (y - a) + gsc::hp1();
-    *sinx = copysign(gsc::do_cos(a, da), x);
-    *cosx = gsc::do_sin(a, da);
+  if (k < 0x3e400000) {  // |x| < 2^-27
+    *sinx = x;
+    *cosx = 1.0;
     return;
   }
   double a, da;
-  const int n = gsc::reduce(x, a, da);
-  *sinx = gsc::do_sincos(a, da, n);
-  *cosx = gsc::do_sincos(a, da, n + 1);
+  int n;
+  bool mid = false;
+  if (k < 0x3feb6000) {  // |x| < 0.855469: sin = do_sin(x, 0), cos = do_cos(x, 0)
+    a = x;
+    da = 0.0;
+    n = 0;
+  } else if (k < 0x400368fd) {  // |x| < 2.426265: sin = copysign(do_cos(a, da), x), cos = do_sin(a, da)
+    const double y = gsc::hp0() - fabs(x);
+    a = y + gsc::hp1();
+    da = (y - a) + gsc::hp1();
+    n = 1;
+    mid = true;
+  } else {  // quadrant n: sin = +-(n odd ? do_cos : do_sin), cos = the other, sign of quadrant n + 1
+    n = gsc::reduce(x, a, da);
+  }
+  const double s = gsc::do_sin(a, da), c = gsc::do_cos(a, da);
+  const double rs = (n & 1) ? c : s, rc = (n & 1) ? s : c;
+  if (mid) {
+    *sinx = copysign(rs, x);
+    *cosx = rc;
+    return;
+  }
+  *sinx = (n & 2) ? -rs : rs;
+  *cosx = ((n + 1) & 2) ? -rc : rc;
 }
 
 }  // namespace ppg

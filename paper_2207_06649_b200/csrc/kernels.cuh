@@ -32,6 +32,7 @@ struct ResolveArgs {
   int E;
   const int* idx = nullptr;    // optional env-slot indirection (lockstep / expand)
   const int* E_dev = nullptr;  // optional device-side count (overrides E)
+  int* work_counter = nullptr; // resolve_warp_kernel: persistent warps take envs from this counter
 };
 
 struct SampleArgs {

@@ -73,28 +73,35 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kPoly ? 4 : 1) resolve_wa
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
   build_pairs(pij, C.n);
   const int wib = threadIdx.x >> 5;
-  const int e = blockIdx.x * kWarpsPerBlock + wib;
   const int E = a.E_dev ? *a.E_dev : a.E;
-  if (e >= E) return;
-  const int ee = a.idx ? a.idx[e] : e;
-  WarpEnv W(blk[wib], C.n, static_cast<int>(threadIdx.x & 31));
-  const ShapeView S = a.S.view(a.S.T == 1 ? 0 : ee);
   const int n = C.n;
   const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
-  const PolyShape O = warp_load_any<kPoly>(W, G, a.poses_in + static_cast<size_t>(ee) * n * 3, S);
-  const double* pu = a.pushes + static_cast<size_t>(ee) * 4;
-  double residual = 0.0;
-  const int st = warp_resolve_any<NW, kPoly>(W, G, O, S, C, pij, V2{pu[0], pu[1]}, V2{pu[2], pu[3]}, true,
-                                             &residual);
-  if (W.lane == 0) {
-    a.status[ee] = st;
-    if (a.residual) a.residual[ee] = residual;
-  }
-  double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
-  if (st == 0) {
-    warp_store(W, out);
-  } else {
-    for (int i = W.lane; i < n * 3; i += 32) out[i] = 0.0;
+  // one env per warp; with a work counter the warps are persistent and take
+  // the next env when done (envs differ widely in cost)
+  for (int e = blockIdx.x * kWarpsPerBlock + wib; e < E;) {
+    const int ee = a.idx ? a.idx[e] : e;
+    WarpEnv W(blk[wib], n, static_cast<int>(threadIdx.x & 31));
+    const ShapeView S = a.S.view(a.S.T == 1 ? 0 : ee);
+    const PolyShape O = warp_load_any<kPoly>(W, G, a.poses_in + static_cast<size_t>(ee) * n * 3, S);
+    const double* pu = a.pushes + static_cast<size_t>(ee) * 4;
+    double residual = 0.0;
+    const int st = warp_resolve_any<NW, kPoly>(W, G, O, S, C, pij, V2{pu[0], pu[1]}, V2{pu[2], pu[3]}, true,
+                                               &residual);
+    if (W.lane == 0) {
+      a.status[ee] = st;
+      if (a.residual) a.residual[ee] = residual;
+    }
+    double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
+    if (st == 0) {
+      warp_store(W, out);
+    } else {
+      for (int i = W.lane; i < n * 3; i += 32) out[i] = 0.0;
+    }
+    if (!a.work_counter) break;
+    int nx = 0;
+    if (W.lane == 0) nx = atomicAdd(a.work_counter, 1);
+    e = gridDim.x * kWarpsPerBlock + __shfl_sync(kFull, nx, 0);
+    __syncwarp();  // the warp's shared blocks are reused by the next env
   }
 }
 

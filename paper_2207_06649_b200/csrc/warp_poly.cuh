@@ -68,14 +68,12 @@ PPG_DI void lane_poly(const WarpPoly& G, int i, int nv, Poly& out) {
 PPG_DI void lane_refresh(const WarpEnv& W, const WarpPoly& G, const ShapeView& S, int i, int nv) {
   const double s = W.view().s(i), c = W.view().c(i);
   const V2 pos{W.x[i], W.y[i]};
-  Poly p;
-  p.n = nv;
+  PPG_ROLLED
   for (int k = 0; k < nv; ++k) {
     const V2 v = S.vert(i, k);
-    p.p[k] = pos + V2{c * v.x - s * v.y, s * v.x + c * v.y};
-    G.wv[i * kMaxV + k] = p.p[k];
+    G.wv[i * kMaxV + k] = pos + V2{c * v.x - s * v.y, s * v.x + c * v.y};
   }
-  G.cen[i] = polygon_centroid(p);
+  G.cen[i] = polygon_centroid(PolyRef{G.wv + i * kMaxV, nv});
 }
 
 // Loads the trig cache and the world polygons of every polygon object (lane
@@ -242,9 +240,7 @@ PPG_DI void warp_apply_motion(const WarpEnv& W, const WarpPoly& G, const ShapeVi
   }
   __syncwarp();
   if (kind != 0) {
-    Poly p;
-    lane_poly(G, i, nv, p);
-    const V2 cen = polygon_centroid(p);  // identical in every lane
+    const V2 cen = polygon_centroid(PolyRef{G.wv + i * kMaxV, nv});  // identical in every lane
     __syncwarp();
     if (l == 0) G.cen[i] = cen;
     __syncwarp();
@@ -296,15 +292,9 @@ PPG_NI double lane_pair_depth(const WarpEnv& W, const WarpPoly& G, int a, int ka
                               int nb, double rb) {
   const V2 pa{W.x[a], W.y[a]}, pb{W.x[b], W.y[b]};
   if (ka == 0 && kb == 0) return disc_disc_overlap(pa, ra, pb, rb).depth;
+  if (ka == 0) return disc_polygon_overlap(pa, ra, PolyRef{G.wv + b * kMaxV, nb}).depth;
+  if (kb == 0) return disc_polygon_overlap(pb, rb, PolyRef{G.wv + a * kMaxV, na}).depth;
   Poly A, B;
-  if (ka == 0) {
-    lane_poly(G, b, nb, B);
-    return disc_polygon_overlap(pa, ra, B).depth;
-  }
-  if (kb == 0) {
-    lane_poly(G, a, na, A);
-    return disc_polygon_overlap(pb, rb, A).depth;
-  }
   lane_poly(G, a, na, A);
   lane_poly(G, b, nb, B);
   return polygon_polygon_overlap(A, B, false).depth;
@@ -336,9 +326,7 @@ PPG_DI int warp_resolve_poly(WarpEnv& W, const WarpPoly& G, const PolyShape& O, 
       if (O.kind == 0) {
         d = dmax(0.0, norm(start - V2{X[l], Y[l]}) - O.r);
       } else {
-        Poly p;
-        lane_poly(G, l, O.nv, p);
-        d = dmax(0.0, signed_dist_point_polygon(start, p));
+        d = dmax(0.0, signed_dist_point_polygon(start, PolyRef{G.wv + l * kMaxV, O.nv}));
       }
       col = d < rr;
     }
@@ -385,9 +373,7 @@ PPG_DI int warp_resolve_poly(WarpEnv& W, const WarpPoly& G, const PolyShape& O, 
           if (O.kind == 0) {
             o = disc_disc_overlap(tc, tr, pos, O.r);
           } else {
-            Poly p;
-            lane_poly(G, l, O.nv, p);
-            o = disc_polygon_overlap(tc, tr, p);
+            o = disc_polygon_overlap(tc, tr, PolyRef{G.wv + l * kMaxV, O.nv});
           }
           if (o.depth > 0.0) {
             const V2 t = o.dir * o.depth;
