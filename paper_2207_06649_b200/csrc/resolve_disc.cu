@@ -157,7 +157,13 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   double* const yl = dsm + NMAX * kDB + tid;
   double* const rl = dsm + 2 * NMAX * kDB + tid;
 
-  double x[NMAX], y[NMAX], r[NMAX];
+  // Float copies of the positions and margin-padded radii (r + m/2) for the
+  // broad-phase filters: every float test is a strict superset of the
+  // reference's FP64 test (margin m, set per environment), and every
+  // candidate is re-tested exactly in FP64 from shared memory, so results
+  // are unchanged while the uniform all-pairs work runs on the FP32 pipe.
+  float xf[NMAX], yf[NMAX], rm[NMAX];
+  float trm = 0.f, hclf = 0.f;
   double fx0[NMAX], fy0[NMAX];  // fixed-point check copies (local memory)
   uint32_t active = 0;
   Mask<W> pact;  // pairs with both objects active
@@ -183,29 +189,43 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         ee = a.idx ? a.idx[e] : e;  // environment slot (indirection for the lockstep engine)
         const double* src = a.poses_in + static_cast<size_t>(ee) * n * 3;
         const int t = a.S.T == 1 ? 0 : ee;
+        // poses -> shared memory (the exact FP64 copy) and float registers
+        // (broad-phase filters only); B bounds every coordinate / radius
+        double B = C.side / 2.0 + C.tip_r;
         static_for<NMAX>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           const bool real = i < n;
-          x[i] = real ? src[i * 3] : 0.0;
-          y[i] = real ? src[i * 3 + 1] : 0.0;
-          r[i] = real ? __ldg(a.S.rad + i * a.S.T + t) : 0.0;
-          xl[i * kDB] = x[i];
-          yl[i * kDB] = y[i];
-          rl[i * kDB] = r[i];
+          const double xi = real ? src[i * 3] : 0.0;
+          const double yi = real ? src[i * 3 + 1] : 0.0;
+          const double ri = real ? __ldg(a.S.rad + i * a.S.T + t) : 0.0;
+          xl[i * kDB] = xi;
+          yl[i * kDB] = yi;
+          rl[i * kDB] = ri;
+          xf[i] = static_cast<float>(xi);
+          yf[i] = static_cast<float>(yi);
+          B = fmax(B, fmax(fmax(fabs(xi), fabs(yi)), 4.0 * ri));
         });
         const double* pu = a.pushes + static_cast<size_t>(ee) * 4;
         start = V2{pu[0], pu[1]};
         const V2 end{pu[2], pu[3]};
+        B = fmax(B, fmax(fmax(fabs(start.x), fabs(start.y)), fmax(fabs(end.x), fabs(end.y))));
+        // filter margin: float rounding of coordinates <= B moves a distance
+        // by < 2^-20 B; 2^-15 B keeps the float tests strict supersets
+        const double m = B * 0x1p-15;
+        static_for<NMAX>([&](auto ic) {
+          constexpr int i = decltype(ic)::value;
+          rm[i] = static_cast<float>(rl[i * kDB] + 0.5 * m);
+        });
+        trm = static_cast<float>(tr + 0.5 * m);
+        hclf = static_cast<float>(hcl - m);
         // collides_gripper_start (world.cpp:154-164)
         bool collide = false;
         {
           const double rr = C.tip_r + C.tip_clear;
           const double h = C.side / 2.0;
           if (start.x - rr < -h || start.x + rr > h || start.y - rr < -h || start.y + rr > h) collide = true;
-          static_for<NMAX>([&](auto ic) {
-            constexpr int i = decltype(ic)::value;
-            if (i < n && dmax(0.0, norm(start - V2{x[i], y[i]}) - r[i]) < rr) collide = true;
-          });
+          for (int i = 0; i < n; ++i)
+            if (dmax(0.0, norm(start - V2{xl[i * kDB], yl[i * kDB]}) - rl[i * kDB]) < rr) collide = true;
         }
         if (collide) {
           a.status[ee] = 1;
@@ -217,16 +237,11 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         }
         delta = (end - start) * (1.0 / C.substeps);
         double max_diam = 0.0;
-        static_for<NMAX>([&](auto ic) {
-          constexpr int i = decltype(ic)::value;
-          if (i < n) max_diam = dmax(max_diam, 2.0 * r[i]);
-        });
+        for (int i = 0; i < n; ++i) max_diam = dmax(max_diam, 2.0 * rl[i * kDB]);
         const double reach = (C.push_distance + C.tip_r) + 2.0 * max_diam;
         active = 0;
-        static_for<NMAX>([&](auto ic) {
-          constexpr int i = decltype(ic)::value;
-          if (i < n && dist_point_segment(V2{x[i], y[i]}, start, end) <= reach + r[i]) active |= 1u << i;
-        });
+        for (int i = 0; i < n; ++i)
+          if (dist_point_segment(V2{xl[i * kDB], yl[i * kDB]}, start, end) <= reach + rl[i * kDB]) active |= 1u << i;
         pact.clear();
         static_for<P>([&](auto pc) {
           constexpr int p = decltype(pc)::value;
@@ -253,16 +268,19 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
       static_for<P>([&](auto pc) {
         constexpr int p = decltype(pc)::value;
         constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
-        const double dx = x[i] - x[j], dy = y[i] - y[j];
-        const double rr = r[i] + r[j];
-        if (j < n && !(dx * dx + dy * dy > rr * rr)) fin.w[p >> 6] |= 1ull << (p & 63);
+        const float dx = xf[i] - xf[j], dy = yf[i] - yf[j];
+        const float rr = rm[i] + rm[j];
+        if (j < n && !(__fmaf_rn(dx, dx, dy * dy) > rr * rr)) fin.w[p >> 6] |= 1ull << (p & 63);
       });
       double worst = 0.0;
       while (fin.any()) {
         const int ij = pij[fin.pop()];
         const int i = ij & 0xff, j = ij >> 8;
         const double bx = xl[i * kDB] - xl[j * kDB], by = yl[i * kDB] - yl[j * kDB];
-        worst = dmax(worst, rl[i * kDB] + rl[j * kDB] - sqrt(bx * bx + by * by));  // == norm(pos_j - pos_i)
+        const double rr = rl[i * kDB] + rl[j * kDB];
+        const double d2 = bx * bx + by * by;
+        if (d2 > rr * rr) continue;  // the exact FP64 filter
+        worst = dmax(worst, rr - sqrt(d2));  // == norm(pos_j - pos_i)
       }
       const int st = worst > C.eps_pen ? 2 : 0;
       a.status[ee] = st;
@@ -297,20 +315,26 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     }
     // 1-2. tip vs objects (push_sim.cpp:90-100)
     uint32_t tcand = 0;
-    static_for<NMAX>([&](auto ic) {
-      constexpr int i = decltype(ic)::value;
-      const double dx = x[i] - tc.x, dy = y[i] - tc.y;
-      const double reach = tr + r[i];
-      if ((active >> i & 1u) && !(dx * dx + dy * dy > reach * reach)) tcand |= 1u << i;
-    });
+    {
+      const float tcx = static_cast<float>(tc.x), tcy = static_cast<float>(tc.y);
+      static_for<NMAX>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        const float dx = xf[i] - tcx, dy = yf[i] - tcy;
+        const float reach = trm + rm[i];
+        if ((active >> i & 1u) && !(__fmaf_rn(dx, dx, dy * dy) > reach * reach)) tcand |= 1u << i;
+      });
+    }
     if (tcand) {
       do {
         const int i = __ffs(tcand) - 1;
         tcand &= tcand - 1;
         const double xi = xl[i * kDB], yi = yl[i * kDB], ri = rl[i * kDB];
         const double dx = xi - tc.x, dy = yi - tc.y;
-        const double dist = sqrt(dx * dx + dy * dy);
-        const double depth = tr + ri - dist;
+        const double reach = tr + ri;
+        const double d2 = dx * dx + dy * dy;
+        if (d2 > reach * reach) continue;  // the exact FP64 filter
+        const double dist = sqrt(d2);
+        const double depth = reach - dist;
         if (depth > 0.0) {
           double ux = 1.0, uy = 0.0;
           if (dist > 0.0) {
@@ -325,8 +349,8 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
       } while (tcand);
       static_for<NMAX>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        x[i] = xl[i * kDB];
-        y[i] = yl[i * kDB];
+        xf[i] = static_cast<float>(xl[i * kDB]);
+        yf[i] = static_cast<float>(yl[i * kDB]);
       });
     }
     // 3-4. object pairs, lexicographic Gauss-Seidel (push_sim.cpp:101-117)
@@ -339,10 +363,10 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     static_for<P>([&](auto pc) {
       constexpr int p = decltype(pc)::value;
       constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
-      const double dx = x[i] - x[j], dy = y[i] - y[j];
-      const double rr = r[i] + r[j];
-      const double d2 = dx * dx + dy * dy;
-      const double rn = rr + kNear;
+      const float dx = xf[i] - xf[j], dy = yf[i] - yf[j];
+      const float rr = rm[i] + rm[j];
+      const float d2 = __fmaf_rn(dx, dx, dy * dy);
+      const float rn = rr + static_cast<float>(kNear);
       if (!(d2 > rr * rr)) cand.w[p >> 6] |= 1ull << (p & 63);
       if (!(d2 > rn * rn)) near.w[p >> 6] |= 1ull << (p & 63);
     });
@@ -392,25 +416,30 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     }
     // 5. clamp every object (push_sim.cpp:118 -> :48-54).  clamp(v,-h,h) == v
     // whenever |v| <= h, so the clamp itself only runs for objects at a wall.
+    // The float test is conservative (hclf = hcl - m); objects near a wall
+    // take the exact path from shared memory.
     bool inside = true;
     static_for<NMAX>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       if (moved) {
-        x[i] = xl[i * kDB];
-        y[i] = yl[i * kDB];
+        xf[i] = static_cast<float>(xl[i * kDB]);
+        yf[i] = static_cast<float>(yl[i * kDB]);
       }
-      inside = inside && fabs(x[i]) <= hcl && fabs(y[i]) <= hcl;
+      inside = inside && fabsf(xf[i]) <= hclf && fabsf(yf[i]) <= hclf;
     });
     if (!inside) {
-      static_for<NMAX>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        const double cx = fclampd(x[i], -hcl, hcl), cy = fclampd(y[i], -hcl, hcl);
-        if (cx != x[i] || cy != y[i]) {
-          x[i] = cx;
-          y[i] = cy;
+      for (int i = 0; i < n; ++i) {
+        const double xi = xl[i * kDB], yi = yl[i * kDB];
+        const double cx = fclampd(xi, -hcl, hcl), cy = fclampd(yi, -hcl, hcl);
+        if (cx != xi || cy != yi) {
           xl[i * kDB] = cx;
           yl[i * kDB] = cy;
         }
+      }
+      static_for<NMAX>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        xf[i] = static_cast<float>(xl[i * kDB]);
+        yf[i] = static_cast<float>(yl[i * kDB]);
       });
     }
     // Fixed point: the iteration left every position bit-identical, so each
