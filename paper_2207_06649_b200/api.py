@@ -197,15 +197,25 @@ class Context:
         self._scene_key = key
 
     # ---- batched primitives -------------------------------------------------
-    def batch_resolve_arrays(self, table: Optional[ShapeTable], poses: np.ndarray, pushes: np.ndarray):
+    def batch_resolve_arrays(self, table: Optional[ShapeTable], poses: np.ndarray, pushes: np.ndarray, out=None):
+        """`out` = optional caller-owned (poses_out, status, residual) arrays;
+        pinned host buffers (e.g. numpy views of pinned torch tensors) let the
+        kernel write results directly (zero-copy output)."""
         poses = np.ascontiguousarray(poses, np.float64)
         pushes = np.ascontiguousarray(pushes, np.float64)
         E = poses.shape[0]
         if pushes.shape[0] != E:
             raise SimError("batch_resolve: states and pushes must have equal length")
-        out = np.empty_like(poses)
-        status = np.empty(E, np.int32)
-        resid = np.empty(E, np.float64)
+        if out is not None:
+            out, status, resid = out
+            if (out.shape != poses.shape or out.dtype != np.float64 or not out.flags.c_contiguous or
+                    status.shape != (E,) or status.dtype != np.int32 or resid.shape != (E,) or
+                    resid.dtype != np.float64):
+                raise ValueError("batch_resolve_arrays: out arrays must match the batch (f64 poses, i32, f64)")
+        else:
+            out = np.empty_like(poses)
+            status = np.empty(E, np.int32)
+            resid = np.empty(E, np.float64)
         sh = ctypes.byref(table.struct()) if table is not None else None
         self._check(self.lib.ppg_batch_resolve(self.ptr, sh, dptr(poses), dptr(pushes), E, dptr(out), iptr(status),
                                                dptr(resid)), "ppg_batch_resolve")

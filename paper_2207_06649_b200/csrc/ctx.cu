@@ -1,6 +1,7 @@
 // ctx.cu — the C-ABI (include/pushplan_gpu.h) over the sm_100a kernels:
 // context, device buffers, shape upload and the host loops that drive the
 // kernels.  The PMBS tree planner that sits on top lives in planner.cpp.
+#include <cuda.h>  // stream memory operation types (entry points resolved at run time)
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -152,7 +153,7 @@ bool for_each_disc_kernel(F&& f) {
   return true;
 }
 
-size_t disc_smem(int nmax) { return static_cast<size_t>(3) * nmax * kDiscBlock * sizeof(double); }
+size_t disc_smem(int nmax) { return static_cast<size_t>(4) * nmax * kDiscBlock * sizeof(double); }  // x | y | r | theta
 
 size_t smem_for(int n) { return static_cast<size_t>(kPosePlanes) * n * kBlock * sizeof(double); }
 
@@ -273,6 +274,10 @@ void ppg_destroy(ppg_ctx* ctx) {
                     &ctx->l_rew, &ctx->l_active, &ctx->l_nactive, &ctx->l_counters, &ctx->l_npose,
                     &ctx->l_nmeta, &ctx->b_counter, &ctx->l_push, &ctx->l_status, &ctx->l_stepping, &ctx->l_rec};
   for (DevBuf* b : bufs) b->release();
+  ctx->b_pipe.release();
+  for (cudaStream_t& s : ctx->pipe_stream)
+    if (s) cudaStreamDestroy(s);
+  if (ctx->pipe_ev) cudaEventDestroy(ctx->pipe_ev);
   dtree_release(ctx);
   for (int k = 0; k < kChunks; ++k) {
     ctx->chunk_in[k].release();
@@ -547,6 +552,184 @@ static int batch_resolve_chunk(ppg_ctx* ctx, const ppg_shapes* shapes, const dou
   return PPG_SUCCESS;
 }
 
+// Device address of a mapped pinned host buffer, or null (pageable memory).
+static void* mapped_host(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// Probes the streamed path once per context: PPG_STREAMED=0 disables it;
+// it needs the driver's stream memory operations.
+static bool streamed_available(ppg_ctx* ctx) {
+  if (ctx->streamed >= 0) return ctx->streamed == 1;
+  ctx->streamed = 0;
+  const char* v = std::getenv("PPG_STREAMED");
+  if (v && v[0] == '0') return false;
+  cudaDriverEntryPointQueryResult q1{}, q2{};
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &ctx->fn_write32, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWaitValue32", &ctx->fn_wait32, cudaEnableDefault, &q2) != cudaSuccess ||
+      q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !ctx->fn_write32 || !ctx->fn_wait32) {
+    cudaGetLastError();
+    return false;
+  }
+  for (cudaStream_t& st : ctx->pipe_stream)
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return false;
+  if (cudaEventCreateWithFlags(&ctx->pipe_ev, cudaEventDisableTiming) != cudaSuccess) return false;
+  if (ctx->b_pipe.ensure(2 * kMaxSlices * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(ctx->b_pipe.p, 0, 2 * kMaxSlices * sizeof(unsigned)) != cudaSuccess)
+    return false;
+  ctx->streamed = 1;
+  return true;
+}
+
+// Streamed host-buffer batch_resolve for disc batches: ONE persistent physics
+// launch (resolve_disc_kernel) overlaps every host<->device copy.
+//   copy-in stream: per slice, poses + pushes + radii (the host [E][n] radius
+//     layout is read as is: no shape transpose, no kind/target upload), then
+//     a stream write of `epoch` into the slice's ready flag;
+//   physics stream: launched once slice 0 is resident; lanes take envs in
+//     slice order and wait on the flag of an env's slice before loading it;
+//     every finished env bumps its slice's done counter;
+//   output: when poses_out / status / residual are pinned host buffers the
+//     kernel writes them directly (each finished env's poses in one
+//     warp-coalesced write), so the copy-back overlaps the physics env by env
+//     (PPG_ZC_OUT=0 disables); otherwise a copy-out stream waits per slice
+//     until the done counter reaches the slice's size and copies it back.
+// Results are element-wise, identical to the one-launch path
+// (tests/test_gpu_parity.py).
+static int batch_resolve_streamed(ppg_ctx* ctx, const ppg_shapes* sh, const double* poses_in, const double* pushes,
+                                  int E, double* poses_out, int32_t* status, double* residual) {
+  const int n = sh->n_objects;
+  const size_t row = static_cast<size_t>(n) * 3;
+  static const int per_slice = [] {
+    const char* v = std::getenv("PPG_SLICE_ENVS");  // experiments; default 8K envs per slice
+    return v && std::atoi(v) >= 256 ? std::atoi(v) : 8192;
+  }();
+  const int want = (E + per_slice - 1) / per_slice;
+  const int slices = want < 2 ? 2 : (want > kMaxSlices ? kMaxSlices : want);
+  // multiples of 16 envs: no cache line of any input array spans two slices
+  const int slice_envs = ((E + slices - 1) / slices + 15) / 16 * 16;
+  const int ns = (E + slice_envs - 1) / slice_envs;
+  CK(ctx->shape_in.ensure(static_cast<size_t>(E) * n * sizeof(double)));
+  double* rad = ctx->shape_in.as<double>();
+  unsigned* ready = ctx->b_pipe.as<unsigned>();
+  unsigned* done = ready + kMaxSlices;
+  const unsigned epoch = ++ctx->pipe_epoch == 0 ? ++ctx->pipe_epoch : ctx->pipe_epoch;
+  auto write32 = reinterpret_cast<WriteValue32Fn>(ctx->fn_write32);
+  auto wait32 = reinterpret_cast<WaitValue32Fn>(ctx->fn_wait32);
+  cudaStream_t in = ctx->pipe_stream[0], ph = ctx->pipe_stream[1], out = ctx->pipe_stream[2];
+  int* counter = ctx->b_counter.as<int>();
+  CK(cudaStreamSynchronize(ctx->stream));  // earlier work on the context stream
+  // PPG_STREAM_TRACE=1: per-stage event times to stderr (experiments)
+  static const bool trace = std::getenv("PPG_STREAM_TRACE") != nullptr;
+  cudaEvent_t tev[2 * kMaxSlices + 4] = {};
+  int ntev = 0;
+  auto mark = [&](cudaStream_t s) {
+    if (!trace) return;
+    cudaEventCreate(&tev[ntev]);
+    cudaEventRecord(tev[ntev++], s);
+  };
+  mark(in);
+  CK(cudaMemsetAsync(done, 0, kMaxSlices * sizeof(unsigned), in));
+  CK(cudaMemsetAsync(counter, 0, 4, in));
+  double* d_in = ctx->b_in.as<double>();
+  double* d_out = ctx->b_out.as<double>();
+  double* d_push = ctx->b_push.as<double>();
+  int32_t* d_st = ctx->b_status.as<int32_t>();
+  double* d_res = ctx->b_resid.as<double>();
+  for (int k = 0; k < ns; ++k) {
+    const size_t e0 = static_cast<size_t>(k) * slice_envs;
+    const size_t ek = (k + 1 == ns ? E : e0 + slice_envs) - e0;
+    CK(cudaMemcpyAsync(d_in + e0 * row, poses_in + e0 * row, ek * row * 8, cudaMemcpyHostToDevice, in));
+    CK(cudaMemcpyAsync(d_push + e0 * 4, pushes + e0 * 4, ek * 32, cudaMemcpyHostToDevice, in));
+    CK(cudaMemcpyAsync(rad + e0 * n, sh->radius + e0 * n, ek * n * 8, cudaMemcpyHostToDevice, in));
+    if (write32(reinterpret_cast<CUstream>(in), reinterpret_cast<CUdeviceptr>(ready + k), epoch,
+                CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+      ctx->err = "cuStreamWriteValue32 failed";
+      return PPG_ECUDA;
+    }
+    if (k == 0) CK(cudaEventRecord(ctx->pipe_ev, in));
+    mark(in);
+  }
+  // physics: one launch over all E envs once slice 0 is resident
+  CK(cudaStreamWaitEvent(ph, ctx->pipe_ev, 0));
+  const SimConst C = make_const(ctx->params, n, sh->side_length, sh->boundary_margin);
+  ShapesDev S;
+  S.rad = rad;
+  S.T = E;
+  S.n = n;
+  ResolveArgs a{S, d_in, d_push, d_out, d_st, d_res, nullptr, E};
+  a.ready = ready;
+  a.done = done;
+  a.epoch = epoch;
+  a.slice_envs = slice_envs;
+  a.rad_env_major = true;
+  static const bool zc_ok = [] {
+    const char* v = std::getenv("PPG_ZC_OUT");
+    return !(v && v[0] == '0');
+  }();
+  void* m_out = zc_ok ? mapped_host(poses_out) : nullptr;
+  void* m_st = zc_ok ? mapped_host(status) : nullptr;
+  void* m_res = zc_ok && residual ? mapped_host(residual) : nullptr;
+  if (m_out && m_st && (m_res || !residual)) {
+    a.poses_out = static_cast<double*>(m_out);
+    a.status = static_cast<int32_t*>(m_st);
+    a.residual = static_cast<double*>(m_res);
+    a.zc_out = true;
+    a.done = nullptr;
+  }
+  const int rc = launch_disc(ctx, C, a, n, E, ph, false, 0, false);
+  if (rc != PPG_SUCCESS) return rc;
+  mark(ph);
+  if (a.zc_out) {
+    CK(cudaStreamSynchronize(ph));
+    CK(cudaStreamSynchronize(in));
+    if (trace) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[ntev - 1]);
+      std::fprintf(stderr, "stream trace (zero-copy out): kernel done %.3f ms\n", ms);
+      for (int i = 0; i < ntev; ++i) cudaEventDestroy(tev[i]);
+    }
+    return PPG_SUCCESS;
+  }
+  // copy-out, slice by slice as each completes
+  CK(cudaStreamWaitEvent(out, ctx->pipe_ev, 0));  // after the done counters were zeroed
+  for (int k = 0; k < ns; ++k) {
+    const size_t e0 = static_cast<size_t>(k) * slice_envs;
+    const size_t ek = (k + 1 == ns ? E : e0 + slice_envs) - e0;
+    if (wait32(reinterpret_cast<CUstream>(out), reinterpret_cast<CUdeviceptr>(done + k), static_cast<cuuint32_t>(ek),
+               CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+      ctx->err = "cuStreamWaitValue32 failed";
+      return PPG_ECUDA;
+    }
+    CK(cudaMemcpyAsync(poses_out + e0 * row, d_out + e0 * row, ek * row * 8, cudaMemcpyDeviceToHost, out));
+    CK(cudaMemcpyAsync(status + e0, d_st + e0, ek * 4, cudaMemcpyDeviceToHost, out));
+    if (residual) CK(cudaMemcpyAsync(residual + e0, d_res + e0, ek * 8, cudaMemcpyDeviceToHost, out));
+    mark(out);
+  }
+  CK(cudaStreamSynchronize(out));
+  CK(cudaStreamSynchronize(ph));
+  if (trace) {
+    std::fprintf(stderr, "stream trace (ms from start): in");
+    for (int i = 1; i < ntev; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      std::fprintf(stderr, i == ns + 1 ? " | kernel %.3f | out" : " %.3f", ms);
+    }
+    std::fprintf(stderr, "\n");
+    for (int i = 0; i < ntev; ++i) cudaEventDestroy(tev[i]);
+  }
+  return PPG_SUCCESS;
+}
+
 int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in, const double* pushes,
                       int E, double* poses_out, int32_t* status, double* residual) {
   if (!ctx || E < 0) return PPG_EINVAL;
@@ -573,6 +756,9 @@ int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* pose
   CK(ctx->b_status.ensure(static_cast<size_t>(E) * sizeof(int32_t)));
   CK(ctx->b_resid.ensure(static_cast<size_t>(E) * sizeof(double)));
   CK(ctx->b_counter.ensure(64));
+  if (E >= kPipelineMinEnvs && shapes && shapes->n_tables == E && host_all_discs(shapes) && use_disc(ctx, true, n) &&
+      !use_warp(ctx, true, n, E, false) && streamed_available(ctx))
+    return batch_resolve_streamed(ctx, shapes, poses_in, pushes, E, poses_out, status, residual);
   const int chunks = E >= kPipelineMinEnvs ? kChunks : 1;
   if (chunks == 1) {
     int rc = batch_resolve_chunk(ctx, shapes, poses_in, pushes, 0, E, poses_out, status, residual, ctx->stream, 0);

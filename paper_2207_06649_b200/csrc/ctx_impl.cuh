@@ -34,6 +34,7 @@ __global__ void lock_step_warp_kernel(const __grid_constant__ SimConst C, LockAr
 constexpr int kWarpMaxN = 23;
 constexpr int kPolyMaxN = 16;  // warp_poly.cuh
 constexpr int kChunks = 4;     // slices of a pipelined host-buffer batch_resolve
+constexpr int kMaxSlices = 32; // slices of a streamed host-buffer batch_resolve
 constexpr int kWarpsPerBlock = 4;
 // pair-mask words of the latency-mode kernels (warp_env.cuh warp_words_for)
 constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 : 8; }
@@ -164,7 +165,18 @@ struct ppg_ctx {
   int hybrid_min_envs = 8192;            // lockstep rounds with >= this many active envs (discs, n <= 16)
                                           // run the hybrid warp-sampler / lane-physics round; PPG_HYBRID_MIN
   bool warp_max_explicit = false;        // PPG_WARP_MAX given: a hard cap for every scene type
-  bool warp_poly = true;                  // polygon scenes in latency mode; PPG_WARP_POLY=0 disables               // latency mode (one warp per env) up to this many envs; PPG_WARP_MAX
+  bool warp_poly = true;                  // polygon scenes in latency mode; PPG_WARP_POLY=0 disables
+  // streamed batch_resolve (host buffers, disc batches): ONE physics launch
+  // overlapping the slice copies; stream memory operations (driver API)
+  // signal "slice k resident" to the kernel and "slice k finished" to the
+  // copy-back stream
+  ppg::DevBuf b_pipe;                    // ready flags [kMaxSlices] | done counters [kMaxSlices]
+  unsigned pipe_epoch = 0;
+  int streamed = -1;                      // -1 not probed, 0 off (PPG_STREAMED=0 / no stream mem ops), 1 on
+  void* fn_write32 = nullptr;             // cuStreamWriteValue32
+  void* fn_wait32 = nullptr;              // cuStreamWaitValue32
+  cudaStream_t pipe_stream[3] = {};       // host->device copies, physics, device->host copies
+  cudaEvent_t pipe_ev = nullptr;          // slice 0 resident
 };
 
 SimConst make_const(const ppg_params& p, int n, double side, double margin);

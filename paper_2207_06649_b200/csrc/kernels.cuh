@@ -33,6 +33,16 @@ struct ResolveArgs {
   const int* idx = nullptr;    // optional env-slot indirection (lockstep / expand)
   const int* E_dev = nullptr;  // optional device-side count (overrides E)
   int* work_counter = nullptr; // resolve_warp_kernel: persistent warps take envs from this counter
+  // streamed host batches (resolve_disc_kernel): inputs arrive slice by slice
+  // while the kernel runs; slice k = env / slice_envs
+  const unsigned* ready = nullptr;  // [slices]: == epoch once slice k's inputs are resident
+  unsigned* done = nullptr;         // [slices]: finished envs (the copy-back stream waits on it)
+  unsigned epoch = 0;
+  int slice_envs = 0;
+  bool rad_env_major = false;       // S.rad in the host layout [E][n] instead of [n][T]
+  // poses_out / status / residual are mapped pinned HOST memory: each
+  // finished env's poses leave in one warp-coalesced write (no copy-back)
+  bool zc_out = false;
 };
 
 struct SampleArgs {

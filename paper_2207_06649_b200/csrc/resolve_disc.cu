@@ -120,6 +120,21 @@ struct Mask {
 constexpr double kNear = 0.002;  // metres, the re-queue filter margin
 constexpr int kFixK = 6;         // check for a fixed point from this iteration of a substep on
 
+// Streamed batches: is the slice holding env e resident?  (The copy stream
+// writes `epoch` into its flag after the slice's copies.)
+PPG_DI bool slice_ready(const ResolveArgs& a, int e) {
+  const unsigned* f = a.ready + e / a.slice_envs;
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v == a.epoch;
+}
+
+// Streamed batches: env e's outputs are written; count it for its slice.
+PPG_DI void slice_done(const ResolveArgs& a, int e) {
+  __threadfence();
+  atomicAdd(a.done + e / a.slice_envs, 1u);
+}
+
 PPG_DI double fclampd(double v, double lo, double hi) {
   // == std::clamp(v, lo, hi) for non-NaN v (positions are finite)
   return fmin(fmax(v, lo), hi);
@@ -132,7 +147,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
                                                                int* next_env) {
   constexpr int P = NMAX * (NMAX - 1) / 2;
   constexpr int W = (P + 63) / 64;
-  extern __shared__ double dsm[];  // [x | y | r][NMAX][kDB]
+  extern __shared__ double dsm[];  // [x | y | r | theta (zc_out only)][NMAX][kDB]
   __shared__ uint16_t pij[P];  // i | j << 8
   __shared__ uint64_t omask[NMAX][W];  // pairs touching object k
 
@@ -156,6 +171,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   double* const xl = dsm + tid;
   double* const yl = dsm + NMAX * kDB + tid;
   double* const rl = dsm + 2 * NMAX * kDB + tid;
+  double* const tl = dsm + 3 * NMAX * kDB + tid;
 
   // Float copies of the positions and margin-padded radii (r + m/2) for the
   // broad-phase filters: every float test is a strict superset of the
@@ -175,17 +191,67 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   // same number of environments; the rest are fetched with one atomic each.
   const int per = min(kDB, (E + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x));
   const int total_threads = gridDim.x * per;
-  int e = tid < per ? blockIdx.x * per + tid : INT_MAX;
+  // Streamed batches: warp-major (warp w of every block before warp w+1; 32
+  // consecutive envs per warp), so the first slices' envs are spread over
+  // every SM and a warp's lanes mostly share one slice.
+  int e = INT_MAX;
+  if (tid < per) {
+    if (a.ready) {
+      const int w = tid >> 5, lanes = min(32, per - (w << 5));
+      e = (w << 5) * static_cast<int>(gridDim.x) + static_cast<int>(blockIdx.x) * lanes + (tid & 31);
+    } else {
+      e = blockIdx.x * per + tid;
+    }
+  }
+  const int rs_i = a.rad_env_major ? 1 : a.S.T;  // radius strides (object, table)
+  const int rs_t = a.rad_env_major ? n : 1;
   int ee = e;
   bool have = false;
   bool need_init = true;
+  bool pending = false;  // streamed: this lane's next env is in a slice not yet resident
+  int zc_env = 0, zc_kind = 0, zc_st = 0;  // zc_out: finished env awaiting its flush (1 poses, 2 zeros)
+  double zc_res = 0.0;
+  const int lane = tid & 31;
+  double* const xw = dsm + (tid - lane);  // this warp's shared-memory columns
+  double* const yw = dsm + NMAX * kDB + (tid - lane);
+  double* const tw = dsm + 3 * NMAX * kDB + (tid - lane);
 
   while (true) {
+    // ---- zc_out: the warp writes each just-finished env's poses to host
+    // memory, one contiguous [n][3] record per env (consecutive lanes ->
+    // consecutive doubles), before the lane's columns are re-used
+    if (a.zc_out) {
+      unsigned m = __ballot_sync(0xffffffffu, zc_kind != 0);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const int se = __shfl_sync(0xffffffffu, zc_env, src);
+        const int sk = __shfl_sync(0xffffffffu, zc_kind, src);
+        const int sst = __shfl_sync(0xffffffffu, zc_st, src);
+        const double sres = __shfl_sync(0xffffffffu, zc_res, src);
+        double* dst = a.poses_out + static_cast<size_t>(se) * n * 3;
+        for (int q = lane; q < n * 3; q += 32) {
+          const int obj = q / 3, c = q - 3 * obj;
+          double v = 0.0;
+          if (sk == 1) v = (c == 0 ? xw : c == 1 ? yw : tw)[obj * kDB + src];
+          dst[q] = v;
+        }
+        if (lane == 0) a.status[se] = sst;
+        if (lane == 1 && a.residual) a.residual[se] = sres;
+      }
+      zc_kind = 0;
+    }
     // ---- environment init: load, precondition, active mask (push_sim.cpp:58-82)
     if (need_init) {
       need_init = false;
       have = false;
+      pending = false;
       while (e < E) {
+        if (a.ready && !slice_ready(a, e)) {  // retried on the next pass; the warp runs on
+          pending = true;
+          need_init = true;
+          break;
+        }
         ee = a.idx ? a.idx[e] : e;  // environment slot (indirection for the lockstep engine)
         const double* src = a.poses_in + static_cast<size_t>(ee) * n * 3;
         const int t = a.S.T == 1 ? 0 : ee;
@@ -195,19 +261,22 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         static_for<NMAX>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           const bool real = i < n;
-          const double xi = real ? src[i * 3] : 0.0;
-          const double yi = real ? src[i * 3 + 1] : 0.0;
-          const double ri = real ? __ldg(a.S.rad + i * a.S.T + t) : 0.0;
+          // inputs are read once, through L2 (.cg: streamed slices are
+          // written by the copy engine while the kernel runs)
+          const double xi = real ? __ldcg(src + i * 3) : 0.0;
+          const double yi = real ? __ldcg(src + i * 3 + 1) : 0.0;
+          const double ri = real ? __ldcg(a.S.rad + static_cast<size_t>(i) * rs_i + static_cast<size_t>(t) * rs_t) : 0.0;
           xl[i * kDB] = xi;
           yl[i * kDB] = yi;
           rl[i * kDB] = ri;
           xf[i] = static_cast<float>(xi);
           yf[i] = static_cast<float>(yi);
+          if (a.zc_out) tl[i * kDB] = real ? __ldcg(src + i * 3 + 2) : 0.0;
           B = fmax(B, fmax(fmax(fabs(xi), fabs(yi)), 4.0 * ri));
         });
         const double* pu = a.pushes + static_cast<size_t>(ee) * 4;
-        start = V2{pu[0], pu[1]};
-        const V2 end{pu[2], pu[3]};
+        start = V2{__ldcg(pu), __ldcg(pu + 1)};
+        const V2 end{__ldcg(pu + 2), __ldcg(pu + 3)};
         B = fmax(B, fmax(fmax(fabs(start.x), fabs(start.y)), fmax(fabs(end.x), fabs(end.y))));
         // filter margin: float rounding of coordinates <= B moves a distance
         // by < 2^-20 B; 2^-15 B keeps the float tests strict supersets
@@ -228,10 +297,18 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
             if (dmax(0.0, norm(start - V2{xl[i * kDB], yl[i * kDB]}) - rl[i * kDB]) < rr) collide = true;
         }
         if (collide) {
-          a.status[ee] = 1;
-          if (a.residual) a.residual[ee] = 0.0;
-          double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
-          for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
+          if (a.zc_out && zc_kind == 0) {  // flushed by the warp
+            zc_env = ee;
+            zc_kind = 2;
+            zc_st = 1;
+            zc_res = 0.0;
+          } else {  // (also a second pending env of this lane: written by the lane itself)
+            a.status[ee] = 1;
+            if (a.residual) a.residual[ee] = 0.0;
+            double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
+            for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
+          }
+          if (a.done) slice_done(a, e);
           e = atomicAdd(next_env, 1) + total_threads;
           continue;
         }
@@ -255,8 +332,11 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         break;
       }
     }
-    if (!__any_sync(0xffffffffu, have)) break;
-    if (!have) continue;
+    if (!__any_sync(0xffffffffu, have || pending)) break;
+    if (!have) {
+      if (pending) __nanosleep(200);
+      continue;
+    }
 
     if (step > C.substeps) {
       // ---- final all-pairs penetration check + output (push_sim.cpp:123-128,
@@ -283,18 +363,26 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         worst = dmax(worst, rr - sqrt(d2));  // == norm(pos_j - pos_i)
       }
       const int st = worst > C.eps_pen ? 2 : 0;
-      a.status[ee] = st;
-      if (a.residual) a.residual[ee] = worst;
       double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
-      if (st == 0) {
-        for (int i = 0; i < n; ++i) {
-          out[i * 3] = xl[i * kDB];
-          out[i * 3 + 1] = yl[i * kDB];
-          out[i * 3 + 2] = a.poses_in[(static_cast<size_t>(ee) * n + i) * 3 + 2];  // discs never rotate (in place: same value)
-        }
+      if (a.zc_out && zc_kind == 0) {  // flushed by the warp at the top of the loop
+        zc_env = ee;
+        zc_kind = st == 0 ? 1 : 2;
+        zc_st = st;
+        zc_res = worst;
       } else {
-        for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
+        a.status[ee] = st;
+        if (a.residual) a.residual[ee] = worst;
+        if (st == 0) {
+          for (int i = 0; i < n; ++i) {
+            out[i * 3] = xl[i * kDB];
+            out[i * 3 + 1] = yl[i * kDB];
+            out[i * 3 + 2] = __ldcg(a.poses_in + (static_cast<size_t>(ee) * n + i) * 3 + 2);  // discs never rotate (in place: same value)
+          }
+        } else {
+          for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
+        }
       }
+      if (a.done) slice_done(a, e);
       e = atomicAdd(next_env, 1) + total_threads;
       need_init = true;
       have = false;
