@@ -153,7 +153,10 @@ bool for_each_disc_kernel(F&& f) {
   return true;
 }
 
-size_t disc_smem(int nmax) { return static_cast<size_t>(4) * nmax * kDiscBlock * sizeof(double); }  // x | y | r | theta
+// resolve_disc_kernel: doubles x | y | r | theta (theta for nmax <= 14), floats xf | yf
+size_t disc_smem(int nmax) {
+  return (static_cast<size_t>(nmax <= 14 ? 4 : 3) * sizeof(double) + 2 * sizeof(float)) * nmax * kDiscBlock;
+}
 
 size_t smem_for(int n) { return static_cast<size_t>(kPosePlanes) * n * kBlock * sizeof(double); }
 

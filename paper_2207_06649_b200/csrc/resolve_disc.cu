@@ -147,7 +147,11 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
                                                                int* next_env) {
   constexpr int P = NMAX * (NMAX - 1) / 2;
   constexpr int W = (P + 63) / 64;
-  extern __shared__ double dsm[];  // [x | y | r | theta (zc_out only)][NMAX][kDB]
+  // dynamic shared memory (disc_smem): doubles [x | y | r | theta][NMAX][kDB]
+  // (theta only for NMAX <= 14), then the float shadows [xf | yf][NMAX][kDB]
+  // of x / y, written together with them (no conversions on the refreshes)
+  extern __shared__ double dsm[];
+  constexpr int kDPlanes = NMAX <= 14 ? 4 : 3;
   __shared__ uint16_t pij[P];  // i | j << 8
   __shared__ uint64_t omask[NMAX][W];  // pairs touching object k
 
@@ -171,7 +175,9 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   double* const xl = dsm + tid;
   double* const yl = dsm + NMAX * kDB + tid;
   double* const rl = dsm + 2 * NMAX * kDB + tid;
-  double* const tl = dsm + 3 * NMAX * kDB + tid;
+  double* const tl = dsm + 3 * NMAX * kDB + tid;  // (kDPlanes == 4 only)
+  float* const xs = reinterpret_cast<float*>(dsm + kDPlanes * NMAX * kDB) + tid;
+  float* const ys = xs + NMAX * kDB;
 
   // Float copies of the positions and margin-padded radii (r + m/2) for the
   // broad-phase filters: every float test is a strict superset of the
@@ -233,7 +239,9 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         for (int q = lane; q < n * 3; q += 32) {
           const int obj = q / 3, c = q - 3 * obj;
           double v = 0.0;
-          if (sk == 1) v = (c == 0 ? xw : c == 1 ? yw : tw)[obj * kDB + src];
+          if (sk == 1)
+            v = c < 2 || kDPlanes == 4 ? (c == 0 ? xw : c == 1 ? yw : tw)[obj * kDB + src]
+                                       : __ldcg(a.poses_in + static_cast<size_t>(se) * n * 3 + q);
           dst[q] = v;
         }
         if (lane == 0) a.status[se] = sst;
@@ -271,7 +279,9 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
           rl[i * kDB] = ri;
           xf[i] = static_cast<float>(xi);
           yf[i] = static_cast<float>(yi);
-          if (a.zc_out) tl[i * kDB] = real ? __ldcg(src + i * 3 + 2) : 0.0;
+          xs[i * kDB] = xf[i];
+          ys[i * kDB] = yf[i];
+          if (kDPlanes == 4) tl[i * kDB] = real ? __ldcg(src + i * 3 + 2) : 0.0;
           B = fmax(B, fmax(fmax(fabs(xi), fabs(yi)), 4.0 * ri));
         });
         const double* pu = a.pushes + static_cast<size_t>(ee) * 4;
@@ -376,7 +386,8 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
           for (int i = 0; i < n; ++i) {
             out[i * 3] = xl[i * kDB];
             out[i * 3 + 1] = yl[i * kDB];
-            out[i * 3 + 2] = __ldcg(a.poses_in + (static_cast<size_t>(ee) * n + i) * 3 + 2);  // discs never rotate (in place: same value)
+            out[i * 3 + 2] = kDPlanes == 4 ? tl[i * kDB]  // discs never rotate (in place: same value)
+                                            : __ldcg(a.poses_in + (static_cast<size_t>(ee) * n + i) * 3 + 2);
           }
         } else {
           for (int i = 0; i < n * 3; ++i) out[i] = 0.0;
@@ -430,15 +441,18 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
             ux = dx * inv;
             uy = dy * inv;
           }
-          xl[i * kDB] = xi + ux * depth;
-          yl[i * kDB] = yi + uy * depth;
+          const double nx = xi + ux * depth, ny = yi + uy * depth;
+          xl[i * kDB] = nx;
+          yl[i * kDB] = ny;
+          xs[i * kDB] = static_cast<float>(nx);
+          ys[i * kDB] = static_cast<float>(ny);
           max_pen = dmax(max_pen, depth);
         }
       } while (tcand);
       static_for<NMAX>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        xf[i] = static_cast<float>(xl[i * kDB]);
-        yf[i] = static_cast<float>(yl[i * kDB]);
+        xf[i] = xs[i * kDB];
+        yf[i] = ys[i * kDB];
       });
     }
     // 3-4. object pairs, lexicographic Gauss-Seidel (push_sim.cpp:101-117)
@@ -487,10 +501,15 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         }
         const double s = 0.5 * depth;
         const double mx = ux * s, my = uy * s;
-        xl[i * kDB] = xi - mx;
-        yl[i * kDB] = yi - my;
-        xl[j * kDB] = xj + mx;
-        yl[j * kDB] = yj + my;
+        const double nxi = xi - mx, nyi = yi - my, nxj = xj + mx, nyj = yj + my;
+        xl[i * kDB] = nxi;
+        yl[i * kDB] = nyi;
+        xl[j * kDB] = nxj;
+        yl[j * kDB] = nyj;
+        xs[i * kDB] = static_cast<float>(nxi);
+        ys[i * kDB] = static_cast<float>(nyi);
+        xs[j * kDB] = static_cast<float>(nxj);
+        ys[j * kDB] = static_cast<float>(nyj);
         max_pen = dmax(max_pen, depth);
         moved = true;
         // i and j moved: every LATER active pair touching them is re-queued
@@ -510,8 +529,8 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     static_for<NMAX>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       if (moved) {
-        xf[i] = static_cast<float>(xl[i * kDB]);
-        yf[i] = static_cast<float>(yl[i * kDB]);
+        xf[i] = xs[i * kDB];
+        yf[i] = ys[i * kDB];
       }
       inside = inside && fabsf(xf[i]) <= hclf && fabsf(yf[i]) <= hclf;
     });
@@ -522,12 +541,14 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         if (cx != xi || cy != yi) {
           xl[i * kDB] = cx;
           yl[i * kDB] = cy;
+          xs[i * kDB] = static_cast<float>(cx);
+          ys[i * kDB] = static_cast<float>(cy);
         }
       }
       static_for<NMAX>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        xf[i] = static_cast<float>(xl[i * kDB]);
-        yf[i] = static_cast<float>(yl[i * kDB]);
+        xf[i] = xs[i * kDB];
+        yf[i] = ys[i * kDB];
       });
     }
     // Fixed point: the iteration left every position bit-identical, so each
