@@ -184,7 +184,15 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
   // reference's FP64 test (margin m, set per environment), and every
   // candidate is re-tested exactly in FP64 from shared memory, so results
   // are unchanged while the uniform all-pairs work runs on the FP32 pipe.
-  float xf[NMAX], yf[NMAX], rm[NMAX];
+  // Stored as float2 pairs (objects 2m, 2m+1) so the broad phases run on the
+  // packed FP32x2 pipe (sm_100 FFMA2/FADD2/FMUL2): XF(i) / YF(i) / RM(i).
+  constexpr int NP = (NMAX + 1) / 2;
+  float2 xp[NP], yp[NP], rp[NP];
+#define XF(i) ((((i) & 1) ? xp[(i) >> 1].y : xp[(i) >> 1].x))
+#define YF(i) ((((i) & 1) ? yp[(i) >> 1].y : yp[(i) >> 1].x))
+#define RM(i) ((((i) & 1) ? rp[(i) >> 1].y : rp[(i) >> 1].x))
+#pragma unroll
+  for (int k = 0; k < NP; ++k) xp[k] = yp[k] = rp[k] = make_float2(0.f, 0.f);
   float trm = 0.f, hclf = 0.f;
   double fx0[NMAX], fy0[NMAX];  // fixed-point check copies (local memory)
   uint32_t active = 0;
@@ -277,10 +285,10 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
           xl[i * kDB] = xi;
           yl[i * kDB] = yi;
           rl[i * kDB] = ri;
-          xf[i] = static_cast<float>(xi);
-          yf[i] = static_cast<float>(yi);
-          xs[i * kDB] = xf[i];
-          ys[i * kDB] = yf[i];
+          XF(i) = static_cast<float>(xi);
+          YF(i) = static_cast<float>(yi);
+          xs[i * kDB] = XF(i);
+          ys[i * kDB] = YF(i);
           if (kDPlanes == 4) tl[i * kDB] = real ? __ldcg(src + i * 3 + 2) : 0.0;
           B = fmax(B, fmax(fmax(fabs(xi), fabs(yi)), 4.0 * ri));
         });
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
         const double m = B * 0x1p-15;
         static_for<NMAX>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
-          rm[i] = static_cast<float>(rl[i * kDB] + 0.5 * m);
+          RM(i) = static_cast<float>(rl[i * kDB] + 0.5 * m);
         });
         trm = static_cast<float>(tr + 0.5 * m);
         hclf = static_cast<float>(hcl - m);
@@ -358,8 +366,8 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
       static_for<P>([&](auto pc) {
         constexpr int p = decltype(pc)::value;
         constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
-        const float dx = xf[i] - xf[j], dy = yf[i] - yf[j];
-        const float rr = rm[i] + rm[j];
+        const float dx = XF(i) - XF(j), dy = YF(i) - YF(j);
+        const float rr = RM(i) + RM(j);
         if (j < n && !(__fmaf_rn(dx, dx, dy * dy) > rr * rr)) fin.w[p >> 6] |= 1ull << (p & 63);
       });
       double worst = 0.0;
@@ -416,12 +424,18 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     uint32_t tcand = 0;
     {
       const float tcx = static_cast<float>(tc.x), tcy = static_cast<float>(tc.y);
-      static_for<NMAX>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        const float dx = xf[i] - tcx, dy = yf[i] - tcy;
-        const float reach = trm + rm[i];
-        if ((active >> i & 1u) && !(__fmaf_rn(dx, dx, dy * dy) > reach * reach)) tcand |= 1u << i;
+      const float2 tx2 = make_float2(tcx, tcx), ty2 = make_float2(tcy, tcy), tr2 = make_float2(trm, trm);
+      const float2 m1 = make_float2(-1.f, -1.f);
+      static_for<NP>([&](auto mc) {
+        constexpr int mm = decltype(mc)::value;
+        const float2 dx = __ffma2_rn(tx2, m1, xp[mm]), dy = __ffma2_rn(ty2, m1, yp[mm]);
+        const float2 reach = __fadd2_rn(tr2, rp[mm]);
+        const float2 d2 = __ffma2_rn(dx, dx, __fmul2_rn(dy, dy));
+        const float2 q = __fmul2_rn(reach, reach);
+        if (!(d2.x > q.x)) tcand |= 1u << (2 * mm);
+        if (2 * mm + 1 < NMAX && !(d2.y > q.y)) tcand |= 1u << (2 * mm + 1);
       });
+      tcand &= active;
     }
     if (tcand) {
       do {
@@ -451,8 +465,8 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
       } while (tcand);
       static_for<NMAX>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        xf[i] = xs[i * kDB];
-        yf[i] = ys[i * kDB];
+        XF(i) = xs[i * kDB];
+        YF(i) = ys[i * kDB];
       });
     }
     // 3-4. object pairs, lexicographic Gauss-Seidel (push_sim.cpp:101-117)
@@ -462,16 +476,41 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     Mask<W> cand, near;
     cand.clear();
     near.clear();
-    static_for<P>([&](auto pc) {
-      constexpr int p = decltype(pc)::value;
-      constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
-      const float dx = xf[i] - xf[j], dy = yf[i] - yf[j];
-      const float rr = rm[i] + rm[j];
-      const float d2 = __fmaf_rn(dx, dx, dy * dy);
-      const float rn = rr + static_cast<float>(kNear);
-      if (!(d2 > rr * rr)) cand.w[p >> 6] |= 1ull << (p & 63);
-      if (!(d2 > rn * rn)) near.w[p >> 6] |= 1ull << (p & 63);
-    });
+    {
+      // row i: pair (i, i+1) alone when i+1 is odd, then couples (j, j+1)
+      // with j even, so {XF(j), XF(j+1)} is the stored float2
+      const float2 m1 = make_float2(-1.f, -1.f);
+      const float2 kn2 = make_float2(static_cast<float>(kNear), static_cast<float>(kNear));
+      static_for<NMAX>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        constexpr int p0 = i * (2 * NMAX - i - 1) / 2;  // pair (i, i+1)
+        const float2 xi2 = make_float2(XF(i), XF(i)), yi2 = make_float2(YF(i), YF(i));
+        const float2 ri2 = make_float2(RM(i), RM(i));
+        static_for<NMAX>([&](auto jc) {
+          constexpr int j = decltype(jc)::value;
+          constexpr int p = p0 + (j - i - 1);
+          if constexpr (j > i && (j & 1) == 0 && j + 1 < NMAX) {
+            const float2 dx = __ffma2_rn(xp[j >> 1], m1, xi2), dy = __ffma2_rn(yp[j >> 1], m1, yi2);
+            const float2 rr = __fadd2_rn(ri2, rp[j >> 1]);
+            const float2 d2 = __ffma2_rn(dx, dx, __fmul2_rn(dy, dy));
+            const float2 q = __fmul2_rn(rr, rr);
+            const float2 rn = __fadd2_rn(rr, kn2);
+            const float2 qn = __fmul2_rn(rn, rn);
+            if (!(d2.x > q.x)) cand.w[p >> 6] |= 1ull << (p & 63);
+            if (!(d2.y > q.y)) cand.w[(p + 1) >> 6] |= 1ull << ((p + 1) & 63);
+            if (!(d2.x > qn.x)) near.w[p >> 6] |= 1ull << (p & 63);
+            if (!(d2.y > qn.y)) near.w[(p + 1) >> 6] |= 1ull << ((p + 1) & 63);
+          } else if constexpr (j > i && ((j == i + 1 && (j & 1) == 1) || ((j & 1) == 0 && j + 1 == NMAX))) {
+            const float dx = XF(i) - XF(j), dy = YF(i) - YF(j);
+            const float rr = RM(i) + RM(j);
+            const float d2 = __fmaf_rn(dx, dx, dy * dy);
+            const float rn = rr + static_cast<float>(kNear);
+            if (!(d2 > rr * rr)) cand.w[p >> 6] |= 1ull << (p & 63);
+            if (!(d2 > rn * rn)) near.w[p >> 6] |= 1ull << (p & 63);
+          }
+        });
+      });
+    }
 #pragma unroll
     for (int k = 0; k < W; ++k) {
       cand.w[k] &= pact.w[k];
@@ -529,10 +568,10 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
     static_for<NMAX>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
       if (moved) {
-        xf[i] = xs[i * kDB];
-        yf[i] = ys[i * kDB];
+        XF(i) = xs[i * kDB];
+        YF(i) = ys[i * kDB];
       }
-      inside = inside && fabsf(xf[i]) <= hclf && fabsf(yf[i]) <= hclf;
+      inside = inside && fabsf(XF(i)) <= hclf && fabsf(YF(i)) <= hclf;
     });
     if (!inside) {
       for (int i = 0; i < n; ++i) {
@@ -547,8 +586,8 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
       }
       static_for<NMAX>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        xf[i] = xs[i * kDB];
-        yf[i] = ys[i * kDB];
+        XF(i) = xs[i * kDB];
+        YF(i) = ys[i * kDB];
       });
     }
     // Fixed point: the iteration left every position bit-identical, so each
@@ -567,6 +606,9 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(c
       iter = 0;
     }
   }
+#undef XF
+#undef YF
+#undef RM
 }
 
 #define PPG_DISC_INST(N)                                                                                       \
