@@ -368,14 +368,13 @@ bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
   return all_discs && n <= 16 && ctx->disc_kernels && !ctx->force_generic;
 }
 
-// Latency mode: one warp per environment (warp_env.cu) for small batches.
-// Latency mode (one warp per env) vs the lane-per-env kernels.  For PMBS
-// work (expansion, lockstep rounds: sample + pick + resolve + graspable per
+// Latency mode (one warp per env, warp_env.cu) vs the lane-per-env kernels.
+// For PMBS work (expansion, lockstep rounds: sample + pick + resolve + graspable per
 // env-step) latency mode always wins — its sampler and graspable run across
 // the lanes, and a round costs its slowest env-step (measured: case_18 at
 // N_e = 16K, 1.02 s -> 0.44 s).  For plain batch_resolve throughput the
-// lane-per-env disc kernel wins above 4,096 envs (discs, n <= 16); scenes
-// without it (discs with n > 16, polygons) stay in latency mode.
+// lane-per-env disc kernel (discs, n <= 16) wins above 2,048 envs (measured
+// with 10 and 16 discs); scenes without it (discs with n > 16, polygons) stay in latency mode.
 // PPG_WARP_MAX, if set, caps latency mode everywhere.
 bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs) {
   if (ctx->force_generic) return false;

@@ -161,7 +161,7 @@ struct ppg_ctx {
   DevBuf chunk_in[ppg::kChunks], chunk_buf[ppg::kChunks];
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
-  int warp_max_envs = 4096;
+  int warp_max_envs = 2048;             // batch_resolve on discs (n <= 16): latency mode up to this many envs; PPG_WARP_MAX
   int hybrid_min_envs = 8192;            // lockstep rounds with >= this many active envs (discs, n <= 16)
                                           // run the hybrid warp-sampler / lane-physics round; PPG_HYBRID_MIN
   bool warp_max_explicit = false;        // PPG_WARP_MAX given: a hard cap for every scene type
