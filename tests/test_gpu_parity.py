@@ -509,3 +509,39 @@ def test_streamed_host_batch_resolve_equals_chunked(ctx, monkeypatch):
     assert np.array_equal(st[idx], s3)
     ok = s3 == 0
     assert _bitwise(out[idx][ok], o3[ok]).all()
+
+
+@pytest.mark.parametrize("n", [2, 5, 10, 13, 16])
+def test_disc_kernel_walls_and_wild_inputs(n):
+    """The lane kernel's float broad-phase filters and conservative clamp test
+    on inputs the scene generator never makes: objects overlapping each other,
+    at / beyond the walls (clamped on the first iteration), pushes into the
+    walls, pushes starting far outside the workspace (the per-env margin
+    scales with the largest coordinate) and zero-length pushes — bitwise
+    against the oracle in lane, latency and generic mode."""
+    rng = np.random.default_rng(100 + n)
+    E = 2500
+    h = 0.144
+    poses = np.zeros((E, n, 3))
+    poses[:, :, 0:2] = rng.uniform(-1.15 * h, 1.15 * h, (E, n, 2))
+    poses[:, :, 2] = rng.uniform(-3.1, 3.1, (E, n))
+    wall = rng.random((E, n)) < 0.3  # snap to a wall
+    poses[:, :, 0] = np.where(wall, np.sign(poses[:, :, 0]) * (h - 1e-9 - rng.uniform(0, 2e-4, (E, n))), poses[:, :, 0])
+    radius = rng.uniform(0.008, 0.03, (E, n))
+    ang = rng.uniform(-np.pi, np.pi, E)
+    start = rng.uniform(-h, h, (E, 2))
+    far = rng.random(E) < 0.05
+    start[far] *= 40.0
+    length = np.where(rng.random(E) < 0.05, 0.0, rng.uniform(0.01, 0.08, E))
+    end = start + length[:, None] * np.stack([np.cos(ang), np.sin(ang)], 1)
+    pushes = np.ascontiguousarray(np.concatenate([start, end], 1))
+    t = ShapeTable(np.zeros((E, n), np.int32), np.ascontiguousarray(radius), np.zeros((E, n), np.int32),
+                   np.zeros((E, n, 8, 2)), np.zeros(E, np.int32), 0.288, 0.0, n, E)
+    o3, s3, r3 = port.batch_resolve(t, poses, pushes, P)
+    for mode in ("lane", "warp", "generic"):
+        c = _ctx_with(**MODES[mode])
+        out, st, res = c.batch_resolve_arrays(t, poses, pushes)
+        c.close()
+        assert np.array_equal(st, s3), mode
+        assert _bitwise(out, o3).all(), mode
+        assert np.array_equal(res.view(np.uint64), r3.view(np.uint64)), mode
