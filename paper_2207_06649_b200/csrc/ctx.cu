@@ -143,9 +143,11 @@ bool for_each_disc_kernel(F&& f) {
 #define PPG_DISC_FN(N, X) reinterpret_cast<const void*>(&resolve_disc_kernel<N, X>)
   const void* fns[2][kNumDisc] = {
       {PPG_DISC_FN(4, false), PPG_DISC_FN(6, false), PPG_DISC_FN(8, false), PPG_DISC_FN(10, false),
-       PPG_DISC_FN(11, false), PPG_DISC_FN(12, false), PPG_DISC_FN(14, false), PPG_DISC_FN(16, false)},
+       PPG_DISC_FN(11, false), PPG_DISC_FN(12, false), PPG_DISC_FN(14, false), PPG_DISC_FN(16, false),
+       PPG_DISC_FN(18, false), PPG_DISC_FN(20, false)},
       {PPG_DISC_FN(4, true), PPG_DISC_FN(6, true), PPG_DISC_FN(8, true), PPG_DISC_FN(10, true),
-       PPG_DISC_FN(11, true), PPG_DISC_FN(12, true), PPG_DISC_FN(14, true), PPG_DISC_FN(16, true)}};
+       PPG_DISC_FN(11, true), PPG_DISC_FN(12, true), PPG_DISC_FN(14, true), PPG_DISC_FN(16, true),
+       PPG_DISC_FN(18, true), PPG_DISC_FN(20, true)}};
 #undef PPG_DISC_FN
   for (int v = 1; v >= 0; --v)  // occupancy is taken from the last call: the plain variant
     for (int k = 0; k < kNumDisc; ++k)
@@ -357,7 +359,9 @@ int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, in
     case 11: PPG_DISC_LAUNCH(11); break;
     case 12: PPG_DISC_LAUNCH(12); break;
     case 14: PPG_DISC_LAUNCH(14); break;
-    default: PPG_DISC_LAUNCH(16); break;
+    case 16: PPG_DISC_LAUNCH(16); break;
+    case 18: PPG_DISC_LAUNCH(18); break;
+    default: PPG_DISC_LAUNCH(20); break;
   }
 #undef PPG_DISC_LAUNCH
   CK(cudaGetLastError());
@@ -365,7 +369,7 @@ int launch_disc(ppg_ctx* ctx, const SimConst& C, const ResolveArgs& a, int n, in
 }
 
 bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
-  return all_discs && n <= 16 && ctx->disc_kernels && !ctx->force_generic;
+  return all_discs && n <= kDiscMaxN && ctx->disc_kernels && !ctx->force_generic;
 }
 
 // Latency mode (one warp per env, warp_env.cu) vs the lane-per-env kernels.
@@ -373,7 +377,7 @@ bool use_disc(const ppg_ctx* ctx, bool all_discs, int n) {
 // env-step) latency mode always wins — its sampler and graspable run across
 // the lanes, and a round costs its slowest env-step (measured: case_18 at
 // N_e = 16K, 1.02 s -> 0.44 s).  For plain batch_resolve throughput the
-// lane-per-env disc kernel (discs, n <= 16) wins above 2,048 envs (measured
+// lane-per-env disc kernel (discs, n <= kDiscMaxN) wins above 2,048 envs (measured
 // with 10 and 16 discs); scenes without it (discs with n > 16, polygons) stay in latency mode.
 // PPG_WARP_MAX, if set, caps latency mode everywhere.
 bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs) {
@@ -381,13 +385,13 @@ bool use_warp(const ppg_ctx* ctx, bool all_discs, int n, int envs, bool pmbs) {
   const bool shape_ok = all_discs ? n <= kWarpMaxN : (ctx->warp_poly && n <= kPolyMaxN);
   if (!shape_ok) return false;
   if (ctx->warp_max_explicit) return envs <= ctx->warp_max_envs;
-  if (!pmbs && all_discs && n <= 16 && ctx->disc_kernels) return envs <= ctx->warp_max_envs;
+  if (!pmbs && all_discs && n <= kDiscMaxN && ctx->disc_kernels) return envs <= ctx->warp_max_envs;
   return true;
 }
 
 RoundMode round_mode(const ppg_ctx* ctx, int n, int envs) {
   if (use_warp(ctx, ctx->scene_all_discs, n, envs, true)) {
-    const bool hybrid_ok = ctx->scene_all_discs && n <= 16 && ctx->disc_kernels && !ctx->warp_max_explicit;
+    const bool hybrid_ok = ctx->scene_all_discs && n <= kDiscMaxN && ctx->disc_kernels && !ctx->warp_max_explicit;
     return hybrid_ok && envs >= ctx->hybrid_min_envs ? RoundMode::kHybrid : RoundMode::kWarp;
   }
   if (use_disc(ctx, ctx->scene_all_discs, n)) return RoundMode::kLaneDisc;

@@ -71,8 +71,9 @@ __global__ void resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveA
 
 constexpr int kBlock = 128;
 constexpr int kDiscBlock = 128;  // resolve_disc.cu kDB
-constexpr int kNumDisc = 8;
-constexpr int kDiscSizes[kNumDisc] = {4, 6, 8, 10, 11, 12, 14, 16};
+constexpr int kNumDisc = 10;
+constexpr int kDiscSizes[kNumDisc] = {4, 6, 8, 10, 11, 12, 14, 16, 18, 20};
+constexpr int kDiscMaxN = 20;  // the lane-per-env disc kernel's largest object count
 constexpr size_t kMaxSmem = kPosePlanes * kMaxObjects * kBlock * sizeof(double);
 
 }  // namespace ppg
@@ -161,8 +162,8 @@ struct ppg_ctx {
   DevBuf chunk_in[ppg::kChunks], chunk_buf[ppg::kChunks];
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
-  int warp_max_envs = 2048;             // batch_resolve on discs (n <= 16): latency mode up to this many envs; PPG_WARP_MAX
-  int hybrid_min_envs = 8192;            // lockstep rounds with >= this many active envs (discs, n <= 16)
+  int warp_max_envs = 2048;             // batch_resolve on discs (n <= kDiscMaxN): latency mode up to this many envs; PPG_WARP_MAX
+  int hybrid_min_envs = 8192;            // lockstep rounds with >= this many active envs (discs, n <= kDiscMaxN)
                                           // run the hybrid warp-sampler / lane-physics round; PPG_HYBRID_MIN
   bool warp_max_explicit = false;        // PPG_WARP_MAX given: a hard cap for every scene type
   bool warp_poly = true;                  // polygon scenes in latency mode; PPG_WARP_POLY=0 disables

@@ -143,7 +143,7 @@ PPG_DI double fclampd(double v, double lo, double hi) {
 }  // namespace
 
 template <int NMAX, bool kFix>
-__global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : 3) resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a,
+__global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) resolve_disc_kernel(const __grid_constant__ SimConst C, ResolveArgs a,
                                                                int* next_env) {
   constexpr int P = NMAX * (NMAX - 1) / 2;
   constexpr int W = (P + 63) / 64;
@@ -622,6 +622,8 @@ PPG_DISC_INST(11)
 PPG_DISC_INST(12)
 PPG_DISC_INST(14)
 PPG_DISC_INST(16)
+PPG_DISC_INST(18)
+PPG_DISC_INST(20)
 #undef PPG_DISC_INST
 
 }  // namespace ppg
