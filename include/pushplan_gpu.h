@@ -144,7 +144,11 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes);
 /* batch_resolve (push_sim.hpp:48-51, push_sim.cpp:132-152): element-wise
  * resolve_push (push_sim.cpp:58-130) with per-element status; never aborts
  * siblings.  residual[e] = final max pairwise penetration (NULL allowed).
- * shapes == NULL uses the context scene.  Synchronous w.r.t. host buffers. */
+ * shapes == NULL uses the context scene.  Synchronous w.r.t. host buffers.
+ * All-disc batches of >= 32K envs with per-env shapes are streamed (the
+ * copies overlap one physics launch); when poses_out / status / residual are
+ * pinned host memory (cudaHostAlloc, pinned torch tensors) the kernel writes
+ * the results into them directly.  Pageable buffers work too (copy-back). */
 int ppg_batch_resolve(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses_in,
                       const double* pushes, int E, double* poses_out, int32_t* status,
                       double* residual);

@@ -545,3 +545,39 @@ def test_disc_kernel_walls_and_wild_inputs(n):
         assert np.array_equal(st, s3), mode
         assert _bitwise(out, o3).all(), mode
         assert np.array_equal(res.view(np.uint64), r3.view(np.uint64)), mode
+
+
+@pytest.mark.parametrize("n", [16, 20])
+def test_streamed_zero_copy_large_object_counts(n, monkeypatch):
+    """Streamed + zero-copy output with records longer than a warp (3n > 32
+    doubles per env; n > 14 has no theta plane, so theta is re-read from the
+    device input): identical to the chunked path, pinned outputs, 33K envs of
+    random clutter (walls, overlaps, start collisions)."""
+    import torch
+    from paper_2207_06649_b200 import Context
+    rng = np.random.default_rng(7 + n)
+    E, h = 33003, 0.144
+    poses = np.zeros((E, n, 3))
+    poses[:, :, 0:2] = rng.uniform(-h, h, (E, n, 2))
+    poses[:, :, 2] = rng.uniform(-3.1, 3.1, (E, n))
+    radius = rng.uniform(0.006, 0.016, (E, n))
+    ang = rng.uniform(-np.pi, np.pi, E)
+    start = rng.uniform(-0.12, 0.12, (E, 2))
+    end = start + 0.05 * np.stack([np.cos(ang), np.sin(ang)], 1)
+    pushes = np.ascontiguousarray(np.concatenate([start, end], 1))
+    t = ShapeTable(np.zeros((E, n), np.int32), np.ascontiguousarray(radius), np.zeros((E, n), np.int32),
+                   np.zeros((E, n, 8, 2)), np.zeros(E, np.int32), 0.288, 0.0, n, E)
+    c1 = Context(0, P)
+    po = torch.empty(poses.shape, dtype=torch.float64).pin_memory().numpy()
+    ps = torch.empty((E,), dtype=torch.int32).pin_memory().numpy()
+    pr = torch.empty((E,), dtype=torch.float64).pin_memory().numpy()
+    c1.batch_resolve_arrays(t, poses, pushes, out=(po, ps, pr))
+    c1.close()
+    monkeypatch.setenv("PPG_STREAMED", "0")
+    c2 = Context(0, P)
+    o2, s2, r2 = c2.batch_resolve_arrays(t, poses, pushes)
+    c2.close()
+    assert len(np.unique(s2)) >= 2
+    assert np.array_equal(ps, s2)
+    assert _bitwise(po, o2).all()
+    assert np.array_equal(pr.view(np.uint64), r2.view(np.uint64))
