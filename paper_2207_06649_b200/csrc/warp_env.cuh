@@ -153,6 +153,31 @@ PPG_DI bool pair_eval(const double* X, const double* Y, int a, int b, double rr2
 //    holds many touched pairs.
 // A candidate whose narrow test finds no overlap changes nothing, so the
 // speculative variant keeps hit masks only.
+// pair_eval without branches (same results): the re-tests of both words
+// after a hit run as two independent dependency chains that overlap.
+// (`live` = the lane re-tests this pair; other lanes take a benign 1.0 so
+// no lane enters the sqrt / reciprocal special-case paths: d2 = 0 for the
+// padding pairs)
+PPG_DI bool pair_eval_bf(const double* X, const double* Y, int a, int b, double rr2, double rsum, bool live,
+                         double& nxa, double& nya, double& nxb, double& nyb, double& depth) {
+  const double xa = X[a], ya = Y[a], xb = X[b], yb = Y[b];
+  const double ex = xa - xb, ey = ya - yb;
+  const double d2 = live ? ex * ex + ey * ey : 1.0;
+  const double dist = sqrt(d2);  // == norm(pos_b - pos_a)
+  depth = rsum - dist;
+  const bool pos = dist > 0.0;
+  const double inv = __drcp_rn(pos ? dist : 1.0);  // == 1.0 / dist
+  const double ux = pos ? (xb - xa) * inv : 1.0;
+  const double uy = pos ? (yb - ya) * inv : 0.0;
+  const double s = 0.5 * depth;
+  const double mx = ux * s, my = uy * s;
+  nxa = xa - mx;
+  nya = ya - my;
+  nxb = xb + mx;
+  nyb = yb + my;
+  return !(d2 > rr2) && depth > 0.0;
+}
+
 template <int NW>
 PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 start, V2 end, bool check_start,
                         double* residual) {
@@ -233,11 +258,20 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
       __syncwarp();
       if constexpr (kSpec) {
         unsigned hit[NW];
+        if constexpr (NW == 2) {  // both words' chains side by side, branch-free
+          const bool h0 = pair_eval_bf(X, Y, pa[0], pb[0], rr2[0], rs[0], om[0] != 0u, nxa[0], nya[0], nxb[0], nyb[0],
+                                       dep[0]) && om[0] != 0u;
+          const bool h1 = pair_eval_bf(X, Y, pa[1], pb[1], rr2[1], rs[1], om[1] != 0u, nxa[1], nya[1], nxb[1], nyb[1],
+                                       dep[1]) && om[1] != 0u;
+          hit[0] = __ballot_sync(kFull, h0);
+          hit[1] = __ballot_sync(kFull, h1);
+        } else {
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const bool h = om[w] != 0u && pair_eval(X, Y, pa[w], pb[w], rr2[w], rs[w], nxa[w], nya[w], nxb[w],
-                                                   nyb[w], dep[w]);
-          hit[w] = __ballot_sync(kFull, h);
+          for (int w = 0; w < NW; ++w) {
+            const bool h = om[w] != 0u && pair_eval(X, Y, pa[w], pb[w], rr2[w], rs[w], nxa[w], nya[w], nxb[w],
+                                                     nyb[w], dep[w]);
+            hit[w] = __ballot_sync(kFull, h);
+          }
         }
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
@@ -254,6 +288,36 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
               mp = dmax(mp, dep[w]);
             }
             __syncwarp();
+            if constexpr (NW == 2) {
+              if (w == 0) {
+                // both words: the two re-tests are independent chains, run
+                // branch-free side by side (a lane keeps its old results
+                // where it does not re-test)
+                const bool t0 = (om[0] & hm) != 0u && l > b;
+                const bool t1 = (om[1] & hm) != 0u;
+                double a0, a1, a2, a3, a4, c0, c1, c2, c3, c4;
+                const bool h0 = pair_eval_bf(X, Y, pa[0], pb[0], rr2[0], rs[0], t0, a0, a1, a2, a3, a4);
+                const bool h1 = pair_eval_bf(X, Y, pa[1], pb[1], rr2[1], rs[1], t1, c0, c1, c2, c3, c4);
+                if (t0) {
+                  nxa[0] = a0;
+                  nya[0] = a1;
+                  nxb[0] = a2;
+                  nyb[0] = a3;
+                  dep[0] = a4;
+                }
+                if (t1) {
+                  nxa[1] = c0;
+                  nya[1] = c1;
+                  nxb[1] = c2;
+                  nyb[1] = c3;
+                  dep[1] = c4;
+                }
+                const unsigned tm0 = __ballot_sync(kFull, t0), tm1 = __ballot_sync(kFull, t1);
+                hit[0] = (hit[0] & ~tm0) | __ballot_sync(kFull, t0 && h0);
+                hit[1] = (hit[1] & ~tm1) | __ballot_sync(kFull, t1 && h1);
+                continue;
+              }
+            }
 #pragma unroll
             for (int v = w; v < NW; ++v) {
               const bool touch = (om[v] & hm) != 0u && (v > w || l > b);
