@@ -233,26 +233,22 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
       double mp = 0.0;  // this lane's part of max_pen (order-free max)
       const double xs = kSpec ? 0.0 : xo, ys = kSpec ? 0.0 : yo;  // own object at the iteration start
       // tip vs own object (push_sim.cpp:90-100)
-      if (mine) {
+      {  // branch-free; lanes without an active object take benign inputs
         const double dx = xo - tc.x, dy = yo - tc.y;
-        const double d2 = dx * dx + dy * dy;
+        const double d2r = dx * dx + dy * dy;
         const double rt = tr + ro;
-        if (!(d2 > rt * rt)) {
-          const double dist = sqrt(d2);
-          const double depth = tr + ro - dist;
-          if (depth > 0.0) {
-            double ux = 1.0, uy = 0.0;
-            if (dist > 0.0) {
-              const double inv = __drcp_rn(dist);  // == 1.0 / dist
-              ux = dx * inv;
-              uy = dy * inv;
-            }
-            xo = xo + ux * depth;
-            yo = yo + uy * depth;
-            X[l] = xo;
-            Y[l] = yo;
-            mp = depth;
-          }
+        const bool near = mine && !(d2r > rt * rt);
+        const double dist = sqrt(near ? d2r : 1.0);
+        const double depth = tr + ro - dist;
+        const bool pos = dist > 0.0;
+        const double inv = __drcp_rn(pos ? dist : 1.0);  // == 1.0 / dist
+        const double ux = pos ? dx * inv : 1.0, uy = pos ? dy * inv : 0.0;
+        if (near && depth > 0.0) {
+          xo = xo + ux * depth;
+          yo = yo + uy * depth;
+          X[l] = xo;
+          Y[l] = yo;
+          mp = depth;
         }
       }
       __syncwarp();
