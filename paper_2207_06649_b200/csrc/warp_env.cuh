@@ -99,37 +99,6 @@ PPG_DI void warp_store(const WarpEnv& W, double* poses) {
 // run-time guards.
 PPG_HD constexpr int warp_words_for(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 : 8; }
 
-// One disc pair's broad + narrow phase (push_sim.cpp:107-108; disc_disc_
-// overlap geometry.cpp:107-115 via object_pair_overlap push_sim.cpp:20-32)
-// evaluated speculatively by the lane that owns the pair, on the current
-// positions.  Returns "hit" (broad test passes and depth > 0); for a hit,
-// depth and the two moved positions (apply_contact_motion with -/+ half the
-// depth, :36-46) are the reference's values.
-PPG_DI bool pair_eval(const double* X, const double* Y, int a, int b, double rr2, double rsum, double& nxa,
-                      double& nya, double& nxb, double& nyb, double& depth) {
-  const double xa = X[a], ya = Y[a], xb = X[b], yb = Y[b];
-  const double ex = xa - xb, ey = ya - yb;
-  const double d2 = ex * ex + ey * ey;
-  depth = 0.0;
-  if (d2 > rr2) return false;
-  const double dist = sqrt(d2);  // == norm(pos_b - pos_a)
-  depth = rsum - dist;
-  if (!(depth > 0.0)) return false;
-  double ux = 1.0, uy = 0.0;
-  if (dist > 0.0) {
-    const double inv = __drcp_rn(dist);  // == 1.0 / dist
-    ux = (xb - xa) * inv;
-    uy = (yb - ya) * inv;
-  }
-  const double s = 0.5 * depth;
-  const double mx = ux * s, my = uy * s;
-  nxa = xa - mx;
-  nya = ya - my;
-  nxb = xb + mx;
-  nyb = yb + my;
-  return true;
-}
-
 // resolve_push (push_sim.cpp:58-130) for a disc scene, one warp.  Returns
 // 0 ok, 1 start collision, 2 not converged (uniform); *residual = final max
 // pairwise penetration.
@@ -153,11 +122,15 @@ PPG_DI bool pair_eval(const double* X, const double* Y, int a, int b, double rr2
 //    holds many touched pairs.
 // A candidate whose narrow test finds no overlap changes nothing, so the
 // speculative variant keeps hit masks only.
-// pair_eval without branches (same results): the re-tests of both words
-// after a hit run as two independent dependency chains that overlap.
-// (`live` = the lane re-tests this pair; other lanes take a benign 1.0 so
-// no lane enters the sqrt / reciprocal special-case paths: d2 = 0 for the
-// padding pairs)
+// One disc pair's broad + narrow phase (push_sim.cpp:107-108; disc_disc_
+// overlap geometry.cpp:107-115 via object_pair_overlap push_sim.cpp:20-32)
+// evaluated speculatively by the lane that owns the pair, on the current
+// positions.  Returns "hit" (broad test passes and depth > 0); for a hit,
+// depth and the two moved positions (apply_contact_motion with -/+ half the
+// depth, :36-46) are the reference's values.  Branch-free, so the chains of
+// a lane's pairs in different words overlap; `live` = the lane evaluates
+// this pair — other lanes take a benign d2 = 1 so no lane enters the sqrt /
+// reciprocal special-case paths (d2 = 0 for the padding pairs).
 PPG_DI bool pair_eval_bf(const double* X, const double* Y, int a, int b, double rr2, double rsum, bool live,
                          double& nxa, double& nya, double& nxb, double& nyb, double& depth) {
   const double xa = X[a], ya = Y[a], xb = X[b], yb = Y[b];
@@ -176,6 +149,32 @@ PPG_DI bool pair_eval_bf(const double* X, const double* Y, int a, int b, double 
   nxb = xb + mx;
   nyb = yb + my;
   return !(d2 > rr2) && depth > 0.0;
+}
+
+// The branched form of pair_eval_bf (early exits; same results).
+PPG_DI bool pair_eval(const double* X, const double* Y, int a, int b, double rr2, double rsum, double& nxa,
+                      double& nya, double& nxb, double& nyb, double& depth) {
+  const double xa = X[a], ya = Y[a], xb = X[b], yb = Y[b];
+  const double ex = xa - xb, ey = ya - yb;
+  const double d2 = ex * ex + ey * ey;
+  depth = 0.0;
+  if (d2 > rr2) return false;
+  const double dist = sqrt(d2);  // == norm(pos_b - pos_a)
+  depth = rsum - dist;
+  if (!(depth > 0.0)) return false;
+  double ux = 1.0, uy = 0.0;
+  if (dist > 0.0) {
+    const double inv = __drcp_rn(dist);  // == 1.0 / dist
+    ux = (xb - xa) * inv;
+    uy = (yb - ya) * inv;
+  }
+  const double s = 0.5 * depth;
+  const double mx = ux * s, my = uy * s;
+  nxa = xa - mx;
+  nya = ya - my;
+  nxb = xb + mx;
+  nyb = yb + my;
+  return true;
 }
 
 template <int NW>
@@ -254,21 +253,14 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
       __syncwarp();
       if constexpr (kSpec) {
         unsigned hit[NW];
-        if constexpr (NW == 2) {  // both words' chains side by side, branch-free
-          const bool h0 = pair_eval_bf(X, Y, pa[0], pb[0], rr2[0], rs[0], om[0] != 0u, nxa[0], nya[0], nxb[0], nyb[0],
-                                       dep[0]) && om[0] != 0u;
-          const bool h1 = pair_eval_bf(X, Y, pa[1], pb[1], rr2[1], rs[1], om[1] != 0u, nxa[1], nya[1], nxb[1], nyb[1],
-                                       dep[1]) && om[1] != 0u;
-          hit[0] = __ballot_sync(kFull, h0);
-          hit[1] = __ballot_sync(kFull, h1);
-        } else {
+        // every word's chain side by side, branch-free
+        bool h[NW];
 #pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            const bool h = om[w] != 0u && pair_eval(X, Y, pa[w], pb[w], rr2[w], rs[w], nxa[w], nya[w], nxb[w],
-                                                     nyb[w], dep[w]);
-            hit[w] = __ballot_sync(kFull, h);
-          }
-        }
+        for (int w = 0; w < NW; ++w)
+          h[w] = pair_eval_bf(X, Y, pa[w], pb[w], rr2[w], rs[w], om[w] != 0u, nxa[w], nya[w], nxb[w], nyb[w], dep[w]) &&
+                 om[w] != 0u;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) hit[w] = __ballot_sync(kFull, h[w]);
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
           while (hit[w]) {
@@ -314,22 +306,29 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
                 continue;
               }
             }
-#pragma unroll
-            for (int v = w; v < NW; ++v) {
-              const bool touch = (om[v] & hm) != 0u && (v > w || l > b);
-              if (v == w) {  // the hit's own word nearly always holds later touched pairs: no vote
-                bool h = false;
-                if (touch) h = pair_eval(X, Y, pa[v], pb[v], rr2[v], rs[v], nxa[v], nya[v], nxb[v], nyb[v], dep[v]);
-                const unsigned tm = __ballot_sync(kFull, touch);
-                hit[v] = (hit[v] & ~tm) | __ballot_sync(kFull, h);
-              } else {
-                const unsigned tm = __ballot_sync(kFull, touch);
-                if (tm) {
-                  bool h = false;
-                  if (touch) h = pair_eval(X, Y, pa[v], pb[v], rr2[v], rs[v], nxa[v], nya[v], nxb[v], nyb[v], dep[v]);
-                  hit[v] = (hit[v] & ~tm) | __ballot_sync(kFull, h);
-                }
+            // w is the last word here: only its later pairs touching the
+            // moved objects are re-tested — branch-free for one word (n <= 8,
+            // measured 15 % faster), branched for the second of two words
+            // (the branch skips the re-test when no lane holds one)
+            if constexpr (NW == 2) {
+              const bool t = (om[w] & hm) != 0u && l > b;
+              bool h = false;
+              if (t) h = pair_eval(X, Y, pa[w], pb[w], rr2[w], rs[w], nxa[w], nya[w], nxb[w], nyb[w], dep[w]);
+              const unsigned tm = __ballot_sync(kFull, t);
+              hit[w] = (hit[w] & ~tm) | __ballot_sync(kFull, h);
+            } else {
+              const bool t = (om[w] & hm) != 0u && l > b;
+              double a0, a1, a2, a3, a4;
+              const bool h = pair_eval_bf(X, Y, pa[w], pb[w], rr2[w], rs[w], t, a0, a1, a2, a3, a4);
+              if (t) {
+                nxa[w] = a0;
+                nya[w] = a1;
+                nxb[w] = a2;
+                nyb[w] = a3;
+                dep[w] = a4;
               }
+              const unsigned tm = __ballot_sync(kFull, t);
+              hit[w] = (hit[w] & ~tm) | __ballot_sync(kFull, t && h);
             }
           }
         }
