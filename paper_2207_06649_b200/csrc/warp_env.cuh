@@ -372,20 +372,21 @@ PPG_DI int warp_resolve(WarpEnv& W, const SimConst& C, const uint16_t* pij, V2 s
               }
               __syncwarp();
               mp = dmax(mp, depth);
-              // re-test the later active pairs touching i or j
+              // re-test the later active pairs touching i or j: every word's
+              // broad test side by side (independent, branch-free), then the
+              // votes
               const unsigned hm = (1u << i) | (1u << j);
+              bool touch[NW], pass[NW];
+#pragma unroll
+              for (int v = 0; v < NW; ++v) {
+                touch[v] = v >= w && (om[v] & hm) != 0u && 32 * v + l > p;
+                const double fx = X[pa[v]] - X[pb[v]], fy = Y[pa[v]] - Y[pb[v]];
+                pass[v] = touch[v] && !(fx * fx + fy * fy > rr2[v]);
+              }
 #pragma unroll
               for (int v = w; v < NW; ++v) {
-                const bool touch = (om[v] & hm) != 0u && 32 * v + l > p;
-                const unsigned tm = __ballot_sync(kFull, touch);
-                if (v == w || tm) {  // the hit's own word: no branch on the vote
-                  bool pass = false;
-                  if (touch) {
-                    const double fx = X[pa[v]] - X[pb[v]], fy = Y[pa[v]] - Y[pb[v]];
-                    pass = !(fx * fx + fy * fy > rr2[v]);
-                  }
-                  cand[v] = (cand[v] & ~tm) | __ballot_sync(kFull, pass);
-                }
+                const unsigned tm = __ballot_sync(kFull, touch[v]);
+                cand[v] = (cand[v] & ~tm) | __ballot_sync(kFull, pass[v]);
               }
             }
           }
