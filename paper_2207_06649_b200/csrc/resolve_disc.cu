@@ -223,7 +223,6 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
   bool have = false;
   bool need_init = true;
   bool pending = false;  // streamed: this lane's next env is in a slice not yet resident
-  uint64_t wait_t0 = 0;  // streamed: when this lane started waiting for a slice
   int zc_env = 0, zc_kind = 0, zc_st = 0;  // zc_out: finished env awaiting its flush (1 poses, 2 zeros)
   double zc_res = 0.0;
   const int lane = tid & 31;
@@ -353,15 +352,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
     }
     if (!__any_sync(0xffffffffu, have || pending)) break;
     if (!have) {
-      if (pending) {
-        // a slice that never arrives (its copy failed) must not hang the
-        // GPU: after 10 s of waiting the launch fails instead
-        uint64_t now;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-        if (wait_t0 == 0) wait_t0 = now;
-        else if (now - wait_t0 > 10000000000ull) __trap();
-        __nanosleep(200);
-      }
+      if (pending) __nanosleep(200);
       continue;
     }
 
