@@ -431,9 +431,9 @@ def run_ours(args, world, rank, local):
             "frac": achieved / peak.value,
             # DRAM bytes per launch of resolve_disc_kernel<10> at E = 65,536 from one
             # `ncu --set full` capture of this launch (dram__bytes_read.sum 23.19 MB = the
-            # inputs once + dram__bytes_write.sum 41.73 MB: the outputs plus write-backs of
-            # the L2-flush buffer's dirty lines evicted during the launch; profiles/README.md)
-            "traffic": 64.92e6 if E == E_DEFAULT and n == 10 else None,
+            # inputs once + dram__bytes_write.sum 41 KB: the outputs stay in L2;
+            # profiles/README.md)
+            "traffic": 23.23e6 if E == E_DEFAULT and n == 10 else None,
             "traffic_unit": "bytes per launch (ncu)",
             "note": "algorithmic FP64 ops (+,-,*,/,sqrt = 1 each, SURVEY 8d formula, counted on this workload) per "
                     "step / step time; peak = measured DFMA instr/s (= FP64 FLOP/s / 2) on this GPU; HBM is not "
