@@ -236,10 +236,48 @@ def pmbs_decisions(ctx, with_reference: bool):
                 row = out[f"n_envs_{ne}"]
                 row["reference_s"] = time.perf_counter() - t0
                 row["same_decision"] = bool(list(q["action"]) == list(r.action) and q["sig_fnv"] == r.signature_fnv)
+    out["c1"] = c1_decisions(ctx, with_reference)
     out["c4"] = c4_decision(ctx, with_reference)
     out["c3"] = c3_episodes(ctx, with_reference)
     out["c2_polygons"] = c2_polygons(ctx, with_reference)
     out["rollouts"] = rollout_throughput(ctx)
+    return out
+
+
+def c1_decisions(ctx, with_reference: bool):
+    """BASELINE config 1 / SURVEY 8d C1: the smallest proj/cases scenes, one
+    PMBS decision at the reference default N_e = 64 — case_01 (fewest
+    objects, lowest id: 1 iteration, expansions only) and case_13 (the
+    smallest case whose first decision runs lockstep rollouts).  Best of 3
+    on the GPU vs the reference run_pmbs with WorkerPool(nproc)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_io
+    from paper_2207_06649_b200 import Budget, ParallelConfig, run_pmbs
+    cases = {cc["case_id"]: (cc, st) for cc, st in golden_io.cases()}
+    out = {}
+    for cid in ("case_01", "case_13"):
+        c, st = cases[cid]
+        cfg = ParallelConfig(rng_seed=int(c["seed"]), n_envs=64, budget=Budget.seconds(60.0))
+        run_pmbs(st, cfg, ctx=ctx)
+        best, r = None, None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            r = run_pmbs(st, cfg, ctx=ctx)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        row = {"gpu_s": best, "iterations": r.iterations, "env_steps": r.env_steps}
+        if with_reference:
+            from oracle import ref
+            if ref.available():
+                rbest = None
+                for _ in range(3):
+                    t0 = time.perf_counter()
+                    q = ref.run_search(st, cfg.to_params(), threads=os.cpu_count() or 1)
+                    dt = time.perf_counter() - t0
+                    rbest = dt if rbest is None else min(rbest, dt)
+                row["reference_s"] = rbest
+                row["same_decision"] = bool(list(q["action"]) == list(r.action) and q["sig_fnv"] == r.signature_fnv)
+        out[cid] = row
     return out
 
 
