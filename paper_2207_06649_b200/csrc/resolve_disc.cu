@@ -10,23 +10,37 @@
 // arithmetic on every shared-memory pose access.  Here, per projection
 // iteration and per lane (= environment):
 //
-//   1. tip broad phase over all objects from REGISTERS (fully unrolled, no
-//      divergence) -> candidate bitmask;
-//   2. tip narrow tests in a loop over the set bits (poses in shared memory,
-//      dynamic index) — objects are independent in the tip loop
-//      (push_sim.cpp:90-100), so any order is exact;
-//   3. pair broad phase over all i<j from registers -> flat pair bitmask;
-//   4. pair narrow tests in lexicographic order over the set bits.  A hit on
-//      (i,j) moves i and j, so every LATER pair touching i or j is re-queued
-//      for evaluation (its broad result is stale); a pair not re-queued has
-//      unchanged inputs, so its broad result still holds.  This reproduces
-//      the reference's in-place Gauss-Seidel sweep (push_sim.cpp:101-117)
-//      exactly while running ~1 narrow test per lane per iteration;
-//   5. clamp (push_sim.cpp:48-54) in registers, write back.
+//   1. tip broad phase over all objects from FLOAT registers on the packed
+//      FP32x2 pipe (FFMA2 / FADD2 / FMUL2, two objects per instruction; a
+//      conservative superset of the FP64 test, see below) -> candidates;
+//   2. tip narrow tests in a loop over the set bits (exact FP64 poses in
+//      shared memory, dynamic index), each re-tested first with the
+//      reference's FP64 broad expression — objects are independent in the
+//      tip loop (push_sim.cpp:90-100), so any order is exact;
+//   3. pair broad phase over all i<j, packed FP32x2 -> flat pair bitmask
+//      (+ a `near` mask for the re-queue filter);
+//   4. pair narrow tests in lexicographic order over the set bits, each
+//      re-tested exactly in FP64 first.  A hit on (i,j) moves i and j, so
+//      every LATER pair touching i or j is re-queued for evaluation (its
+//      broad result is stale); a pair not re-queued has unchanged inputs, so
+//      its broad result still holds.  This reproduces the reference's
+//      in-place Gauss-Seidel sweep (push_sim.cpp:101-117) exactly while
+//      running ~1 narrow test per lane per iteration;
+//   5. clamp (push_sim.cpp:48-54): a conservative float test, the exact
+//      clamp from shared memory for objects near a wall.
+//
+// Float filters: per environment, margin m = 2^-15 B (B bounds every
+// coordinate, radius and push endpoint); float rounding moves a distance by
+// < 2^-20 B, so a float test with radii padded by m/2 accepts everything the
+// FP64 test accepts, and every float candidate is re-tested in FP64 — the
+// candidate sequence, hence every result bit, is the reference's.
 //
 // The (substep, iteration) double loop is flattened per lane and lanes are
 // persistent: a lane that finishes its environment fetches the next one, so
 // warps stay full until the batch drains (no per-warp max-iteration tail).
+// Streamed host batches (ctx.cu batch_resolve_streamed) add per-slice ready
+// flags / done counters and, for pinned outputs, warp-coalesced writes of
+// each finished env's record straight to host memory.
 #include <cuda_runtime.h>
 
 #include <climits>
