@@ -545,7 +545,7 @@ def run_ours(args, world, rank, local):
                        "parallelism": f"{world} independent env shards (weak)"},
             "e2e": {"value": E * world * args.steps / e2e_total, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "api": "ppg_batch_resolve (host C-ABI, pinned buffers): inputs copied in 8K-env slices "
+                    "api": "ppg_batch_resolve (host C-ABI, pinned buffers): inputs copied in 16K-env slices "
                            "while ONE physics launch runs (stream-memop ready flags), results written by the "
                            "kernel straight to the pinned host buffers"},
             "roofline": roof, "clocks": clk, "gpu_launches": 2 * args.steps,
