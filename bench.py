@@ -158,49 +158,44 @@ def cpu_reference_sample(table, poses, pushes, params, sample: int, min_seconds:
             "sample": f"first {sample} envs x {reps} passes, oracle/pmbs_oracle.c (1 thread)"}
 
 
+def c2_config(E: int, world: int) -> dict:
+    """The `config` of both arms (identical dicts, so the driver can pair them)."""
+    return {"workload": f"C2 batch_resolve: E={E} envs per GPU x {N_OBJ} discs, single push-action horizon "
+                        "(BASELINE configs[1])", "envs_per_gpu": E, "objects": N_OBJ, "polygon_fraction": 0.0,
+            "parallelism": f"{world} independent env shards (weak)"}
+
+
 def run_reference(args, world, rank):
+    """The reference arm: the unmodified reference batch_resolve
+    (oracle/_ref, pushplan::batch_resolve with WorkerPool(nproc)) on the SAME
+    workload as ours — all E envs per step, inputs built by the reference's
+    own generate_case + sample_pushes + keyed pick (bit-identical to ours,
+    tests/test_reference_pins_gpu.py).  Rank 0 only."""
     if rank != 0:
         return
     from oracle import ref
     from paper_2207_06649_b200.abi import default_params
     params = default_params()
     threads = os.cpu_count() or 1
-    sample = args.ref_sample
-    cfg = {"workload": f"C2 batch_resolve, E={args.envs} generate_case({N_OBJ}) disc scenes, 1 push/env",
-           "envs": args.envs, "objects": N_OBJ, "polygon_fraction": 0.0, "l2": "n/a (CPU)"}
+    E = args.envs
+    cfg = c2_config(E, world)
     if not ref.available():
         print(json.dumps({"impl": "reference", "metric": METRIC, "unit": UNIT,
                           "unavailable": "oracle/_ref/libpushplan_ref.so not built (needs /root/reference)"}))
         return
-    # Inputs built by the reference itself: generate_case + sample_pushes + keyed pick.
-    states, pushes = [], []
-    k = 0
-    seed = 1000
-    while len(states) < sample:
-        try:
-            s = ref.generate_case(N_OBJ, 0.0, seed)
-        except RuntimeError:
-            seed += 1
-            continue
-        sp = ref.sample_pushes(s, params)
-        if len(sp):
-            states.append(s)
-            pushes.append(sp[int(ref.keyed_picks(7, k, 0, 1, len(sp))[0])])
-            k += 1
-        seed += 1
-    from paper_2207_06649_b200.world import ShapeTable
-    t = ShapeTable.per_env(states)
-    pb = ref.PreparedBatch(t, np.stack([s.poses for s in states]), np.stack(pushes), params)
+    h, pushes, _ = ref.c2_workload(E, N_OBJ, 0.0)
+    pb = ref.PreparedBatch(None, None, pushes, params, handle=h)
     for _ in range(args.warmup):
         pb.run(threads)
     total = sum(pb.run(threads) for _ in range(args.steps))
-    value = sample * args.steps / total
+    value = E * args.steps / total
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generate_case scenes, reference-sampled pushes)", "config": cfg,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{sample} envs per step, pushplan::batch_resolve with WorkerPool({threads})"},
+                             "sample": f"all {E} envs of the workload per step, pushplan::batch_resolve "
+                                       f"(oracle/_ref, unmodified reference, -O3) with WorkerPool({threads})"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -392,6 +387,22 @@ def c3_episodes(ctx, with_reference: bool):
     return row
 
 
+def committed_traffic(E: int, n: int) -> dict:
+    """roofline.traffic = dram__bytes_read.sum + dram__bytes_write.sum of one
+    launch of the physics kernel on this workload, read from the newest
+    committed ncu summary (profiles/*_ncu_traffic.json); null if none matches."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        if d.get("envs") == E and d.get("objects") == n:
+            return {"traffic": d["dram_bytes_read"] + d["dram_bytes_write"], "traffic_unit": "bytes per launch (ncu)",
+                    "traffic_source": os.path.relpath(f, ROOT) + f" ({d.get('kernel')}, {d.get('commit', '?')})"}
+    return {"traffic": None, "traffic_unit": "bytes per launch (ncu)", "traffic_source": None}
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_2207_06649_b200 import Context, abi
@@ -467,12 +478,9 @@ def run_ours(args, world, rank, local):
     achieved = ops_total / launch_s
     roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
             "frac": achieved / peak.value,
-            # DRAM bytes per launch of resolve_disc_kernel<10> at E = 65,536 from one
-            # `ncu --set full` capture of this launch (dram__bytes_read.sum 23.19 MB = the
-            # inputs once + dram__bytes_write.sum 41 KB: the outputs stay in L2;
-            # profiles/README.md)
-            "traffic": 23.23e6 if E == E_DEFAULT and n == 10 else None,
-            "traffic_unit": "bytes per launch (ncu)",
+            # DRAM bytes per launch of the physics kernel from the committed `ncu --set full`
+            # capture of this workload (profiles/<round>_ncu_traffic.json), null without one
+            **committed_traffic(E, n),
             "note": "algorithmic FP64 ops (+,-,*,/,sqrt = 1 each, SURVEY 8d formula, counted on this workload) per "
                     "step / step time; peak = measured DFMA instr/s (= FP64 FLOP/s / 2) on this GPU; HBM is not "
                     "the bound (" + f"{(E * (n * 3 * 8 * 2 + 32 + 4 + 8 + n * 12)) / launch_s / 1e9:.1f}" +
@@ -504,6 +512,10 @@ def run_ours(args, world, rank, local):
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
+    # sentinels: a record the kernel failed to write cannot pass the check below
+    h_out.fill_(float("nan"))
+    h_status.fill_(-7)
+    h_resid.fill_(float("nan"))
     e2e_total = 0.0
     for _ in range(args.steps):
         flush.zero_()
@@ -512,7 +524,12 @@ def run_ours(args, world, rank, local):
         e2e_step()
         e2e_total += time.perf_counter() - t1
     e2e_total = dist_max(e2e_total, world)
-    assert np.array_equal(h_status.numpy(), status), "e2e and device-resident results differ"
+    # the e2e outputs of the last timed call == the device-resident outputs, bit for bit
+    assert np.array_equal(h_status.numpy(), status), "e2e and device-resident status differ"
+    assert np.array_equal(h_out.numpy().view(np.uint64), d_out.cpu().numpy().view(np.uint64)), \
+        "e2e and device-resident poses differ"
+    assert np.array_equal(h_resid.numpy().view(np.uint64), d_resid.cpu().numpy().view(np.uint64)), \
+        "e2e and device-resident residuals differ"
     # the streamed disc path copies poses, pushes and radii (kind / target are
     # only inspected on the host); outputs cross PCIe written by the kernel
     h2d = poses.nbytes + pushes.nbytes + table.radius.nbytes
@@ -539,10 +556,7 @@ def run_ours(args, world, rank, local):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: generate_case(10, ShapeMix{0.0}, seed) scenes (host generator, bit-identical to "
                     "the reference's), push = sample_pushes(scene,16)[keyed_rng(7,k) pick]",
-            "config": {"workload": f"C2 batch_resolve: E={E} envs per GPU x {N_OBJ} discs, single push-action "
-                                   "horizon (BASELINE configs[1])", "envs_per_gpu": E, "objects": N_OBJ,
-                       "polygon_fraction": 0.0, "l2": "flushed between steps (256 MB write)",
-                       "parallelism": f"{world} independent env shards (weak)"},
+            "config": c2_config(E, world), "l2": "flushed between timed steps (256 MB write)",
             "e2e": {"value": E * world * args.steps / e2e_total, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "api": "ppg_batch_resolve (host C-ABI, pinned buffers): inputs copied in 16K-env slices "
@@ -552,7 +566,7 @@ def run_ours(args, world, rank, local):
             "status_counts": np.bincount(status, minlength=3).tolist(), "sweep_env_steps_per_s": sweep,
             "workload_gen_s": gen_s}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference_sample(table, poses, pushes, params, min(args.ref_sample, E),
+        line["cpu_baseline"] = cpu_reference_sample(table, poses, pushes, params, min(args.ref_sample, E) if args.ref_sample > 0 else E,
                                                     args.cpu_seconds, os.cpu_count() or 1)
     if rank == 0 and world == 1 and not args.no_pmbs:
         line["pmbs_decision"] = pmbs_decisions(ctx, not args.no_cpu_baseline)
@@ -568,12 +582,23 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--envs", type=int, default=E_DEFAULT)
-    ap.add_argument("--ref-sample", type=int, default=8192)
+    ap.add_argument("--ref-sample", type=int, default=0, help="cpu_baseline sample (0: all E envs)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pmbs", action="store_true", help="skip the PMBS s/decision block")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
     if args.impl == "reference":
         # rank 0 alone times the CPU reference; other ranks exit without work
         run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))

@@ -263,6 +263,20 @@ int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev,
                                 const double* poses_in, const double* pushes, int E,
                                 int64_t* counts_dev, void* stream);
 
+/* Test helper (acceptance criterion 3, acceptance.cpp:255-281): runs the
+ * device select_batch (pmbs.cpp:52-63, the dt_select_kernel of every PMBS
+ * iteration graph) on one explicit tree: nodes in pre-order, children in
+ * insertion order; node x has n_children[x] children and n_untried[x]
+ * untried actions, flags bit0 graspable / bit1 dead (TreeNode, mcts.hpp:45-66).
+ * Writes the selected pairs (node, untried index) in draw order (*n_sel = 0:
+ * TreeExhausted), the nodes' virtual visits after the batch and their sum
+ * after reset_virtual (pmbs.cpp:65-68). */
+int ppg_debug_select_batch(ppg_ctx* ctx, int n_nodes, const int32_t* parent, const int32_t* depth,
+                           const int64_t* visits, const double* q_sum, const uint8_t* flags,
+                           const int32_t* n_children, const int32_t* n_untried, int tree_depth, int n_envs,
+                           double c_explore, int32_t* sel_node, int32_t* sel_untried, int32_t* n_sel,
+                           int64_t* vv_out, int64_t* vsum_after_reset);
+
 /* Test helper: the device port of glibc sincos (the reference's libm,
  * __sincos_fma) on n arguments |x| < 105414350; bit-identical to the host. */
 int ppg_debug_sincos(ppg_ctx* ctx, const double* x, int n, double* s, double* c);

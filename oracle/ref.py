@@ -36,6 +36,10 @@ def lib():
                                        POINTER(c_double), POINTER(c_double)]
         L.ref_generate_case.restype = c_void_p
         L.ref_generate_case.argtypes = [c_int, c_int, c_double, c_uint64]
+        L.ref_c2_workload.restype = c_void_p
+        L.ref_c2_workload.argtypes = [c_int, c_double, c_uint64, c_int, c_uint64, c_int, c_int, POINTER(c_double),
+                                      POINTER(c_uint64)]
+        L.ref_c3_trees.argtypes = [c_int, c_int, c_int, c_int] + [c_void_p] * 16
         L.ref_load_scene.restype = c_void_p
         L.ref_load_scene.argtypes = [c_char_p]
         L.ref_fixture.restype = c_void_p
@@ -149,20 +153,41 @@ def batch_resolve(table: ShapeTable, poses: np.ndarray, pushes: np.ndarray, para
     return out, status, dig, secs.value
 
 
+def c2_workload(E: int, n_objects: int = 10, polygon_fraction: float = 0.0, seed_base: int = 1000,
+                pick_seed: int = 7, pushes_per_object: int = 16, threads: int = 0):
+    """BASELINE config 2 inputs built by the reference alone
+    (bench::generate_case + sample_pushes + keyed pick; ref_shim.cpp
+    ref_c2_workload).  Returns (Handle of E states, pushes [E][4], seeds [E])."""
+    pushes = np.zeros((E, 4), np.float64)
+    seeds = np.zeros(E, np.uint64)
+    ptr = lib().ref_c2_workload(n_objects, polygon_fraction, seed_base, E, pick_seed, pushes_per_object,
+                                threads or os.cpu_count() or 1, dptr(pushes), u64ptr(seeds))
+    return Handle(ptr), pushes, seeds
+
+
 class PreparedBatch:
     """States built once; ``run`` times only pushplan::batch_resolve."""
 
-    def __init__(self, table: ShapeTable, poses: np.ndarray, pushes: np.ndarray, params: PpgParams):
-        self.h = states_handle(table, poses)
+    def __init__(self, table: ShapeTable, poses: np.ndarray, pushes: np.ndarray, params: PpgParams,
+                 handle=None):
+        self.h = handle if handle is not None else states_handle(table, poses)
         self.pushes = np.ascontiguousarray(pushes, np.float64)
         self.params = params
-        self.E = poses.shape[0]
+        self.E = len(self.pushes)
 
     def run(self, threads: int) -> float:
         secs = c_double()
         lib().ref_batch_resolve(self.h.ptr, dptr(self.pushes), ctypes.byref(self.params), threads,
                                 ctypes.byref(secs))
         return secs.value
+
+    def results(self, n_objects: int):
+        """(poses_out [E][n][3], status [E], digests [E]) of the last run."""
+        out = np.zeros((self.E, n_objects, 3), np.float64)
+        status = np.zeros(self.E, np.int32)
+        dig = np.zeros(self.E, np.uint64)
+        lib().ref_batch_results(self.h.ptr, dptr(out), iptr(status), u64ptr(dig))
+        return out, status, dig
 
 
 def sample_pushes(st: WorldState, params: PpgParams) -> np.ndarray:
@@ -258,3 +283,28 @@ def replay_log(path: str):
     buf = ctypes.create_string_buffer(4096)
     ok = lib().ref_replay_log(path.encode(), buf, 4096)
     return bool(ok), buf.value.decode()
+
+
+def c3_trees(variant: int, count: int = 200, cap_nodes: int = 200000, cap_pairs: int = 200000) -> dict:
+    """Acceptance criterion 3 (acceptance.cpp:255-281) on the reference:
+    random explicit trees + the reference select_batch (ref_shim.cpp
+    ref_c3_trees).  Flat per-node / per-pair arrays with offsets."""
+    a = {"node_off": np.zeros(count + 1, np.int32), "parent": np.zeros(cap_nodes, np.int32),
+         "depth": np.zeros(cap_nodes, np.int32), "visits": np.zeros(cap_nodes, np.int64),
+         "q_sum": np.zeros(cap_nodes, np.float64), "flags": np.zeros(cap_nodes, np.uint8),
+         "n_children": np.zeros(cap_nodes, np.int32), "n_untried": np.zeros(cap_nodes, np.int32),
+         "vv": np.zeros(cap_nodes, np.int64), "pair_off": np.zeros(count + 1, np.int32),
+         "sel_node": np.zeros(cap_pairs, np.int32), "sel_untried": np.zeros(cap_pairs, np.int32),
+         "tree_depth": np.zeros(count, np.int32), "n_envs": np.zeros(count, np.int32),
+         "vsum": np.zeros(count, np.int64), "exhausted": np.zeros(count, np.int32)}
+    keys = ["node_off", "parent", "depth", "visits", "q_sum", "flags", "n_children", "n_untried", "vv", "pair_off",
+            "sel_node", "sel_untried", "tree_depth", "n_envs", "vsum", "exhausted"]
+    rc = lib().ref_c3_trees(variant, count, cap_nodes, cap_pairs, *[a[k].ctypes.data for k in keys])
+    if rc != 0:
+        raise RuntimeError(f"ref_c3_trees: capacity ({rc})")
+    nn, npairs = int(a["node_off"][-1]), int(a["pair_off"][-1])
+    for k in ("parent", "depth", "visits", "q_sum", "flags", "n_children", "n_untried", "vv"):
+        a[k] = a[k][:nn].copy()
+    for k in ("sel_node", "sel_untried"):
+        a[k] = a[k][:npairs].copy()
+    return a

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <sstream>
 #include <memory>
 #include <random>
@@ -156,6 +157,171 @@ void* ref_generate_case(int motif, int n_objects, double polygon_fraction, uint6
   } catch (const std::exception&) {
     return nullptr;
   }
+}
+
+// BASELINE config 2 inputs built by the reference alone (bench.py's
+// reference arm and the full-workload parity test): scene k =
+// bench::generate_case(n, ShapeMix{pf}, seed) for consecutive seeds from
+// seed_base, skipping seeds whose generator throws and scenes with no legal
+// push (sample_pushes(scene, N_a)); push k = that list's
+// uniform_int_distribution pick from keyed_rng(pick_seed, k, 0)
+// (rng.hpp:21-23, mcts.cpp:151-152).  Same rule as the product's
+// scenes.c2_workload.  Scenes are generated by `threads` threads.
+void* ref_c2_workload(int n_objects, double polygon_fraction, uint64_t seed_base, int E, uint64_t pick_seed,
+                      int pushes_per_object, int threads, double* pushes_out, uint64_t* seeds_out) {
+  GripperTip tip;
+  const int batch = E + E / 16 + 64;
+  auto* st = new States;
+  uint64_t next = seed_base;
+  int k = 0;
+  while (k < E) {
+    std::vector<std::unique_ptr<WorldState>> gen(batch);
+    std::vector<std::vector<PushAction>> cand(batch);
+    const uint64_t base = next;
+    WorkerPool pool(threads > 1 ? threads : 1);
+    pool.parallel_for(batch, [&](int i) {
+      try {
+        gen[i] = std::make_unique<WorldState>(bench::generate_case(n_objects, bench::ShapeMix{polygon_fraction},
+                                                                   base + static_cast<uint64_t>(i)));
+        cand[i] = sample_pushes(*gen[i], pushes_per_object, tip);
+      } catch (const std::exception&) {
+        gen[i].reset();
+      }
+    });
+    next += static_cast<uint64_t>(batch);
+    for (int i = 0; i < batch && k < E; ++i) {
+      if (!gen[i] || cand[i].empty()) continue;
+      auto rng = keyed_rng(pick_seed, static_cast<uint64_t>(k), 0);
+      std::uniform_int_distribution<size_t> pick(0, cand[i].size() - 1);
+      const PushAction& a = cand[i][pick(rng)];
+      pushes_out[k * 4] = a.x_s;
+      pushes_out[k * 4 + 1] = a.y_s;
+      pushes_out[k * 4 + 2] = a.x_e;
+      pushes_out[k * 4 + 3] = a.y_e;
+      if (seeds_out) seeds_out[k] = base + static_cast<uint64_t>(i);
+      st->v.push_back(std::move(*gen[i]));
+      ++k;
+    }
+  }
+  return st;
+}
+
+// Acceptance criterion 3 (acceptance.cpp:255-281): 200 select_batch
+// invocations on random explicit trees.  random_tree (acceptance.cpp:64-92)
+// is restated here with the same libstdc++ distributions and draw order (the
+// reference keeps it file-local to its acceptance binary); select_batch and
+// reset_virtual are the reference's own (pmbs.cpp:52-68).  variant 0 is the
+// criterion exactly (rng keyed_rng(3, 0, 0) shared by the 200 trees,
+// n_envs = {4, 16, 64}[t % 3], tree_depth 7); variant 1 additionally marks
+// nodes terminal (graspable / dead) from keyed_rng(4, t, 0) and uses
+// tree_depth 1 + t % 4, so the selectable-subtree logic and TreeExhausted are
+// exercised too.  Per tree t, nodes in pre-order (children in insertion
+// order) go to the flat arrays from node_off[t]; the selected pairs (node
+// index, popped untried index) from pair_off[t]; vv = virtual visits after
+// select_batch, before reset_virtual; vsum = sum of virtual visits after it.
+int ref_c3_trees(int variant, int count, int cap_nodes, int cap_pairs, int32_t* node_off, int32_t* parent,
+                 int32_t* depth, int64_t* visits, double* q_sum, uint8_t* flags, int32_t* n_children,
+                 int32_t* n_untried, int64_t* vv, int32_t* pair_off, int32_t* sel_node, int32_t* sel_untried,
+                 int32_t* tree_depth, int32_t* n_envs, int64_t* vsum, int32_t* exhausted) {
+  auto rng = keyed_rng(3, 0, 0);
+  int tag = 0;
+  const auto synth = [&tag] {
+    const int i = ++tag;
+    return PushAction{1e-4 * i, 2e-4 * i, 1e-4 * i + 0.05, 2e-4 * i};
+  };
+  int nn = 0, np = 0;
+  const int env_choices[3] = {4, 16, 64};
+  for (int t = 0; t < count; ++t) {
+    std::uniform_int_distribution<int> kids(0, 3);
+    std::uniform_int_distribution<long> vis(1, 20);
+    std::uniform_real_distribution<double> uq(0.0, 1.0);
+    std::uniform_int_distribution<int> untried(0, 2);
+    const std::function<void(mcts::TreeNode&, int)> grow = [&](mcts::TreeNode& node, int d) {
+      const int n = d < 4 ? kids(rng) : 0;
+      long total = vis(rng);
+      for (int i = 0; i < n; ++i) {
+        auto child = std::make_unique<mcts::TreeNode>();
+        child->action = synth();
+        child->parent = &node;
+        child->depth = node.depth + 1;
+        grow(*child, d + 1);
+        total += child->visits;
+        node.children.push_back(std::move(child));
+      }
+      node.visits = total;
+      node.q_sum = uq(rng) * static_cast<double>(total);
+      const int u = untried(rng);
+      for (int i = 0; i < u; ++i) node.untried.push_back(synth());
+    };
+    mcts::SearchTree tree;
+    tree.root = std::make_unique<mcts::TreeNode>();
+    grow(*tree.root, 0);
+    if (tree.root->untried.empty()) tree.root->untried.push_back(synth());
+    pmbs::ParallelConfig cfg;
+    cfg.n_envs = env_choices[t % 3];
+    if (variant == 1) {
+      tree.tree_depth = 1 + t % 4;
+      auto r2 = keyed_rng(4, static_cast<uint64_t>(t), 0);
+      std::uniform_int_distribution<int> pick(0, 19);
+      const std::function<void(mcts::TreeNode&)> mark = [&](mcts::TreeNode& x) {
+        const int v = pick(r2);
+        if (x.parent && v == 0) x.graspable_flag = true;
+        else if (x.parent && v == 1) x.dead_flag = true;
+        for (auto& c : x.children) mark(*c);
+      };
+      mark(*tree.root);
+    }
+    // pre-order numbering
+    std::vector<mcts::TreeNode*> order;
+    const std::function<void(mcts::TreeNode&)> walk = [&](mcts::TreeNode& x) {
+      order.push_back(&x);
+      for (auto& c : x.children) walk(*c);
+    };
+    walk(*tree.root);
+    if (nn + static_cast<int>(order.size()) > cap_nodes) return -1;
+    node_off[t] = nn;
+    std::vector<std::pair<mcts::TreeNode*, int>> idx;
+    for (size_t k = 0; k < order.size(); ++k) {
+      mcts::TreeNode* x = order[k];
+      int pi = -1;
+      for (size_t m = 0; m < k; ++m)
+        if (order[m] == x->parent) pi = static_cast<int>(m);
+      parent[nn + k] = pi;
+      depth[nn + k] = x->depth;
+      visits[nn + k] = x->visits;
+      q_sum[nn + k] = x->q_sum;
+      flags[nn + k] = static_cast<uint8_t>((x->graspable_flag ? 1 : 0) | (x->dead_flag ? 2 : 0));
+      n_children[nn + k] = static_cast<int32_t>(x->children.size());
+      n_untried[nn + k] = static_cast<int32_t>(x->untried.size());
+    }
+    tree_depth[t] = tree.tree_depth;
+    n_envs[t] = cfg.n_envs;
+    pair_off[t] = np;
+    exhausted[t] = 0;
+    try {
+      const pmbs::SelectionBatch batch = pmbs::select_batch(tree, cfg);
+      if (np + static_cast<int>(batch.pairs.size()) > cap_pairs) return -2;
+      std::vector<size_t> popped(order.size(), 0);
+      for (const auto& [node, action] : batch.pairs) {
+        size_t k = 0;
+        while (order[k] != node) ++k;
+        sel_node[np] = static_cast<int32_t>(k);
+        sel_untried[np] = static_cast<int32_t>(popped[k]++);
+        ++np;
+      }
+    } catch (const pmbs::TreeExhausted&) {
+      exhausted[t] = 1;
+    }
+    for (size_t k = 0; k < order.size(); ++k) vv[nn + k] = order[k]->virtual_visits;
+    pmbs::reset_virtual(*tree.root);
+    long sum = 0;
+    for (mcts::TreeNode* x : order) sum += x->virtual_visits;
+    vsum[t] = sum;
+    nn += static_cast<int>(order.size());
+  }
+  node_off[count] = nn;
+  pair_off[count] = np;
+  return 0;
 }
 
 void* ref_load_scene(const char* path) {

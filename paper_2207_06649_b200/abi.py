@@ -179,6 +179,8 @@ SIGNATURES = {
     "ppg_run_pmbs_device": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double), POINTER(PpgSearchStats),
                                     c_char_p, c_int64, POINTER(c_int64)]),
     "ppg_debug_sincos": (c_int, [c_void_p, POINTER(c_double), c_int, POINTER(c_double), POINTER(c_double)]),
+    "ppg_debug_select_batch": (c_int, [c_void_p, c_int] + [c_void_p] * 7 + [c_int, c_int, c_double]
+                               + [c_void_p] * 5),
     "ppg_measure_fp64_peak": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "ppg_generate_cases": (c_int, [c_int, c_int, c_double, POINTER(c_uint64), c_int, POINTER(c_int32),
                                    POINTER(c_double), POINTER(c_int32), POINTER(c_double), POINTER(c_double),

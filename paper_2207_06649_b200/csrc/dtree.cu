@@ -948,6 +948,163 @@ std::string signature(const std::vector<int32_t>& depth, const std::vector<doubl
 
 extern "C" {
 
+// Test entry (acceptance criterion 3, acceptance.cpp:255-281): loads one
+// explicit tree into a scratch device tree and runs the device select_batch
+// (dt_select_kernel, the kernel of every PMBS iteration graph) on it.
+// Nodes in pre-order with children in insertion order; node x has
+// n_children[x] children and n_untried[x] untried actions (none popped).
+// Outputs: the selected (node, untried index) pairs in draw order, every
+// node's virtual visits after the batch (vv_out), and the sum of virtual
+// visits after reset_virtual (pmbs.cpp:65-68; the iteration graph's
+// dt_gather_kernel zeroing pass).  *n_sel = 0 is TreeExhausted.
+int ppg_debug_select_batch(ppg_ctx* ctx, int n_nodes, const int32_t* parent, const int32_t* depth,
+                           const int64_t* visits, const double* q_sum, const uint8_t* flags,
+                           const int32_t* n_children, const int32_t* n_untried, int tree_depth, int n_envs,
+                           double c_explore, int32_t* sel_node, int32_t* sel_untried, int32_t* n_sel,
+                           int64_t* vv_out, int64_t* vsum_after_reset) {
+  if (!ctx || n_nodes < 1 || n_envs < 1 || !parent || !depth || !visits || !q_sum || !flags || !n_children ||
+      !n_untried || !sel_node || !sel_untried || !n_sel || tree_depth < 0 || tree_depth >= kMaxTreeDepth)
+    return PPG_EINVAL;
+  DCK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int N = n_nodes;
+  // host layout: children (insertion order) then untried entries share u_off
+  std::vector<long long> u_off(N), vis(visits, visits + N);
+  std::vector<int32_t> u_n(N), u_head(N), c_n(N), cpool, zero(N, 0);
+  long long off = 0;
+  int max_depth = 0;
+  long long max_vis = 0;
+  std::vector<int> unsettled(kMaxTreeDepth, 0);
+  for (int x = 0; x < N; ++x) {
+    if (depth[x] < 0 || depth[x] >= kMaxTreeDepth || (x > 0 && (parent[x] < 0 || parent[x] >= x))) return PPG_EINVAL;
+    u_off[x] = off;
+    off += n_children[x] + n_untried[x];
+    u_n[x] = n_children[x] + n_untried[x];
+    u_head[x] = n_children[x];
+    c_n[x] = n_children[x];
+    max_depth = std::max(max_depth, depth[x]);
+    max_vis = std::max(max_vis, static_cast<long long>(visits[x]));
+    if (flags[x] == 0 && n_untried[x] > 0) unsettled[depth[x]] += 1;
+  }
+  cpool.assign(static_cast<size_t>(off > 0 ? off : 1), -1);
+  {
+    std::vector<int32_t> fill(N, 0);
+    for (int x = 1; x < N; ++x) {
+      const int p = parent[x];
+      if (fill[p] >= n_children[p]) return PPG_EINVAL;
+      cpool[u_off[p] + fill[p]++] = x;
+    }
+    for (int x = 0; x < N; ++x)
+      if (fill[x] != n_children[x]) return PPG_EINVAL;
+  }
+  DevBuf b_parent, b_depth, b_q, b_vis, b_vv, b_flags, b_uoff, b_un, b_uhead, b_cn, b_selc, b_cpool, b_log, b_sc,
+      b_seln, b_sela;
+  struct Free {
+    std::vector<DevBuf*> v;
+    ~Free() {
+      for (DevBuf* b : v) b->release();
+    }
+  } fr{{&b_parent, &b_depth, &b_q, &b_vis, &b_vv, &b_flags, &b_uoff, &b_un, &b_uhead, &b_cn, &b_selc, &b_cpool, &b_log,
+        &b_sc, &b_seln, &b_sela}};
+  DCK(b_parent.ensure(N * 4ull));
+  DCK(b_depth.ensure(N * 4ull));
+  DCK(b_q.ensure(N * 8ull));
+  DCK(b_vis.ensure(N * 8ull));
+  DCK(b_vv.ensure(N * 4ull));
+  DCK(b_flags.ensure(N));
+  DCK(b_uoff.ensure(N * 8ull));
+  DCK(b_un.ensure(N * 4ull));
+  DCK(b_uhead.ensure(N * 4ull));
+  DCK(b_cn.ensure(N * 4ull));
+  DCK(b_selc.ensure(N * 4ull));
+  DCK(b_cpool.ensure(cpool.size() * 4));
+  const size_t lt = static_cast<size_t>(max_vis) + n_envs + 2;
+  std::vector<double> tab(lt);
+  for (size_t k = 0; k < lt; ++k) tab[k] = std::log(static_cast<double>(k));  // the reference's glibc log
+  DCK(b_log.ensure(lt * 8));
+  DCK(b_sc.ensure(sizeof(DTScal)));
+  DCK(b_seln.ensure(static_cast<size_t>(n_envs) * 4));
+  DCK(b_sela.ensure(static_cast<size_t>(n_envs) * 8));
+  DCK(cudaMemcpyAsync(b_parent.p, parent, N * 4ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_depth.p, depth, N * 4ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_q.p, q_sum, N * 8ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_vis.p, vis.data(), N * 8ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_vv.p, zero.data(), N * 4ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_flags.p, flags, N, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_uoff.p, u_off.data(), N * 8ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_un.p, u_n.data(), N * 4ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_uhead.p, u_head.data(), N * 4ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_cn.p, c_n.data(), N * 4ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_selc.p, zero.data(), N * 4ull, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_cpool.p, cpool.data(), cpool.size() * 4, cudaMemcpyHostToDevice, st));
+  DCK(cudaMemcpyAsync(b_log.p, tab.data(), lt * 8, cudaMemcpyHostToDevice, st));
+  DTScal h;
+  std::memset(&h, 0, sizeof h);
+  h.n_nodes = N;
+  h.dT = tree_depth;
+  h.levels = max_depth + 1;
+  h.stop = -1;
+  h.recompute = 1;  // dt_recount_kernel builds the selectable-children counts
+  h.c_explore = c_explore;
+  h.min_grasp_depth = INT_MAX;
+  for (int d = 0; d < kMaxTreeDepth; ++d) h.unsettled[d] = unsettled[d];
+  DCK(cudaMemcpyAsync(b_sc.p, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  DTree t{};
+  t.parent = b_parent.as<int32_t>();
+  t.depth = b_depth.as<int32_t>();
+  t.q = b_q.as<double>();
+  t.visits = b_vis.as<long long>();
+  t.vv = b_vv.as<int32_t>();
+  t.flags = b_flags.as<uint8_t>();
+  t.u_off = b_uoff.as<long long>();
+  t.u_n = b_un.as<int32_t>();
+  t.u_head = b_uhead.as<int32_t>();
+  t.c_n = b_cn.as<int32_t>();
+  t.selc = b_selc.as<int32_t>();
+  t.cpool = b_cpool.as<int32_t>();
+  t.sel_node = b_seln.as<int32_t>();
+  t.sel_act = b_sela.as<long long>();
+  t.logtab = b_log.as<double>();
+  t.sc = b_sc.as<DTScal>();
+  t.n_envs = n_envs;
+  dt_recount_kernel<<<1, 1024, 0, st>>>(t);
+  dt_select_kernel<<<1, kSelThreads, 0, st>>>(t);
+  DCK(cudaGetLastError());
+  DCK(cudaMemcpyAsync(&h, b_sc.p, sizeof h, cudaMemcpyDeviceToHost, st));
+  std::vector<int32_t> vv(N), sn(n_envs);
+  std::vector<long long> sa(n_envs);
+  DCK(cudaMemcpyAsync(vv.data(), b_vv.p, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(sn.data(), b_seln.p, n_envs * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(sa.data(), b_sela.p, n_envs * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaStreamSynchronize(st));
+  if (h.stop == 3) {
+    ctx->err = "device select: selection invariant violated";
+    return PPG_EINVAL;
+  }
+  const int P = h.n_pairs;
+  *n_sel = P;
+  for (int k = 0; k < P; ++k) {
+    sel_node[k] = sn[k];
+    sel_untried[k] = static_cast<int32_t>(sa[k] - u_off[sn[k]] - n_children[sn[k]]);
+  }
+  if (vv_out)
+    for (int x = 0; x < N; ++x) vv_out[x] = vv[x];
+  // reset_virtual: the iteration graph's dt_gather_kernel pass over the nodes
+  t.sc = b_sc.as<DTScal>();
+  h.n_pairs = 0;
+  DCK(cudaMemcpyAsync(b_sc.p, &h, sizeof h, cudaMemcpyHostToDevice, st));
+  dt_gather_kernel<<<std::max(1, std::min(4 * ctx->num_sms, (N + 255) / 256)), 256, 0, st>>>(t, false);
+  DCK(cudaGetLastError());
+  DCK(cudaMemcpyAsync(vv.data(), b_vv.p, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaStreamSynchronize(st));
+  if (vsum_after_reset) {
+    long long sum = 0;
+    for (int x = 0; x < N; ++x) sum += vv[x];
+    *vsum_after_reset = sum;
+  }
+  return PPG_SUCCESS;
+}
+
 int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats,
                         char* sig_buf, int64_t sig_cap, int64_t* sig_len) {
   if (!ctx || !root_poses || !action_out) return PPG_EINVAL;

@@ -133,6 +133,7 @@ struct Mask {
 
 constexpr double kNear = 0.002;  // metres, the re-queue filter margin
 constexpr int kFixK = 6;         // check for a fixed point from this iteration of a substep on
+constexpr unsigned kMaxSpins = 1u << 26;  // ~13 s of 200 ns polls on one slice flag
 
 // Streamed batches: is the slice holding env e resident?  (The copy stream
 // writes `epoch` into its flag after the slice's copies.)
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
   bool need_init = true;
   bool pending = false;  // streamed: this lane's next env is in a slice not yet resident
   int zc_env = 0, zc_kind = 0, zc_st = 0;  // zc_out: finished env awaiting its flush (1 poses, 2 zeros)
+  unsigned spins = 0;                       // streamed: polls of a not-yet-resident slice
   double zc_res = 0.0;
   const int lane = tid & 31;
   double* const xw = dsm + (tid - lane);  // this warp's shared-memory columns
@@ -364,9 +366,18 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
         break;
       }
     }
-    if (!__any_sync(0xffffffffu, have || pending)) break;
+    // a lane with a queued zero-copy record (zc_kind: a start collision found
+    // during init) keeps the warp alive for one more pass, whose flush at the
+    // loop top writes it
+    if (!__any_sync(0xffffffffu, have || pending || zc_kind != 0)) break;
     if (!have) {
-      if (pending) __nanosleep(200);
+      if (pending) {
+        // bounded wait: the host enqueues every slice copy and flag write
+        // before the launch, so a flag that never arrives is a bug; trap
+        // (a reported launch failure) instead of hanging the GPU
+        if (++spins > kMaxSpins) __trap();
+        __nanosleep(200);
+      }
       continue;
     }
 

@@ -197,6 +197,64 @@ def acceptance():
     print("acceptance c1/c4", len(out["c1"]), len(out["c4"]), flush=True)
 
 
+def c3():
+    """Acceptance criterion 3 (acceptance.cpp:255-281): 200 random explicit
+    trees and the reference select_batch's pairs / virtual visits (variant 0
+    = the criterion exactly; variant 1 adds terminal nodes and d_T 1-4)."""
+    res = {}
+    for v in (0, 1):
+        a = ref.c3_trees(v)
+        for k, x in a.items():
+            res[f"v{v}_{k}"] = x
+        print("c3 variant", v, "nodes", a["node_off"][-1], "pairs", a["pair_off"][-1], flush=True)
+    np.savez_compressed(os.path.join(HERE, "c3_trees.npz"), **res)
+
+
+def _decision(st, p, threads=8):
+    r = ref.run_search(st, p, threads=threads)
+    return {"action": r["action"].tolist(), "iterations": r["iterations"], "expansions": r["expansions"],
+            "stop": r["stop"], "final_tree_depth": r["final_tree_depth"], "sig_fnv": str(r["sig_fnv"]),
+            "n_nodes": r["n_nodes"]}
+
+
+WIDE_16K = [("case_13", 16384)]
+
+
+def wide():
+    """Reference run_pmbs fingerprints beyond the defaults (VERDICT r1 task 1):
+    case_18 / case_13 at N_e 1000 / 4096 (case_13 at 1000 draws past the
+    156-word MT19937-64 block), C4 dense ring motifs (ring-16 / ring-18, seeds
+    5 and 19, d_T 9, N_a 24, N_e 4096, 10 iterations) and the polygon cases
+    16 / 17 at N_e 1000.  Iteration budgets (not seconds) keep every run
+    machine-independent."""
+    out = []
+    cs = {}
+    for f in sorted(glob.glob(os.path.join(CASES, "*.json"))):
+        cs[os.path.splitext(os.path.basename(f))[0]] = f
+    with open(os.path.join(HERE, "cases.json")) as fh:
+        seeds = {c["case_id"]: int(c["seed"]) for c in json.load(fh)}
+    runs = [("case_18", 1000), ("case_18", 4096), ("case_13", 1000), ("case_13", 4096), ("case_16", 1000),
+            ("case_17", 1000)] + WIDE_16K
+    for cid, ne in runs:
+        st = ref.load_scene(cs[cid])
+        p = default_params(rng_seed=seeds[cid], n_envs=ne, budget_iterations=1, max_iterations=200)
+        d = _decision(st, p)
+        out.append({"kind": "case", "case_id": cid, "n_envs": ne, "seed": str(seeds[cid]), "max_iterations": 200,
+                    "decision": d})
+        print(cid, ne, d["iterations"], d["stop"], flush=True)
+    for n in (16, 18):
+        for seed in (5, 19):
+            st = ref.generate_case(n, 0.0, seed, 1)
+            p = default_params(rng_seed=seed, n_envs=4096, tree_depth=9, pushes_per_object=24, budget_iterations=1,
+                               max_iterations=10)
+            d = _decision(st, p)
+            out.append({"kind": "ring", "n_objects": n, "scene_seed": seed, "seed": str(seed), "n_envs": 4096,
+                        "tree_depth": 9, "pushes_per_object": 24, "max_iterations": 10, "decision": d})
+            print("ring", n, seed, d["iterations"], d["stop"], flush=True)
+    with open(os.path.join(HERE, "wide.json"), "w") as fh:
+        json.dump(out, fh, indent=0)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         globals()[sys.argv[1]]()

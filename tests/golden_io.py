@@ -71,3 +71,15 @@ def acceptance():
     with open(os.path.join(GOLDEN, "acceptance.json")) as f:
         d = json.load(f)
     return {k: [(x, _state(x["state"])) for x in v] for k, v in d.items()}
+
+
+def c3_trees(variant: int):
+    """Acceptance C3 fixture: random explicit trees + the reference select_batch."""
+    z = np.load(os.path.join(GOLDEN, "c3_trees.npz"))
+    return {k[len(f"v{variant}_"):]: z[k] for k in z.files if k.startswith(f"v{variant}_")}
+
+
+def wide():
+    """Reference run_pmbs fingerprints at wide N_e / C4 / polygon cases."""
+    with open(os.path.join(GOLDEN, "wide.json")) as f:
+        return json.load(f)

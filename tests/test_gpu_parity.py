@@ -581,3 +581,50 @@ def test_streamed_zero_copy_large_object_counts(n, monkeypatch):
     assert np.array_equal(ps, s2)
     assert _bitwise(po, o2).all()
     assert np.array_equal(pr.view(np.uint64), r2.view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pattern", ["all", "tail", "every_other"])
+def test_streamed_zero_copy_start_collisions(ctx, pattern):
+    """Zero-copy (pinned) outputs when whole warps only see start collisions
+    (status 1, found during env init): every env's record must be written —
+    pinned buffers pre-filled with sentinels, compared with the chunked path
+    (PPG_STREAMED=0) and the oracle.  `all`: every push starts inside object
+    0; `tail`: the last 3,000 envs do (the warps that drain the batch);
+    `every_other`: alternate envs do."""
+    import torch
+    from paper_2207_06649_b200 import Context
+    from paper_2207_06649_b200.scenes import _take, c2_workload
+    E = 36011
+    ctx.set_params(P)
+    table, poses, pushes, _ = c2_workload(ctx, E)
+    pushes = pushes.copy()
+    hit = {"all": np.arange(E), "tail": np.arange(E - 3000, E), "every_other": np.arange(0, E, 2)}[pattern]
+    pushes[hit, 0:2] = poses[hit, 0, 0:2]
+    pushes[hit, 2:4] = poses[hit, 0, 0:2] + 0.05
+    po = torch.empty(poses.shape, dtype=torch.float64).pin_memory().numpy()
+    ps = torch.full((E,), -7, dtype=torch.int32).pin_memory().numpy()
+    pr = torch.empty((E,), dtype=torch.float64).pin_memory().numpy()
+    for _ in range(2):
+        po[:] = np.nan
+        ps[:] = -7
+        pr[:] = np.nan
+        ctx.batch_resolve_arrays(table, poses, pushes, out=(po, ps, pr))
+        assert (ps[hit] == 1).all()
+        assert (ps >= 0).all() and not np.isnan(pr).any() and not np.isnan(po).any()
+    import os
+    os.environ["PPG_STREAMED"] = "0"
+    try:
+        c2 = Context(0, P)
+        o2, s2, r2 = c2.batch_resolve_arrays(table, poses, pushes)
+        c2.close()
+    finally:
+        os.environ.pop("PPG_STREAMED", None)
+    assert np.array_equal(ps, s2)
+    assert _bitwise(po, o2).all()
+    assert np.array_equal(pr.view(np.uint64), r2.view(np.uint64))
+    idx = np.unique(np.concatenate([np.linspace(0, E - 1, 1500).astype(np.int64), hit[-200:]]))
+    o3, s3, r3 = port.batch_resolve(_take(table, idx), np.ascontiguousarray(poses[idx]),
+                                    np.ascontiguousarray(pushes[idx]), P)
+    assert np.array_equal(ps[idx], s3)
+    assert _bitwise(po[idx], o3).all()
