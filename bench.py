@@ -235,7 +235,7 @@ def pmbs_decisions(ctx, with_reference: bool):
     out["c4"] = c4_decision(ctx, with_reference)
     out["c3"] = c3_episodes(ctx, with_reference)
     out["c2_polygons"] = c2_polygons(ctx, with_reference)
-    out["rollouts"] = rollout_throughput(ctx)
+    out["rollouts"] = rollout_throughput(ctx, with_reference)
     return out
 
 
@@ -276,26 +276,40 @@ def c1_decisions(ctx, with_reference: bool):
     return out
 
 
-def rollout_throughput(ctx):
+def rollout_throughput(ctx, with_reference: bool):
     """SURVEY §8d's second C2 metric, rollout env-steps/s (the fused
     RolloutCursor::step: sample + pick + resolve + graspable): one lockstep
     batch_simulate of 65,536 envs from case_18's root (cap d_T + d_s = 10,
-    leaf parallel, re-purposing on), through ppg_simulate."""
+    leaf parallel, re-purposing on), through ppg_simulate, vs the unmodified
+    reference pmbs::batch_simulate with WorkerPool(nproc) on the same call
+    (same rewards; the reference's rollout-step count equals the GPU's
+    because every result is bit-identical)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import golden_io
     from paper_2207_06649_b200.abi import default_params
     c, st = {cc["case_id"]: (cc, s) for cc, s in golden_io.cases()}["case_18"]
     ne = 65536
-    ctx.set_params(default_params(n_envs=ne, rng_seed=int(c["seed"])))
+    p = default_params(n_envs=ne, rng_seed=int(c["seed"]))
+    ctx.set_params(p)
     ctx.set_scene(st)
     meta = np.zeros((1, 3), np.int32)
     ctx.simulate_arrays(st.poses[None], meta, ne, True, int(c["seed"]), 0, 10)  # warm-up
     t0 = time.perf_counter()
-    _, ctr = ctx.simulate_arrays(st.poses[None], meta, ne, True, int(c["seed"]), 1, 10)
+    rew, ctr = ctx.simulate_arrays(st.poses[None], meta, ne, True, int(c["seed"]), 1, 10)
     dt = time.perf_counter() - t0
-    return {"workload": "ppg_simulate: 65,536 envs from proj/cases/case_18's root, cap 10", "unit": UNIT,
-            "rollout_steps": int(ctr[0]), "resolve_calls": int(ctr[3]), "rounds": int(ctr[1]),
-            "repurposes": int(ctr[2]), "seconds": dt, "rollout_env_steps_per_s": int(ctr[0]) / dt}
+    row = {"workload": "ppg_simulate: 65,536 envs from proj/cases/case_18's root, cap 10, iteration 1", "unit": UNIT,
+           "rollout_steps": int(ctr[0]), "resolve_calls": int(ctr[3]), "rounds": int(ctr[1]),
+           "repurposes": int(ctr[2]), "seconds": dt, "rollout_env_steps_per_s": int(ctr[0]) / dt}
+    if with_reference:
+        from oracle import ref
+        if ref.available():
+            threads = os.cpu_count() or 1
+            rr, secs = ref.batch_simulate([st], meta, p, 1, 10, threads=threads)
+            row["reference"] = {"seconds": secs, "rollout_env_steps_per_s": int(ctr[0]) / secs, "cores": threads,
+                                "kind": "reference", "same_rewards": bool(np.array_equal(rr.view(np.uint64),
+                                                                                         rew.view(np.uint64))),
+                                "sample": "the same batch_simulate call (pmbs::batch_simulate, WorkerPool(nproc))"}
+    return row
 
 
 def c2_polygons(ctx, with_reference: bool):
@@ -385,6 +399,50 @@ def c3_episodes(ctx, with_reference: bool):
     if ref_d:
         row.update({"reference_s_per_decision": ref_t / ref_d, "same_outcomes": bool(same)})
     return row
+
+
+def c5_sharded_rollouts(world: int, rank: int, local: int) -> dict:
+    """BASELINE config 5 / SURVEY 8d C5: PMBS decisions with the rollout batch
+    sharded over the job's GPUs by the library itself (csrc/multi.cu: one
+    NCCL all-reduce of the per-node remaining work per lockstep round, one
+    reward max per iteration; the tree replicated).  Scene: the C4 dense ring
+    (generate_case_motif(Ring, 16), seed 5), d_T 9, N_a 24, iteration budget
+    10.  weak: N_e = 32,768 x G; strong: N_e = 65,536 at every G — its tree
+    signature must equal the G = 1 run's (printed, compared across the
+    driver's N runs).  Seconds = max over ranks of one decision (after a
+    warm-up decision); env-steps = expansions + rollout steps of the whole
+    batch (all shards)."""
+    import torch
+    from paper_2207_06649_b200 import Budget, Context, ParallelConfig, run_pmbs
+    from paper_2207_06649_b200.scenes import generate_case
+    os.environ.setdefault("PPG_NCCL_TIMEOUT_S", "90")  # a broken exchange errors out instead of hanging the job
+    out = {"scene": "ring16 seed 5 (generate_case_motif Ring, 16 discs)", "tree_depth": 9, "pushes_per_object": 24,
+           "budget_iterations": 10, "unit": "s/decision", "transport": None}
+    try:
+        if world > 1:
+            from paper_2207_06649_b200.sharded import rank_context
+            ctx = rank_context(local)
+        else:
+            ctx = Context.rank(local, 0, 1, None)
+        out["transport"] = ctx.shard_info()
+        st = generate_case(16, 0.0, 5, "ring")
+        for name, ne in (("weak", 32768 * world), ("strong", 65536)):
+            cfg = ParallelConfig(rng_seed=5, n_envs=ne, tree_depth=9, pushes_per_object=24,
+                                 budget=Budget.iterations(10))
+            run_pmbs(st, cfg, ctx=ctx)  # warm-up (graph capture, buffers)
+            dist_barrier(world)
+            t0 = time.perf_counter()
+            r = run_pmbs(st, cfg, ctx=ctx)
+            torch.cuda.synchronize()
+            dt = dist_max(time.perf_counter() - t0, world)
+            out[name] = {"n_envs": ne, "s_per_decision": dt, "env_steps": int(r.env_steps),
+                         "env_steps_per_s": r.env_steps / dt, "iterations": int(r.iterations),
+                         "lockstep_rounds": int(r.lockstep_rounds), "signature_fnv": str(r.signature_fnv),
+                         "action": [float(x) for x in r.action]}
+        ctx.close()
+    except Exception as e:  # reported, never fatal for the headline line
+        out["error"] = f"{type(e).__name__}: {e}"
+    return out
 
 
 def committed_traffic(E: int, n: int) -> dict:
@@ -565,6 +623,8 @@ def run_ours(args, world, rank, local):
             "roofline": roof, "clocks": clk, "gpu_launches": 2 * args.steps,
             "status_counts": np.bincount(status, minlength=3).tolist(), "sweep_env_steps_per_s": sweep,
             "workload_gen_s": gen_s}
+    if not args.no_c5:
+        line["c5_sharded_rollouts"] = c5_sharded_rollouts(world, rank, local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference_sample(table, poses, pushes, params, min(args.ref_sample, E) if args.ref_sample > 0 else E,
                                                     args.cpu_seconds, os.cpu_count() or 1)
@@ -586,6 +646,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pmbs", action="store_true", help="skip the PMBS s/decision block")
+    ap.add_argument("--no-c5", action="store_true", help="skip the sharded-rollout (C5) block")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:

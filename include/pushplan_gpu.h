@@ -192,6 +192,34 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
                  int n_envs, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap,
                  double* rewards_out, int64_t* counters);
 
+/* ---- multi-GPU contexts (BASELINE configs[4]) ----
+ * The rollout batch of every PMBS iteration (batch_simulate, pmbs.cpp:207-234)
+ * is sharded by environment over G GPUs: shard r owns a contiguous range of
+ * the global env batch (RNG keys and the env -> node split stay global), the
+ * search tree is replicated, and each lockstep round exchanges ONE vector —
+ * the per-node remaining work W (pmbs.cpp:157-163), all-reduced (sum) over
+ * NVLink — so every shard re-purposes its own finished envs to the same
+ * argmax node as the reference's sequential harvest (pmbs.cpp:165-187).
+ * Per-node rewards are all-reduced (max) once per iteration.  Results
+ * (decision, tree, rewards) are bit-identical for every G.  ppg_simulate and
+ * ppg_run_pmbs* on such a context run sharded; every other call runs on the
+ * context's own device.  All ranks / shards must make the same calls (SPMD).
+ *
+ * ppg_create_rank: one process per GPU (torchrun); rank 0 makes the NCCL id
+ * with ppg_nccl_unique_id and the caller broadcasts it (128 bytes).
+ * ppg_create_multi: one process driving n_dev GPUs (ncclCommInitAll);
+ * flags PPG_MULTI_EMULATE: n_dev shards on ONE device (devices all equal)
+ * exchanging through a device kernel — the test double of the NCCL path on a
+ * single GPU.  ppg_destroy on the returned context releases every shard. */
+#define PPG_MULTI_EMULATE 1
+int ppg_nccl_unique_id(uint8_t* id /* 128 bytes */);
+ppg_ctx* ppg_create_rank(int device, int rank, int world, const uint8_t* nccl_id, const ppg_params* params,
+                         int* err);
+ppg_ctx* ppg_create_multi(const int* devices, int n_dev, int flags, const ppg_params* params, int* err);
+/* rank = global shard index of this context's first shard; transport 0 none,
+ * 1 NCCL, 2 emulated (one device). */
+int ppg_shard_info(ppg_ctx* ctx, int* rank, int* world, int* shards_here, int* transport);
+
 /* ---- sharded lockstep (multi-GPU batch_simulate) ----
  * The lockstep engine split by environment: this context owns global envs
  * [env_lo, env_hi) of a batch of used_envs (= n_envs with leaf parallelism,

@@ -40,6 +40,8 @@ def lib():
         L.ref_c2_workload.argtypes = [c_int, c_double, c_uint64, c_int, c_uint64, c_int, c_int, POINTER(c_double),
                                       POINTER(c_uint64)]
         L.ref_c3_trees.argtypes = [c_int, c_int, c_int, c_int] + [c_void_p] * 16
+        L.ref_batch_simulate.argtypes = [c_void_p, POINTER(c_int32), c_int, POINTER(PpgParams), c_uint64, c_int, c_int,
+                                         POINTER(c_double), POINTER(c_double)]
         L.ref_load_scene.restype = c_void_p
         L.ref_load_scene.argtypes = [c_char_p]
         L.ref_fixture.restype = c_void_p
@@ -308,3 +310,21 @@ def c3_trees(variant: int, count: int = 200, cap_nodes: int = 200000, cap_pairs:
     for k in ("sel_node", "sel_untried"):
         a[k] = a[k][:npairs].copy()
     return a
+
+
+def batch_simulate(states, node_meta: np.ndarray, params: PpgParams, iteration: int, depth_cap: int,
+                   threads: int = 1):
+    """pmbs::batch_simulate (pmbs.cpp:207-234) on explicit nodes (one
+    WorldState per node, node_meta [n][3] = depth, graspable, dead).  Returns
+    (rewards, seconds of the reference call)."""
+    from paper_2207_06649_b200.world import ShapeTable as _ST
+    node_meta = np.ascontiguousarray(node_meta, np.int32)
+    n = len(node_meta)
+    h = states_handle(_ST.per_env(list(states)), np.stack([s.poses for s in states]))
+    rew = np.zeros(n, np.float64)
+    secs = c_double()
+    rc = lib().ref_batch_simulate(h.ptr, iptr(node_meta), n, ctypes.byref(params), iteration, depth_cap, threads,
+                                  dptr(rew), ctypes.byref(secs))
+    if rc != 0:
+        raise RuntimeError("ref_batch_simulate failed")
+    return rew, secs.value

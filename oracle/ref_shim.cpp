@@ -560,6 +560,39 @@ int ref_first_iteration(void* h, int i, const ppg_params* p, uint64_t iteration,
   return static_cast<int>(children.size());
 }
 
+// batch_simulate (pmbs.cpp:207-234) with WorkerPool(threads) on explicit new
+// nodes: state i of the handle with node_meta[i] = {depth, graspable, dead};
+// the tree's d_T / d_s are set so that d_T + d_s == depth_cap.  Times the
+// reference call alone (bench.py's rollout CPU baseline).
+int ref_batch_simulate(void* h, const int32_t* node_meta, int n_nodes, const ppg_params* p, uint64_t iteration,
+                       int depth_cap, int threads, double* rewards, double* seconds) {
+  States* st = static_cast<States*>(h);
+  if (static_cast<int>(st->v.size()) < n_nodes) return -1;
+  pmbs::ParallelConfig cfg = to_cfg(p);
+  mcts::SearchTree tree;
+  tree.tree_depth = depth_cap;
+  tree.rollout_depth = 0;
+  std::vector<std::unique_ptr<mcts::TreeNode>> own;
+  std::vector<mcts::TreeNode*> nodes;
+  for (int i = 0; i < n_nodes; ++i) {
+    auto x = std::make_unique<mcts::TreeNode>();
+    x->state = st->v[i];
+    x->depth = node_meta[i * 3];
+    x->graspable_flag = node_meta[i * 3 + 1] != 0;
+    x->dead_flag = node_meta[i * 3 + 2] != 0;
+    nodes.push_back(x.get());
+    own.push_back(std::move(x));
+  }
+  std::unique_ptr<WorkerPool> pool;
+  if (threads > 1) pool = std::make_unique<WorkerPool>(threads);
+  const auto t0 = std::chrono::steady_clock::now();
+  const auto r = pmbs::batch_simulate(tree, nodes, cfg, pool.get(), iteration);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+  for (int i = 0; i < n_nodes; ++i) rewards[i] = r[i];
+  return 0;
+}
+
 // run_episode (bench.cpp:54-126) with the reference planner; returns actions
 // used, sets completed and planning seconds.
 int ref_run_episode(void* h, int i, const char* case_id, int trial, const ppg_params* p,

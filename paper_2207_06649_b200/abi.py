@@ -20,6 +20,7 @@ PPG_MAX_OBJECTS = 32
 PPG_MAX_VERTICES = 8
 
 PPG_SUCCESS = 0
+PPG_MULTI_EMULATE = 1
 PPG_PLANNER_AUTO, PPG_PLANNER_HOST, PPG_PLANNER_DEVICE = 0, 1, 2
 PPG_EINVAL = -1
 PPG_ECUDA = -2
@@ -181,6 +182,10 @@ SIGNATURES = {
     "ppg_debug_sincos": (c_int, [c_void_p, POINTER(c_double), c_int, POINTER(c_double), POINTER(c_double)]),
     "ppg_debug_select_batch": (c_int, [c_void_p, c_int] + [c_void_p] * 7 + [c_int, c_int, c_double]
                                + [c_void_p] * 5),
+    "ppg_nccl_unique_id": (c_int, [c_void_p]),
+    "ppg_create_rank": (c_void_p, [c_int, c_int, c_int, c_void_p, POINTER(PpgParams), POINTER(c_int)]),
+    "ppg_create_multi": (c_void_p, [c_void_p, c_int, c_int, POINTER(PpgParams), POINTER(c_int)]),
+    "ppg_shard_info": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ppg_measure_fp64_peak": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "ppg_generate_cases": (c_int, [c_int, c_int, c_double, POINTER(c_uint64), c_int, POINTER(c_int32),
                                    POINTER(c_double), POINTER(c_int32), POINTER(c_double), POINTER(c_double),
@@ -195,11 +200,33 @@ SIMULATE_FN = ctypes.CFUNCTYPE(c_int, c_void_p, POINTER(c_double), POINTER(c_int
 _LIB = None
 
 
+def _torch_nccl_path():
+    """The libnccl that torch ships (nvidia-nccl wheel), found without
+    importing torch.  The library loads NCCL at run time; pointing it at
+    torch's copy keeps one NCCL build per process whichever of the two is
+    loaded first (a system libnccl.so.2 loaded before torch would shadow
+    torch's by soname)."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        f = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(f):
+            return f
+    return None
+
+
 def load_library(path: str = LIB_PATH):
     """Loads the in-tree CUDA library; raises (no fallback) when absent."""
     global _LIB
     if _LIB is not None and path == LIB_PATH:
         return _LIB
+    if "PPG_NCCL_LIB" not in os.environ:
+        nccl = _torch_nccl_path()
+        if nccl:
+            os.environ["PPG_NCCL_LIB"] = nccl
     if not os.path.exists(path):
         raise RuntimeError(
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

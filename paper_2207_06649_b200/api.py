@@ -149,15 +149,46 @@ class Context:
     """One device context (the reference WorkerPool seam).  Not thread-safe:
     one context per host thread, as the C-ABI states."""
 
-    def __init__(self, device: int = 0, params: Optional[PpgParams] = None):
+    def __init__(self, device: int = 0, params: Optional[PpgParams] = None, _create=None):
         self.lib = abi.load_library()
         err = ctypes.c_int()
         self.params = params if params is not None else abi.default_params()
-        self.ptr = self.lib.ppg_create(device, ctypes.byref(self.params), ctypes.byref(err))
+        if _create is None:
+            self.ptr = self.lib.ppg_create(device, ctypes.byref(self.params), ctypes.byref(err))
+        else:
+            self.ptr = _create(self.lib, self.params, err)
         if not self.ptr:
-            raise DeviceError(f"ppg_create failed: {_ERRS.get(err.value, err.value)}")
+            raise DeviceError(f"context creation failed: {_ERRS.get(err.value, err.value)}")
         self.device = device
         self._scene_key = None
+
+    # ---- multi-GPU contexts (csrc/multi.cu; SURVEY 8(e)) ----------------------
+    @classmethod
+    def multi(cls, devices: Sequence[int], params: Optional[PpgParams] = None, emulate: bool = False) -> "Context":
+        """One process driving several GPUs (ncclCommInitAll): batch_simulate
+        and run_pmbs shard the rollout batch over `devices`.  emulate=True:
+        the shards all live on one device and exchange through a device
+        kernel (the single-GPU test double of the NCCL path)."""
+        devs = (ctypes.c_int * len(devices))(*devices)
+        flags = abi.PPG_MULTI_EMULATE if emulate else 0
+        return cls(devices[0], params, lambda lib, p, err: lib.ppg_create_multi(devs, len(devices), flags,
+                                                                              ctypes.byref(p), ctypes.byref(err)))
+
+    @classmethod
+    def rank(cls, device: int, rank: int, world: int, nccl_id: Optional[bytes],
+             params: Optional[PpgParams] = None) -> "Context":
+        """One shard per process (torchrun): rank `rank` of `world`, NCCL
+        communicator from the 128-byte id rank 0 made (nccl_unique_id)."""
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        return cls(device, params, lambda lib, p, err: lib.ppg_create_rank(device, rank, world, buf, ctypes.byref(p),
+                                                                         ctypes.byref(err)))
+
+    def shard_info(self) -> dict:
+        r, w, h, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        self._check(self.lib.ppg_shard_info(self.ptr, ctypes.byref(r), ctypes.byref(w), ctypes.byref(h),
+                                            ctypes.byref(t)), "ppg_shard_info")
+        return {"rank": r.value, "world": w.value, "shards_here": h.value,
+                "transport": {0: "none", 1: "nccl", 2: "emulated"}[t.value]}
 
     def close(self):
         if getattr(self, "ptr", None):
@@ -293,6 +324,16 @@ class Context:
                             int(st.signature_fnv), st.n_nodes, sig,
                             {"select": st.select_s, "expand": st.expand_s, "simulate": st.simulate_s,
                              "backprop": st.backprop_s})
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 makes it, the caller
+    broadcasts the 128 bytes)."""
+    lib = abi.load_library()
+    buf = ctypes.create_string_buffer(128)
+    if lib.ppg_nccl_unique_id(buf) != abi.PPG_SUCCESS:
+        raise DeviceError("ppg_nccl_unique_id: NCCL unavailable")
+    return buf.raw
 
 
 _DEFAULT_CTX: Optional[Context] = None

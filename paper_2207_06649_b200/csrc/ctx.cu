@@ -270,6 +270,7 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
 
 void ppg_destroy(ppg_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->group && ppg::group_member(ctx->group, 0) == ctx) ppg::group_destroy(ctx);  // also the other shards
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   DevBuf* bufs[] = {&ctx->scene_buf, &ctx->scene_in, &ctx->shape_buf, &ctx->shape_in, &ctx->b_in, &ctx->b_push,
@@ -291,6 +292,8 @@ void ppg_destroy(ppg_ctx* ctx) {
     if (ctx->chunk_ev[k]) cudaEventDestroy(ctx->chunk_ev[k]);
   }
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
+  ctx->l_go.release();
+  if (ctx->h_go) cudaFreeHost(ctx->h_go);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -302,6 +305,8 @@ int ppg_set_params(ppg_ctx* ctx, const ppg_params* params) {
   const int rc = check_params(ctx, *params);
   if (rc != PPG_SUCCESS) return rc;
   ctx->params = *params;
+  if (ctx->group && ppg::group_member(ctx->group, 0) == ctx)  // the other shards of a multi-device context
+    for (int k = 1; k < ppg::group_size(ctx->group); ++k) ppg::group_member(ctx->group, k)->params = *params;
   return PPG_SUCCESS;
 }
 
@@ -323,6 +328,18 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
   if (rc != PPG_SUCCESS) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->has_scene = true;
+  if (ctx->group && ppg::group_member(ctx->group, 0) == ctx)  // the other shards of a multi-device context
+    for (int k = 1; k < ppg::group_size(ctx->group); ++k) {
+      ppg_ctx* c = ppg::group_member(ctx->group, k);
+      ppg::Group* g = c->group;
+      c->group = nullptr;  // install on the member alone
+      const int rc2 = ppg_set_scene(c, shapes);
+      c->group = g;
+      if (rc2 != PPG_SUCCESS) {
+        ctx->err = c->err;
+        return rc2;
+      }
+    }
   return PPG_SUCCESS;
 }
 
@@ -947,7 +964,7 @@ int ppg_expand(ppg_ctx* ctx, const double* parent_poses, const double* actions, 
 // Allocates and initialises the lockstep state for `used` local environments
 // (global indices env_lo .. env_lo+used-1 of a batch of used_global) over the
 // given nodes; runs lock_init_kernel.
-static int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used,
+int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used,
                       int used_global, int env_lo, int leaf_parallel, uint64_t seed, uint64_t iteration,
                       int depth_cap) {
   cudaStream_t st = ctx->stream;
@@ -1031,11 +1048,11 @@ static int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* nod
 // One lockstep round over the current active list (at most `act` envs):
 // latency mode (one warp per env), the 3-phase disc pipeline, or the generic
 // one-lane step.
-static int lock_round(ppg_ctx* ctx, int act) {
+int lock_round(ppg_ctx* ctx, int act) {
   return lock_round_on(ctx, ctx->lc, ctx->la, ctx->lra, act, round_mode(ctx, ctx->scene.n, act), ctx->stream);
 }
 
-static int lock_check(ppg_ctx* ctx, int n_nodes, int n_envs, int depth_cap) {
+int lock_check(ppg_ctx* ctx, int n_nodes, int n_envs, int depth_cap) {
   if (n_envs < n_nodes) {
     ctx->err = "lockstep_simulate: fewer environments than nodes";
     return PPG_EINVAL;
@@ -1058,6 +1075,9 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
                  int64_t* counters) {
   if (!ctx) return PPG_EINVAL;
   if (n_nodes <= 0) return PPG_SUCCESS;
+  if (ctx->group)  // multi-GPU: the rollout batch sharded by environment (multi.cu)
+    return ppg::simulate_sharded(ctx, node_poses, node_meta, n_nodes, n_envs, leaf_parallel, seed, iteration,
+                                 depth_cap, rewards_out, counters);
   int rc = lock_check(ctx, n_nodes, n_envs, depth_cap);
   if (rc != PPG_SUCCESS) return rc;
   CK(cudaSetDevice(ctx->device));

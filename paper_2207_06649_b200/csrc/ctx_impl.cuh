@@ -22,6 +22,8 @@ __global__ void grasp_kernel(const __grid_constant__ SimConst C, SampleArgs a);
 __global__ void expand_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
 __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_harvest_local_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_harvest_apply_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
@@ -120,6 +122,7 @@ struct DevBuf {
 namespace ppg {
 struct DTreeState;
 void dtree_release(ppg_ctx* ctx);
+struct Group;  // multi.cu: the shards of a multi-GPU context and their exchange
 }  // namespace ppg
 
 struct ppg_ctx {
@@ -178,6 +181,12 @@ struct ppg_ctx {
   void* fn_wait32 = nullptr;              // cuStreamWaitValue32
   cudaStream_t pipe_stream[3] = {};       // host->device copies, physics, device->host copies
   cudaEvent_t pipe_ev = nullptr;          // slice 0 resident
+  // multi-GPU (multi.cu): a rank context (ppg_create_rank, one process per
+  // GPU) or a multi-device context (ppg_create_multi, one process) points at
+  // its group; batch_simulate / run_pmbs then shard the rollout batch
+  ppg::Group* group = nullptr;
+  ppg::DevBuf l_go;                       // sharded harvest: "any env active" (device int)
+  int32_t* h_go = nullptr;                // pinned copy
 };
 
 SimConst make_const(const ppg_params& p, int n, double side, double margin);
@@ -193,3 +202,32 @@ enum class RoundMode { kWarp, kHybrid, kLaneDisc, kGeneric, kAdaptive };
 RoundMode round_mode(const ppg_ctx* ctx, int n, int envs);
 int lock_round_on(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const ResolveArgs& ra, int work,
                   RoundMode mode, cudaStream_t st);
+int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used,
+               int used_global, int env_lo, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap);
+int lock_round(ppg_ctx* ctx, int act);
+int lock_check(ppg_ctx* ctx, int n_nodes, int n_envs, int depth_cap);
+
+namespace ppg {
+// multi.cu: the shards of a multi-GPU context.  Member k of this process is
+// global shard rank0 + k of `world`; members all run the same calls (SPMD).
+struct Group;
+int group_size(const Group* g);
+ppg_ctx* group_member(const Group* g, int k);
+int group_rank0(const Group* g);
+int group_world(const Group* g);
+// In-place exchange over every shard (all ranks): sum of int32 / max of
+// uint64 (bit patterns of non-negative doubles), enqueued on each member's
+// stream; bufs[k] belongs to member k.
+int group_allreduce_sum_i32(ppg_ctx* ectx, Group* g, int32_t* const* bufs, size_t count);
+int group_allreduce_max_u64(ppg_ctx* ectx, Group* g, unsigned long long* const* bufs, size_t count);
+int group_allreduce_sum_i64(ppg_ctx* ectx, Group* g, long long* const* bufs, size_t count);
+// Waits for every member's stream (bounded by PPG_NCCL_TIMEOUT_S; a timeout
+// aborts the communicators and reports an error instead of hanging).
+int group_wait(ppg_ctx* ectx, Group* g);
+void group_destroy(ppg_ctx* ctx);
+int simulate_sharded(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
+                     int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, double* rewards_out,
+                     int64_t* counters);
+int run_pmbs_sharded(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats,
+                     char* sig_buf, int64_t sig_cap, int64_t* sig_len);
+}  // namespace ppg

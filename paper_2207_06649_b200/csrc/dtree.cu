@@ -493,8 +493,10 @@ struct DTreeState {
   int n_envs = 0, n = 0, na = 0;
   cudaGraphExec_t exec = nullptr;  // the iteration (or its pre part when hooked)
   cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec_post = nullptr;  // hooked: backprop + stop
+  cudaGraphExec_t exec_post = nullptr;  // hooked / sharded: backprop + stop
   cudaGraph_t graph_post = nullptr;
+  cudaGraphExec_t exec_round = nullptr;  // sharded: one lockstep round + the local harvest half
+  cudaGraph_t graph_round = nullptr;
   cudaStream_t st2 = nullptr;
   DTree t{};
   LockArgs la{};
@@ -507,8 +509,10 @@ struct DTreeState {
     if (graph) cudaGraphDestroy(graph);
     if (exec_post) cudaGraphExecDestroy(exec_post);
     if (graph_post) cudaGraphDestroy(graph_post);
-    exec = exec_post = nullptr;
-    graph = graph_post = nullptr;
+    if (exec_round) cudaGraphExecDestroy(exec_round);
+    if (graph_round) cudaGraphDestroy(graph_round);
+    exec = exec_post = exec_round = nullptr;
+    graph = graph_post = graph_round = nullptr;
   }
   void release() {
     release_graph();
@@ -946,6 +950,413 @@ std::string signature(const std::vector<int32_t>& depth, const std::vector<doubl
 
 }  // namespace
 
+namespace {
+
+// Search start (SearchTree::create, mcts.cpp:28-39, + run_pmbs setup,
+// pmbs.cpp:242-260): root sample_pushes / graspable, tree + batch buffers,
+// the graph key (graphs are re-captured when the configuration changes) and
+// the root node + scalars on the device.
+int dt_begin(ppg_ctx* ctx, const double* root_poses, bool sharded) {
+  const ppg_params& p = ctx->params;
+  if (p.n_envs < 1) {
+    ctx->err = "n_envs must be >= 1";
+    return PPG_EINVAL;
+  }
+  if (p.tree_depth + 1 >= kMaxTreeDepth || p.tree_depth + p.rollout_depth + 1 >= kMaxGammaPow) {
+    ctx->err = "device tree: tree_depth too large";
+    return PPG_EINVAL;
+  }
+  DCK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int n = ctx->scene.n, na = p.pushes_per_object;
+  // root: sample_pushes + graspable (SearchTree::create, mcts.cpp:28-39)
+  std::vector<double> root_untried(static_cast<size_t>(n) * na * 4);
+  int32_t cnt = 0;
+  int rc = ppg_sample_pushes(ctx, nullptr, root_poses, 1, root_untried.data(), &cnt);
+  if (rc != PPG_SUCCESS) return rc;
+  uint8_t rg = 0;
+  rc = ppg_graspable(ctx, root_poses, 1, &rg, nullptr, nullptr, nullptr, nullptr);
+  if (rc != PPG_SUCCESS) return rc;
+  if (cnt == 0) {
+    ctx->err = "no legal push action at the root";
+    return PPG_ENOLEGAL;
+  }
+  if (!ctx->dtree) ctx->dtree = new DTreeState;
+  DTreeState& S = *ctx->dtree;
+  {
+    // everything baked into the captured graph: parameters (minus the
+    // per-search values kept in DTScal), scene tables
+    ppg_params kp = p;
+    kp.rng_seed = 0;
+    kp.c_explore = 0.0;
+    kp.budget_iterations = 0;
+    kp.max_iterations = 0;
+    kp.max_seconds = 0.0;
+    std::string key(reinterpret_cast<const char*>(&kp), sizeof kp);
+    key.append(reinterpret_cast<const char*>(&ctx->scene), sizeof ctx->scene);
+    key.append(reinterpret_cast<const char*>(&ctx->side), sizeof ctx->side);
+    key.append(reinterpret_cast<const char*>(&ctx->margin), sizeof ctx->margin);
+    // kernel-mode inputs (which kernels the graph holds)
+    const int modes[8] = {ctx->scene_all_discs ? 1 : 0, ctx->force_generic ? 1 : 0, ctx->warp_poly ? 1 : 0,
+                          ctx->warp_max_envs, ctx->warp_max_explicit ? 1 : 0, ctx->disc_kernels ? 1 : 0,
+                          ctx->hybrid_min_envs, (ctx->sim_hook ? 1 : 0) | (sharded ? 2 : 0)};
+    key.append(reinterpret_cast<const char*>(modes), sizeof modes);
+    if (S.key != key) S.release_graph();
+    S.key = key;
+  }
+  if (S.n != n) {  // per-node pose rows change size: start the tree buffers afresh
+    DevBuf* node_bufs[] = {&S.parent, &S.depth, &S.q, &S.visits, &S.vv, &S.flags, &S.u_off, &S.u_n, &S.u_head,
+                           &S.c_n, &S.selc, &S.action, &S.poses, &S.anc, &S.apool, &S.cpool};
+    DCK(cudaStreamSynchronize(st));
+    for (DevBuf* b : node_bufs) b->release();
+    S.cap_nodes = 0;
+    S.cap_actions = 0;
+    S.release_graph();
+  }
+  S.n_envs = p.n_envs;
+  S.n = n;
+  S.na = na;
+  if (S.logtab.cap < (static_cast<size_t>(S.cap_nodes) + p.n_envs + 2) * 8) {  // log table covers visits + n_envs
+    S.cap_nodes = 0;  // forces dt_reserve to re-grow (contents preserved up to used = 0: fresh search)
+  }
+  {
+    int want = 1 + p.n_envs * (p.budget_iterations ? std::min<long long>(p.max_iterations, 64) : 8);
+    if (const char* cn = std::getenv("PPG_DTREE_NODES")) want = std::max(want, std::atoi(cn));
+    want = std::max(want, 1 + 2 * p.n_envs);
+    if ((rc = dt_reserve(ctx, S, 0, 0, want, static_cast<long long>(want) * n * na)) != PPG_SUCCESS) return rc;
+  }
+  if ((rc = dt_batch(ctx, S)) != PPG_SUCCESS) return rc;
+  dt_views(ctx, S);
+  // root node + scalars
+  {
+    const int32_t zero = 0, m1 = -1;
+    const long long zl = 0;
+    const double zd = 0.0;
+    const uint8_t rf = static_cast<uint8_t>(rg ? 1 : 0);  // dead needs untried.empty(): cnt > 0 here
+    DCK(cudaMemcpyAsync(S.t.parent, &m1, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.depth, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.q, &zd, 8, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.visits, &zl, 8, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.vv, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.flags, &rf, 1, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.u_off, &zl, 8, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.u_n, &cnt, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.u_head, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.c_n, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.selc, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemsetAsync(S.t.action, 0, 32, st));
+    DCK(cudaMemcpyAsync(S.t.poses, root_poses, static_cast<size_t>(n) * 24, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.anc, &zero, 4, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemcpyAsync(S.t.apool, root_untried.data(), static_cast<size_t>(cnt) * 32, cudaMemcpyHostToDevice, st));
+    DTScal h;
+    std::memset(&h, 0, sizeof h);
+    h.n_nodes = 1;
+    h.dT = p.tree_depth;
+    h.dS = p.rollout_depth;
+    h.es_level = 1;
+    h.min_grasp_depth = INT_MAX;
+    h.levels = 1;
+    h.stop = -1;
+    h.a_used = cnt;
+    h.unsettled[0] = rg ? 0 : 1;  // root: non-terminal with untried actions unless graspable
+    h.max_iters = p.budget_iterations ? static_cast<int>(p.max_iterations) : 0;
+    h.c_explore = p.c_explore;
+    h.lock_dyn[4] = static_cast<int>(static_cast<uint32_t>(p.rng_seed));
+    h.lock_dyn[5] = static_cast<int>(static_cast<uint32_t>(p.rng_seed >> 32));
+    DCK(cudaMemcpyAsync(S.t.sc, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    DCK(cudaMemsetAsync(S.la.counters, 0, 32, st));
+  }
+  return PPG_SUCCESS;
+}
+
+// Reads the final tree back once: best_root_child (mcts.cpp:218-235), the
+// tree signature (mcts.cpp:284-300) and the statistics.  ctr = rollout steps,
+// rounds, re-purposes, resolve calls of the whole search.
+int dt_finish(ppg_ctx* ctx, const DTScal& h, int stop, double elapsed_s, double loop_s, const int64_t* ctr_in,
+              double* action_out, ppg_search_stats* stats, char* sig_buf, int64_t sig_cap, int64_t* sig_len) {
+  DTreeState& S = *ctx->dtree;
+  const ppg_params& p = ctx->params;
+  cudaStream_t st = ctx->stream;
+  int64_t ctr[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  if (stop == 3) {
+    ctx->err = "device tree: selection invariant violated";
+    return PPG_EINVAL;
+  }
+  // read the tree back once
+  const int N = h.n_nodes;
+  std::vector<int32_t> depth(N), c_n(N), parent(N);
+  std::vector<double> q(N), action(static_cast<size_t>(N) * 4);
+  std::vector<long long> visits(N), u_off(N);
+  std::vector<uint8_t> flags(N);
+  std::vector<int32_t> cpool(static_cast<size_t>(h.a_used));
+  DCK(cudaMemcpyAsync(depth.data(), S.t.depth, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(c_n.data(), S.t.c_n, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(q.data(), S.t.q, N * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(action.data(), S.t.action, N * 32ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(visits.data(), S.t.visits, N * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(u_off.data(), S.t.u_off, N * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(flags.data(), S.t.flags, N, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(cpool.data(), S.t.cpool, static_cast<size_t>(h.a_used) * 4, cudaMemcpyDeviceToHost, st));
+  DCK(cudaStreamSynchronize(st));
+  // best_root_child (mcts.cpp:218-235)
+  int best = -1;
+  double best_score = -std::numeric_limits<double>::infinity();
+  long long best_visits = -1;
+  for (int k = 0; k < c_n[0]; ++k) {
+    const int ch = cpool[u_off[0] + k];
+    if (visits[ch] == 0) continue;
+    const double score = p.rank_by_ucb ? ucb_score_host(q[ch], static_cast<long>(visits[ch]), static_cast<long>(visits[0]),
+                                                        p.c_explore)
+                                       : q[ch] / static_cast<double>(visits[ch]);
+    if (score > best_score || (score == best_score && visits[ch] > best_visits)) {
+      best_score = score;
+      best_visits = visits[ch];
+      best = ch;
+    }
+  }
+  if (best < 0) {
+    ctx->err = "search produced no evaluated root child";
+    return PPG_EINVAL;
+  }
+  std::memcpy(action_out, &action[static_cast<size_t>(best) * 4], 32);
+  const std::string sig = signature(depth, action, visits, q, flags, u_off, c_n, cpool);
+  if (stats) {
+    ppg_search_stats s;
+    std::memset(&s, 0, sizeof s);
+    s.iterations = h.iteration;
+    s.expansions = h.expansions;
+    s.elapsed_s = elapsed_s;
+    s.stop_reason = stop;
+    s.final_tree_depth = h.dT;
+    s.env_steps = ctr[3] + h.expansions;
+    s.rollout_steps = ctr[0];
+    s.lockstep_rounds = ctr[1];
+    s.signature_fnv = fnv1a(sig);
+    s.n_nodes = N;
+    s.simulate_s = loop_s;  // one graph per iteration: the phases are not timed separately
+    *stats = s;
+  }
+  if (sig_len) *sig_len = static_cast<int64_t>(sig.size());
+  if (sig_buf && sig_cap > 0) {
+    const size_t m = sig.size() < static_cast<size_t>(sig_cap - 1) ? sig.size() : static_cast<size_t>(sig_cap - 1);
+    std::memcpy(sig_buf, sig.data(), m);
+    sig_buf[m] = '\0';
+  }
+  return PPG_SUCCESS;
+}
+
+// Sharded iteration graphs (multi-GPU, multi.cu): pre = select -> expand ->
+// attach -> copy -> lock_init -> local harvest half; round = one lockstep
+// round over this shard's active envs -> local harvest half; post = backprop
+// -> stop.  Between them the host enqueues the per-round W exchange and the
+// apply half of the harvest (lock_harvest_apply_kernel), which writes `go`.
+int dt_capture_sharded(ppg_ctx* ctx, DTreeState& S, int work) {
+  cudaStream_t st = ctx->stream;
+  const int E = S.n_envs;
+  S.la.cond = 0;
+  const RoundMode mode = dt_mode(ctx, S);
+  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  int rc = dt_launch_pre(ctx, S, st);
+  if (rc == PPG_SUCCESS) {
+    lock_init_kernel<<<(E + 255) / 256, 256, 0, st>>>(S.C, S.la);
+    lock_harvest_local_kernel<<<1, 1024, 0, st>>>(S.C, S.la);
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(st, &g);
+  if (rc != PPG_SUCCESS) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  DCK(e);
+  S.graph = g;
+  DCK(cudaGraphInstantiate(&S.exec, S.graph, 0));
+  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  rc = lock_round_on(ctx, S.C, S.la, S.lra, work, mode, st);
+  if (rc == PPG_SUCCESS) lock_harvest_local_kernel<<<1, 1024, 0, st>>>(S.C, S.la);
+  g = nullptr;
+  e = cudaStreamEndCapture(st, &g);
+  if (rc != PPG_SUCCESS) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  DCK(e);
+  S.graph_round = g;
+  DCK(cudaGraphInstantiate(&S.exec_round, S.graph_round, 0));
+  DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  dt_backprop_kernel<<<1, 32, 0, st>>>(S.t);
+  dt_stop_kernel<<<1, 1, 0, st>>>(S.t);
+  DCK(cudaStreamEndCapture(st, &S.graph_post));
+  DCK(cudaGraphInstantiate(&S.exec_post, S.graph_post, 0));
+  return PPG_SUCCESS;
+}
+
+}  // namespace
+
+// run_pmbs (pmbs.cpp:242-292) with the rollout batch sharded over the
+// context's group (multi.cu).  Every shard holds an identical device tree
+// (select / expand / attach / backprop replicated on identical data); each
+// iteration's lockstep is split by environment with ONE W exchange per round
+// and one reward max at the end, so the decision and the tree are
+// bit-identical to the single-GPU search for any shard count.
+namespace ppg {
+
+int run_pmbs_sharded(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats,
+                     char* sig_buf, int64_t sig_cap, int64_t* sig_len) {
+  Group* g = ctx->group;
+  const int M = group_size(g), G = group_world(g), r0 = group_rank0(g);
+  const auto t_start = std::chrono::steady_clock::now();
+  const auto elapsed = [&t_start] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  const ppg_params& p = ctx->params;
+  const int work = (p.n_envs + G - 1) / G;  // the largest shard
+  std::vector<ppg_ctx*> m(M);
+  for (int k = 0; k < M; ++k) m[k] = group_member(g, k);
+  const auto set_shard = [&](int k) {
+    DTreeState& S = *m[k]->dtree;
+    S.la.shard_r = r0 + k;
+    S.la.shard_g = G;
+    S.la.go = m[k]->l_go.as<int32_t>();
+  };
+  for (int k = 0; k < M; ++k) {
+    ppg_ctx* c = m[k];
+    int rc = dt_begin(c, root_poses, true);
+    if (rc != PPG_SUCCESS) {
+      ctx->err = c->err;
+      return rc;
+    }
+    if (c->l_go.ensure(16) != cudaSuccess || (!c->h_go && cudaMallocHost(&c->h_go, 16) != cudaSuccess)) {
+      ctx->err = "sharded run_pmbs: allocation failed";
+      return PPG_ECUDA;
+    }
+    set_shard(k);
+  }
+  std::vector<DTScal> h(M);
+  std::vector<int32_t*> wb(M);
+  std::vector<unsigned long long*> rb(M), vb(M);
+  std::vector<long long*> cb(M);
+  int stop = -1;
+  const long long per_iter_actions = static_cast<long long>(p.n_envs) * m[0]->dtree->n * m[0]->dtree->na;
+  const auto t_loop = std::chrono::steady_clock::now();
+  int rc = PPG_SUCCESS;
+  for (;;) {
+    for (int k = 0; k < M; ++k) {
+      DTreeState& S = *m[k]->dtree;
+      DCK(cudaSetDevice(m[k]->device));
+      DCK(cudaMemcpyAsync(&h[k], S.t.sc, sizeof(DTScal), cudaMemcpyDeviceToHost, m[k]->stream));
+      DCK(cudaStreamSynchronize(m[k]->stream));
+      if (h[k].round_guard < 0 || h[k].err[0]) {
+        ctx->err = "sharded device tree: lockstep round limit or corrupt ancestor row";
+        return PPG_EINVAL;
+      }
+      if (h[k].stop != h[0].stop || h[k].iteration != h[0].iteration || h[k].n_nodes != h[0].n_nodes) {
+        ctx->err = "sharded device tree: shards diverged";
+        return PPG_EINVAL;
+      }
+    }
+    if (h[0].stop >= 0) {
+      stop = h[0].stop;
+      break;
+    }
+    if (!p.budget_iterations && h[0].iteration > 0) {
+      // seconds budget: every shard must stop at the same iteration, so the
+      // shards vote (max) instead of each reading its own clock
+      const unsigned long long vote = elapsed() >= p.max_seconds ? 1ull : 0ull;
+      for (int k = 0; k < M; ++k) {
+        vb[k] = reinterpret_cast<unsigned long long*>(m[k]->l_go.as<char>() + 8);
+        DCK(cudaSetDevice(m[k]->device));
+        DCK(cudaMemcpyAsync(vb[k], &vote, 8, cudaMemcpyHostToDevice, m[k]->stream));
+      }
+      if ((rc = group_allreduce_max_u64(ctx, g, vb.data(), 1)) != PPG_SUCCESS) return rc;
+      for (int k = 0; k < M; ++k) {
+        DCK(cudaSetDevice(m[k]->device));
+        DCK(cudaMemcpyAsync(m[k]->h_go + 2, vb[k], 8, cudaMemcpyDeviceToHost, m[k]->stream));
+      }
+      if ((rc = group_wait(ctx, g)) != PPG_SUCCESS) return rc;
+      if (*reinterpret_cast<unsigned long long*>(m[0]->h_go + 2)) {
+        stop = 0;
+        break;
+      }
+    }
+    for (int k = 0; k < M; ++k) {
+      ppg_ctx* c = m[k];
+      DTreeState& S = *c->dtree;
+      DCK(cudaSetDevice(c->device));
+      if (h[k].n_nodes + p.n_envs > S.cap_nodes || h[k].a_used + per_iter_actions > S.cap_actions) {
+        const int want = std::max(2 * S.cap_nodes, h[k].n_nodes + p.n_envs);
+        const long long wa = std::max(2 * S.cap_actions, h[k].a_used + per_iter_actions);
+        if ((rc = dt_reserve(c, S, h[k].n_nodes, h[k].a_used, want, wa)) != PPG_SUCCESS) {
+          ctx->err = c->err;
+          return rc;
+        }
+        dt_views(c, S);
+        set_shard(k);
+      }
+      if (!S.exec && (rc = dt_capture_sharded(c, S, work)) != PPG_SUCCESS) {
+        cudaStreamCaptureStatus cs;
+        if (cudaStreamIsCapturing(c->stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+          cudaGraph_t junk = nullptr;
+          cudaStreamEndCapture(c->stream, &junk);
+          if (junk) cudaGraphDestroy(junk);
+        }
+        cudaGetLastError();
+        S.release_graph();
+        ctx->err = c->err;
+        return rc;
+      }
+      wb[k] = S.la.W;
+      rb[k] = S.la.rew;
+      cb[k] = S.la.counters;
+      DCK(cudaGraphLaunch(S.exec, c->stream));  // select ... lock_init, local harvest half
+      DCK(cudaMemcpyAsync(c->h_go + 2, &S.t.sc->n_pairs, 4, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if ((rc = group_wait(ctx, g)) != PPG_SUCCESS) return rc;
+    const int P = m[0]->h_go[2];
+    if (P > 0) {
+      for (;;) {
+        if ((rc = group_allreduce_sum_i32(ctx, g, wb.data(), static_cast<size_t>(P))) != PPG_SUCCESS) return rc;
+        for (int k = 0; k < M; ++k) {
+          DTreeState& S = *m[k]->dtree;
+          DCK(cudaSetDevice(m[k]->device));
+          lock_harvest_apply_kernel<<<1, 1024, 0, m[k]->stream>>>(S.C, S.la);
+          DCK(cudaGetLastError());
+          DCK(cudaMemcpyAsync(m[k]->h_go, S.la.go, 4, cudaMemcpyDeviceToHost, m[k]->stream));
+        }
+        if ((rc = group_wait(ctx, g)) != PPG_SUCCESS) return rc;
+        const int go = m[0]->h_go[0];
+        for (int k = 1; k < M; ++k)
+          if (m[k]->h_go[0] != go) {
+            ctx->err = "sharded lockstep: shards disagree on termination";
+            return PPG_EINVAL;
+          }
+        if (!go) break;
+        for (int k = 0; k < M; ++k) {
+          DCK(cudaSetDevice(m[k]->device));
+          DCK(cudaGraphLaunch(m[k]->dtree->exec_round, m[k]->stream));
+        }
+      }
+      if ((rc = group_allreduce_max_u64(ctx, g, rb.data(), static_cast<size_t>(P))) != PPG_SUCCESS) return rc;
+    }
+    for (int k = 0; k < M; ++k) {
+      DCK(cudaSetDevice(m[k]->device));
+      DCK(cudaGraphLaunch(m[k]->dtree->exec_post, m[k]->stream));
+    }
+  }
+  const double loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_loop).count();
+  for (int k = 0; k < M; ++k) cb[k] = m[k]->dtree->la.counters;
+  if ((rc = group_allreduce_sum_i64(ctx, g, cb.data(), 4)) != PPG_SUCCESS) return rc;
+  int64_t ctr[4];
+  DCK(cudaSetDevice(m[0]->device));
+  DCK(cudaMemcpyAsync(ctr, cb[0], 32, cudaMemcpyDeviceToHost, m[0]->stream));
+  if ((rc = group_wait(ctx, g)) != PPG_SUCCESS) return rc;
+  ctr[1] /= G;  // every shard counts every round
+  rc = dt_finish(m[0], h[0], stop, elapsed(), loop_s, ctr, action_out, stats, sig_buf, sig_cap, sig_len);
+  if (rc != PPG_SUCCESS && m[0] != ctx) ctx->err = m[0]->err;
+  return rc;
+}
+
+}  // namespace ppg
+
 extern "C" {
 
 // Test entry (acceptance criterion 3, acceptance.cpp:255-281): loads one
@@ -1112,120 +1523,18 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     ctx->err = "no scene installed";
     return PPG_EINVAL;
   }
+  if (ctx->group) return ppg::run_pmbs_sharded(ctx, root_poses, action_out, stats, sig_buf, sig_cap, sig_len);
   const auto t_start = std::chrono::steady_clock::now();
   const auto elapsed = [&t_start] {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   };
+  int rc = dt_begin(ctx, root_poses, false);
+  if (rc != PPG_SUCCESS) return rc;
   const ppg_params& p = ctx->params;
-  if (p.n_envs < 1) {
-    ctx->err = "n_envs must be >= 1";
-    return PPG_EINVAL;
-  }
-  if (p.tree_depth + 1 >= kMaxTreeDepth || p.tree_depth + p.rollout_depth + 1 >= kMaxGammaPow) {
-    ctx->err = "device tree: tree_depth too large";
-    return PPG_EINVAL;
-  }
-  DCK(cudaSetDevice(ctx->device));
-  cudaStream_t st = ctx->stream;
-  const int n = ctx->scene.n, na = p.pushes_per_object;
-  // root: sample_pushes + graspable (SearchTree::create, mcts.cpp:28-39)
-  std::vector<double> root_untried(static_cast<size_t>(n) * na * 4);
-  int32_t cnt = 0;
-  int rc = ppg_sample_pushes(ctx, nullptr, root_poses, 1, root_untried.data(), &cnt);
-  if (rc != PPG_SUCCESS) return rc;
-  uint8_t rg = 0;
-  rc = ppg_graspable(ctx, root_poses, 1, &rg, nullptr, nullptr, nullptr, nullptr);
-  if (rc != PPG_SUCCESS) return rc;
-  if (cnt == 0) {
-    ctx->err = "no legal push action at the root";
-    return PPG_ENOLEGAL;
-  }
-  if (!ctx->dtree) ctx->dtree = new DTreeState;
   DTreeState& S = *ctx->dtree;
-  {
-    // everything baked into the captured graph: parameters (minus the
-    // per-search values kept in DTScal), scene tables
-    ppg_params kp = p;
-    kp.rng_seed = 0;
-    kp.c_explore = 0.0;
-    kp.budget_iterations = 0;
-    kp.max_iterations = 0;
-    kp.max_seconds = 0.0;
-    std::string key(reinterpret_cast<const char*>(&kp), sizeof kp);
-    key.append(reinterpret_cast<const char*>(&ctx->scene), sizeof ctx->scene);
-    key.append(reinterpret_cast<const char*>(&ctx->side), sizeof ctx->side);
-    key.append(reinterpret_cast<const char*>(&ctx->margin), sizeof ctx->margin);
-    // kernel-mode inputs (which kernels the graph holds)
-    const int modes[8] = {ctx->scene_all_discs ? 1 : 0, ctx->force_generic ? 1 : 0, ctx->warp_poly ? 1 : 0,
-                          ctx->warp_max_envs, ctx->warp_max_explicit ? 1 : 0, ctx->disc_kernels ? 1 : 0,
-                          ctx->hybrid_min_envs, ctx->sim_hook ? 1 : 0};
-    key.append(reinterpret_cast<const char*>(modes), sizeof modes);
-    if (S.key != key) S.release_graph();
-    S.key = key;
-  }
-  if (S.n != n) {  // per-node pose rows change size: start the tree buffers afresh
-    DevBuf* node_bufs[] = {&S.parent, &S.depth, &S.q, &S.visits, &S.vv, &S.flags, &S.u_off, &S.u_n, &S.u_head,
-                           &S.c_n, &S.selc, &S.action, &S.poses, &S.anc, &S.apool, &S.cpool};
-    DCK(cudaStreamSynchronize(st));
-    for (DevBuf* b : node_bufs) b->release();
-    S.cap_nodes = 0;
-    S.cap_actions = 0;
-    S.release_graph();
-  }
-  S.n_envs = p.n_envs;
-  S.n = n;
-  S.na = na;
-  const long long per_iter_actions = static_cast<long long>(p.n_envs) * n * na;
-  if (S.logtab.cap < (static_cast<size_t>(S.cap_nodes) + p.n_envs + 2) * 8) {  // log table covers visits + n_envs
-    S.cap_nodes = 0;  // forces dt_reserve to re-grow (contents preserved up to used = 0: fresh search)
-  }
-  {
-    int want = 1 + p.n_envs * (p.budget_iterations ? std::min<long long>(p.max_iterations, 64) : 8);
-    if (const char* cn = std::getenv("PPG_DTREE_NODES")) want = std::max(want, std::atoi(cn));
-    want = std::max(want, 1 + 2 * p.n_envs);
-    if ((rc = dt_reserve(ctx, S, 0, 0, want, static_cast<long long>(want) * n * na)) != PPG_SUCCESS) return rc;
-  }
-  if ((rc = dt_batch(ctx, S)) != PPG_SUCCESS) return rc;
-  dt_views(ctx, S);
-  // root node + scalars
-  {
-    const int32_t zero = 0, m1 = -1;
-    const long long zl = 0;
-    const double zd = 0.0;
-    const uint8_t rf = static_cast<uint8_t>(rg ? 1 : 0);  // dead needs untried.empty(): cnt > 0 here
-    DCK(cudaMemcpyAsync(S.t.parent, &m1, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.depth, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.q, &zd, 8, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.visits, &zl, 8, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.vv, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.flags, &rf, 1, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.u_off, &zl, 8, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.u_n, &cnt, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.u_head, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.c_n, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.selc, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemsetAsync(S.t.action, 0, 32, st));
-    DCK(cudaMemcpyAsync(S.t.poses, root_poses, static_cast<size_t>(n) * 24, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.anc, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.apool, root_untried.data(), static_cast<size_t>(cnt) * 32, cudaMemcpyHostToDevice, st));
-    DTScal h;
-    std::memset(&h, 0, sizeof h);
-    h.n_nodes = 1;
-    h.dT = p.tree_depth;
-    h.dS = p.rollout_depth;
-    h.es_level = 1;
-    h.min_grasp_depth = INT_MAX;
-    h.levels = 1;
-    h.stop = -1;
-    h.a_used = cnt;
-    h.unsettled[0] = rg ? 0 : 1;  // root: non-terminal with untried actions unless graspable
-    h.max_iters = p.budget_iterations ? static_cast<int>(p.max_iterations) : 0;
-    h.c_explore = p.c_explore;
-    h.lock_dyn[4] = static_cast<int>(static_cast<uint32_t>(p.rng_seed));
-    h.lock_dyn[5] = static_cast<int>(static_cast<uint32_t>(p.rng_seed >> 32));
-    DCK(cudaMemcpyAsync(S.t.sc, &h, sizeof h, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemsetAsync(S.la.counters, 0, 32, st));
-  }
+  cudaStream_t st = ctx->stream;
+  const int n = S.n;
+  const long long per_iter_actions = static_cast<long long>(p.n_envs) * n * S.na;
   DTScal h;
   std::memset(&h, 0, sizeof h);
   int stop = -1;
@@ -1333,74 +1642,11 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     }
   }
   const double loop_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_loop).count();
-  if (stop == 3) {
-    ctx->err = "device tree: selection invariant violated";
-    return PPG_EINVAL;
-  }
-  // read the tree back once
-  const int N = h.n_nodes;
-  std::vector<int32_t> depth(N), c_n(N), parent(N);
-  std::vector<double> q(N), action(static_cast<size_t>(N) * 4);
-  std::vector<long long> visits(N), u_off(N);
-  std::vector<uint8_t> flags(N);
-  std::vector<int32_t> cpool(static_cast<size_t>(h.a_used));
   int64_t ctr[4];
-  DCK(cudaMemcpyAsync(depth.data(), S.t.depth, N * 4ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(c_n.data(), S.t.c_n, N * 4ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(q.data(), S.t.q, N * 8ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(action.data(), S.t.action, N * 32ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(visits.data(), S.t.visits, N * 8ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(u_off.data(), S.t.u_off, N * 8ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(flags.data(), S.t.flags, N, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(cpool.data(), S.t.cpool, static_cast<size_t>(h.a_used) * 4, cudaMemcpyDeviceToHost, st));
   DCK(cudaMemcpyAsync(ctr, S.la.counters, 32, cudaMemcpyDeviceToHost, st));
   DCK(cudaStreamSynchronize(st));
   for (int k = 0; k < 4; ++k) ctr[k] += hook_ctr[k];
-  // best_root_child (mcts.cpp:218-235)
-  int best = -1;
-  double best_score = -std::numeric_limits<double>::infinity();
-  long long best_visits = -1;
-  for (int k = 0; k < c_n[0]; ++k) {
-    const int ch = cpool[u_off[0] + k];
-    if (visits[ch] == 0) continue;
-    const double score = p.rank_by_ucb ? ucb_score_host(q[ch], static_cast<long>(visits[ch]), static_cast<long>(visits[0]),
-                                                        p.c_explore)
-                                       : q[ch] / static_cast<double>(visits[ch]);
-    if (score > best_score || (score == best_score && visits[ch] > best_visits)) {
-      best_score = score;
-      best_visits = visits[ch];
-      best = ch;
-    }
-  }
-  if (best < 0) {
-    ctx->err = "search produced no evaluated root child";
-    return PPG_EINVAL;
-  }
-  std::memcpy(action_out, &action[static_cast<size_t>(best) * 4], 32);
-  const std::string sig = signature(depth, action, visits, q, flags, u_off, c_n, cpool);
-  if (stats) {
-    ppg_search_stats s;
-    std::memset(&s, 0, sizeof s);
-    s.iterations = h.iteration;
-    s.expansions = h.expansions;
-    s.elapsed_s = elapsed();
-    s.stop_reason = stop;
-    s.final_tree_depth = h.dT;
-    s.env_steps = ctr[3] + h.expansions;
-    s.rollout_steps = ctr[0];
-    s.lockstep_rounds = ctr[1];
-    s.signature_fnv = fnv1a(sig);
-    s.n_nodes = N;
-    s.simulate_s = loop_s;  // one graph per iteration: the phases are not timed separately
-    *stats = s;
-  }
-  if (sig_len) *sig_len = static_cast<int64_t>(sig.size());
-  if (sig_buf && sig_cap > 0) {
-    const size_t m = sig.size() < static_cast<size_t>(sig_cap - 1) ? sig.size() : static_cast<size_t>(sig_cap - 1);
-    std::memcpy(sig_buf, sig.data(), m);
-    sig_buf[m] = '\0';
-  }
-  return PPG_SUCCESS;
+  return dt_finish(ctx, h, stop, elapsed(), loop_s, ctr, action_out, stats, sig_buf, sig_cap, sig_len);
 }
 
 }  // extern "C"

@@ -301,22 +301,20 @@ __global__ void lock_repurpose_kernel(const __grid_constant__ SimConst C, LockAr
   if (!a.env_done[e]) a.active[atomicAdd(a.n_active, 1)] = e;
 }
 
-// harvest_and_repurpose (pmbs.cpp:165-187) + next round's active list.  One
-// block.  Rewards are order-free (max of non-negative doubles via their bit
-// patterns); per-node remaining work W by atomics; the re-purposing target is
-// one block-wide argmax of W (see below).  This reproduces the reference's
-// O(E*N*E) sequential rescan exactly in O(E + N).
-__global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
-  lock_dyn(a);
-  const int tid = threadIdx.x;
-  const int B = blockDim.x;
-  __shared__ int s_active;
-  __shared__ long long s_rep;
-  if (tid == 0) {
-    s_active = 0;
-    s_rep = 0;
-    *a.n_stepping = 0;
-  }
+// harvest_and_repurpose (pmbs.cpp:165-187) + next round's active list, as
+// block-wide device functions (one block).  Rewards are order-free (max of
+// non-negative doubles via their bit patterns); per-node remaining work W by
+// atomics; the re-purposing target is one block-wide argmax of W (see
+// harvest_apply).  This reproduces the reference's O(E*N*E) sequential rescan
+// exactly in O(E + N).
+//
+// Part 1 (local to a shard): W[node] = sum over this shard's not-done envs of
+// cap - pushes (pmbs.cpp:157-163, evaluated at the start of the pass: only
+// re-purposes change it during the pass, see below); done, unharvested envs
+// are harvested (reward max) and flagged for re-purposing when they finished
+// by grasp under leaf parallelism.
+PPG_DI void harvest_local(const LockArgs& a) {
+  const int tid = threadIdx.x, B = blockDim.x;
   for (int i = tid; i < a.n_nodes; i += B) a.W[i] = 0;
   __syncthreads();
   for (int e = tid; e < a.used; e += B) {
@@ -332,17 +330,37 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     }
   }
   __syncthreads();
-  if (a.leaf_parallel) {
-    // Re-purposing (pmbs.cpp:171-185): each by-grasp env of the pass goes to
-    // argmax_i remaining_work(i) (strict >, W > 0, lowest node on ties), and
-    // the only change to W during the pass is W[best] += the new cursor's
-    // remaining work (>= 0): best stays the argmax, so every re-purposed env
-    // of the pass goes to the SAME node, found by one block-wide argmax.
-    __shared__ int s_bw[32], s_bi[32];
-    __shared__ int s_best;
+}
+
+// Part 2, with W summed over every shard (the whole batch).  Re-purposing
+// (pmbs.cpp:171-185): each by-grasp env of the pass goes to argmax_i W[i]
+// (strict >, W > 0, lowest node on ties), and the only change to W during the
+// pass is W[best] += the new cursor's remaining work (>= 0): best stays the
+// argmax, so every re-purposed env of the pass — on every shard — goes to the
+// SAME node, found by one block-wide argmax of the global W.  `sharded`: the
+// loop condition is sum(W) > 0 (a not-done env contributes cap - pushes >= 1;
+// a re-purpose needs W[best] > 0), identical on every shard; unsharded it is
+// the local active count (the same predicate).
+PPG_DI void harvest_apply(const SimConst& C, const LockArgs& a, bool sharded) {
+  const int tid = threadIdx.x;
+  const int B = blockDim.x;
+  __shared__ int s_active;
+  __shared__ long long s_rep;
+  __shared__ int s_bw[32], s_bi[32];
+  __shared__ long long s_sum[32];
+  __shared__ int s_best;
+  __shared__ long long s_total;
+  if (tid == 0) {
+    s_active = 0;
+    s_rep = 0;
+    *a.n_stepping = 0;
+  }
+  if (a.leaf_parallel || sharded) {
     int bw = 0, bi = -1;
+    long long sum = 0;
     for (int i = tid; i < a.n_nodes; i += B) {
       const int w = a.W[i];
+      sum += w;
       if (w > bw) {
         bw = w;
         bi = i;
@@ -352,6 +370,7 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     for (int off = 16; off > 0; off >>= 1) {
       const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      sum += __shfl_xor_sync(0xffffffffu, sum, off);
       if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
         bw = ow;
         bi = oi;
@@ -360,22 +379,28 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
     if ((tid & 31) == 0) {
       s_bw[tid >> 5] = bw;
       s_bi[tid >> 5] = bi;
+      s_sum[tid >> 5] = sum;
     }
     __syncthreads();
     if (tid < 32) {
       const int nw = B >> 5;
       bw = tid < nw ? s_bw[tid] : 0;
       bi = tid < nw ? s_bi[tid] : -1;
+      sum = tid < nw ? s_sum[tid] : 0;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) {
         const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
         const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        sum += __shfl_xor_sync(0xffffffffu, sum, off);
         if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
           bw = ow;
           bi = oi;
         }
       }
-      if (tid == 0) s_best = bi;
+      if (tid == 0) {
+        s_best = a.leaf_parallel ? bi : -1;
+        s_total = sum;
+      }
     }
     __syncthreads();
     const int best = s_best;
@@ -415,16 +440,35 @@ __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constan
   if (tid == 0) {
     *a.n_active = s_active;
     a.counters[2] += s_rep;
-    if (s_active > 0) a.counters[1] += 1;
+    bool go = sharded ? s_total > 0 : s_active > 0;
+    if (go) a.counters[1] += 1;
     if (a.round_mode) *a.round_mode = s_active >= a.hybrid_min ? 1 : 0;
-    bool go = s_active > 0;
     if (a.round_guard && go && ++*a.round_guard > kLockRoundLimit) {
       *a.round_guard = -1;  // non-terminating lockstep: reported by the host
       go = false;
     }
+    if (a.go) *a.go = go ? 1 : 0;
     // device tree graph: the lockstep WHILE node runs another round iff envs remain
     if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), go ? 1u : 0u);
   }
+}
+
+__global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
+  harvest_local(a);
+  harvest_apply(C, a, false);
+}
+
+// Sharded lockstep (multi.cu): the two halves of one harvest pass, with the
+// exchange of W (a sum over the shards, in place) between them.
+__global__ void __launch_bounds__(1024) lock_harvest_local_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
+  harvest_local(a);
+}
+
+__global__ void __launch_bounds__(1024) lock_harvest_apply_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
+  harvest_apply(C, a, true);
 }
 
 // sample_pushes for a lockstep env + the Lemire pick from its MT stream

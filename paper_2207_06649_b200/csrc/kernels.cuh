@@ -125,6 +125,15 @@ struct LockArgs {
   // WHILE loop (and marks the counter negative) past kLockRoundLimit, so a
   // bug surfaces as an error instead of a hung graph
   int* round_guard = nullptr;
+  // sharded lockstep (multi-GPU, multi.cu): shard shard_r of shard_g owns a
+  // contiguous range of the global env batch (with `dyn`, the range follows
+  // the iteration's used-env count on the device).  The harvest is split
+  // around ONE exchange per round: lock_harvest_local_kernel writes this
+  // shard's W, the exchange sums W over the shards in place, and
+  // lock_harvest_apply_kernel re-purposes with the global W and writes `go`
+  // (any environment active anywhere) for the host.
+  int shard_r = 0, shard_g = 1;
+  int32_t* go = nullptr;
 };
 
 constexpr int kLockRoundLimit = 1 << 20;
@@ -135,6 +144,13 @@ __device__ __forceinline__ void lock_dyn(LockArgs& a) {
     a.n_nodes = a.dyn[0];
     a.used = a.dyn[1];
     a.used_global = a.dyn[1];
+    if (a.shard_g > 1) {  // this shard's contiguous part of the global batch
+      const long long ug = a.dyn[1];
+      const int lo = static_cast<int>(ug * a.shard_r / a.shard_g);
+      const int hi = static_cast<int>(ug * (a.shard_r + 1) / a.shard_g);
+      a.env_lo = lo;
+      a.used = hi - lo;
+    }
     a.cap = a.dyn[2];
     a.iteration = static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[3]));
     a.seed = static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[4])) |

@@ -1,26 +1,30 @@
 """Multi-GPU batch_simulate: the lockstep engine (pmbs.cpp:133-205) sharded by
-environment.
+environment — the Python restatement of the exchange protocol that the
+library runs natively (csrc/multi.cu, ppg_create_rank / ppg_create_multi),
+used as the test double of that protocol on CPU (gloo, world_size 2) and
+behind ppg_set_simulate_hook.
 
 Each rank owns a contiguous range of global environment indices.  The
 env -> node split and the RNG keys (pmbs.cpp:138-149, 211-213) use global
 indices, so the union of the shards is the unsharded batch.  Environments
 only interact through harvest_and_repurpose (pmbs.cpp:165-187): an env that
-finishes by grasp moves to the node with the most remaining rollout work at
-that moment.  That is one small exchange per lockstep round:
+finishes by grasp moves to argmax_i W[i], W[i] = the remaining rollout work
+of node i.  Within one pass the only change to W is W[best] += (>= 0), so
+every re-purpose of the pass goes to the argmax of W at the start of the
+pass.  That makes ONE exchange per lockstep round exact:
 
-    report (device)   -> this shard's newly finished envs, W_local
-    allgather         -> all records, in global env order (ranks own
-                         contiguous ranges, concatenated in rank order)
-    allreduce(sum)    -> W
-    harvest (host)    -> the reference's sequential pass, identical on every
-                         rank: reward max per node; re-purpose by grasp-finished
-                         envs to argmax W (strict >, W > 0, lowest node)
+    report (device)   -> this shard's newly finished envs (rewards, grasp
+                         flags) and W_local
+    allreduce(sum)    -> W (the only collective of the round)
+    harvest (local)   -> reward max per node; this shard's by-grasp envs go
+                         to argmax W (strict >, W > 0, lowest node)
     repurpose (device)-> local envs restart at their new node
     step (device)     -> one round for the local active envs
+    (loop while sum(W) > 0: a not-done env contributes cap - pushes >= 1)
 
-The reward vector is built from the records every rank sees, so no final
-reduction is needed.  `Comm` abstracts the two collectives: torch.distributed
-(NCCL on GPUs, gloo on CPU) or in-process shards on one device.
+Per-node rewards are a max, all-reduced once at the end.  `Comm` abstracts
+the collectives: torch.distributed (NCCL on GPUs, gloo on CPU) or in-process
+shards.
 """
 from __future__ import annotations
 
@@ -60,29 +64,28 @@ def env_range(used: int, world: int, rank: int):
     return lo, lo + base + (1 if rank < rem else 0)
 
 
-def harvest(rec: Records, W: np.ndarray, node_depth: np.ndarray, cap: int, leaf_parallel: bool,
-            rewards: np.ndarray):
-    """harvest_and_repurpose (pmbs.cpp:165-187) over the finished envs of one
-    round in global env order.  Updates `rewards` (max) and W in place and
-    returns the re-purposing assignments (env, node)."""
-    out_env, out_node = [], []
-    best = None
+def best_node(W: np.ndarray) -> int:
+    """argmax_i W[i] with strict > and W > 0, lowest node on ties (-1: none)
+    — the reference's scan (pmbs.cpp:172-180) on the summed W."""
+    if len(W) == 0:
+        return -1
+    b = int(np.argmax(W))
+    return b if W[b] > 0 else -1
+
+
+def harvest_local(rec: Records, best: int, leaf_parallel: bool, rewards: np.ndarray):
+    """This shard's part of one harvest pass (pmbs.cpp:165-187): reward max of
+    its newly finished envs; its by-grasp envs are re-purposed to `best` (the
+    argmax of the GLOBAL W).  Returns the assignments (env, node)."""
     for k in range(len(rec.env)):
         nd = int(rec.node[k])
         r = float(rec.reward[k])
         if rewards[nd] < r:
             rewards[nd] = r
-        if not leaf_parallel or not rec.grasp[k]:
-            continue
-        if best is None:
-            # argmax W, first maximum == lowest node on ties.  Within a pass W
-            # only grows at the chosen node, so the target never changes.
-            best = int(np.argmax(W)) if len(W) else -1
-        if best >= 0 and W[best] > 0:
-            W[best] += cap - int(node_depth[best])
-            out_env.append(int(rec.env[k]))
-            out_node.append(best)
-    return np.asarray(out_env, np.int32), np.asarray(out_node, np.int32)
+    if not leaf_parallel or best < 0:
+        return np.zeros(0, np.int32), np.zeros(0, np.int32)
+    env = rec.env[rec.grasp != 0].astype(np.int32)
+    return env, np.full(len(env), best, np.int32)
 
 
 class DeviceShard:
@@ -144,6 +147,9 @@ class InProcessComm:
     def sum_int(self, v: int) -> int:
         return v
 
+    def max(self, arr: np.ndarray) -> np.ndarray:
+        return arr
+
 
 class TorchComm:
     """One shard per process; collectives over a torch.distributed group
@@ -190,11 +196,18 @@ class TorchComm:
     def sum_int(self, v: int) -> int:
         return int(self.sum(np.array([v], np.int64))[0])
 
+    def max(self, arr: np.ndarray) -> np.ndarray:
+        """Element-wise max of non-negative float64 rewards (exact)."""
+        t = self._t(arr.astype(np.float64))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t.cpu().numpy()
+
 
 def sharded_simulate(shards, comm, node_poses, node_meta, n_envs: int, leaf_parallel: bool, seed: int,
                      iteration: int, depth_cap: int, ranges=None):
     """batch_simulate over the local `shards` (each with its global env range)
-    of a batch sharded across `comm`.  Returns (rewards, counters)."""
+    of a batch sharded across `comm`: one W all-reduce per round, one reward
+    max at the end.  Returns (rewards, counters)."""
     node_meta = np.ascontiguousarray(node_meta, np.int32)
     n_nodes = len(node_meta)
     used = n_envs if leaf_parallel else n_nodes
@@ -202,24 +215,21 @@ def sharded_simulate(shards, comm, node_poses, node_meta, n_envs: int, leaf_para
         raise ValueError("lockstep_simulate: fewer environments than nodes")
     for sh, (lo, hi) in zip(shards, ranges):
         sh.begin(node_poses, node_meta, n_nodes, used, lo, hi, leaf_parallel, seed, iteration, depth_cap)
-    depth = node_meta[:, 0]
     rewards = np.zeros(n_nodes, np.float64)
     rounds = 0
     while True:
         reps = [sh.report() for sh in shards]
-        rec = comm.gather_records([r[0] for r in reps])
-        W = comm.sum(np.sum([r[1] for r in reps], axis=0).astype(np.int64))
-        env, node = harvest(rec, W, depth, depth_cap, leaf_parallel, rewards)
-        active = sum(r[2] for r in reps)
-        for sh, (lo, hi) in zip(shards, ranges):
-            sel = (env >= lo) & (env < hi)
-            sh.repurpose(env[sel], node[sel])
-            active += int(sel.sum())
-        if comm.sum_int(active) == 0:
+        W = comm.sum(np.sum([r[1] for r in reps], axis=0).astype(np.int64))  # the round's one exchange
+        best = best_node(W) if leaf_parallel else -1
+        for sh, rep in zip(shards, reps):
+            env, node = harvest_local(rep[0], best, leaf_parallel, rewards)
+            sh.repurpose(env, node)
+        if int(W.sum()) == 0:
             break
         for sh in shards:
             sh.step()
         rounds += 1
+    rewards = comm.max(rewards)
     ctr = np.sum([sh.counters() for sh in shards], axis=0).astype(np.int64)
     ctr = comm.sum(ctr)
     ctr[1] = rounds
@@ -263,3 +273,18 @@ class ShardedSimulateHook:
 
     def remove(self):
         self.ctx.lib.ppg_set_simulate_hook(self.ctx.ptr, None, None)
+
+
+def rank_context(device: int, params=None, group=None):
+    """The library-native multi-GPU context of this process (one shard per
+    rank under torchrun): rank 0 makes the NCCL id, torch.distributed
+    broadcasts it, every rank creates ppg_create_rank over its own GPU.
+    ppg_simulate / ppg_run_pmbs on it then shard the rollout batch with the
+    per-round W all-reduce inside the library (csrc/multi.cu)."""
+    import torch.distributed as dist
+
+    from .api import Context, nccl_unique_id
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return Context.rank(device, rank, world, obj[0], params)

@@ -217,7 +217,7 @@ def _decision(st, p, threads=8):
             "n_nodes": r["n_nodes"]}
 
 
-WIDE_16K = [("case_13", 16384)]
+WIDE_16K = [("case_13", 16384), ("case_18", 16384)]
 
 
 def wide():

@@ -60,3 +60,19 @@ def test_state_digest_host_helper_matches_golden():
         poses = np.ascontiguousarray(st.poses.reshape(1, st.n, 3))
         assert lib.ppg_state_digest(ctypes.byref(t.struct()), abi.dptr(poses), 1, abi.u64ptr(out)) == 0
         assert int(out[0]) == int(c["digest"])
+
+
+def test_nccl_loaded_before_torch_is_torchs_build():
+    """The library loads NCCL at run time; loaded before torch it must be the
+    copy torch ships (a system libnccl.so.2 would shadow torch's by soname
+    and break `import torch`).  Runs in a fresh interpreter."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2207_06649_b200 as p\n"
+            "assert len(p.nccl_unique_id()) == 128\n"
+            "import torch, torch.distributed\n"
+            "print('ok', torch.cuda.nccl.version())\n") % root
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stderr[-2000:]
