@@ -10,6 +10,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <chrono>
+#include <thread>
 
 #include "ctx.h"
 #include "kernels.cuh"
@@ -613,6 +615,39 @@ static bool streamed_available(ppg_ctx* ctx) {
   return true;
 }
 
+// Waits for the streamed physics launch with a bound: every slice copy and
+// ready-flag write is enqueued before the launch, so lanes waiting on a flag
+// always get it — unless that invariant is ever broken.  Then, instead of a
+// hung GPU, the flags are released from a side stream (the lanes finish on
+// whatever the buffers hold) and the call reports an error.
+static int wait_streamed(ppg_ctx* ctx, cudaStream_t ph, unsigned* ready, unsigned epoch) {
+  static const double limit = [] {
+    const char* v = std::getenv("PPG_STREAM_TIMEOUT_S");
+    return v ? std::atof(v) : 120.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spins = 0;; ++spins) {
+    const cudaError_t e = cudaStreamQuery(ph);
+    if (e == cudaSuccess) return PPG_SUCCESS;
+    if (e != cudaErrorNotReady) {
+      ctx->err = std::string("streamed batch_resolve: ") + cudaGetErrorString(e);
+      return PPG_ECUDA;
+    }
+    if (spins > 256) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > limit) {
+      cudaStream_t rescue = nullptr;
+      std::vector<unsigned> fl(kMaxSlices, epoch);
+      if (cudaStreamCreateWithFlags(&rescue, cudaStreamNonBlocking) == cudaSuccess) {
+        cudaMemcpyAsync(ready, fl.data(), kMaxSlices * sizeof(unsigned), cudaMemcpyHostToDevice, rescue);
+        cudaStreamSynchronize(ph);
+        cudaStreamDestroy(rescue);
+      }
+      ctx->err = "streamed batch_resolve: slice ready flags never arrived (PPG_STREAM_TIMEOUT_S); released";
+      return PPG_ECUDA;
+    }
+  }
+}
+
 // Streamed host-buffer batch_resolve for disc batches: ONE persistent physics
 // launch (resolve_disc_kernel) overlaps every host<->device copy.
 //   copy-in stream: per slice, poses + pushes + radii (the host [E][n] radius
@@ -713,7 +748,7 @@ static int batch_resolve_streamed(ppg_ctx* ctx, const ppg_shapes* sh, const doub
   if (rc != PPG_SUCCESS) return rc;
   mark(ph);
   if (a.zc_out) {
-    CK(cudaStreamSynchronize(ph));
+    if (const int wrc = wait_streamed(ctx, ph, ready, epoch); wrc != PPG_SUCCESS) return wrc;
     CK(cudaStreamSynchronize(in));
     if (trace) {
       float ms = 0.f;
@@ -738,8 +773,8 @@ static int batch_resolve_streamed(ppg_ctx* ctx, const ppg_shapes* sh, const doub
     if (residual) CK(cudaMemcpyAsync(residual + e0, d_res + e0, ek * 8, cudaMemcpyDeviceToHost, out));
     mark(out);
   }
+  if (const int wrc = wait_streamed(ctx, ph, ready, epoch); wrc != PPG_SUCCESS) return wrc;
   CK(cudaStreamSynchronize(out));
-  CK(cudaStreamSynchronize(ph));
   if (trace) {
     std::fprintf(stderr, "stream trace (ms from start): in");
     for (int i = 1; i < ntev; ++i) {
