@@ -280,6 +280,19 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
 int ppg_run_pmbs_sig(ppg_ctx* ctx, const double* root_poses, double* action_out,
                      ppg_search_stats* stats, char* sig_buf, int64_t sig_cap, int64_t* sig_len);
 
+/* The search tree of the context's last ppg_run_pmbs* decision (the device
+ * tree), for SearchResult::tree (mcts.hpp:87-91, pmbs.hpp:91): nodes in
+ * creation order (root 0; a node's children in insertion order = increasing
+ * index), parent[N] (-1 at the root), depth[N], action[N][4] (the push that
+ * produced the node; zeros at the root), visits[N], q_sum[N], flags[N]
+ * (bit0 graspable, bit1 dead), poses[N][n][3], untried_count[N] (untried
+ * actions not yet expanded) and untried[U][4] (those actions, concatenated in
+ * node order); scal[4] = {tree_depth, rollout_depth, es_level, n_objects} at
+ * return.  Pass NULL arrays to read *n_nodes / *n_untried first. */
+int ppg_tree_export(ppg_ctx* ctx, int64_t* n_nodes, int64_t* n_untried, int32_t* parent, int32_t* depth,
+                    double* action, int64_t* visits, double* q_sum, uint8_t* flags, double* poses,
+                    int32_t* untried_count, double* untried, int32_t* scal);
+
 /* FNV-1a state digest (world.cpp:166-191) of E states sharing `shapes`
  * (n_tables 1 or E): bit-exact state identity. Host-only helper. */
 int ppg_state_digest(const ppg_shapes* shapes, const double* poses, int E, uint64_t* out);

@@ -64,9 +64,12 @@ extern "C" int adapter_check_pmbs(const char* case_path, const char* case_id, in
   pmbs::ParallelConfig cfg;
   cfg.rng_seed = mix_keys(bench::episode_seed(0, case_id, 0), 0);
   const mcts::SearchResult ref = pmbs::run_pmbs(scene, cfg);
-  const gpu::PlanResult got = backend.run_pmbs(scene, cfg);
+  const mcts::SearchResult got = backend.run_pmbs(scene, cfg);
   *same_action = ref.action == got.action ? 1 : 0;
-  *same_sig = fnv(mcts::tree_signature(*ref.tree)) == got.tree_signature_fnv ? 1 : 0;
+  // the whole tree, rebuilt on the host from the device tree, prints the
+  // reference's signature text (and its FNV equals the device's own)
+  const std::string sig = mcts::tree_signature(*got.tree);
+  *same_sig = (sig == mcts::tree_signature(*ref.tree) && fnv(sig) == backend.last_device_stats().signature_fnv) ? 1 : 0;
   *same_stats = (ref.stats.iterations == got.stats.iterations && ref.stats.expansions == got.stats.expansions &&
                  ref.stats.stop_reason == got.stats.stop_reason)
                     ? 1

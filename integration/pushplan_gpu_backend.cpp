@@ -2,8 +2,12 @@
 // into the flat C-ABI arrays and back.
 #include "pushplan_gpu_backend.hpp"
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
 #include <tuple>
 
 namespace pushplan::gpu {
@@ -112,15 +116,16 @@ std::vector<PushResult> Backend::batch_resolve(std::span<const WorldState> state
       } else if (status[k] == PPG_START_COLLISION) {
         r.error = "resolve_push: gripper start pose collides or leaves the workspace";
       } else {
-        r.error = "resolve_push: projection did not converge, residual penetration " + std::to_string(resid[k]) +
-                  " m";
+        std::ostringstream msg;  // the reference's own formatting (push_sim.cpp:124-126)
+        msg << "resolve_push: projection did not converge, residual penetration " << resid[k] << " m";
+        r.error = msg.str();
       }
     }
   }
   return results;
 }
 
-PlanResult Backend::run_pmbs(const WorldState& state, const pmbs::ParallelConfig& cfg) {
+mcts::SearchResult Backend::run_pmbs(const WorldState& state, const pmbs::ParallelConfig& cfg) {
   ppg_params p = to_params(cfg.tip, cfg.sim);
   p.finger_width = cfg.grasp.finger_width;
   p.finger_thickness = cfg.grasp.finger_thickness;
@@ -146,19 +151,74 @@ PlanResult Backend::run_pmbs(const WorldState& state, const pmbs::ParallelConfig
   const ppg_shapes sh = f.shapes(n, 1, state.workspace);
   if (ppg_set_scene(ctx_, &sh) != PPG_SUCCESS) throw BackendError(ppg_last_error(ctx_));
   double action[4];
-  ppg_search_stats st;
-  const int rc = ppg_run_pmbs(ctx_, f.poses.data(), action, &st);
+  const int rc = ppg_run_pmbs(ctx_, f.poses.data(), action, &last_);
+  // the reference's messages (mcts.cpp:244, pmbs.cpp:248)
   if (rc == PPG_ENOLEGAL) throw mcts::SearchError("no legal push action at the root");
   if (rc != PPG_SUCCESS) throw BackendError(ppg_last_error(ctx_));
-  PlanResult r;
+  mcts::SearchResult r;
   r.action = PushAction{action[0], action[1], action[2], action[3]};
-  r.stats.iterations = st.iterations;
-  r.stats.expansions = st.expansions;
-  r.stats.elapsed_s = st.elapsed_s;
-  r.stats.stop_reason = st.stop_reason == 0 ? "budget" : (st.stop_reason == 1 ? "explored" : "early_stop");
-  r.tree_signature_fnv = st.signature_fnv;
-  r.env_steps = st.env_steps;
+  r.stats.iterations = last_.iterations;
+  r.stats.expansions = last_.expansions;
+  r.stats.elapsed_s = last_.elapsed_s;
+  r.stats.stop_reason = last_.stop_reason == 0 ? "budget" : (last_.stop_reason == 1 ? "explored" : "early_stop");
+  // the tree: one export of the device tree's node arrays
+  int64_t N = 0, U = 0;
+  if (ppg_tree_export(ctx_, &N, &U, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      nullptr) != PPG_SUCCESS)
+    throw BackendError(ppg_last_error(ctx_));
+  std::vector<int32_t> parent(N), depth(N), ucount(N), scal(4);
+  std::vector<double> act(N * 4), q(N), poses(N * n * 3), untried(U * 4);
+  std::vector<int64_t> visits(N);
+  std::vector<uint8_t> flags(N);
+  if (ppg_tree_export(ctx_, &N, &U, parent.data(), depth.data(), act.data(), visits.data(), q.data(), flags.data(),
+                      poses.data(), ucount.data(), untried.data(), scal.data()) != PPG_SUCCESS)
+    throw BackendError(ppg_last_error(ctx_));
+  auto tree = std::make_unique<mcts::SearchTree>();
+  std::vector<mcts::TreeNode*> node(N, nullptr);
+  size_t uk = 0;
+  for (int64_t x = 0; x < N; ++x) {
+    std::unique_ptr<mcts::TreeNode> own = std::make_unique<mcts::TreeNode>();
+    mcts::TreeNode* t = own.get();
+    t->state = state;
+    for (int o = 0; o < n; ++o) {
+      t->state.objects[o].pose.x = poses[(x * n + o) * 3];
+      t->state.objects[o].pose.y = poses[(x * n + o) * 3 + 1];
+      t->state.objects[o].pose.theta = poses[(x * n + o) * 3 + 2];
+    }
+    t->action = PushAction{act[x * 4], act[x * 4 + 1], act[x * 4 + 2], act[x * 4 + 3]};
+    t->depth = depth[x];
+    t->q_sum = q[x];
+    t->visits = static_cast<long>(visits[x]);
+    t->graspable_flag = (flags[x] & 1) != 0;
+    t->dead_flag = (flags[x] & 2) != 0;
+    for (int k = 0; k < ucount[x]; ++k, ++uk)
+      t->untried.push_back(PushAction{untried[uk * 4], untried[uk * 4 + 1], untried[uk * 4 + 2], untried[uk * 4 + 3]});
+    if (static_cast<size_t>(t->depth) >= tree->levels.size()) tree->levels.resize(t->depth + 1);
+    tree->levels[t->depth].push_back(t);
+    if (t->graspable_flag) tree->graspable_nodes.push_back(t);
+    node[x] = t;
+    if (x == 0) {
+      tree->root = std::move(own);
+    } else {
+      t->parent = node[parent[x]];
+      t->parent->children.push_back(std::move(own));
+    }
+  }
+  tree->tree_depth = scal[0];
+  tree->rollout_depth = scal[1];
+  tree->es_level = scal[2];
+  r.tree = std::move(tree);
   return r;
+}
+
+Backend& shared_backend() {
+  static std::unique_ptr<Backend> b;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* d = std::getenv("PPG_DEVICE");
+    b = std::make_unique<Backend>(d ? std::atoi(d) : 0);
+  });
+  return *b;
 }
 
 }  // namespace pushplan::gpu

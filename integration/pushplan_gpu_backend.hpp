@@ -26,13 +26,6 @@ class BackendError : public std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
-struct PlanResult {
-  PushAction action;
-  mcts::SearchStats stats;
-  uint64_t tree_signature_fnv = 0;  // FNV-1a of mcts::tree_signature text
-  long env_steps = 0;
-};
-
 class Backend {
  public:
   explicit Backend(int device = 0);
@@ -46,10 +39,22 @@ class Backend {
                                         const GripperTip& tip, const SimParams& params);
 
   // pmbs.hpp:91 semantics: throws mcts::SearchError without a legal push.
-  PlanResult run_pmbs(const WorldState& state, const pmbs::ParallelConfig& cfg);
+  // The returned SearchResult carries the whole search tree (rebuilt on the
+  // host from the device-resident tree, ppg_tree_export), so callers of
+  // mcts::tree_signature(*result.tree) work unchanged.
+  mcts::SearchResult run_pmbs(const WorldState& state, const pmbs::ParallelConfig& cfg);
+
+  // Device-side statistics of the last run_pmbs (not in mcts::SearchStats).
+  const ppg_search_stats& last_device_stats() const { return last_; }
 
  private:
   ppg_ctx* ctx_ = nullptr;
+  ppg_search_stats last_{};
 };
+
+// The process-wide backend used by pushplan_core_gpu (the drop-in build of
+// pushplan::core whose batch_resolve / pmbs::run_pmbs run on the device);
+// device from PPG_DEVICE (default 0).
+Backend& shared_backend();
 
 }  // namespace pushplan::gpu

@@ -503,6 +503,10 @@ struct DTreeState {
   ResolveArgs lra{};
   SimConst C{};
   std::string key;  // configuration the graph was captured for
+  // the last finished search (ppg_tree_export)
+  bool last_valid = false;
+  int last_nodes = 0, last_dT = 0, last_dS = 0, last_es = 0;
+  long long last_a_used = 0;
 
   void release_graph() {
     if (exec) cudaGraphExecDestroy(exec);
@@ -983,6 +987,7 @@ int dt_begin(ppg_ctx* ctx, const double* root_poses, bool sharded) {
   }
   if (!ctx->dtree) ctx->dtree = new DTreeState;
   DTreeState& S = *ctx->dtree;
+  S.last_valid = false;
   {
     // everything baked into the captured graph: parameters (minus the
     // per-search values kept in DTScal), scene tables
@@ -1078,10 +1083,17 @@ int dt_finish(ppg_ctx* ctx, const DTScal& h, int stop, double elapsed_s, double 
   const ppg_params& p = ctx->params;
   cudaStream_t st = ctx->stream;
   int64_t ctr[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  S.last_valid = false;
   if (stop == 3) {
     ctx->err = "device tree: selection invariant violated";
     return PPG_EINVAL;
   }
+  S.last_valid = true;
+  S.last_nodes = h.n_nodes;
+  S.last_a_used = h.a_used;
+  S.last_dT = h.dT;
+  S.last_dS = h.dS;
+  S.last_es = h.es_level;
   // read the tree back once
   const int N = h.n_nodes;
   std::vector<int32_t> depth(N), c_n(N), parent(N);
@@ -1358,6 +1370,59 @@ int run_pmbs_sharded(ppg_ctx* ctx, const double* root_poses, double* action_out,
 }  // namespace ppg
 
 extern "C" {
+
+// The tree of the last search (SearchResult::tree, mcts.hpp:87-91): see the
+// header.  One read of the device tree's node arrays.
+int ppg_tree_export(ppg_ctx* ctx, int64_t* n_nodes, int64_t* n_untried, int32_t* parent, int32_t* depth,
+                    double* action, int64_t* visits, double* q_sum, uint8_t* flags, double* poses,
+                    int32_t* untried_count, double* untried, int32_t* scal) {
+  if (!ctx || !n_nodes || !n_untried) return PPG_EINVAL;
+  if (!ctx->dtree || !ctx->dtree->last_valid) {
+    ctx->err = "tree export: no finished device-tree search on this context";
+    return PPG_EINVAL;
+  }
+  DTreeState& S = *ctx->dtree;
+  DCK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int N = S.last_nodes, n = S.n;
+  std::vector<long long> u_off(N);
+  std::vector<int32_t> u_n(N), u_head(N);
+  DCK(cudaMemcpyAsync(u_off.data(), S.u_off.p, N * 8ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(u_n.data(), S.u_n.p, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaMemcpyAsync(u_head.data(), S.u_head.p, N * 4ull, cudaMemcpyDeviceToHost, st));
+  DCK(cudaStreamSynchronize(st));
+  long long U = 0;
+  for (int x = 0; x < N; ++x) U += u_n[x] - u_head[x];
+  *n_nodes = N;
+  *n_untried = U;
+  if (parent) DCK(cudaMemcpyAsync(parent, S.parent.p, N * 4ull, cudaMemcpyDeviceToHost, st));
+  if (depth) DCK(cudaMemcpyAsync(depth, S.depth.p, N * 4ull, cudaMemcpyDeviceToHost, st));
+  if (action) DCK(cudaMemcpyAsync(action, S.action.p, N * 32ull, cudaMemcpyDeviceToHost, st));
+  if (visits) DCK(cudaMemcpyAsync(visits, S.visits.p, N * 8ull, cudaMemcpyDeviceToHost, st));
+  if (q_sum) DCK(cudaMemcpyAsync(q_sum, S.q.p, N * 8ull, cudaMemcpyDeviceToHost, st));
+  if (flags) DCK(cudaMemcpyAsync(flags, S.flags.p, N, cudaMemcpyDeviceToHost, st));
+  if (poses) DCK(cudaMemcpyAsync(poses, S.poses.p, static_cast<size_t>(N) * n * 24, cudaMemcpyDeviceToHost, st));
+  if (untried_count)
+    for (int x = 0; x < N; ++x) untried_count[x] = u_n[x] - u_head[x];
+  if (untried) {
+    long long k = 0;
+    for (int x = 0; x < N; ++x) {
+      const int m = u_n[x] - u_head[x];
+      if (m > 0)
+        DCK(cudaMemcpyAsync(untried + k * 4, S.apool.as<double>() + (u_off[x] + u_head[x]) * 4, m * 32ull,
+                            cudaMemcpyDeviceToHost, st));
+      k += m;
+    }
+  }
+  DCK(cudaStreamSynchronize(st));
+  if (scal) {
+    scal[0] = S.last_dT;
+    scal[1] = S.last_dS;
+    scal[2] = S.last_es;
+    scal[3] = n;
+  }
+  return PPG_SUCCESS;
+}
 
 // Test entry (acceptance criterion 3, acceptance.cpp:255-281): loads one
 // explicit tree into a scratch device tree and runs the device select_batch

@@ -49,3 +49,24 @@ def test_adapter_run_pmbs_equals_reference(tmp_path, idx):
     assert L.adapter_check_pmbs(str(path).encode(), c["case_id"].encode(), ctypes.byref(a), ctypes.byref(s),
                                 ctypes.byref(t)) == 0
     assert a.value == 1 and s.value == 1 and t.value == 1
+
+
+ACCEPTANCE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                          "acceptance_gpu")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(ACCEPTANCE), reason="acceptance_gpu not built (needs /root/reference)")
+@pytest.mark.parametrize("criterion", [1, 2, 3, 4, 8, 9])
+def test_reference_acceptance_binary_on_the_gpu_core(criterion):
+    """The reference's UNCHANGED acceptance suite (proj/tests/acceptance.cpp)
+    linked against pushplan_core_gpu — the reference core whose
+    batch_resolve and pmbs::run_pmbs are the device path (oracle/Makefile
+    core_gpu): C1 (N_e = 1 PMBS tree == serial MCTS tree, via
+    SearchResult::tree rebuilt from the device tree), C4 (identical trees
+    across pool sizes), C8 (GPU batch_resolve == the reference resolve_push,
+    bitwise digests), C2 / C3 / C9 on the reference functions it still uses."""
+    import subprocess
+    r = subprocess.run([ACCEPTANCE, "--criterion", str(criterion)], capture_output=True, text=True, timeout=1200)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith(f"criterion {criterion}:")]
+    assert line and ": PASS" in line[0], (r.stdout[-2000:], r.stderr[-2000:])
