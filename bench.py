@@ -300,6 +300,19 @@ def rollout_throughput(ctx, with_reference: bool):
     row = {"workload": "ppg_simulate: 65,536 envs from proj/cases/case_18's root, cap 10, iteration 1", "unit": UNIT,
            "rollout_steps": int(ctr[0]), "resolve_calls": int(ctr[3]), "rounds": int(ctr[1]),
            "repurposes": int(ctr[2]), "seconds": dt, "rollout_env_steps_per_s": int(ctr[0]) / dt}
+    # roofline: the same rollouts' algorithmic FP64 work (instrumented one-lane
+    # step kernel, bit-identical trajectory; untimed) over the measured time
+    ops, ctr2 = ctx.simulate_count_arrays(st.poses[None], meta, ne, True, int(c["seed"]), 1, 10)
+    peak = ctypes.c_double()
+    ctx.lib.ppg_measure_fp64_peak(ctx.ptr, ctypes.byref(peak), None)
+    total = float(ops.sum())
+    row["roofline"] = {"bound": "fp64", "achieved": total / dt / 1e12, "peak": peak.value / 1e12, "unit": "TFLOP/s",
+                       "frac": total / dt / peak.value, "traffic": None,
+                       "ops_per_rollout_step": total / max(1, int(ctr[0])),
+                       "ops_split": {"resolve": int(ops[0]), "sample": int(ops[1]), "grasp": int(ops[2])},
+                       "same_trajectory": bool(np.array_equal(ctr, ctr2)),
+                       "note": "W = W_resolve + W_sample + W_grasp per RolloutCursor::step (SURVEY 8d), counted "
+                               "on this call; whole-call time (rounds, harvests, launches) in the denominator"}
     if with_reference:
         from oracle import ref
         if ref.available():

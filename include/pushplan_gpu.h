@@ -192,6 +192,14 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
                  int n_envs, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap,
                  double* rewards_out, int64_t* counters);
 
+/* ppg_simulate's algorithmic work (the rollout roofline numerator, SURVEY
+ * 8d): the same lockstep (bit-identical rollouts) through an instrumented
+ * one-lane step kernel; ops_out[3] = FP64 ops (+,-,*,/,sqrt = 1 each) of the
+ * resolve_push, sample_pushes and graspable calls of every rollout step. */
+int ppg_simulate_count(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
+                       int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, int64_t* ops_out,
+                       int64_t* counters);
+
 /* ---- multi-GPU contexts (BASELINE configs[4]) ----
  * The rollout batch of every PMBS iteration (batch_simulate, pmbs.cpp:207-234)
  * is sharded by environment over G GPUs: shard r owns a contiguous range of

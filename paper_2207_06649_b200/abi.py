@@ -187,6 +187,8 @@ SIGNATURES = {
     "ppg_create_multi": (c_void_p, [c_void_p, c_int, c_int, POINTER(PpgParams), POINTER(c_int)]),
     "ppg_shard_info": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ppg_tree_export": (c_int, [c_void_p] + [c_void_p] * 12),
+    "ppg_simulate_count": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int32), c_int, c_int, c_int, c_uint64,
+                                   c_uint64, c_int, POINTER(c_int64), POINTER(c_int64)]),
     "ppg_measure_fp64_peak": (c_int, [c_void_p, POINTER(c_double), POINTER(c_double)]),
     "ppg_generate_cases": (c_int, [c_int, c_int, c_double, POINTER(c_uint64), c_int, POINTER(c_int32),
                                    POINTER(c_double), POINTER(c_int32), POINTER(c_double), POINTER(c_double),

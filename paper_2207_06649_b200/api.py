@@ -301,6 +301,19 @@ class Context:
                                           dptr(rewards), i64ptr(ctr)), "ppg_simulate")
         return rewards, ctr
 
+    def simulate_count_arrays(self, node_poses: np.ndarray, node_meta: np.ndarray, n_envs: int,
+                              leaf_parallel: bool, seed: int, iteration: int, depth_cap: int):
+        """The algorithmic FP64 work of a simulate_arrays call (same rollouts):
+        (ops[3] = resolve, sample, grasp, counters[4])."""
+        node_poses = np.ascontiguousarray(node_poses, np.float64)
+        node_meta = np.ascontiguousarray(node_meta, np.int32)
+        ops = np.zeros(3, np.int64)
+        ctr = np.zeros(4, np.int64)
+        self._check(self.lib.ppg_simulate_count(self.ptr, dptr(node_poses), iptr(node_meta), node_poses.shape[0],
+                                                n_envs, int(leaf_parallel), seed & 0xFFFFFFFFFFFFFFFF, iteration,
+                                                depth_cap, i64ptr(ops), i64ptr(ctr)), "ppg_simulate_count")
+        return ops, ctr
+
     def run_pmbs_arrays(self, root_poses: np.ndarray, want_sig: bool = False) -> SearchResult:
         root_poses = np.ascontiguousarray(root_poses, np.float64)
         action = np.zeros(4, np.float64)

@@ -232,6 +232,7 @@ ppg_ctx* ppg_create(int device, const ppg_params* params, int* err) {
   ok = ok && cudaFuncSetAttribute(grasp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(lock_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  ok = ok && cudaFuncSetAttribute(lock_step_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(lock_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(expand_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
   ok = ok && cudaFuncSetAttribute(lock_post_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
@@ -1131,6 +1132,38 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
     if (rc != PPG_SUCCESS) return rc;
   }
   CK(cudaMemcpyAsync(rewards_out, ctx->la.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
+  if (counters) CK(cudaMemcpyAsync(counters, ctx->la.counters, 32, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+int ppg_simulate_count(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
+                       int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, int64_t* ops_out,
+                       int64_t* counters) {
+  if (!ctx || !ops_out) return PPG_EINVAL;
+  if (n_nodes <= 0) return PPG_SUCCESS;
+  int rc = lock_check(ctx, n_nodes, n_envs, depth_cap);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int used = leaf_parallel ? n_envs : n_nodes;
+  rc = lock_setup(ctx, node_poses, node_meta, n_nodes, used, used, 0, leaf_parallel, seed, iteration, depth_cap);
+  if (rc != PPG_SUCCESS) return rc;
+  CK(ctx->b_e.ensure(64));
+  unsigned long long* ops = ctx->b_e.as<unsigned long long>();
+  CK(cudaMemsetAsync(ops, 0, 24, st));
+  const int n = ctx->scene.n;
+  for (;;) {
+    lock_harvest_kernel<<<1, 1024, 0, st>>>(ctx->lc, ctx->la);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_nactive, ctx->la.n_active, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int act = *ctx->h_nactive;
+    if (act == 0) break;
+    lock_step_count_kernel<<<(act + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(ctx->lc, ctx->la, ops);
+    CK(cudaGetLastError());
+  }
+  CK(cudaMemcpyAsync(ops_out, ops, 24, cudaMemcpyDeviceToHost, st));
   if (counters) CK(cudaMemcpyAsync(counters, ctx->la.counters, 32, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return PPG_SUCCESS;

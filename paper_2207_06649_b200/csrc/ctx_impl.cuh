@@ -25,6 +25,7 @@ __global__ void lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs
 __global__ void lock_harvest_local_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_harvest_apply_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_step_count_kernel(const __grid_constant__ SimConst C, LockArgs a, unsigned long long* ops);
 __global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
 template <int NW, bool kPoly>

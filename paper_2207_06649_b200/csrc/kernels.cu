@@ -599,6 +599,134 @@ __global__ void __launch_bounds__(128) lock_post_kernel(const __grid_constant__ 
   rollout_finish_step(P, S, C, a, e);
 }
 
+// ---- algorithmic-work counting for rollout steps (the rollout roofline
+// numerator): W = W_resolve + W_sample + W_grasp per
+// RolloutCursor::step, +,-,*,/,sqrt = 1 op each, from the reference source.
+//   W_sample = sum over the n * N_a candidates of (31 + 7 m), m = objects the
+//              start-collision filter tests (collides_gripper_start,
+//              world.cpp:154-164) up to its first hit, n when valid, 0 when a
+//              geometric test rejects the candidate first (actions.cpp:55-70);
+//   W_grasp  = sum over the 16 angles of (150 + 226 m'), m' = obstacles tested
+//              before the angle is found infeasible (actions.cpp:118-140);
+//   W_resolve as for batch_resolve (the instrumented resolve_push<true>).
+PPG_DI long long sample_ops(const PoseView& P, const ShapeView& S, const SimConst& C) {
+  long long ops = 0;
+  const double r = C.tip_r + C.tip_clear, h = C.side / 2.0;
+  for (int o = 0; o < S.n; ++o)
+    for (int k = 0; k < C.na; ++k) {
+      ops += 31;
+      V2 s, t;
+      if (!push_candidate(P, S, C, o, k, false, s, t)) continue;  // rejected before the collision filter
+      if (s.x - r < -h || s.x + r > h || s.y - r < -h || s.y + r > h) continue;
+      int m = 0;
+      for (int i = 0; i < S.n; ++i) {
+        ++m;
+        if (object_point_distance(P, S, i, s) < r) break;
+      }
+      ops += 7ll * m;
+    }
+  return ops;
+}
+
+PPG_DI long long grasp_ops(const PoseView& P, const ShapeView& S, const SimConst& C, int target) {
+  long long ops = 0;
+  for (int k = 0; k < kGraspAngles; ++k) {
+    ops += 150;
+    double margin, cx, cy;
+    // m' = obstacles tested: all n - 1 when feasible, else up to the first
+    // blocking one (0 when the extent or the walls reject the angle)
+    if (grasp_angle(P, S, C, target, k, &margin, &cx, &cy)) {
+      ops += 226ll * (S.n - 1);
+      continue;
+    }
+    const double ht = C.finger_thickness / 2.0, hw = C.finger_width / 2.0;
+    const V2 u{C.g_cos[k], C.g_sin[k]};
+    const V2 v = perp(u);
+    double lo_u, hi_u, lo_v, hi_v;
+    if (S.kind_(target) == 0) {
+      const V2 tp = P.pos(target);
+      const double rr = S.rad_(target);
+      lo_u = dot(tp, u) - rr;
+      hi_u = dot(tp, u) + rr;
+      lo_v = dot(tp, v) - rr;
+      hi_v = dot(tp, v) + rr;
+    } else {
+      Poly tpoly;
+      world_polygon(P, S, target, tpoly);
+      hi_u = support_extent(tpoly, u);
+      lo_u = -support_extent(tpoly, -u);
+      hi_v = support_extent(tpoly, v);
+      lo_v = -support_extent(tpoly, -v);
+    }
+    if (!(hi_u - lo_u < C.opening - 2.0 * C.approach_clearance)) continue;
+    const V2 center = u * ((lo_u + hi_u) / 2.0) + v * ((lo_v + hi_v) / 2.0);
+    Poly ra, rb;
+    const V2 ca = center + u * (-(C.opening / 2.0 + ht));
+    const V2 cb = center + u * (C.opening / 2.0 + ht);
+    ra.n = rb.n = 4;
+    ra.p[0] = ca - u * ht - v * hw;
+    ra.p[1] = ca + u * ht - v * hw;
+    ra.p[2] = ca + u * ht + v * hw;
+    ra.p[3] = ca - u * ht + v * hw;
+    rb.p[0] = cb - u * ht - v * hw;
+    rb.p[1] = cb + u * ht - v * hw;
+    rb.p[2] = cb + u * ht + v * hw;
+    rb.p[3] = cb - u * ht + v * hw;
+    if (dmin(rect_min_wall_clearance(ra, C.side), rect_min_wall_clearance(rb, C.side)) <= 0.0) continue;
+    int m = 0;
+    for (int i = 0; i < S.n; ++i) {
+      if (i == target) continue;
+      ++m;
+      if (dmin(rect_object_distance(ra, P, S, i), rect_object_distance(rb, P, S, i)) <= 0.0) break;
+    }
+    ops += 226ll * m;
+  }
+  return ops;
+}
+
+PPG_DI long long resolve_ops(const Counts& c, int n) {
+  return 7 * c.tb + 15 * c.tn + 4 * c.ht + 7 * c.pb + 15 * c.pn + 10 * c.hp + 4 * c.s + 17ll * n +
+         7ll * n * (n - 1) / 2 + 15 * c.pfinal;
+}
+
+// lock_step_kernel with the work counters: the same RolloutCursor::step
+// (bit-identical trajectory), plus the algorithmic ops of each step added to
+// ops[0..2] = resolve, sample, grasp.
+__global__ void __launch_bounds__(128) lock_step_count_kernel(const __grid_constant__ SimConst C, LockArgs a,
+                                                              unsigned long long* ops) {
+  lock_dyn(a);
+  extern __shared__ double smem[];
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_act = *a.n_active;
+  if (gid >= n_act) return;
+  const int e = a.active[gid];
+  const int n = C.n;
+  double* env = a.env_poses + static_cast<size_t>(e) * n * 3;
+  const ShapeView S = a.S.view(0);
+  const PoseView P = stage_poses(smem, n, env, S);
+  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
+  atomicAdd(&ops[1], static_cast<unsigned long long>(sample_ops(P, S, C)));
+  V2 s, t;
+  if (!rollout_pick(P, S, C, a, e, s, t)) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), 1ull);
+  double residual;
+  Counts cnt{0, 0, 0, 0, 0, 0, 0, 0};
+  const int st = resolve_push<true>(P, S, C, s, t, false, &residual, &cnt);
+  atomicAdd(&ops[0], static_cast<unsigned long long>(resolve_ops(cnt, n)));
+  if (st != 0) {
+    a.env_done[e] = 1;
+    a.env_reward[e] = 0.0;
+    return;
+  }
+  atomicAdd(&ops[2], static_cast<unsigned long long>(grasp_ops(P, S, C, a.S.target[0])));
+  rollout_finish_step(P, S, C, a, e);
+  unstage_poses(P, env);
+}
+
 }  // namespace ppg
 
 namespace ppg {

@@ -628,3 +628,20 @@ def test_streamed_zero_copy_start_collisions(ctx, pattern):
                                     np.ascontiguousarray(pushes[idx]), P)
     assert np.array_equal(ps[idx], s3)
     assert _bitwise(po[idx], o3).all()
+
+
+@pytest.mark.gpu
+def test_simulate_count_same_trajectory(ctx):
+    """ppg_simulate_count (the rollout roofline numerator) runs the same
+    rollouts: rewards-defining counters equal ppg_simulate's; every rollout
+    step contributes sample + resolve work and grasp work after a resolve."""
+    cases = {c["case_id"]: s for c, s in golden_io.cases()}
+    for cid, ne, seed, cap, nposes, meta, rewards in golden_io.simulate_sets():
+        ctx.set_params(default_params(n_envs=ne, rng_seed=seed))
+        ctx.set_scene(cases[cid])
+        r, ctr = ctx.simulate_arrays(nposes, meta, ne, True, seed, 0, cap)
+        ops, ctr2 = ctx.simulate_count_arrays(nposes, meta, ne, True, seed, 0, cap)
+        assert np.array_equal(ctr, ctr2), cid
+        if ctr[0] > 0:
+            assert ops[1] >= 31 * ctr[0] * cases[cid].n * 16  # every candidate of every step
+            assert ops[0] > 0 and ops[2] >= 150 * 16
