@@ -1121,15 +1121,35 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   const int used = leaf_parallel ? n_envs : n_nodes;
   rc = lock_setup(ctx, node_poses, node_meta, n_nodes, used, used, 0, leaf_parallel, seed, iteration, depth_cap);
   if (rc != PPG_SUCCESS) return rc;
-  for (;;) {
+  // PPG_ROUND_TRACE=1: per-round active count, mode and device time to stderr (experiments)
+  static const bool trace = std::getenv("PPG_ROUND_TRACE") != nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (trace) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+  }
+  for (int round = 0;; ++round) {
     lock_harvest_kernel<<<1, 1024, 0, st>>>(ctx->lc, ctx->la);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(ctx->h_nactive, ctx->la.n_active, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const int act = *ctx->h_nactive;
     if (act == 0) break;
+    if (trace) cudaEventRecord(t0, st);
     rc = lock_round(ctx, act);
     if (rc != PPG_SUCCESS) return rc;
+    if (trace) {
+      cudaEventRecord(t1, st);
+      cudaEventSynchronize(t1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t0, t1);
+      std::fprintf(stderr, "round %d active %d mode %d ms %.4f\n", round, act,
+                   static_cast<int>(round_mode(ctx, ctx->scene.n, act)), ms);
+    }
+  }
+  if (trace) {
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
   }
   CK(cudaMemcpyAsync(rewards_out, ctx->la.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
   if (counters) CK(cudaMemcpyAsync(counters, ctx->la.counters, 32, cudaMemcpyDeviceToHost, st));

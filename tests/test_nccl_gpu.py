@@ -71,3 +71,20 @@ def test_nccl_run_pmbs_through_sharded_hook(nccl_group):
     assert hook.error is None
     assert list(r.action) == d["action"] and r.signature_fnv == int(d["sig_fnv"])
     ctx.close()
+
+
+def test_rank_context_library_native(nccl_group):
+    """sharded.rank_context — the path bench.py's C5 block takes under
+    torchrun: rank 0 makes the NCCL id, torch.distributed broadcasts it,
+    ppg_create_rank builds the library's own communicator; run_pmbs on it
+    (sharded device tree, in-library W all-reduce) == reference fingerprints."""
+    from paper_2207_06649_b200.sharded import rank_context
+    ctx = rank_context(0)
+    try:
+        assert ctx.shard_info() == {"rank": 0, "world": 1, "shards_here": 1, "transport": "nccl"}
+        for idx in (4, 12, 17):
+            cc, st = golden_io.cases()[idx]
+            r = run_pmbs(st, ParallelConfig(rng_seed=int(cc["seed"])), ctx=ctx)
+            assert list(r.action) == cc["decision"]["action"] and r.signature_fnv == int(cc["decision"]["sig_fnv"])
+    finally:
+        ctx.close()
