@@ -196,7 +196,11 @@ void ppg_params_default(ppg_params* p) {
   p->leaf_parallel = 1;
 }
 
-const char* ppg_version(void) { return "pmbs_b200 0.1 sm_100a fp64 fmad=false"; }
+#ifdef PPG_FMA_VARIANT
+const char* ppg_version(void) { return "pmbs_b200 0.2 sm_100a fp64 fmad=true (FMA variant: tolerance, not bit-exact)"; }
+#else
+const char* ppg_version(void) { return "pmbs_b200 0.2 sm_100a fp64 fmad=false"; }
+#endif
 
 int ppg_device_count(void) {
   int n = 0;
