@@ -300,6 +300,8 @@ void ppg_destroy(ppg_ctx* ctx) {
   }
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
   ctx->l_go.release();
+  for (DevBuf* b : {&ctx->l_around, &ctx->l_astate, &ctx->l_aW, &ctx->l_actr, &ctx->l_adl, &ctx->l_actl, &ctx->trace_buf})
+    b->release();
   if (ctx->h_go) cudaFreeHost(ctx->h_go);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -465,6 +467,50 @@ int lock_round_on(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const Reso
   }
   CK(cudaGetLastError());
   return PPG_SUCCESS;
+}
+
+bool async_enabled(const ppg_ctx* ctx) {
+  if (ctx->async_mode < 0) {
+    const char* v = std::getenv("PPG_ASYNC");
+    const_cast<ppg_ctx*>(ctx)->async_mode = (v && v[0] == '0') ? 0 : 1;
+  }
+  return ctx->async_mode == 1 && !ctx->force_generic;
+}
+
+template <int NW, bool kPoly>
+static int launch_async_t(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st) {
+  static int bps[2] = {-1, -1};
+  const void* fn = reinterpret_cast<const void*>(&lock_async_kernel<NW, kPoly>);
+  int& b = bps[kPoly ? 1 : 0];
+  if (b < 0) {
+    int v = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lock_async_kernel<NW, kPoly>, kWarpsPerBlock * 32, 0));
+    b = v > 0 ? v : 1;
+  }
+  const int want = (work + 1 + kWarpsPerBlock - 1) / kWarpsPerBlock;  // + the harvester warp
+  const int grid = want < b * ctx->num_sms ? want : b * ctx->num_sms;
+  lock_async_init_kernel<<<(work + 255) / 256 + 1, 256, 0, st>>>(C, a);
+  CK(cudaGetLastError());
+  // every warp must be resident (workers and the harvester wait on each other)
+  SimConst c_arg = C;
+  LockArgs a_arg = a;
+  void* args[] = {&c_arg, &a_arg};
+  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kWarpsPerBlock * 32), args, 0, st));
+  return PPG_SUCCESS;
+}
+
+int launch_async(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st) {
+  CK(cudaMemsetAsync(a.a_ctl, 0, 32, st));
+  const int n = ctx->scene.n, w = warp_words(n);
+  if (!ctx->scene_all_discs) {
+    if (w == 1) return launch_async_t<1, true>(ctx, C, a, work, st);
+    if (w == 2) return launch_async_t<2, true>(ctx, C, a, work, st);
+    return launch_async_t<4, true>(ctx, C, a, work, st);
+  }
+  if (w == 1) return launch_async_t<1, false>(ctx, C, a, work, st);
+  if (w == 2) return launch_async_t<2, false>(ctx, C, a, work, st);
+  if (w == 4) return launch_async_t<4, false>(ctx, C, a, work, st);
+  return launch_async_t<8, false>(ctx, C, a, work, st);
 }
 
 // Polygon batches (one warp per env): past one resident wave the grid is
@@ -1031,6 +1077,12 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   CK(ctx->l_status.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_stepping.ensure(static_cast<size_t>(E) * 4 + 16));
   CK(ctx->l_rec.ensure(static_cast<size_t>(E) * (4 + 4 + 1 + 8) + 64));
+  CK(ctx->l_around.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_astate.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_aW.ensure(static_cast<size_t>(kAsyncK) * n_nodes * 4));
+  CK(ctx->l_actr.ensure(static_cast<size_t>(kAsyncK) * 16));
+  CK(ctx->l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
+  CK(ctx->l_actl.ensure(64));
   CK(cudaMemcpyAsync(ctx->l_npose.p, node_poses, static_cast<size_t>(n_nodes) * n * 3 * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ctx->l_nmeta.p, node_meta, static_cast<size_t>(n_nodes) * 3 * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ctx->l_counters.p, 0, 32, st));
@@ -1076,6 +1128,13 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
     a.rec_reward = reinterpret_cast<double*>(r + 16 + static_cast<size_t>(E) * 8 + 8 - ((16 + E * 8) % 8));
     a.rec_grasp = reinterpret_cast<uint8_t*>(a.rec_reward + E);
   }
+  a.env_round = ctx->l_around.as<int32_t>();
+  a.env_state = ctx->l_astate.as<int32_t>();
+  a.a_W = ctx->l_aW.as<int32_t>();
+  a.a_ctr = ctx->l_actr.as<int32_t>();
+  a.a_dl = ctx->l_adl.as<int32_t>();
+  a.a_ctl = ctx->l_actl.as<int32_t>();
+  a.a_wcap = n_nodes;
   ctx->lra = ResolveArgs{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, 0};
   ctx->lra.idx = a.stepping;
   ctx->lra.E_dev = a.n_stepping;
@@ -1108,6 +1167,38 @@ int lock_check(ppg_ctx* ctx, int n_nodes, int n_envs, int depth_cap) {
   return PPG_SUCCESS;
 }
 
+unsigned long long* step_trace_buffer(ppg_ctx* ctx) {
+  static const char* path = std::getenv("PPG_STEP_TRACE");
+  if (!path) return nullptr;
+  constexpr unsigned long long kRecs = 1ull << 22;
+  if (ctx->trace_buf.cap == 0) {
+    if (ctx->trace_buf.ensure((2 + 4 * kRecs) * 8) != cudaSuccess) return nullptr;
+    const unsigned long long hdr[2] = {0ull, kRecs};
+    cudaMemcpy(ctx->trace_buf.p, hdr, 16, cudaMemcpyHostToDevice);
+  }
+  return ctx->trace_buf.as<unsigned long long>();
+}
+
+void step_trace_dump(ppg_ctx* ctx) {
+  static const char* path = std::getenv("PPG_STEP_TRACE");
+  if (!path || ctx->trace_buf.cap == 0) return;
+  cudaStreamSynchronize(ctx->stream);
+  unsigned long long hdr[2];
+  cudaMemcpy(hdr, ctx->trace_buf.p, 16, cudaMemcpyDeviceToHost);
+  const unsigned long long k = hdr[0] < hdr[1] ? hdr[0] : hdr[1];
+  std::vector<unsigned long long> rec(4 * k);
+  if (k) cudaMemcpy(rec.data(), ctx->trace_buf.as<unsigned long long>() + 2, 32 * k, cudaMemcpyDeviceToHost);
+  if (FILE* f = std::fopen(path, "ab")) {
+    const unsigned long long marker = ~0ull;  // one call per block of records
+    std::fwrite(&marker, 8, 1, f);
+    std::fwrite(&k, 8, 1, f);
+    std::fwrite(rec.data(), 32, k, f);
+    std::fclose(f);
+  }
+  const unsigned long long zero = 0;
+  cudaMemcpy(ctx->trace_buf.p, &zero, 8, cudaMemcpyHostToDevice);
+}
+
 extern "C" {
 
 int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
@@ -1125,6 +1216,7 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   const int used = leaf_parallel ? n_envs : n_nodes;
   rc = lock_setup(ctx, node_poses, node_meta, n_nodes, used, used, 0, leaf_parallel, seed, iteration, depth_cap);
   if (rc != PPG_SUCCESS) return rc;
+  ctx->la.step_trace = step_trace_buffer(ctx);
   // PPG_ROUND_TRACE=1: per-round active count, mode and device time to stderr (experiments)
   static const bool trace = std::getenv("PPG_ROUND_TRACE") != nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -1140,8 +1232,21 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
     const int act = *ctx->h_nactive;
     if (act == 0) break;
     if (trace) cudaEventRecord(t0, st);
-    rc = lock_round(ctx, act);
-    if (rc != PPG_SUCCESS) return rc;
+    const bool go_async = async_enabled(ctx) && round_mode(ctx, ctx->scene.n, act) == RoundMode::kWarp;
+    if (go_async) {  // every remaining round, barrier-free (warp_env.cu lock_async_kernel)
+      rc = launch_async(ctx, ctx->lc, ctx->la, used, st);
+      if (rc != PPG_SUCCESS) return rc;
+      int32_t ctl[4];
+      CK(cudaMemcpyAsync(ctl, ctx->la.a_ctl, 16, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (ctl[3] != 0) {
+        ctx->err = "asynchronous lockstep stalled (protocol error)";
+        return PPG_ECUDA;
+      }
+    } else {
+      rc = lock_round(ctx, act);
+      if (rc != PPG_SUCCESS) return rc;
+    }
     if (trace) {
       cudaEventRecord(t1, st);
       cudaEventSynchronize(t1);
@@ -1158,6 +1263,7 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
   CK(cudaMemcpyAsync(rewards_out, ctx->la.rew, static_cast<size_t>(n_nodes) * 8, cudaMemcpyDeviceToHost, st));
   if (counters) CK(cudaMemcpyAsync(counters, ctx->la.counters, 32, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (ctx->la.step_trace) step_trace_dump(ctx);
   return PPG_SUCCESS;
 }
 

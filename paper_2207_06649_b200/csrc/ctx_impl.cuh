@@ -62,6 +62,9 @@ constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 
     }                                                                                       \
   } while (0)
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
+template <int NW, bool kPoly>
+__global__ void lock_async_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_sample_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_post_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_report_kernel(const __grid_constant__ SimConst C, LockArgs a);
@@ -187,6 +190,9 @@ struct ppg_ctx {
   // its group; batch_simulate / run_pmbs then shard the rollout batch
   ppg::Group* group = nullptr;
   ppg::DevBuf l_go;                       // sharded harvest: "any env active" (device int)
+  ppg::DevBuf trace_buf;                  // PPG_STEP_TRACE: per-step records (experiments)
+  ppg::DevBuf l_around, l_astate, l_aW, l_actr, l_adl, l_actl;  // asynchronous lockstep state
+  int async_mode = -1;                    // -1 not read, 0 off (PPG_ASYNC=0), 1 on
   int32_t* h_go = nullptr;                // pinned copy
 };
 
@@ -203,10 +209,17 @@ enum class RoundMode { kWarp, kHybrid, kLaneDisc, kGeneric, kAdaptive };
 RoundMode round_mode(const ppg_ctx* ctx, int n, int envs);
 int lock_round_on(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const ResolveArgs& ra, int work,
                   RoundMode mode, cudaStream_t st);
+// Asynchronous lockstep (warp_env.cu lock_async_kernel): runs every remaining
+// round of the current lockstep call; `work` = the most envs it may own.
+// PPG_ASYNC=0 disables it (lockstep rounds everywhere).
+bool async_enabled(const ppg_ctx* ctx);
+int launch_async(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st);
 int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used,
                int used_global, int env_lo, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap);
 int lock_round(ppg_ctx* ctx, int act);
 int lock_check(ppg_ctx* ctx, int n_nodes, int n_envs, int depth_cap);
+unsigned long long* step_trace_buffer(ppg_ctx* ctx);  // PPG_STEP_TRACE set: the record buffer, else null
+void step_trace_dump(ppg_ctx* ctx);                   // appends the records to $PPG_STEP_TRACE
 
 namespace ppg {
 // multi.cu: the shards of a multi-GPU context.  Member k of this process is

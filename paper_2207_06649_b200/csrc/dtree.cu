@@ -69,6 +69,7 @@ struct DTScal {
   int err[4];                    // first invariant violation seen on the device (debug)
   int round_mode;                // adaptive lockstep rounds (LockArgs.round_mode)
   int round_guard;               // rounds of this iteration's lockstep (< 0: limit hit)
+  int async_ctl[8];              // asynchronous lockstep control (LockArgs.a_ctl; [3] != 0: stalled)
 };
 
 struct DTree {
@@ -487,7 +488,7 @@ struct DTreeState {
   DevBuf sel_node, sel_act, gp, ga, cp, st, gr, nu, un, meta, logtab, sc;
   // lockstep state
   DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx, l_W, l_rew, l_active,
-      l_nactive, l_counters, l_push, l_status, l_stepping;
+      l_nactive, l_counters, l_push, l_status, l_stepping, l_around, l_astate, l_aW, l_actr, l_adl;
   int cap_nodes = 0;
   long long cap_actions = 0;
   int n_envs = 0, n = 0, na = 0;
@@ -526,7 +527,7 @@ struct DTreeState {
                       &poses, &anc, &apool, &cpool, &sel_node, &sel_act, &gp, &ga, &cp, &st, &gr, &nu, &un,
                       &meta, &logtab, &sc, &l_node, &l_pushes, &l_done, &l_byg, &l_harv, &l_flag, &l_reward,
                       &l_poses, &l_mt, &l_mtidx, &l_W, &l_rew, &l_active, &l_nactive, &l_counters, &l_push,
-                      &l_status, &l_stepping};
+                      &l_status, &l_stepping, &l_around, &l_astate, &l_aW, &l_actr, &l_adl};
     for (DevBuf* b : bufs) b->release();
   }
 };
@@ -662,6 +663,11 @@ int dt_batch(ppg_ctx* ctx, DTreeState& S) {
   DCK(S.l_push.ensure(static_cast<size_t>(E) * 32));
   DCK(S.l_status.ensure(static_cast<size_t>(E) * 4));
   DCK(S.l_stepping.ensure(static_cast<size_t>(E) * 4 + 16));
+  DCK(S.l_around.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_astate.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_aW.ensure(static_cast<size_t>(kAsyncK) * E * 4));
+  DCK(S.l_actr.ensure(static_cast<size_t>(kAsyncK) * 16));
+  DCK(S.l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(ctx->b_counter.ensure(16));  // launch_disc's work counter (no allocation during capture)
   return PPG_SUCCESS;
 }
@@ -737,6 +743,14 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
   a.n_active = S.l_nactive.as<int32_t>();
   a.counters = S.l_counters.as<long long>();
   a.dyn = t.sc->lock_dyn;
+  a.step_trace = step_trace_buffer(ctx);
+  a.env_round = S.l_around.as<int32_t>();
+  a.env_state = S.l_astate.as<int32_t>();
+  a.a_W = S.l_aW.as<int32_t>();
+  a.a_ctr = S.l_actr.as<int32_t>();
+  a.a_dl = S.l_adl.as<int32_t>();
+  a.a_ctl = t.sc->async_ctl;
+  a.a_wcap = S.n_envs;
   a.round_mode = nullptr;  // set by dt_mode for adaptive graphs
   a.round_guard = &t.sc->round_guard;
   a.hybrid_min = ctx->hybrid_min_envs;
@@ -757,7 +771,17 @@ RoundMode dt_mode(ppg_ctx* ctx, DTreeState& S) {
   return m;
 }
 
+// One WHILE-body round: a lockstep round, or (warp mode / the warp half of
+// adaptive mode) the asynchronous lockstep, which runs every remaining round
+// of the call (its kernels return at once when the harvest picked hybrid).
 int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, RoundMode m) {
+  if (async_enabled(ctx) && (m == RoundMode::kWarp || m == RoundMode::kAdaptive)) {
+    if (m == RoundMode::kAdaptive) {  // the hybrid half (returns at once in warp rounds)
+      const int rc = lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, RoundMode::kHybrid, st);
+      if (rc != PPG_SUCCESS) return rc;
+    }
+    return launch_async(ctx, S.C, S.la, S.n_envs, st);
+  }
   return lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, m, st);
 }
 
@@ -1083,6 +1107,7 @@ int dt_finish(ppg_ctx* ctx, const DTScal& h, int stop, double elapsed_s, double 
   const ppg_params& p = ctx->params;
   cudaStream_t st = ctx->stream;
   int64_t ctr[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  if (S.la.step_trace) step_trace_dump(ctx);
   S.last_valid = false;
   if (stop == 3) {
     ctx->err = "device tree: selection invariant violated";
@@ -1631,6 +1656,10 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     if (h.round_guard < 0) {
       ctx->err = "device tree: lockstep rounds exceeded the safety limit";
       return PPG_EINVAL;
+    }
+    if (h.async_ctl[3] != 0) {
+      ctx->err = "device tree: asynchronous lockstep stalled (protocol error)";
+      return PPG_ECUDA;
     }
     if (h.err[0]) {
       char m[256];

@@ -187,32 +187,6 @@ __global__ void __launch_bounds__(128) expand_post_kernel(const __grid_constant_
 
 // ---------------- lockstep engine ----------------
 
-// RolloutCursor ctor (mcts.cpp:121-140) for env e at node `node`.
-PPG_DI void cursor_init(const SimConst& C, const LockArgs& a, int e, int node) {
-  const int32_t* m = a.node_meta + node * 3;
-  const int depth = m[0];
-  a.env_node[e] = node;
-  a.env_pushes[e] = depth;
-  uint8_t done = 0, byg = 0;
-  double reward = 0.0;
-  if (m[1]) {
-    done = 1;
-    byg = 1;
-    reward = C.gamma_pow[depth];
-  } else if (m[2]) {
-    done = 1;
-  } else if (depth >= a.cap) {
-    done = 1;
-  }
-  a.env_done[e] = done;
-  a.env_bygrasp[e] = byg;
-  a.env_reward[e] = reward;
-  const int n = C.n;
-  const double* src = a.node_poses + static_cast<size_t>(node) * n * 3;
-  double* dst = a.env_poses + static_cast<size_t>(e) * n * 3;
-  for (int i = 0; i < 3 * n; ++i) dst[i] = src[i];
-}
-
 __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
   lock_dyn(a);
   const int e = blockIdx.x * blockDim.x + threadIdx.x;

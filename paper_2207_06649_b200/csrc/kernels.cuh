@@ -134,9 +134,26 @@ struct LockArgs {
   // (any environment active anywhere) for the host.
   int shard_r = 0, shard_g = 1;
   int32_t* go = nullptr;
+  // asynchronous lockstep (warp_env.cu lock_async_kernel): per env its
+  // completed rounds and state (0 runnable, 1 awaiting the harvest of its
+  // round, 2 gone, 3 + node: re-purposed to node, not yet applied); a ring
+  // of kAsyncK rounds: W [K][a_wcap], counters [K][4] (arrived, gone at this
+  // round, done-list length, -), done lists [K][E]; control [8] (harvested
+  // round H, finished, gone so far, error, ...)
+  int32_t* env_round = nullptr;
+  int32_t* env_state = nullptr;
+  int32_t* a_W = nullptr;
+  int32_t* a_ctr = nullptr;
+  int32_t* a_dl = nullptr;
+  int32_t* a_ctl = nullptr;
+  int a_wcap = 0;
+  // PPG_STEP_TRACE (experiments): one record per latency-mode env-step
+  // {env, round, start/end globaltimer ns, flags} appended at step_trace[1 + k]
+  unsigned long long* step_trace = nullptr;
 };
 
 constexpr int kLockRoundLimit = 1 << 20;
+constexpr int kAsyncK = 8;  // rounds a runnable env may run ahead of the harvest
 
 // Applies the device-side per-iteration overrides (device tree mode).
 __device__ __forceinline__ void lock_dyn(LockArgs& a) {
@@ -156,6 +173,32 @@ __device__ __forceinline__ void lock_dyn(LockArgs& a) {
     a.seed = static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[4])) |
              static_cast<uint64_t>(static_cast<uint32_t>(a.dyn[5])) << 32;
   }
+}
+
+// RolloutCursor ctor (mcts.cpp:121-140) for env e at node `node`.
+PPG_DI void cursor_init(const SimConst& C, const LockArgs& a, int e, int node) {
+  const int32_t* m = a.node_meta + node * 3;
+  const int depth = m[0];
+  a.env_node[e] = node;
+  a.env_pushes[e] = depth;
+  uint8_t done = 0, byg = 0;
+  double reward = 0.0;
+  if (m[1]) {
+    done = 1;
+    byg = 1;
+    reward = C.gamma_pow[depth];
+  } else if (m[2]) {
+    done = 1;
+  } else if (depth >= a.cap) {
+    done = 1;
+  }
+  a.env_done[e] = done;
+  a.env_bygrasp[e] = byg;
+  a.env_reward[e] = reward;
+  const int n = C.n;
+  const double* src = a.node_poses + static_cast<size_t>(node) * n * 3;
+  double* dst = a.env_poses + static_cast<size_t>(e) * n * 3;
+  for (int i = 0; i < 3 * n; ++i) dst[i] = src[i];
 }
 
 }  // namespace ppg

@@ -166,29 +166,40 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
   }
 }
 
-// RolloutCursor::step (mcts.cpp:142-171), one warp per active environment.
+// RolloutCursor::step (mcts.cpp:142-171) of env e by the calling warp:
+// sample + pick + resolve + graspable, state in HBM (env_*), the warp's
+// shared blocks `blk` / `valid` / the polygon caches as scratch.
 template <int NW, bool kPoly>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(const __grid_constant__ SimConst C,
-                                                                            LockArgs a) {
-  PPG_POLY_SMEM
-  lock_dyn(a);
-  if (a.round_mode && *a.round_mode != 0) return;  // adaptive: a hybrid round
-  __shared__ double blk[kWarpsPerBlock][160];
-  __shared__ unsigned valid[kWarpsPerBlock][32];
-  __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
-  build_pairs(pij, C.n);
-  const int wib = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kWarpsPerBlock + wib;
-  if (gw >= *a.n_active) return;
-  const int e = a.active[gw];
+PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, double* blk, unsigned* valid,
+                              const uint16_t* pij, const WarpPoly& G) {
   const int n = C.n, l = threadIdx.x & 31;
-  WarpEnv W(blk[wib], n, l);
+  WarpEnv W(blk, n, l);
   const ShapeView S = a.S.view(0);
   double* env = a.env_poses + static_cast<size_t>(e) * n * 3;
-  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
   const PolyShape O = warp_load_any<kPoly>(W, G, env, S);
   if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
-  const int count = warp_sample_mask(W, S, C, valid[wib]);
+  unsigned long long t_start = 0;
+  if (a.step_trace && l == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  struct TraceGuard {  // writes the record on every exit path
+    const LockArgs& a;
+    int e, l;
+    unsigned long long t0;
+    __device__ ~TraceGuard() {
+      if (!a.step_trace || l != 0) return;
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      const unsigned long long k = atomicAdd(a.step_trace, 1ull);
+      if (k < a.step_trace[1]) {
+        unsigned long long* r = a.step_trace + 2 + 4 * k;
+        r[0] = static_cast<unsigned long long>(a.env_lo + e) | static_cast<unsigned long long>(a.counters[1]) << 32;
+        r[1] = t0;
+        r[2] = t1;
+        r[3] = static_cast<unsigned long long>(a.env_done[e]) | static_cast<unsigned long long>(a.env_bygrasp[e]) << 1 |
+               static_cast<unsigned long long>(a.env_node[e]) << 8 | (a.iteration & 0xffffffull) << 40;
+      }
+    }
+  } trace_guard{a, e, l, t_start};
+  const int count = warp_sample_mask(W, S, C, valid);
   if (count == 0) {  // no legal push: reward 0 (mcts.cpp:146-150)
     if (l == 0) {
       a.env_done[e] = 1;
@@ -202,8 +213,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(con
   if (l == 0) a.mt_idx[e] = idx;
   // k-th valid candidate in (object, angle) order
   int w = 0, seen = 0;
-  while (seen + __popc(valid[wib][w]) <= static_cast<int>(k)) seen += __popc(valid[wib][w++]);
-  unsigned bits = valid[wib][w];
+  while (seen + __popc(valid[w]) <= static_cast<int>(k)) seen += __popc(valid[w++]);
+  unsigned bits = valid[w];
   for (int drop = static_cast<int>(k) - seen; drop > 0; --drop) bits &= bits - 1;
   const int c = 32 * w + __ffs(bits) - 1;
   V2 s, t;
@@ -232,6 +243,255 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(con
     }
   }
   warp_store(W, env);
+}
+
+// RolloutCursor::step (mcts.cpp:142-171), one warp per active environment.
+template <int NW, bool kPoly>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_step_warp_kernel(const __grid_constant__ SimConst C,
+                                                                            LockArgs a) {
+  PPG_POLY_SMEM
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode != 0) return;  // adaptive: a hybrid round
+  __shared__ double blk[kWarpsPerBlock][160];
+  __shared__ unsigned valid[kWarpsPerBlock][32];
+  __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
+  build_pairs(pij, C.n);
+  const int wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  if (gw >= *a.n_active) return;
+  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  warp_rollout_step<NW, kPoly>(C, a, a.active[gw], blk[wib], valid[wib], pij, G);
+}
+
+// ---------------------------------------------------------------------------
+// Asynchronous lockstep (the latency-bound rounds of lockstep_simulate,
+// pmbs.cpp:188-203): the reference's rounds are a barrier — every active env
+// steps once, then the sequential harvest — so a round costs its SLOWEST
+// env-step.  But an env's trajectory depends on the others only through the
+// harvest of the round in which it finished by grasp (its re-purposing
+// target, argmax of W at that round).  So envs run their steps back to back,
+// each tagged with its round; a harvester warp performs the harvest of round
+// r as soon as every env has finished round r, with W(r) accumulated by the
+// steps of round r themselves (W[node] += cap - pushes of each env still
+// running after its step), and an env finished by grasp waits only for the
+// harvest of ITS round.  Every env sees exactly the steps, RNG draws and
+// re-purposing decisions of the lockstep run, so results are bit-identical;
+// the critical path becomes max over envs of their own chains instead of the
+// sum over rounds of the slowest step.
+//
+// Ownership: env e is stepped only by worker warp (e mod n_workers), which
+// is the only writer of its state (the harvester publishes a re-purposing
+// decision in env_state and the owner applies it), so no env data crosses
+// SMs except through the harvester's L2 reads of finished envs.  The ring of
+// kAsyncK rounds bounds how far envs run ahead.  All warps must be resident
+// (cooperative launch, grid <= occupancy); every wait is bounded by
+// globaltimer (a stuck protocol sets the error word and exits).
+
+PPG_DI int ld_volatile(const int32_t* p) { return *reinterpret_cast<const volatile int32_t*>(p); }
+PPG_DI unsigned long long now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+constexpr unsigned long long kAsyncStallNs = 20ull * 1000 * 1000 * 1000;  // 20 s without progress: error
+
+// Ring views
+PPG_DI int32_t* ring_ctr(const LockArgs& a, int r) { return a.a_ctr + 4 * (r % kAsyncK); }
+
+__global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode != 0) return;  // adaptive: a hybrid round
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int G = gridDim.x * blockDim.x;
+  for (int e = tid; e < a.used; e += G) {
+    a.env_round[e] = 0;
+    a.env_state[e] = a.env_done[e] ? 2 : 0;  // the lockstep harvest just harvested every done env
+    if (a.env_done[e]) atomicAdd(&a.a_ctl[2], 1);
+  }
+  for (int i = tid; i < kAsyncK * a.n_nodes; i += G) a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
+  if (tid < 4 * kAsyncK) a.a_ctr[tid] = 0;
+}
+
+template <int NW, bool kPoly>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(const __grid_constant__ SimConst C,
+                                                                        LockArgs a) {
+  PPG_POLY_SMEM
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode != 0) return;  // adaptive: a hybrid round
+  __shared__ double blk[kWarpsPerBlock][160];
+  __shared__ unsigned valid[kWarpsPerBlock][32];
+  __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
+  build_pairs(pij, C.n);
+  const int wib = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  const int used = a.used;
+  int32_t* ctl = a.a_ctl;
+  if (gw == 0) {
+    // ---- harvester: harvest_and_repurpose (pmbs.cpp:165-187) of rounds 1, 2, ... in order
+    int gone = ld_volatile(&ctl[2]);  // envs that will not step again (done, not re-purposed)
+    if (gone >= used) {
+      if (l == 0) atomicExch(&ctl[1], 1);
+      return;
+    }
+    for (int r = 1;; ++r) {
+      int32_t* rc = ring_ctr(a, r);
+      gone += ld_volatile(&rc[1]);  // final: set by round r-1's steps and harvest
+      const int need = used - gone;
+      unsigned long long t0 = now_ns();
+      while (ld_volatile(&rc[0]) < need) {
+        if (now_ns() - t0 > kAsyncStallNs) {
+          if (l == 0) {
+            atomicExch(&ctl[3], 1);
+            atomicExch(&ctl[1], 1);
+          }
+          return;
+        }
+        __nanosleep(64);
+      }
+      __threadfence();
+      // W(r): remaining work per node after round r (pmbs.cpp:157-163); best = argmax, strict >, W > 0, lowest
+      const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
+      int bw = 0, bi = -1;
+      for (int i = l; i < a.n_nodes; i += 32) {
+        const int w = ld_volatile(&W[i]);
+        if (w > bw) {
+          bw = w;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const int ow = __shfl_xor_sync(kFull, bw, off);
+        const int oi = __shfl_xor_sync(kFull, bi, off);
+        if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
+          bw = ow;
+          bi = oi;
+        }
+      }
+      const int best = a.leaf_parallel ? bi : -1;
+      // the envs that finished in round r: reward max (order-free); by-grasp
+      // envs (state 1) are re-purposed to best, or retire when there is none
+      const int nd = ld_volatile(&rc[2]);
+      const int32_t* dl = a.a_dl + static_cast<size_t>(r % kAsyncK) * a.E;
+      int rep = 0, retired = 0;
+      for (int k = l; k < nd; k += 32) {
+        const int e = ld_volatile(&dl[k]);
+        const int node = ld_volatile(&a.env_node[e]);
+        const double rw = __ldcg(&a.env_reward[e]);
+        atomicMax(&a.rew[node], static_cast<unsigned long long>(__double_as_longlong(rw)));
+        a.env_harvested[e] = 1;
+        if (ld_volatile(&a.env_state[e]) == 1) {
+          __threadfence();
+          if (best >= 0) {
+            atomicExch(&a.env_state[e], 3 + best);  // the owner applies it (cursor_init at best)
+            ++rep;
+          } else {
+            atomicExch(&a.env_state[e], 2);
+            ++retired;
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        rep += __shfl_xor_sync(kFull, rep, off);
+        retired += __shfl_xor_sync(kFull, retired, off);
+      }
+      if (l == 0) {
+        a.counters[2] += rep;
+        if (retired) atomicAdd(&ring_ctr(a, r + 1)[1], retired);  // gone from round r + 1
+      }
+      __syncwarp();
+      __threadfence();
+      // free the slot of round r for round r + K
+      int32_t* Wm = a.a_W + (r % kAsyncK) * a.a_wcap;
+      for (int i = l; i < a.n_nodes; i += 32) Wm[i] = 0;
+      __syncwarp();
+      if (l == 0) {
+        rc[0] = 0;
+        rc[1] = 0;
+        rc[2] = 0;
+        __threadfence();
+        atomicExch(&ctl[0], r);  // harvest of round r published
+      }
+      __syncwarp();
+      // finished when nothing will step in round r + 1; otherwise round r + 1
+      // runs (the lockstep harvest counts a round when envs remain active)
+      const int gone_next = gone + ld_volatile(&ring_ctr(a, r + 1)[1]);
+      if (gone_next >= used) {
+        if (l == 0) atomicExch(&ctl[1], 1);
+        return;
+      }
+      if (l == 0) a.counters[1] += 1;
+    }
+  }
+  // ---- workers: warp w owns envs w, w + n_workers, ... (the only writer of their state)
+  const int nwk = gridDim.x * kWarpsPerBlock - 1;
+  const int wk = gw - 1;
+  if (wk >= used) return;  // owns no env
+  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  unsigned long long t_idle = now_ns();
+  for (;;) {
+    int fin = 0, H = 0;
+    if (l == 0) {
+      fin = ld_volatile(&ctl[1]);
+      H = ld_volatile(&ctl[0]);
+    }
+    fin = __shfl_sync(kFull, fin, 0);
+    H = __shfl_sync(kFull, H, 0);
+    if (fin) return;
+    bool progress = false;
+    for (int e = wk; e < used; e += nwk) {
+      int st = l == 0 ? ld_volatile(&a.env_state[e]) : 0;
+      st = __shfl_sync(kFull, st, 0);
+      if (st >= 3) {  // re-purposed at the harvest of its round: RolloutCursor ctor at the new node
+        __threadfence();
+        if (l == 0) {
+          cursor_init(C, a, e, st - 3);
+          a.env_harvested[e] = 0;
+        }
+        __syncwarp();
+        if (l == 0) a.env_state[e] = 0;
+        st = 0;
+        progress = true;
+      }
+      if (st != 0) continue;
+      const int r = a.env_round[e] + 1;
+      if (r > H + kAsyncK - 1) continue;  // ring bound: at most K rounds ahead of the harvest
+      warp_rollout_step<NW, kPoly>(C, a, e, blk[wib], valid[wib], pij, G);
+      __syncwarp();
+      if (l == 0) {
+        a.env_round[e] = r;
+        int32_t* rc = ring_ctr(a, r);
+        if (!a.env_done[e]) {
+          atomicAdd(&a.a_W[(r % kAsyncK) * a.a_wcap + a.env_node[e]], a.cap - a.env_pushes[e]);
+        } else {
+          a.a_dl[static_cast<size_t>(r % kAsyncK) * a.E + atomicAdd(&rc[2], 1)] = e;
+          if (a.leaf_parallel && a.env_bygrasp[e]) {
+            a.env_state[e] = 1;  // awaits the harvest of round r
+          } else {
+            a.env_state[e] = 2;
+            atomicAdd(&ring_ctr(a, r + 1)[1], 1);  // does not step in round r + 1
+          }
+        }
+        __threadfence();
+        atomicAdd(&rc[0], 1);
+      }
+      __syncwarp();
+      progress = true;
+    }
+    if (progress) {
+      t_idle = now_ns();
+    } else {
+      if (now_ns() - t_idle > kAsyncStallNs) {
+        if (l == 0) {
+          atomicExch(&ctl[3], 2);
+          atomicExch(&ctl[1], 1);
+        }
+        return;
+      }
+      __nanosleep(256);
+    }
+  }
 }
 
 // Hybrid lockstep round for large disc batches: the sampler + pick and the
@@ -326,7 +586,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_post_warp_kernel(con
 #define PPG_WARP_INST(NW, P)                                                                            \
   template __global__ void resolve_warp_kernel<NW, P>(const __grid_constant__ SimConst, ResolveArgs);  \
   template __global__ void expand_warp_kernel<NW, P>(const __grid_constant__ SimConst, ExpandArgs);    \
-  template __global__ void lock_step_warp_kernel<NW, P>(const __grid_constant__ SimConst, LockArgs);
+  template __global__ void lock_step_warp_kernel<NW, P>(const __grid_constant__ SimConst, LockArgs);        \
+  template __global__ void lock_async_kernel<NW, P>(const __grid_constant__ SimConst, LockArgs);
 PPG_WARP_INST(1, false)
 PPG_WARP_INST(2, false)
 PPG_WARP_INST(4, false)
