@@ -1254,6 +1254,9 @@ int run_pmbs_sharded(ppg_ctx* ctx, const double* root_poses, double* action_out,
     S.la.shard_r = r0 + k;
     S.la.shard_g = G;
     S.la.go = m[k]->l_go.as<int32_t>();
+    // the apply kernel runs outside the graphs: it must carry the adaptive
+    // round-mode flag the captured round graph reads (dt_views cleared it)
+    dt_mode(m[k], S);
   };
   for (int k = 0; k < M; ++k) {
     ppg_ctx* c = m[k];
