@@ -300,7 +300,8 @@ void ppg_destroy(ppg_ctx* ctx) {
   }
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
   ctx->l_go.release();
-  for (DevBuf* b : {&ctx->l_around, &ctx->l_astate, &ctx->l_aW, &ctx->l_actr, &ctx->l_adl, &ctx->l_actl, &ctx->trace_buf})
+  for (DevBuf* b : {&ctx->l_around, &ctx->l_astate, &ctx->l_aW, &ctx->l_actr, &ctx->l_adl, &ctx->l_actl, &ctx->trace_buf,
+                    &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract})
     b->release();
   if (ctx->h_go) cudaFreeHost(ctx->h_go);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -478,7 +479,7 @@ bool async_enabled(const ppg_ctx* ctx) {
 }
 
 template <int NW, bool kPoly>
-static int launch_async_t(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st) {
+static int launch_async_t(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st, bool cont) {
   static int bps[2] = {-1, -1};
   const void* fn = reinterpret_cast<const void*>(&lock_async_kernel<NW, kPoly>);
   int& b = bps[kPoly ? 1 : 0];
@@ -489,8 +490,10 @@ static int launch_async_t(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, in
   }
   const int want = (work + 1 + kWarpsPerBlock - 1) / kWarpsPerBlock;  // + the harvester warp
   const int grid = want < b * ctx->num_sms ? want : b * ctx->num_sms;
-  lock_async_init_kernel<<<(work + 255) / 256 + 1, 256, 0, st>>>(C, a);
-  CK(cudaGetLastError());
+  if (!cont) {
+    lock_async_init_kernel<<<(work + 255) / 256 + 1, 256, 0, st>>>(C, a);
+    CK(cudaGetLastError());
+  }
   // every warp must be resident (workers and the harvester wait on each other)
   SimConst c_arg = C;
   LockArgs a_arg = a;
@@ -499,18 +502,54 @@ static int launch_async_t(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, in
   return PPG_SUCCESS;
 }
 
-int launch_async(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st) {
-  CK(cudaMemsetAsync(a.a_ctl, 0, 32, st));
+bool wave_enabled(const ppg_ctx* ctx) {
+  if (ctx->wave_mode < 0) {
+    ppg_ctx* c = const_cast<ppg_ctx*>(ctx);
+    const char* v = std::getenv("PPG_WAVE");
+    c->wave_mode = (v && v[0] == '0') ? 0 : 1;
+    const char* b = std::getenv("PPG_WAVE_BUDGET");
+    if (b && std::atoi(b) > 0) c->wave_budget = std::atoi(b);
+    const char* w = std::getenv("PPG_WAVE_SWITCH");
+    if (w) c->wave_switch = std::atoi(w);
+  }
+  return ctx->wave_mode == 1 && async_enabled(ctx);
+}
+
+// One wave (see warp_env.cu): harvest of the complete rounds + lists, sample,
+// budgeted lane physics (in place, resumable), post.  `work` sizes the grids.
+int launch_wave(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const ResolveArgs& ra_in, int work,
+                cudaStream_t st) {
+  const int gw = (work + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  wave_harvest_kernel<<<1, 1024, 0, st>>>(C, a);
+  CK(cudaGetLastError());
+  wave_sample_kernel<<<gw, kWarpsPerBlock * 32, 0, st>>>(C, a);
+  CK(cudaGetLastError());
+  ResolveArgs ra = ra_in;
+  ra.resume_si = a.resume_si;
+  ra.resume_active = a.resume_active;
+  ra.fin_list = a.fin_list;
+  ra.fin_count = a.fin_count;
+  ra.budget = ctx->wave_budget;
+  ra.budget_dev = a.a_ctl + 8;  // set by the harvest: the budget, or unbounded in the hand-over wave
+  const int rc = launch_disc(ctx, C, ra, ctx->scene.n, work, st, true, 0, true);
+  if (rc != PPG_SUCCESS) return rc;
+  wave_post_kernel<<<gw, kWarpsPerBlock * 32, 0, st>>>(C, a);
+  CK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
+// cont: continue from a wave-round state (no re-initialisation)
+int launch_async(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st, bool cont) {
   const int n = ctx->scene.n, w = warp_words(n);
   if (!ctx->scene_all_discs) {
-    if (w == 1) return launch_async_t<1, true>(ctx, C, a, work, st);
-    if (w == 2) return launch_async_t<2, true>(ctx, C, a, work, st);
-    return launch_async_t<4, true>(ctx, C, a, work, st);
+    if (w == 1) return launch_async_t<1, true>(ctx, C, a, work, st, cont);
+    if (w == 2) return launch_async_t<2, true>(ctx, C, a, work, st, cont);
+    return launch_async_t<4, true>(ctx, C, a, work, st, cont);
   }
-  if (w == 1) return launch_async_t<1, false>(ctx, C, a, work, st);
-  if (w == 2) return launch_async_t<2, false>(ctx, C, a, work, st);
-  if (w == 4) return launch_async_t<4, false>(ctx, C, a, work, st);
-  return launch_async_t<8, false>(ctx, C, a, work, st);
+  if (w == 1) return launch_async_t<1, false>(ctx, C, a, work, st, cont);
+  if (w == 2) return launch_async_t<2, false>(ctx, C, a, work, st, cont);
+  if (w == 4) return launch_async_t<4, false>(ctx, C, a, work, st, cont);
+  return launch_async_t<8, false>(ctx, C, a, work, st, cont);
 }
 
 // Polygon batches (one warp per env): past one resident wave the grid is
@@ -1083,6 +1122,10 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   CK(ctx->l_actr.ensure(static_cast<size_t>(kAsyncK) * 16));
   CK(ctx->l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   CK(ctx->l_actl.ensure(64));
+  CK(cudaMemsetAsync(ctx->l_actl.p, 0, 64, st));
+  CK(ctx->l_fin.ensure(static_cast<size_t>(E) * 4 + 16));
+  CK(ctx->l_rsi.ensure(static_cast<size_t>(E) * 4));
+  CK(ctx->l_ract.ensure(static_cast<size_t>(E) * 4));
   CK(cudaMemcpyAsync(ctx->l_npose.p, node_poses, static_cast<size_t>(n_nodes) * n * 3 * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ctx->l_nmeta.p, node_meta, static_cast<size_t>(n_nodes) * 3 * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(ctx->l_counters.p, 0, 32, st));
@@ -1135,6 +1178,10 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   a.a_dl = ctx->l_adl.as<int32_t>();
   a.a_ctl = ctx->l_actl.as<int32_t>();
   a.a_wcap = n_nodes;
+  a.fin_count = ctx->l_fin.as<int32_t>();
+  a.fin_list = ctx->l_fin.as<int32_t>() + 4;
+  a.resume_si = ctx->l_rsi.as<int32_t>();
+  a.resume_active = ctx->l_ract.as<uint32_t>();
   ctx->lra = ResolveArgs{ctx->scene, a.env_poses, a.env_push, a.env_poses, a.env_status, nullptr, nullptr, 0};
   ctx->lra.idx = a.stepping;
   ctx->lra.E_dev = a.n_stepping;
@@ -1232,9 +1279,54 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
     const int act = *ctx->h_nactive;
     if (act == 0) break;
     if (trace) cudaEventRecord(t0, st);
+    if (round == 0 && wave_enabled(ctx) && round_mode(ctx, ctx->scene.n, act) == RoundMode::kHybrid) {
+      // large disc batch: wave rounds while the batch is wide, then the
+      // asynchronous kernel for the tail (warp_env.cu)
+      int32_t* ctl = ctx->la.a_ctl;
+      const int32_t one = 1;
+      CK(cudaMemcpyAsync(ctl + 6, &one, 4, cudaMemcpyHostToDevice, st));  // round_mode word: waves
+      LockArgs wa = ctx->la;
+      wa.round_mode = ctl + 6;
+      wa.go = ctl + 7;
+      wa.wave_switch = ctx->wave_switch;
+      wa.wave_budget = ctx->wave_budget;
+      if (trace) cudaEventRecord(t0, st);
+      for (int wave = 0;; ++wave) {
+        rc = launch_wave(ctx, ctx->lc, wa, ctx->lra, used, st);
+        if (rc != PPG_SUCCESS) return rc;
+        int32_t hctl[16];
+        CK(cudaMemcpyAsync(hctl, ctl, 64, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (trace) {
+          cudaEventRecord(t1, st);
+          cudaEventSynchronize(t1);
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, t0, t1);
+          std::fprintf(stderr, "wave %d H %d gone %d switch %d ms %.4f\n", wave, hctl[0], hctl[2], hctl[5], ms);
+          cudaEventRecord(t0, st);
+        }
+        if (hctl[7] == 0) break;  // every env done and harvested
+        if (hctl[5] == 2) {       // the hand-over wave ran: the asynchronous kernel finishes the call
+          rc = launch_async(ctx, ctx->lc, wa, used, st, true);
+          if (rc != PPG_SUCCESS) return rc;
+          CK(cudaMemcpyAsync(hctl, ctl, 16, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          if (hctl[3] != 0) {
+            ctx->err = "asynchronous lockstep stalled (protocol error)";
+            return PPG_ECUDA;
+          }
+          break;
+        }
+        if (wave > kLockRoundLimit) {
+          ctx->err = "wave rounds did not terminate";
+          return PPG_EINVAL;
+        }
+      }
+      break;
+    }
     const bool go_async = async_enabled(ctx) && round_mode(ctx, ctx->scene.n, act) == RoundMode::kWarp;
     if (go_async) {  // every remaining round, barrier-free (warp_env.cu lock_async_kernel)
-      rc = launch_async(ctx, ctx->lc, ctx->la, used, st);
+      rc = launch_async(ctx, ctx->lc, ctx->la, used, st, false);
       if (rc != PPG_SUCCESS) return rc;
       int32_t ctl[4];
       CK(cudaMemcpyAsync(ctl, ctx->la.a_ctl, 16, cudaMemcpyDeviceToHost, st));

@@ -63,6 +63,9 @@ constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 
   } while (0)
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void wave_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void wave_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void wave_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 template <int NW, bool kPoly>
 __global__ void lock_async_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_sample_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
@@ -193,6 +196,10 @@ struct ppg_ctx {
   ppg::DevBuf trace_buf;                  // PPG_STEP_TRACE: per-step records (experiments)
   ppg::DevBuf l_around, l_astate, l_aW, l_actr, l_adl, l_actl;  // asynchronous lockstep state
   int async_mode = -1;                    // -1 not read, 0 off (PPG_ASYNC=0), 1 on
+  int wave_mode = -1;                     // -1 not read, 0 off (PPG_WAVE=0), 1 on
+  int wave_budget = 256;                  // projection iterations per env per wave (PPG_WAVE_BUDGET)
+  int wave_switch = 8192;                 // in-flight env-steps below which waves hand over to async (PPG_WAVE_SWITCH)
+  ppg::DevBuf l_fin, l_rsi, l_ract;       // wave rounds: post list, resumable physics progress
   int32_t* h_go = nullptr;                // pinned copy
 };
 
@@ -213,7 +220,11 @@ int lock_round_on(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const Reso
 // round of the current lockstep call; `work` = the most envs it may own.
 // PPG_ASYNC=0 disables it (lockstep rounds everywhere).
 bool async_enabled(const ppg_ctx* ctx);
-int launch_async(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st);
+int launch_async(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st, bool cont);
+// Wave rounds (warp_env.cu wave_*_kernel): one wave = harvest, sample,
+// budgeted lane physics, post.  PPG_WAVE=0 disables them (barrier hybrid rounds).
+bool wave_enabled(const ppg_ctx* ctx);
+int launch_wave(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const ResolveArgs& ra, int work, cudaStream_t st);
 int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used,
                int used_global, int env_lo, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap);
 int lock_round(ppg_ctx* ctx, int act);

@@ -69,7 +69,7 @@ struct DTScal {
   int err[4];                    // first invariant violation seen on the device (debug)
   int round_mode;                // adaptive lockstep rounds (LockArgs.round_mode)
   int round_guard;               // rounds of this iteration's lockstep (< 0: limit hit)
-  int async_ctl[8];              // asynchronous lockstep control (LockArgs.a_ctl; [3] != 0: stalled)
+  int async_ctl[16];             // asynchronous / wave lockstep control (LockArgs.a_ctl; [3] != 0: stalled)
 };
 
 struct DTree {
@@ -488,7 +488,8 @@ struct DTreeState {
   DevBuf sel_node, sel_act, gp, ga, cp, st, gr, nu, un, meta, logtab, sc;
   // lockstep state
   DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx, l_W, l_rew, l_active,
-      l_nactive, l_counters, l_push, l_status, l_stepping, l_around, l_astate, l_aW, l_actr, l_adl;
+      l_nactive, l_counters, l_push, l_status, l_stepping, l_around, l_astate, l_aW, l_actr, l_adl, l_fin, l_rsi,
+      l_ract;
   int cap_nodes = 0;
   long long cap_actions = 0;
   int n_envs = 0, n = 0, na = 0;
@@ -527,7 +528,7 @@ struct DTreeState {
                       &poses, &anc, &apool, &cpool, &sel_node, &sel_act, &gp, &ga, &cp, &st, &gr, &nu, &un,
                       &meta, &logtab, &sc, &l_node, &l_pushes, &l_done, &l_byg, &l_harv, &l_flag, &l_reward,
                       &l_poses, &l_mt, &l_mtidx, &l_W, &l_rew, &l_active, &l_nactive, &l_counters, &l_push,
-                      &l_status, &l_stepping, &l_around, &l_astate, &l_aW, &l_actr, &l_adl};
+                      &l_status, &l_stepping, &l_around, &l_astate, &l_aW, &l_actr, &l_adl, &l_fin, &l_rsi, &l_ract};
     for (DevBuf* b : bufs) b->release();
   }
 };
@@ -668,6 +669,10 @@ int dt_batch(ppg_ctx* ctx, DTreeState& S) {
   DCK(S.l_aW.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_actr.ensure(static_cast<size_t>(kAsyncK) * 16));
   DCK(S.l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
+  DCK(S.l_fin.ensure(static_cast<size_t>(E) * 4 + 16));
+  DCK(S.l_rsi.ensure(static_cast<size_t>(E) * 4));
+  DCK(S.l_ract.ensure(static_cast<size_t>(E) * 4));
+  wave_enabled(ctx);  // reads PPG_WAVE / PPG_WAVE_BUDGET / PPG_WAVE_SWITCH
   DCK(ctx->b_counter.ensure(16));  // launch_disc's work counter (no allocation during capture)
   return PPG_SUCCESS;
 }
@@ -751,6 +756,12 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
   a.a_dl = S.l_adl.as<int32_t>();
   a.a_ctl = t.sc->async_ctl;
   a.a_wcap = S.n_envs;
+  a.fin_count = S.l_fin.as<int32_t>();
+  a.fin_list = S.l_fin.as<int32_t>() + 4;
+  a.resume_si = S.l_rsi.as<int32_t>();
+  a.resume_active = S.l_ract.as<uint32_t>();
+  a.wave_switch = ctx->wave_switch;
+  a.wave_budget = ctx->wave_budget;
   a.round_mode = nullptr;  // set by dt_mode for adaptive graphs
   a.round_guard = &t.sc->round_guard;
   a.hybrid_min = ctx->hybrid_min_envs;
@@ -776,11 +787,15 @@ RoundMode dt_mode(ppg_ctx* ctx, DTreeState& S) {
 // of the call (its kernels return at once when the harvest picked hybrid).
 int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, RoundMode m) {
   if (async_enabled(ctx) && (m == RoundMode::kWarp || m == RoundMode::kAdaptive)) {
-    if (m == RoundMode::kAdaptive) {  // the hybrid half (returns at once in warp rounds)
-      const int rc = lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, RoundMode::kHybrid, st);
+    if (m == RoundMode::kAdaptive) {
+      // the large-batch half: wave rounds (harvest, sample, budgeted physics,
+      // post) or barrier hybrid rounds; their kernels return at once when the
+      // call runs asynchronously (round_mode 0)
+      const int rc = wave_enabled(ctx) ? launch_wave(ctx, S.C, S.la, S.lra, S.n_envs, st)
+                                       : lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, RoundMode::kHybrid, st);
       if (rc != PPG_SUCCESS) return rc;
     }
-    return launch_async(ctx, S.C, S.la, S.n_envs, st);
+    return launch_async(ctx, S.C, S.la, S.n_envs, st, false);
   }
   return lock_round_on(ctx, S.C, S.la, S.lra, S.n_envs, m, st);
 }

@@ -196,6 +196,8 @@ __global__ void lock_init_kernel(const __grid_constant__ SimConst C, LockArgs a)
   // Even split of the GLOBAL batch, remainder to earlier nodes
   // (pmbs.cpp:138-149); the RNG key is the global env index (pmbs.cpp:211-213),
   // so a shard reproduces exactly its part of the unsharded batch.
+  if (e == 0 && a.a_ctl)
+    for (int k = 0; k < 16; ++k) a.a_ctl[k] = 0;  // asynchronous / wave protocol state of this call
   const int ge = a.env_lo + e;
   const int used = a.used_global > 0 ? a.used_global : a.used;
   const int base = used / a.n_nodes, rem = used % a.n_nodes;
@@ -429,6 +431,7 @@ PPG_DI void harvest_apply(const SimConst& C, const LockArgs& a, bool sharded) {
 
 __global__ void __launch_bounds__(1024) lock_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
   lock_dyn(a);
+  if (a.a_ctl && a.a_ctl[4] == 1) return;  // this lockstep call runs in waves (their harvest is wave_harvest_kernel)
   harvest_local(a);
   harvest_apply(C, a, false);
 }

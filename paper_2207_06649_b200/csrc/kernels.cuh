@@ -43,6 +43,17 @@ struct ResolveArgs {
   // poses_out / status / residual are mapped pinned HOST memory: each
   // finished env's poses leave in one warp-coalesced write (no copy-back)
   bool zc_out = false;
+  // wave rounds (rollouts, resolve_disc_kernel<N, true>): an env runs at most
+  // `budget` projection iterations per launch; an unfinished one yields
+  // (positions in place, progress (step << 8 | iter, active mask) saved,
+  // status 3) and resumes in the next launch; finished envs are appended
+  // to fin_list.  resume_si[e] < 0: a fresh push.
+  int32_t* resume_si = nullptr;
+  uint32_t* resume_active = nullptr;
+  int32_t* fin_list = nullptr;
+  int32_t* fin_count = nullptr;
+  int budget = 0;
+  const int* budget_dev = nullptr;  // if set, the budget is read on the device (the graph's last wave: unbounded)
 };
 
 struct SampleArgs {
@@ -139,7 +150,8 @@ struct LockArgs {
   // round, 2 gone, 3 + node: re-purposed to node, not yet applied); a ring
   // of kAsyncK rounds: W [K][a_wcap], counters [K][4] (arrived, gone at this
   // round, done-list length, -), done lists [K][E]; control [8] (harvested
-  // round H, finished, gone so far, error, ...)
+  // round H, finished, gone so far, error, wave set up, switch to
+  // asynchronous, host round-mode word, host go word, wave budget)
   int32_t* env_round = nullptr;
   int32_t* env_state = nullptr;
   int32_t* a_W = nullptr;
@@ -147,6 +159,14 @@ struct LockArgs {
   int32_t* a_dl = nullptr;
   int32_t* a_ctl = nullptr;
   int a_wcap = 0;
+  // wave rounds (warp_env.cu wave_*_kernel): envs whose physics finished in
+  // this wave (post pending), and the resumable physics progress
+  int32_t* fin_list = nullptr;
+  int32_t* fin_count = nullptr;
+  int32_t* resume_si = nullptr;
+  uint32_t* resume_active = nullptr;
+  int wave_switch = 0;   // in-flight env-steps below which the waves hand over to the asynchronous kernel
+  int wave_budget = 0;   // projection iterations per env per wave
   // PPG_STEP_TRACE (experiments): one record per latency-mode env-step
   // {env, round, start/end globaltimer ns, flags} appended at step_trace[1 + k]
   unsigned long long* step_trace = nullptr;

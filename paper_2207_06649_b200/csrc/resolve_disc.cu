@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
   Mask<W> pact;  // pairs with both objects active
   V2 start{0.0, 0.0}, delta{0.0, 0.0};
   int step = 0, iter = 0;
+  int budget_left = 0;  // wave rounds (kFix): iterations left in this launch
   const int E = a.E_dev ? *a.E_dev : a.E;
   // First environments: an even share per block (`per` <= kDB), so a full
   // wave of blocks (the launch fills every SM equally) gives every SM the
@@ -319,6 +320,27 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
         });
         trm = static_cast<float>(tr + 0.5 * m);
         hclf = static_cast<float>(hcl - m);
+        int rsi = -1;  // wave rounds: saved progress of a yielded push
+        if constexpr (kFix) {
+          if (a.resume_si) {
+            rsi = __ldcg(a.resume_si + ee);
+            budget_left = a.budget_dev ? __ldcg(a.budget_dev) : a.budget;
+          }
+        }
+        if (kFix && rsi >= 0) {  // resume: progress saved at the yield, the precondition already passed
+          delta = (end - start) * (1.0 / C.substeps);
+          active = __ldcg(a.resume_active + ee);
+          pact.clear();
+          static_for<P>([&](auto pc) {
+            constexpr int p = decltype(pc)::value;
+            constexpr int i = pair_i(p, NMAX), j = pair_j(p, NMAX);
+            if ((active >> i & 1u) && (active >> j & 1u)) pact.w[p >> 6] |= 1ull << (p & 63);
+          });
+          step = rsi >> 8;
+          iter = rsi & 0xff;
+          have = true;
+          break;
+        }
         // collides_gripper_start (world.cpp:154-164)
         bool collide = false;
         {
@@ -330,6 +352,9 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
         }
         if (collide) {
           if (a.done) slice_done(a, e);
+          if constexpr (kFix) {
+            if (a.fin_list) a.fin_list[atomicAdd(a.fin_count, 1)] = ee;  // wave rounds: post pending
+          }
           const int next = atomicAdd(next_env, 1) + total_threads;
           // zc_out: queued for the warp's coalesced flush only while this lane
           // has a next env (it then stays in the loop, so the flush at the loop
@@ -424,6 +449,9 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
         }
       }
       if (a.done) slice_done(a, e);
+      if constexpr (kFix) {
+        if (a.fin_list) a.fin_list[atomicAdd(a.fin_count, 1)] = ee;  // wave rounds: post pending
+      }
       e = atomicAdd(next_env, 1) + total_threads;
       need_init = true;
       have = false;
@@ -626,6 +654,22 @@ __global__ void __launch_bounds__(kDB, NMAX <= 10 ? 4 : NMAX <= 16 ? 3 : 2) reso
     if (max_pen <= C.eps_pen || fixed || ++iter >= C.max_iters) {
       ++step;
       iter = 0;
+    }
+    if constexpr (kFix) {
+      if (a.resume_si && --budget_left <= 0 && step <= C.substeps) {
+        // wave rounds: yield — positions in place (discs do not rotate), progress saved
+        double* out = a.poses_out + static_cast<size_t>(ee) * n * 3;
+        for (int i = 0; i < n; ++i) {
+          out[i * 3] = xl[i * kDB];
+          out[i * 3 + 1] = yl[i * kDB];
+        }
+        a.resume_si[ee] = step << 8 | iter;
+        a.resume_active[ee] = active;
+        a.status[ee] = 3;
+        e = atomicAdd(next_env, 1) + total_threads;
+        need_init = true;
+        have = false;
+      }
     }
   }
 #undef XF

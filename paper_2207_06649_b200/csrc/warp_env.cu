@@ -317,7 +317,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
                                                                         LockArgs a) {
   PPG_POLY_SMEM
   lock_dyn(a);
-  if (a.round_mode && *a.round_mode != 0) return;  // adaptive: a hybrid round
+  int32_t* ctl = a.a_ctl;
+  // runs in the asynchronous regime, or to finish a wave-round call once its
+  // batch has shrunk (ctl[5] == 2: continues from the wave state)
+  if (a.round_mode && *a.round_mode != 0 && ctl[5] != 2) return;
   __shared__ double blk[kWarpsPerBlock][160];
   __shared__ unsigned valid[kWarpsPerBlock][32];
   __shared__ uint16_t pij[kWarpMaxN * (kWarpMaxN - 1) / 2];
@@ -325,15 +328,18 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
   const int wib = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int gw = blockIdx.x * kWarpsPerBlock + wib;
   const int used = a.used;
-  int32_t* ctl = a.a_ctl;
   if (gw == 0) {
     // ---- harvester: harvest_and_repurpose (pmbs.cpp:165-187) of rounds 1, 2, ... in order
     int gone = ld_volatile(&ctl[2]);  // envs that will not step again (done, not re-purposed)
-    if (gone >= used) {
-      if (l == 0) atomicExch(&ctl[1], 1);
+    const int r0 = ld_volatile(&ctl[0]) + 1;  // first unharvested round (1, or where the waves stopped)
+    if (gone + ld_volatile(&ring_ctr(a, r0)[1]) >= used) {
+      if (l == 0) {
+        atomicExch(&ctl[1], 1);
+        if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), 0u);
+      }
       return;
     }
-    for (int r = 1;; ++r) {
+    for (int r = r0;; ++r) {
       int32_t* rc = ring_ctr(a, r);
       gone += ld_volatile(&rc[1]);  // final: set by round r-1's steps and harvest
       const int need = used - gone;
@@ -343,6 +349,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
           if (l == 0) {
             atomicExch(&ctl[3], 1);
             atomicExch(&ctl[1], 1);
+            if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), 0u);
           }
           return;
         }
@@ -418,7 +425,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
       // runs (the lockstep harvest counts a round when envs remain active)
       const int gone_next = gone + ld_volatile(&ring_ctr(a, r + 1)[1]);
       if (gone_next >= used) {
-        if (l == 0) atomicExch(&ctl[1], 1);
+        if (l == 0) {
+          atomicExch(&ctl[1], 1);
+          // the iteration graph's WHILE loop ends here (the wave path skips the lockstep harvest)
+          if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), 0u);
+        }
         return;
       }
       if (l == 0) a.counters[1] += 1;
@@ -491,6 +502,326 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
       }
       __nanosleep(256);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Wave rounds: the asynchronous lockstep for LARGE disc batches, where the
+// physics must stay on the lane-per-env kernel (its throughput) and
+// sample / graspable stay one warp per env.  Same protocol as
+// lock_async_kernel (round-tagged steps, W(r) ring, in-order harvests), but
+// driven by a loop of four ordinary launches ("waves") instead of one
+// persistent kernel — no launch waits on another:
+//   wave_harvest_kernel  harvests every complete round, then lists the envs
+//                        that may start a step (READY, within the ring) and
+//                        the yielded physics to resume;
+//   wave_sample_kernel   sample + pick for the listed READY envs (one warp each);
+//   resolve_disc_kernel<N, true> with a per-launch iteration budget: an env
+//                        that exceeds it yields (progress saved) and resumes
+//                        in the next wave, so one jammed push no longer holds
+//                        up the 64K envs of a barrier round;
+//   wave_post_kernel     graspable + reward + the round's bookkeeping.
+// Env states: 0 READY, 1 AWAIT (finished by grasp, awaits the harvest of
+// its round), 2 GONE, -1 PHYS (physics pending / yielded).
+
+enum : int { kReady = 0, kAwait = 1, kGone = 2, kPhys = -1 };  // (>= 3: lock_async_kernel re-purposing decisions)
+
+// The end of env e's step of round r (lane 0): W(r) for an env still running,
+// else the round's done list; arrival last (after a fence).
+PPG_DI void wave_step_done(const LockArgs& a, int e, int r) {
+  int32_t* rc = ring_ctr(a, r);
+  if (!a.env_done[e]) {
+    atomicAdd(&a.a_W[(r % kAsyncK) * a.a_wcap + a.env_node[e]], a.cap - a.env_pushes[e]);
+    a.env_state[e] = kReady;
+  } else {
+    a.a_dl[static_cast<size_t>(r % kAsyncK) * a.E + atomicAdd(&rc[2], 1)] = e;
+    if (a.leaf_parallel && a.env_bygrasp[e]) {
+      a.env_state[e] = kAwait;
+    } else {
+      a.env_state[e] = kGone;
+      atomicAdd(&ring_ctr(a, r + 1)[1], 1);
+    }
+  }
+  a.env_round[e] = r;
+  __threadfence();
+  atomicAdd(&rc[0], 1);
+}
+
+// Harvest of every complete round (one block), then the wave's lists.
+// a_ctl: [0] harvested round H, [2] envs gone through round H, [4] set up.
+__global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode == 0) return;  // this lockstep call runs asynchronously
+  const int tid = threadIdx.x, B = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int used = a.used;
+  int32_t* ctl = a.a_ctl;
+  __shared__ int s_H, s_G, s_best, s_ns, s_np;
+  __shared__ int s_bw[32], s_bi[32], s_rep[32], s_ret[32];
+  if (ctl[4] == 0) {  // first wave of the call: every env READY or GONE at round 0
+    if (tid == 0) s_G = 0;
+    __syncthreads();
+    int g = 0;
+    for (int e = tid; e < used; e += B) {
+      a.env_round[e] = 0;
+      a.env_state[e] = a.env_done[e] ? kGone : kReady;
+      a.resume_si[e] = -1;
+      g += a.env_done[e] ? 1 : 0;
+    }
+    for (int i = tid; i < kAsyncK * a.n_nodes; i += B) a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
+    if (tid < 4 * kAsyncK) a.a_ctr[tid] = 0;
+    atomicAdd(&s_G, g);
+    __syncthreads();
+    if (tid == 0) {
+      ctl[0] = 0;
+      ctl[2] = s_G;
+      ctl[4] = 1;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    s_H = ctl[0];
+    s_G = ctl[2];
+  }
+  __syncthreads();
+  for (;;) {  // harvest complete rounds in order
+    const int r = s_H + 1;
+    int32_t* rc = ring_ctr(a, r);
+    const int gone_r = s_G + rc[1];
+    if (gone_r >= used || rc[0] < used - gone_r) break;
+    // W(r) argmax (strict >, W > 0, lowest node)
+    const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
+    int bw = 0, bi = -1;
+    for (int i = tid; i < a.n_nodes; i += B) {
+      const int w = W[i];
+      if (w > bw) {
+        bw = w;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const int ow = __shfl_xor_sync(kFull, bw, off);
+      const int oi = __shfl_xor_sync(kFull, bi, off);
+      if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
+        bw = ow;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      s_bw[wid] = bw;
+      s_bi[wid] = bi;
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int nw = B >> 5;
+      bw = tid < nw ? s_bw[tid] : 0;
+      bi = tid < nw ? s_bi[tid] : -1;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const int ow = __shfl_xor_sync(kFull, bw, off);
+        const int oi = __shfl_xor_sync(kFull, bi, off);
+        if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
+          bw = ow;
+          bi = oi;
+        }
+      }
+      if (tid == 0) s_best = a.leaf_parallel ? bi : -1;
+    }
+    __syncthreads();
+    const int best = s_best;
+    const int nd = rc[2];
+    const int32_t* dl = a.a_dl + static_cast<size_t>(r % kAsyncK) * a.E;
+    int rep = 0, ret = 0;
+    for (int k = tid; k < nd; k += B) {
+      const int e = dl[k];
+      atomicMax(&a.rew[a.env_node[e]], static_cast<unsigned long long>(__double_as_longlong(a.env_reward[e])));
+      a.env_harvested[e] = 1;
+      if (a.env_state[e] == kAwait) {
+        if (best >= 0) {  // re-purpose (pmbs.cpp:171-185): a new cursor at best, continues at round r + 1
+          cursor_init(C, a, e, best);
+          a.env_harvested[e] = 0;
+          a.env_state[e] = kReady;
+          ++rep;
+        } else {
+          a.env_state[e] = kGone;
+          ++ret;
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      rep += __shfl_xor_sync(kFull, rep, off);
+      ret += __shfl_xor_sync(kFull, ret, off);
+    }
+    if (lane == 0) {
+      s_rep[wid] = rep;
+      s_ret[wid] = ret;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int tr = 0, tt = 0;
+      for (int w = 0; w < (B >> 5); ++w) {
+        tr += s_rep[w];
+        tt += s_ret[w];
+      }
+      a.counters[2] += tr;
+      ring_ctr(a, r + 1)[1] += tt;
+    }
+    // free the slot of round r
+    int32_t* Wm = a.a_W + (r % kAsyncK) * a.a_wcap;
+    for (int i = tid; i < a.n_nodes; i += B) Wm[i] = 0;
+    __syncthreads();
+    if (tid == 0) {
+      rc[0] = 0;
+      rc[1] = 0;
+      rc[2] = 0;
+      s_G = gone_r;
+      s_H = r;
+      if (s_G + ring_ctr(a, r + 1)[1] < used) a.counters[1] += 1;  // another round runs
+    }
+    __syncthreads();
+  }
+  // lists of this wave: READY envs within the ring, yielded physics
+  if (tid == 0) {
+    s_ns = 0;
+    s_np = 0;
+    *a.n_stepping = 0;
+    *a.fin_count = 0;
+  }
+  __syncthreads();
+  const int H = s_H;
+  for (int e0 = 0; e0 < used; e0 += B) {
+    const int e = e0 + tid;
+    const int st = e < used ? a.env_state[e] : kGone;
+    const bool smp = st == kReady && a.env_round[e] + 1 <= H + kAsyncK - 1;
+    const bool phy = st == kPhys;
+    const unsigned ms = __ballot_sync(kFull, smp), mp = __ballot_sync(kFull, phy);
+    int bs = 0, bp = 0;
+    if (lane == 0) {
+      if (ms) bs = atomicAdd(&s_ns, __popc(ms));
+      if (mp) bp = atomicAdd(&s_np, __popc(mp));
+    }
+    bs = __shfl_sync(kFull, bs, 0);
+    bp = __shfl_sync(kFull, bp, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (smp) a.active[bs + __popc(ms & below)] = e;
+    if (phy) a.stepping[bp + __popc(mp & below)] = e;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    ctl[0] = s_H;
+    ctl[2] = s_G;
+    *a.n_active = s_ns;
+    *a.n_stepping = s_np;
+    const bool finished = s_G + ring_ctr(a, s_H + 1)[1] >= used;
+    // a shrunken batch: finish the yielded pushes unbounded in this wave
+    // (no new samples), then the asynchronous kernel continues the rounds
+    // (switch on the envs still running, not on the in-flight count: envs
+    // held back by the ring bound are still work for the batch)
+    const int remaining = used - (s_G + ring_ctr(a, s_H + 1)[1]);
+    if (!finished && remaining < a.wave_switch) {
+      ctl[5] = 2;
+      ctl[8] = 0x7fffffff;
+      *a.n_active = 0;
+    } else {
+      ctl[8] = a.wave_budget;
+    }
+    bool go = !finished;
+    if (a.round_guard && go && ++*a.round_guard > kLockRoundLimit) {
+      *a.round_guard = -1;  // a non-terminating protocol: reported by the host
+      go = false;
+    }
+    if (a.go) *a.go = go ? 1 : 0;
+    if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), go ? 1u : 0u);
+  }
+}
+
+// Sample + pick (mcts.cpp:145-152) for the wave's READY envs; a push goes to
+// the physics list (fresh progress), no legal push ends the step (reward 0).
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) wave_sample_kernel(const __grid_constant__ SimConst C,
+                                                                         LockArgs a) {
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode == 0) return;
+  __shared__ double blk[kWarpsPerBlock][160];
+  __shared__ unsigned valid[kWarpsPerBlock][32];
+  const int wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  if (gw >= *a.n_active) return;
+  const int e = a.active[gw];
+  const int n = C.n, l = threadIdx.x & 31;
+  WarpEnv W(blk[wib], n, l);
+  const ShapeView S = a.S.view(0);
+  warp_load(W, a.env_poses + static_cast<size_t>(e) * n * 3, S);
+  if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
+  const int count = warp_sample_mask(W, S, C, valid[wib]);
+  if (count == 0) {  // no legal push: reward 0 (mcts.cpp:146-150)
+    if (l == 0) {
+      a.env_done[e] = 1;
+      a.env_reward[e] = 0.0;
+      wave_step_done(a, e, a.env_round[e] + 1);
+    }
+    return;
+  }
+  const MtView g{a.mt + e, a.E};
+  int idx = a.mt_idx[e];
+  const uint64_t k = warp_mt_pick(g, idx, static_cast<uint64_t>(count), l);
+  if (l == 0) a.mt_idx[e] = idx;
+  int w = 0, seen = 0;
+  while (seen + __popc(valid[wib][w]) <= static_cast<int>(k)) seen += __popc(valid[wib][w++]);
+  unsigned bits = valid[wib][w];
+  for (int drop = static_cast<int>(k) - seen; drop > 0; --drop) bits &= bits - 1;
+  const int c = 32 * w + __ffs(bits) - 1;
+  if (l == 0) {
+    V2 s, t;
+    push_candidate(W.view(), S, C, c / C.na, c % C.na, false, s, t);
+    double* pu = a.env_push + static_cast<size_t>(e) * 4;
+    pu[0] = s.x;
+    pu[1] = s.y;
+    pu[2] = t.x;
+    pu[3] = t.y;
+    a.resume_si[e] = -1;
+    a.env_state[e] = kPhys;
+    a.stepping[atomicAdd(a.n_stepping, 1)] = e;
+  }
+}
+
+// The rest of RolloutCursor::step (mcts.cpp:153-170) for the envs whose
+// physics finished in this wave, and the round's bookkeeping.
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) wave_post_kernel(const __grid_constant__ SimConst C,
+                                                                       LockArgs a) {
+  lock_dyn(a);
+  if (a.round_mode && *a.round_mode == 0) return;
+  __shared__ double blk[kWarpsPerBlock][160];
+  const int wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarpsPerBlock + wib;
+  if (gw >= *a.fin_count) return;
+  const int e = a.fin_list[gw];
+  const int n = C.n, l = threadIdx.x & 31;
+  if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), 1ull);
+  if (a.env_status[e] != 0) {  // SimError (mcts.cpp:153-158)
+    if (l == 0) {
+      a.env_done[e] = 1;
+      a.env_reward[e] = 0.0;
+      wave_step_done(a, e, a.env_round[e] + 1);
+    }
+    return;
+  }
+  WarpEnv W(blk[wib], n, l);
+  const ShapeView S = a.S.view(0);
+  warp_load(W, a.env_poses + static_cast<size_t>(e) * n * 3, S);
+  const GraspOut gr = warp_graspable(W, S, C, a.S.target[0]);
+  if (l == 0) {
+    const int pushes = a.env_pushes[e] + 1;
+    a.env_pushes[e] = pushes;
+    if (gr.graspable) {
+      a.env_done[e] = 1;
+      a.env_bygrasp[e] = 1;
+      a.env_reward[e] = C.gamma_pow[pushes];
+    } else if (pushes >= a.cap) {
+      a.env_done[e] = 1;
+      a.env_reward[e] = 0.0;
+    }
+    wave_step_done(a, e, a.env_round[e] + 1);
   }
 }
 
