@@ -1,0 +1,220 @@
+"""The asynchronous lockstep protocol (csrc/warp_env.cu lock_async_kernel and
+the wave rounds) restated in Python and checked on CPU against a literal
+restatement of lockstep_simulate (pmbs.cpp:133-205) under RANDOM
+interleavings: envs step back to back with their round tagged, W(r) is
+accumulated by the steps of round r, the harvest of round r runs only once
+every env still running has finished round r, an env finished by grasp waits
+for the harvest of its own round, and envs run at most K rounds ahead.  Any
+schedule must give the reference's per-node rewards, the same sequence of
+(node, env) cursor creations and the same round count.
+
+Tasks follow RolloutCursor's shape (mcts.cpp:121-171): a cursor at a node
+of depth d starts with pushes = d and is done at creation iff the node is
+terminal (graspable: reward gamma^d, or dead: 0) or d >= cap; each step adds
+a push and finishes by grasp (reward gamma^pushes) at an env-dependent step,
+or at the cap (reward 0); max_remaining = cap - pushes."""
+import random
+from collections import defaultdict
+
+import pytest
+
+GAMMA = 0.8
+
+
+class Cursor:
+    def __init__(self, node, env, nodes, cap, seed, k=0):
+        depth, terminal, grasp_node = nodes[node]
+        self.pushes = depth
+        self.cap = cap
+        self.by_grasp = False
+        self.reward = 0.0
+        self.done = False
+        if terminal:
+            self.done = True
+            if grasp_node:
+                self.by_grasp = True
+                self.reward = GAMMA ** depth
+        elif depth >= cap:
+            self.done = True
+        # the step at which this rollout finds a grasp (None: runs to the cap);
+        # k = the env's cursor count (its RNG stream moves on, as on the device);
+        # from the 6th cursor on no grasps, so every schedule terminates
+        h = (node * 1000003 + env * 9176 + seed * 7919 + k * 104729) % 1000
+        self.grasp_at = depth + 1 + h % (cap - depth) if (not self.done and h % 3 == 0 and k < 6) else None
+
+    def step(self):
+        self.pushes += 1
+        if self.grasp_at is not None and self.pushes == self.grasp_at:
+            self.done, self.by_grasp, self.reward = True, True, GAMMA ** self.pushes
+        elif self.pushes >= self.cap:
+            self.done, self.reward = True, 0.0
+
+    def max_remaining(self):
+        return self.cap - self.pushes
+
+
+def split(used, n_nodes):
+    base, rem = divmod(used, n_nodes)
+    out = []
+    for i in range(n_nodes):
+        out += [i] * (base + (1 if i < rem else 0))
+    return out
+
+
+def lockstep(nodes, n_envs, leaf_parallel, cap, seed):
+    """pmbs.cpp:133-205 literally."""
+    n_nodes = len(nodes)
+    used = n_envs if leaf_parallel else n_nodes
+    env_node = split(used, n_nodes)
+    tasks = [Cursor(env_node[e], e, nodes, cap, seed) for e in range(used)]
+    calls = [(env_node[e], e) for e in range(used)]
+    rewards = [0.0] * n_nodes
+    harvested = [False] * used
+    inc = [0] * used
+
+    def remaining(i):
+        return sum(tasks[e].max_remaining() for e in range(used) if env_node[e] == i and not tasks[e].done)
+
+    def harvest():
+        for e in range(used):
+            if harvested[e] or not tasks[e].done:
+                continue
+            harvested[e] = True
+            rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+            if not leaf_parallel or not tasks[e].by_grasp:
+                continue
+            best, bw = -1, 0
+            for i in range(n_nodes):
+                w = remaining(i)
+                if w > bw:
+                    bw, best = w, i
+            if best >= 0:
+                env_node[e] = best
+                inc[e] += 1
+                tasks[e] = Cursor(best, e, nodes, cap, seed, inc[e])
+                calls.append((best, e))
+                harvested[e] = False
+
+    harvest()
+    rounds = 0
+    while any(not t.done for t in tasks):
+        for t in tasks:
+            if not t.done:
+                t.step()
+        harvest()
+        rounds += 1
+    return rewards, calls, rounds
+
+
+def asynchronous(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
+    """The device protocol with a random schedule."""
+    n_nodes = len(nodes)
+    used = n_envs if leaf_parallel else n_nodes
+    env_node = split(used, n_nodes)
+    tasks = [Cursor(env_node[e], e, nodes, cap, seed) for e in range(used)]
+    calls = [(env_node[e], e) for e in range(used)]
+    rewards = [0.0] * n_nodes
+    # the initial lockstep harvest (round 0), as the device runs it before the protocol
+    inc = [0] * used
+
+    def remaining0(i):
+        return sum(tasks[e].max_remaining() for e in range(used) if env_node[e] == i and not tasks[e].done)
+
+    W0 = [remaining0(i) for i in range(n_nodes)]
+    best0 = max(range(n_nodes), key=lambda i: (W0[i], -i)) if n_nodes else -1
+    best0 = best0 if W0[best0] > 0 else -1
+    for e in range(used):
+        if tasks[e].done:
+            rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+            if leaf_parallel and tasks[e].by_grasp and best0 >= 0:
+                env_node[e] = best0
+                inc[e] += 1
+                tasks[e] = Cursor(best0, e, nodes, cap, seed, inc[e])
+                calls.append((best0, e))
+    READY, AWAIT, GONE = 0, 1, 2
+    state = [GONE if tasks[e].done else READY for e in range(used)]
+    rnd = [0] * used
+    ring_W = defaultdict(lambda: [0] * n_nodes)
+    arrive, gone_at, done_list = defaultdict(int), defaultdict(int), defaultdict(list)
+    H, G = 0, sum(1 for s in state if s == GONE)
+    rounds = 1 if any(s == READY for s in state) else 0
+
+    def harvest_ready():
+        return arrive[H + 1] == used - (G + gone_at[H + 1]) and G + gone_at[H + 1] < used
+
+    while True:
+        runnable = [e for e in range(used) if state[e] == READY and rnd[e] + 1 <= H + K - 1]
+        can_h = harvest_ready()
+        if not runnable and not can_h:
+            assert G + gone_at[H + 1] >= used, "stalled"  # finished
+            break
+        if can_h and (not runnable or rng.random() < 0.3):
+            r = H + 1
+            W = ring_W.pop(r, [0] * n_nodes)
+            bw, best = 0, -1
+            for i in range(n_nodes):
+                if W[i] > bw:
+                    bw, best = W[i], i
+            if not leaf_parallel:
+                best = -1
+            retired = 0
+            for e in done_list.pop(r, []):
+                rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+                if state[e] == AWAIT:
+                    if best >= 0:
+                        env_node[e] = best
+                        inc[e] += 1
+                        tasks[e] = Cursor(best, e, nodes, cap, seed, inc[e])
+                        assert not tasks[e].done  # W[best] > 0: best holds a running cursor
+                        calls.append((best, e))
+                        state[e] = READY
+                    else:
+                        state[e] = GONE
+                        retired += 1
+            gone_at[r + 1] += retired
+            G += gone_at.pop(r, 0)
+            arrive.pop(r, None)
+            H = r
+            if G + gone_at[H + 1] < used:
+                rounds += 1
+            continue
+        e = rng.choice(runnable)
+        r = rnd[e] + 1
+        tasks[e].step()
+        rnd[e] = r
+        if not tasks[e].done:
+            ring_W[r][env_node[e]] += tasks[e].max_remaining()
+        else:
+            done_list[r].append(e)
+            if leaf_parallel and tasks[e].by_grasp:
+                state[e] = AWAIT
+            else:
+                state[e] = GONE
+                gone_at[r + 1] += 1
+        arrive[r] += 1
+    return rewards, calls, rounds
+
+
+def _nodes(seed, n_nodes, cap):
+    rng = random.Random(seed)
+    out = []
+    for i in range(n_nodes):
+        d = rng.randint(1, cap - 1)
+        terminal = rng.random() < 0.15
+        out.append((d, terminal, terminal and rng.random() < 0.5))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("K", [2, 3, 8])
+def test_async_protocol_equals_lockstep(seed, K):
+    cap = 10
+    nodes = _nodes(seed, 3 + seed % 9, cap)
+    n_envs = len(nodes) + 20 + 7 * seed
+    for leaf in (True, False):
+        ref = lockstep(nodes, n_envs, leaf, cap, seed)
+        for sched in range(4):
+            got = asynchronous(nodes, n_envs, leaf, cap, seed, K, random.Random(1000 * seed + sched))
+            assert got[0] == ref[0], (leaf, sched)
+            assert sorted(got[1]) == sorted(ref[1]), (leaf, sched)
+            assert got[2] == ref[2], (leaf, sched)
