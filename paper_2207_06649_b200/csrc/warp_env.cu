@@ -178,6 +178,7 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
   double* env = a.env_poses + static_cast<size_t>(e) * n * 3;
   const PolyShape O = warp_load_any<kPoly>(W, G, env, S);
   if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), 1ull);
+#ifdef PPG_STEP_TRACE_BUILD  // per-step records for tools/async_model.py (build with EXTRA_NVFLAGS=-DPPG_STEP_TRACE_BUILD)
   unsigned long long t_start = 0;
   if (a.step_trace && l == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   struct TraceGuard {  // writes the record on every exit path
@@ -199,6 +200,7 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
       }
     }
   } trace_guard{a, e, l, t_start};
+#endif
   const int count = warp_sample_mask(W, S, C, valid);
   if (count == 0) {  // no legal push: reward 0 (mcts.cpp:146-150)
     if (l == 0) {

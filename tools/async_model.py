@@ -5,7 +5,8 @@ file (latency-mode env-steps: env, round, start/end ns, done/by-grasp):
                       of an env that was re-purposed at the harvest of round
                       r-1 waits until every env finished round r-1
 (unlimited parallelism: valid while active envs < resident warps).
-python tools/async_model.py trace.bin"""
+python tools/async_model.py trace.bin
+(the trace records need a library built with EXTRA_NVFLAGS=-DPPG_STEP_TRACE_BUILD)"""
 import struct
 import sys
 from collections import defaultdict

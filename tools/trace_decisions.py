@@ -1,5 +1,6 @@
-"""Step traces (PPG_STEP_TRACE) of the rollout workload's tail and of PMBS
-decisions: python tools/trace_decisions.py out.bin"""
+"""Step traces (PPG_STEP_TRACE=out.bin) of the rollout workload's tail and of
+PMBS decisions, for tools/async_model.py; needs a library built with
+EXTRA_NVFLAGS=-DPPG_STEP_TRACE_BUILD (make -C paper_2207_06649_b200/csrc)."""
 import os
 import sys
 
