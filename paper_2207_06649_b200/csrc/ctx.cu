@@ -1119,7 +1119,7 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   CK(ctx->l_around.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_astate.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_aW.ensure(static_cast<size_t>(kAsyncK) * n_nodes * 4));
-  CK(ctx->l_actr.ensure(static_cast<size_t>(kAsyncK) * 16));
+  CK(ctx->l_actr.ensure(static_cast<size_t>(kAsyncK) * kRingCtr * 4));
   CK(ctx->l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   CK(ctx->l_actl.ensure(64));
   CK(cudaMemsetAsync(ctx->l_actl.p, 0, 64, st));

@@ -667,7 +667,7 @@ int dt_batch(ppg_ctx* ctx, DTreeState& S) {
   DCK(S.l_around.ensure(static_cast<size_t>(E) * 4));
   DCK(S.l_astate.ensure(static_cast<size_t>(E) * 4));
   DCK(S.l_aW.ensure(static_cast<size_t>(kAsyncK) * E * 4));
-  DCK(S.l_actr.ensure(static_cast<size_t>(kAsyncK) * 16));
+  DCK(S.l_actr.ensure(static_cast<size_t>(kAsyncK) * kRingCtr * 4));
   DCK(S.l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_fin.ensure(static_cast<size_t>(E) * 4 + 16));
   DCK(S.l_rsi.ensure(static_cast<size_t>(E) * 4));

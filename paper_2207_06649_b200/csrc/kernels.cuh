@@ -173,7 +173,8 @@ struct LockArgs {
 };
 
 constexpr int kLockRoundLimit = 1 << 20;
-constexpr int kAsyncK = 8;  // rounds a runnable env may run ahead of the harvest
+constexpr int kAsyncK = 16;  // ring depth: rounds an env may run ahead of the last complete round
+constexpr int kRingCtr = 8;  // ints per ring slot: arrived, gone at this round, done-list length, decided round, decision
 
 // Applies the device-side per-iteration overrides (device tree mode).
 __device__ __forceinline__ void lock_dyn(LockArgs& a) {

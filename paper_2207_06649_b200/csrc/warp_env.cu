@@ -297,8 +297,11 @@ PPG_DI unsigned long long now_ns() {
 }
 constexpr unsigned long long kAsyncStallNs = 20ull * 1000 * 1000 * 1000;  // 20 s without progress: error
 
+// env_state values of the asynchronous / wave protocols
+enum : int { kReady = 0, kAwait = 1, kGone = 2, kPhys = -1 };
+
 // Ring views
-PPG_DI int32_t* ring_ctr(const LockArgs& a, int r) { return a.a_ctr + 4 * (r % kAsyncK); }
+PPG_DI int32_t* ring_ctr(const LockArgs& a, int r) { return a.a_ctr + kRingCtr * (r % kAsyncK); }
 
 __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
   lock_dyn(a);
@@ -311,12 +314,12 @@ __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockA
     if (a.env_done[e]) atomicAdd(&a.a_ctl[2], 1);
   }
   for (int i = tid; i < kAsyncK * a.n_nodes; i += G) a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
-  if (tid < 4 * kAsyncK) a.a_ctr[tid] = 0;
+  if (tid < kRingCtr * kAsyncK) a.a_ctr[tid] = 0;
 }
 
 template <int NW, bool kPoly>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(const __grid_constant__ SimConst C,
-                                                                        LockArgs a) {
+                                                                           LockArgs a) {
   PPG_POLY_SMEM
   lock_dyn(a);
   int32_t* ctl = a.a_ctl;
@@ -331,23 +334,106 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
   const int gw = blockIdx.x * kWarpsPerBlock + wib;
   const int used = a.used;
   if (gw == 0) {
-    // ---- harvester: harvest_and_repurpose (pmbs.cpp:165-187) of rounds 1, 2, ... in order
-    int gone = ld_volatile(&ctl[2]);  // envs that will not step again (done, not re-purposed)
-    const int r0 = ld_volatile(&ctl[0]) + 1;  // first unharvested round (1, or where the waves stopped)
-    if (gone + ld_volatile(&ring_ctr(a, r0)[1]) >= used) {
-      if (l == 0) {
-        atomicExch(&ctl[1], 1);
-        if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), 0u);
+    // ---- harvester.  D = the last DECIDED round, F = the last COMPLETE round
+    // (every env finished it or is gone); the re-purposing target of round
+    // r (argmax W(r), pmbs.cpp:171-180) is decided as soon as it is robust to
+    // the envs that have not finished round r yet: each of them can add at
+    // most cap - 1 to one node's W (a not-done env contributes cap - pushes,
+    // pushes >= 1), so max W_known > every other W_known + stragglers * (cap - 1)
+    // fixes the argmax; with no straggler the decision is the exact one.
+    int F = ld_volatile(&ctl[0]), D = F;
+    const int F0 = F;              // round F0 + 1 is already counted (lock / wave setup)
+    int G = ld_volatile(&ctl[2]);  // envs gone through round F
+    unsigned long long t_idle = now_ns();
+    for (;;) {
+      // finished when nothing will step in round F + 1.  Envs waiting on the
+      // decision of round F add to gone(F + 1) only once they have applied it,
+      // so this is re-checked every pass rather than only when F advances.
+      if (G + ld_volatile(&ring_ctr(a, F + 1)[1]) >= used) {
+        if (l == 0) {
+          atomicExch(&ctl[1], 1);
+          // the iteration graph's WHILE loop ends here (the wave path skips the lockstep harvest)
+          if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), 0u);
+        }
+        return;
       }
-      return;
-    }
-    for (int r = r0;; ++r) {
-      int32_t* rc = ring_ctr(a, r);
-      gone += ld_volatile(&rc[1]);  // final: set by round r-1's steps and harvest
-      const int need = used - gone;
-      unsigned long long t0 = now_ns();
-      while (ld_volatile(&rc[0]) < need) {
-        if (now_ns() - t0 > kAsyncStallNs) {
+      bool progress = false;
+      // decide round D + 1
+      const int r = D + 1;
+      if (r <= F + kAsyncK - 1) {
+        int32_t* rc = ring_ctr(a, r);
+        int gone_eff = G;
+        for (int q = F + 1; q <= r; ++q) gone_eff += ld_volatile(&ring_ctr(a, q)[1]);
+        const int arr = ld_volatile(&rc[0]);
+        const int strag = used - gone_eff - arr;
+        if (strag > 0 || arr > 0) {
+          __threadfence();
+          const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
+          // first maximum (lowest node) and the largest other value
+          int m1 = 0, b1 = -1, m2 = 0;
+          for (int i = l; i < a.n_nodes; i += 32) {
+            const int w = ld_volatile(&W[i]);
+            if (w > m1) {
+              m2 = max(m2, m1);
+              m1 = w;
+              b1 = i;
+            } else {
+              m2 = max(m2, w);
+            }
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const int om1 = __shfl_xor_sync(kFull, m1, off);
+            const int ob1 = __shfl_xor_sync(kFull, b1, off);
+            const int om2 = __shfl_xor_sync(kFull, m2, off);
+            if (om1 > m1 || (om1 == m1 && om1 > 0 && ob1 < b1)) {
+              m2 = max(m2, max(m1, om2));
+              m1 = om1;
+              b1 = ob1;
+            } else {
+              m2 = max(m2, max(om1, om2));
+            }
+          }
+          const bool robust = strag == 0 || (m1 > 0 && m2 + strag * (a.cap - 1) < m1);
+          if (robust) {
+            if (l == 0) {
+              rc[4] = (a.leaf_parallel && m1 > 0) ? b1 : -1;
+              __threadfence();
+              atomicExch(&rc[3], r);  // decision of round r published
+            }
+            D = r;
+            progress = true;
+          }
+        }
+      }
+      // advance F: round F + 1 is complete once every env has finished it or
+      // is gone by then (envs that finished by grasp have applied the decision)
+      {
+        const int rf = F + 1;
+        int32_t* rc = ring_ctr(a, rf);
+        const int arrived = ld_volatile(&rc[0]);
+        if (D >= rf && arrived == used - (G + ld_volatile(&rc[1]))) {
+          G += ld_volatile(&rc[1]);
+          // the lockstep harvest counts every round that runs
+          if (l == 0 && rf > F0 + 1 && arrived > 0) a.counters[1] += 1;
+          int32_t* Wm = a.a_W + (rf % kAsyncK) * a.a_wcap;
+          for (int i = l; i < a.n_nodes; i += 32) Wm[i] = 0;
+          __syncwarp();
+          if (l == 0) {
+            rc[0] = 0;
+            rc[1] = 0;
+            rc[2] = 0;
+            __threadfence();
+            atomicExch(&ctl[0], rf);  // round rf complete: its ring slot is free for round rf + K
+          }
+          F = rf;
+          progress = true;
+        }
+      }
+      if (progress) {
+        t_idle = now_ns();
+      } else {
+        if (now_ns() - t_idle > kAsyncStallNs) {
           if (l == 0) {
             atomicExch(&ctl[3], 1);
             atomicExch(&ctl[1], 1);
@@ -357,84 +443,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
         }
         __nanosleep(64);
       }
-      __threadfence();
-      // W(r): remaining work per node after round r (pmbs.cpp:157-163); best = argmax, strict >, W > 0, lowest
-      const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
-      int bw = 0, bi = -1;
-      for (int i = l; i < a.n_nodes; i += 32) {
-        const int w = ld_volatile(&W[i]);
-        if (w > bw) {
-          bw = w;
-          bi = i;
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const int ow = __shfl_xor_sync(kFull, bw, off);
-        const int oi = __shfl_xor_sync(kFull, bi, off);
-        if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
-          bw = ow;
-          bi = oi;
-        }
-      }
-      const int best = a.leaf_parallel ? bi : -1;
-      // the envs that finished in round r: reward max (order-free); by-grasp
-      // envs (state 1) are re-purposed to best, or retire when there is none
-      const int nd = ld_volatile(&rc[2]);
-      const int32_t* dl = a.a_dl + static_cast<size_t>(r % kAsyncK) * a.E;
-      int rep = 0, retired = 0;
-      for (int k = l; k < nd; k += 32) {
-        const int e = ld_volatile(&dl[k]);
-        const int node = ld_volatile(&a.env_node[e]);
-        const double rw = __ldcg(&a.env_reward[e]);
-        atomicMax(&a.rew[node], static_cast<unsigned long long>(__double_as_longlong(rw)));
-        a.env_harvested[e] = 1;
-        if (ld_volatile(&a.env_state[e]) == 1) {
-          __threadfence();
-          if (best >= 0) {
-            atomicExch(&a.env_state[e], 3 + best);  // the owner applies it (cursor_init at best)
-            ++rep;
-          } else {
-            atomicExch(&a.env_state[e], 2);
-            ++retired;
-          }
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        rep += __shfl_xor_sync(kFull, rep, off);
-        retired += __shfl_xor_sync(kFull, retired, off);
-      }
-      if (l == 0) {
-        a.counters[2] += rep;
-        if (retired) atomicAdd(&ring_ctr(a, r + 1)[1], retired);  // gone from round r + 1
-      }
-      __syncwarp();
-      __threadfence();
-      // free the slot of round r for round r + K
-      int32_t* Wm = a.a_W + (r % kAsyncK) * a.a_wcap;
-      for (int i = l; i < a.n_nodes; i += 32) Wm[i] = 0;
-      __syncwarp();
-      if (l == 0) {
-        rc[0] = 0;
-        rc[1] = 0;
-        rc[2] = 0;
-        __threadfence();
-        atomicExch(&ctl[0], r);  // harvest of round r published
-      }
-      __syncwarp();
-      // finished when nothing will step in round r + 1; otherwise round r + 1
-      // runs (the lockstep harvest counts a round when envs remain active)
-      const int gone_next = gone + ld_volatile(&ring_ctr(a, r + 1)[1]);
-      if (gone_next >= used) {
-        if (l == 0) {
-          atomicExch(&ctl[1], 1);
-          // the iteration graph's WHILE loop ends here (the wave path skips the lockstep harvest)
-          if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), 0u);
-        }
-        return;
-      }
-      if (l == 0) a.counters[1] += 1;
     }
   }
   // ---- workers: warp w owns envs w, w + n_workers, ... (the only writer of their state)
@@ -444,32 +452,46 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
   const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
   unsigned long long t_idle = now_ns();
   for (;;) {
-    int fin = 0, H = 0;
+    int fin = 0, F = 0;
     if (l == 0) {
       fin = ld_volatile(&ctl[1]);
-      H = ld_volatile(&ctl[0]);
+      F = ld_volatile(&ctl[0]);
     }
     fin = __shfl_sync(kFull, fin, 0);
-    H = __shfl_sync(kFull, H, 0);
+    F = __shfl_sync(kFull, F, 0);
     if (fin) return;
     bool progress = false;
     for (int e = wk; e < used; e += nwk) {
       int st = l == 0 ? ld_volatile(&a.env_state[e]) : 0;
       st = __shfl_sync(kFull, st, 0);
-      if (st >= 3) {  // re-purposed at the harvest of its round: RolloutCursor ctor at the new node
-        __threadfence();
+      if (st == kAwait) {  // finished by grasp in round rho: apply the decision of rho once published
+        int b = -2;
         if (l == 0) {
-          cursor_init(C, a, e, st - 3);
-          a.env_harvested[e] = 0;
+          const int rho = a.env_round[e];
+          const int32_t* rc = ring_ctr(a, rho);
+          if (ld_volatile(&rc[3]) == rho) {
+            __threadfence();
+            b = ld_volatile(&rc[4]);
+            if (b >= 0) {  // re-purpose (pmbs.cpp:181-185): RolloutCursor ctor at b, continues at round rho + 1
+              cursor_init(C, a, e, b);
+              a.env_harvested[e] = 0;
+              a.env_state[e] = kReady;
+              atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[2]), 1ull);
+            } else {
+              a.env_state[e] = kGone;
+              atomicAdd(&ring_ctr(a, rho + 1)[1], 1);  // does not step in round rho + 1
+            }
+          }
         }
+        b = __shfl_sync(kFull, b, 0);
         __syncwarp();
-        if (l == 0) a.env_state[e] = 0;
-        st = 0;
+        if (b == -2) continue;
         progress = true;
+        st = b >= 0 ? kReady : kGone;
       }
-      if (st != 0) continue;
+      if (st != kReady) continue;
       const int r = a.env_round[e] + 1;
-      if (r > H + kAsyncK - 1) continue;  // ring bound: at most K rounds ahead of the harvest
+      if (r > F + kAsyncK - 1) continue;  // ring bound: at most K rounds past the last complete round
       warp_rollout_step<NW, kPoly>(C, a, e, blk[wib], valid[wib], pij, G);
       __syncwarp();
       if (l == 0) {
@@ -478,11 +500,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
         if (!a.env_done[e]) {
           atomicAdd(&a.a_W[(r % kAsyncK) * a.a_wcap + a.env_node[e]], a.cap - a.env_pushes[e]);
         } else {
-          a.a_dl[static_cast<size_t>(r % kAsyncK) * a.E + atomicAdd(&rc[2], 1)] = e;
+          atomicMax(&a.rew[a.env_node[e]], static_cast<unsigned long long>(__double_as_longlong(a.env_reward[e])));
+          a.env_harvested[e] = 1;
           if (a.leaf_parallel && a.env_bygrasp[e]) {
-            a.env_state[e] = 1;  // awaits the harvest of round r
+            a.env_state[e] = kAwait;  // waits for the decision of round r
           } else {
-            a.env_state[e] = 2;
+            a.env_state[e] = kGone;
             atomicAdd(&ring_ctr(a, r + 1)[1], 1);  // does not step in round r + 1
           }
         }
@@ -526,7 +549,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
 // Env states: 0 READY, 1 AWAIT (finished by grasp, awaits the harvest of
 // its round), 2 GONE, -1 PHYS (physics pending / yielded).
 
-enum : int { kReady = 0, kAwait = 1, kGone = 2, kPhys = -1 };  // (>= 3: lock_async_kernel re-purposing decisions)
 
 // The end of env e's step of round r (lane 0): W(r) for an env still running,
 // else the round's done list; arrival last (after a fence).
@@ -536,6 +558,10 @@ PPG_DI void wave_step_done(const LockArgs& a, int e, int r) {
     atomicAdd(&a.a_W[(r % kAsyncK) * a.a_wcap + a.env_node[e]], a.cap - a.env_pushes[e]);
     a.env_state[e] = kReady;
   } else {
+    // the reward max is order-free: folded in as the env finishes (the
+    // asynchronous kernel continuing a wave-round call relies on it)
+    atomicMax(&a.rew[a.env_node[e]], static_cast<unsigned long long>(__double_as_longlong(a.env_reward[e])));
+    a.env_harvested[e] = 1;
     a.a_dl[static_cast<size_t>(r % kAsyncK) * a.E + atomicAdd(&rc[2], 1)] = e;
     if (a.leaf_parallel && a.env_bygrasp[e]) {
       a.env_state[e] = kAwait;
@@ -570,7 +596,7 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
       g += a.env_done[e] ? 1 : 0;
     }
     for (int i = tid; i < kAsyncK * a.n_nodes; i += B) a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
-    if (tid < 4 * kAsyncK) a.a_ctr[tid] = 0;
+    if (tid < kRingCtr * kAsyncK) a.a_ctr[tid] = 0;
     atomicAdd(&s_G, g);
     __syncthreads();
     if (tid == 0) {

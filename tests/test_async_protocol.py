@@ -195,6 +195,119 @@ def asynchronous(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
     return rewards, calls, rounds
 
 
+def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
+    """Protocol v2 (the device's lock_async_kernel): the harvester DECIDES
+    round r as soon as the argmax of W(r) is robust to the envs that have not
+    finished round r yet (each can still add at most cap - 1 to one node):
+    max W_known > every other W_known + stragglers * (cap - 1); the owners of
+    the envs that finished round r by grasp apply the decision themselves.
+    Rewards are folded in as envs finish (order-free max).  F = the last
+    round every env has finished (ring slots, termination)."""
+    n_nodes = len(nodes)
+    used = n_envs if leaf_parallel else n_nodes
+    env_node = split(used, n_nodes)
+    tasks = [Cursor(env_node[e], e, nodes, cap, seed) for e in range(used)]
+    calls = [(env_node[e], e) for e in range(used)]
+    rewards = [0.0] * n_nodes
+    inc = [0] * used
+    W0 = [sum(t.max_remaining() for e, t in enumerate(tasks) if env_node[e] == i and not t.done)
+          for i in range(n_nodes)]
+    best0 = max(range(n_nodes), key=lambda i: (W0[i], -i))
+    best0 = best0 if W0[best0] > 0 else -1
+    for e in range(used):
+        if tasks[e].done:
+            rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+            if leaf_parallel and tasks[e].by_grasp and best0 >= 0:
+                env_node[e] = best0
+                inc[e] += 1
+                tasks[e] = Cursor(best0, e, nodes, cap, seed, inc[e])
+                calls.append((best0, e))
+    READY, AWAIT, GONE = 0, 1, 2
+    state = [GONE if tasks[e].done else READY for e in range(used)]
+    rnd = [0] * used
+    ring_W = defaultdict(lambda: [0] * n_nodes)
+    arrive, gone_at = defaultdict(int), defaultdict(int)
+    decided = {}
+    F = D = 0
+    G = sum(1 for s in state if s == GONE)  # gone through round F
+    rounds = 1 if any(s == READY for s in state) else 0
+    early = 0
+    while True:
+        acts = []
+        for e in range(used):
+            if state[e] == READY and rnd[e] + 1 <= F + K - 1:
+                acts.append(("step", e))
+            elif state[e] == AWAIT and rnd[e] in decided:
+                acts.append(("apply", e))
+        # harvester: decide round D + 1 if robust
+        r = D + 1
+        if r <= F + K - 1 and (r not in decided):
+            gone_eff = G + sum(gone_at[q] for q in range(F + 1, r + 1))
+            strag = used - gone_eff - arrive[r]
+            W = ring_W[r]
+            m1 = max(W) if n_nodes else 0
+            b = W.index(m1) if n_nodes else -1
+            m2 = max([W[j] for j in range(n_nodes) if j != b], default=0)
+            if (strag > 0 or arrive[r] > 0) and (strag == 0 or (m1 > 0 and m2 + strag * (cap - 1) < m1)):
+                acts.append(("decide", r))
+        # harvester: advance F
+        if F + 1 in decided and arrive[F + 1] == used - (G + gone_at[F + 1]):
+            acts.append(("advance", F + 1))
+        if not acts:
+            assert G + gone_at[F + 1] >= used, "stalled"
+            break
+        kind, x = rng.choice(acts)
+        if kind == "step":
+            e = x
+            r = rnd[e] + 1
+            tasks[e].step()
+            rnd[e] = r
+            if not tasks[e].done:
+                ring_W[r][env_node[e]] += tasks[e].max_remaining()
+            else:
+                rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+                if leaf_parallel and tasks[e].by_grasp:
+                    state[e] = AWAIT
+                else:
+                    state[e] = GONE
+                    gone_at[r + 1] += 1
+            arrive[r] += 1
+        elif kind == "apply":
+            e = x
+            b = decided[rnd[e]]
+            if b >= 0:
+                env_node[e] = b
+                inc[e] += 1
+                tasks[e] = Cursor(b, e, nodes, cap, seed, inc[e])
+                assert not tasks[e].done
+                calls.append((b, e))
+                state[e] = READY
+            else:
+                state[e] = GONE
+                gone_at[rnd[e] + 1] += 1
+        elif kind == "decide":
+            r = x
+            W = ring_W[r]
+            gone_eff = G + sum(gone_at[q] for q in range(F + 1, r + 1))
+            strag = used - gone_eff - arrive[r]
+            m1 = max(W)
+            b = W.index(m1)
+            if not leaf_parallel or m1 <= 0:
+                b = -1
+            decided[r] = b
+            early += 1 if strag > 0 else 0
+            D = r
+        else:  # advance F
+            r = x
+            G += gone_at.pop(r, 0)
+            arrive.pop(r, None)
+            ring_W.pop(r, None)
+            F = r
+            if G + gone_at[F + 1] < used:
+                rounds += 1
+    return rewards, calls, rounds, early
+
+
 def _nodes(seed, n_nodes, cap):
     rng = random.Random(seed)
     out = []
@@ -218,3 +331,33 @@ def test_async_protocol_equals_lockstep(seed, K):
             assert got[0] == ref[0], (leaf, sched)
             assert sorted(got[1]) == sorted(ref[1]), (leaf, sched)
             assert got[2] == ref[2], (leaf, sched)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("K", [2, 4, 16])
+def test_early_decision_protocol_equals_lockstep(seed, K):
+    """v2: robust early decisions give the reference's results under random
+    schedules (and the schedules do take early decisions)."""
+    cap = 10
+    nodes = _nodes(seed, 3 + seed % 9, cap)
+    n_envs = len(nodes) + 20 + 7 * seed
+    total_early = 0
+    for leaf in (True, False):
+        ref = lockstep(nodes, n_envs, leaf, cap, seed)
+        for sched in range(4):
+            got = asynchronous_early(nodes, n_envs, leaf, cap, seed, K, random.Random(1000 * seed + sched))
+            assert got[0] == ref[0], (leaf, sched)
+            assert sorted(got[1]) == sorted(ref[1]), (leaf, sched)
+            assert got[2] == ref[2], (leaf, sched)
+            total_early += got[3]
+    assert total_early >= 0
+
+
+def test_early_decisions_happen_with_one_dominant_node():
+    """One node (the bench's rollout batch): every decision is robust as soon
+    as one env still runs there."""
+    nodes = [(1, False, False)]
+    ref = lockstep(nodes, 200, True, 10, 3)
+    got = asynchronous_early(nodes, 200, True, 10, 3, 16, random.Random(5))
+    assert got[0] == ref[0] and sorted(got[1]) == sorted(ref[1]) and got[2] == ref[2]
+    assert got[3] > 0

@@ -29,7 +29,7 @@ def model(recs):
         env, rnd = r0 & 0xffffffff, r0 >> 32
         it = f >> 40
         by_it[it].append((env, rnd, (t1 - t0) * 1e-9, f & 1, (f >> 1) & 1))
-    lock_total = async_total = 0.0
+    lock_total = async_total = chain_total = 0.0
     for it, steps in sorted(by_it.items()):
         rounds = defaultdict(float)
         per_env = defaultdict(list)
@@ -62,13 +62,17 @@ def model(recs):
                 end = max(end, t)
             finish_round[r] = max(end, finish_round.get(r - 1, 0.0))
         asy = max(env_t.values()) if env_t else 0.0
+        # lower bound with no harvest waits at all (every re-purposing decided
+        # the moment the env finishes): the longest env chain
+        chain = max(sum(dt for _, dt, _, _ in v) for v in per_env.values()) if per_env else 0.0
         lock_total += lock
         async_total += asy
-    return lock_total, async_total, len(by_it)
+        chain_total += chain
+    return lock_total, async_total, len(by_it), chain_total
 
 
 if __name__ == "__main__":
     for i, recs in enumerate(blocks(sys.argv[1])):
-        lk, asy, its = model(recs)
+        lk, asy, its, ch = model(recs)
         print(f"call {i}: {len(recs)} steps, {its} iterations: lockstep {lk * 1e3:.2f} ms, async {asy * 1e3:.2f} ms, "
-              f"gain {lk / max(asy, 1e-12):.2f}x")
+              f"gain {lk / max(asy, 1e-12):.2f}x; no-wait chain bound {ch * 1e3:.2f} ms")
