@@ -1311,6 +1311,13 @@ int ppg_simulate(ppg_ctx* ctx, const double* node_poses, const int32_t* node_met
           if (rc != PPG_SUCCESS) return rc;
           CK(cudaMemcpyAsync(hctl, ctl, 16, cudaMemcpyDeviceToHost, st));
           CK(cudaStreamSynchronize(st));
+          if (trace) {
+            cudaEventRecord(t1, st);
+            cudaEventSynchronize(t1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, t1);
+            std::fprintf(stderr, "async tail from H %d: complete round %d ms %.4f\n", wa.wave_switch, hctl[0], ms);
+          }
           if (hctl[3] != 0) {
             ctx->err = "asynchronous lockstep stalled (protocol error)";
             return PPG_ECUDA;

@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(cons
     // most cap - 1 to one node's W (a not-done env contributes cap - pushes,
     // pushes >= 1), so max W_known > every other W_known + stragglers * (cap - 1)
     // fixes the argmax; with no straggler the decision is the exact one.
-    int F = ld_volatile(&ctl[0]), D = F;
+    int F = ld_volatile(&ctl[0]);
+    int D = max(F, ld_volatile(&ctl[9]));  // rounds the wave harvests already decided
     const int F0 = F;              // round F0 + 1 is already counted (lock / wave setup)
     int G = ld_volatile(&ctl[2]);  // envs gone through round F
     unsigned long long t_idle = now_ns();
@@ -575,16 +576,34 @@ PPG_DI void wave_step_done(const LockArgs& a, int e, int r) {
   atomicAdd(&rc[0], 1);
 }
 
-// Harvest of every complete round (one block), then the wave's lists.
-// a_ctl: [0] harvested round H, [2] envs gone through round H, [4] set up.
+// (max, first index of the max, largest other value) merge of two partial
+// scans of W (strict >, W > 0, lowest node wins a tie: pmbs.cpp:171-180)
+PPG_DI void top2_merge(int& m1, int& b1, int& m2, int om1, int ob1, int om2) {
+  if (om1 > m1 || (om1 == m1 && om1 > 0 && ob1 < b1)) {
+    m2 = max(m2, max(m1, om2));
+    m1 = om1;
+    b1 = ob1;
+  } else {
+    m2 = max(m2, max(om1, om2));
+  }
+}
+
+// Between waves (one block): decide every round whose re-purposing target is
+// already fixed (the early decision of lock_async_kernel: max W_known > every
+// other W_known + stragglers * (cap - 1)), apply the decisions to the
+// by-grasp envs waiting on them, complete rounds in order, then the wave's
+// lists.  a_ctl: [0] complete round F, [2] envs gone through round F,
+// [4] set up, [9] decided round D.  Ring slot: [0] arrived, [1] gone at this
+// round, [2] done-list length, [3] decided round, [4] decision, [5] done-list
+// entries already applied.
 __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a) {
   lock_dyn(a);
   if (a.round_mode && *a.round_mode == 0) return;  // this lockstep call runs asynchronously
   const int tid = threadIdx.x, B = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int used = a.used;
   int32_t* ctl = a.a_ctl;
-  __shared__ int s_H, s_G, s_best, s_ns, s_np;
-  __shared__ int s_bw[32], s_bi[32], s_rep[32], s_ret[32];
+  __shared__ int s_H, s_G, s_D, s_ns, s_np, s_prog, s_strag, s_try;
+  __shared__ int s_m1[32], s_b1[32], s_m2[32], s_rep[32], s_ret[32];
   if (ctl[4] == 0) {  // first wave of the call: every env READY or GONE at round 0
     if (tid == 0) s_G = 0;
     __syncthreads();
@@ -603,99 +622,121 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
       ctl[0] = 0;
       ctl[2] = s_G;
       ctl[4] = 1;
+      ctl[9] = 0;
     }
     __syncthreads();
   }
   if (tid == 0) {
     s_H = ctl[0];
     s_G = ctl[2];
+    s_D = ctl[9];
   }
   __syncthreads();
-  for (;;) {  // harvest complete rounds in order
+  for (;;) {
+    __syncthreads();  // every thread has read the previous pass's shared state
+    if (tid == 0) {
+      s_prog = 0;
+      // (1) can round D + 1 be decided?
+      const int r = s_D + 1;
+      s_try = 0;
+      if (r <= s_H + kAsyncK - 1) {
+        int gone_eff = s_G;
+        for (int q = s_H + 1; q <= r; ++q) gone_eff += ring_ctr(a, q)[1];
+        const int arr = ring_ctr(a, r)[0];
+        s_strag = used - gone_eff - arr;
+        s_try = (s_strag > 0 || arr > 0) ? 1 : 0;
+      }
+    }
+    __syncthreads();
+    if (s_try) {
+      const int r = s_D + 1;
+      const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
+      int m1 = 0, b1 = -1, m2 = 0;
+      for (int i = tid; i < a.n_nodes; i += B) top2_merge(m1, b1, m2, W[i], i, 0);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        top2_merge(m1, b1, m2, __shfl_xor_sync(kFull, m1, off), __shfl_xor_sync(kFull, b1, off),
+                   __shfl_xor_sync(kFull, m2, off));
+      if (lane == 0) {
+        s_m1[wid] = m1;
+        s_b1[wid] = b1;
+        s_m2[wid] = m2;
+      }
+      __syncthreads();
+      if (tid < 32) {
+        const int nw = B >> 5;
+        m1 = tid < nw ? s_m1[tid] : 0;
+        b1 = tid < nw ? s_b1[tid] : -1;
+        m2 = tid < nw ? s_m2[tid] : 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+          top2_merge(m1, b1, m2, __shfl_xor_sync(kFull, m1, off), __shfl_xor_sync(kFull, b1, off),
+                     __shfl_xor_sync(kFull, m2, off));
+        if (tid == 0) {
+          const int strag = s_strag;
+          if (strag == 0 || (m1 > 0 && m2 + strag * (a.cap - 1) < m1)) {
+            int32_t* rc = ring_ctr(a, r);
+            rc[4] = (a.leaf_parallel && m1 > 0) ? b1 : -1;
+            rc[3] = r;
+            s_D = r;
+            s_prog = 1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // (2) apply the decided rounds' decisions to their newly listed done envs
+    for (int q = s_H + 1; q <= s_D; ++q) {
+      int32_t* rc = ring_ctr(a, q);
+      const int k0 = rc[5], nd = rc[2];
+      if (k0 == nd) continue;
+      const int best = rc[4];
+      const int32_t* dl = a.a_dl + static_cast<size_t>(q % kAsyncK) * a.E;
+      int rep = 0, ret = 0;
+      for (int k = k0 + tid; k < nd; k += B) {
+        const int e = dl[k];
+        if (a.env_state[e] == kAwait) {
+          if (best >= 0) {  // re-purpose (pmbs.cpp:181-185): a new cursor at best, continues at round q + 1
+            cursor_init(C, a, e, best);
+            a.env_harvested[e] = 0;
+            a.env_state[e] = kReady;
+            ++rep;
+          } else {
+            a.env_state[e] = kGone;
+            ++ret;
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        rep += __shfl_xor_sync(kFull, rep, off);
+        ret += __shfl_xor_sync(kFull, ret, off);
+      }
+      if (lane == 0) {
+        s_rep[wid] = rep;
+        s_ret[wid] = ret;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int tr = 0, tt = 0;
+        for (int w = 0; w < (B >> 5); ++w) {
+          tr += s_rep[w];
+          tt += s_ret[w];
+        }
+        a.counters[2] += tr;
+        ring_ctr(a, q + 1)[1] += tt;  // retired: do not step in round q + 1
+        rc[5] = nd;
+      }
+      __syncthreads();
+    }
+    // (3) complete round F + 1: decided, every env finished it or is gone, its done list applied
     const int r = s_H + 1;
     int32_t* rc = ring_ctr(a, r);
     const int gone_r = s_G + rc[1];
-    if (gone_r >= used || rc[0] < used - gone_r) break;
-    // W(r) argmax (strict >, W > 0, lowest node)
-    const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
-    int bw = 0, bi = -1;
-    for (int i = tid; i < a.n_nodes; i += B) {
-      const int w = W[i];
-      if (w > bw) {
-        bw = w;
-        bi = i;
-      }
+    if (gone_r >= used || s_D < r || rc[0] < used - gone_r) {
+      if (!s_prog) break;
+      continue;
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const int ow = __shfl_xor_sync(kFull, bw, off);
-      const int oi = __shfl_xor_sync(kFull, bi, off);
-      if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
-        bw = ow;
-        bi = oi;
-      }
-    }
-    if (lane == 0) {
-      s_bw[wid] = bw;
-      s_bi[wid] = bi;
-    }
-    __syncthreads();
-    if (tid < 32) {
-      const int nw = B >> 5;
-      bw = tid < nw ? s_bw[tid] : 0;
-      bi = tid < nw ? s_bi[tid] : -1;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const int ow = __shfl_xor_sync(kFull, bw, off);
-        const int oi = __shfl_xor_sync(kFull, bi, off);
-        if (ow > bw || (ow == bw && ow > 0 && oi < bi)) {
-          bw = ow;
-          bi = oi;
-        }
-      }
-      if (tid == 0) s_best = a.leaf_parallel ? bi : -1;
-    }
-    __syncthreads();
-    const int best = s_best;
-    const int nd = rc[2];
-    const int32_t* dl = a.a_dl + static_cast<size_t>(r % kAsyncK) * a.E;
-    int rep = 0, ret = 0;
-    for (int k = tid; k < nd; k += B) {
-      const int e = dl[k];
-      atomicMax(&a.rew[a.env_node[e]], static_cast<unsigned long long>(__double_as_longlong(a.env_reward[e])));
-      a.env_harvested[e] = 1;
-      if (a.env_state[e] == kAwait) {
-        if (best >= 0) {  // re-purpose (pmbs.cpp:171-185): a new cursor at best, continues at round r + 1
-          cursor_init(C, a, e, best);
-          a.env_harvested[e] = 0;
-          a.env_state[e] = kReady;
-          ++rep;
-        } else {
-          a.env_state[e] = kGone;
-          ++ret;
-        }
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      rep += __shfl_xor_sync(kFull, rep, off);
-      ret += __shfl_xor_sync(kFull, ret, off);
-    }
-    if (lane == 0) {
-      s_rep[wid] = rep;
-      s_ret[wid] = ret;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int tr = 0, tt = 0;
-      for (int w = 0; w < (B >> 5); ++w) {
-        tr += s_rep[w];
-        tt += s_ret[w];
-      }
-      a.counters[2] += tr;
-      ring_ctr(a, r + 1)[1] += tt;
-    }
-    // free the slot of round r
     int32_t* Wm = a.a_W + (r % kAsyncK) * a.a_wcap;
     for (int i = tid; i < a.n_nodes; i += B) Wm[i] = 0;
     __syncthreads();
@@ -703,6 +744,7 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
       rc[0] = 0;
       rc[1] = 0;
       rc[2] = 0;
+      rc[5] = 0;
       s_G = gone_r;
       s_H = r;
       if (s_G + ring_ctr(a, r + 1)[1] < used) a.counters[1] += 1;  // another round runs
@@ -739,6 +781,7 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
   if (tid == 0) {
     ctl[0] = s_H;
     ctl[2] = s_G;
+    ctl[9] = s_D;
     *a.n_active = s_ns;
     *a.n_stepping = s_np;
     const bool finished = s_G + ring_ctr(a, s_H + 1)[1] >= used;
