@@ -299,6 +299,7 @@ void ppg_destroy(ppg_ctx* ctx) {
     if (ctx->chunk_ev[k]) cudaEventDestroy(ctx->chunk_ev[k]);
   }
   if (ctx->h_nactive) cudaFreeHost(ctx->h_nactive);
+  if (ctx->h_epochs) cudaFreeHost(ctx->h_epochs);
   ctx->l_go.release();
   for (DevBuf* b : {&ctx->l_around, &ctx->l_astate, &ctx->l_aW, &ctx->l_actr, &ctx->l_adl, &ctx->l_actl, &ctx->trace_buf,
                     &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract})
@@ -701,6 +702,7 @@ static bool streamed_available(ppg_ctx* ctx) {
   if (ctx->b_pipe.ensure(2 * kMaxSlices * sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(ctx->b_pipe.p, 0, 2 * kMaxSlices * sizeof(unsigned)) != cudaSuccess)
     return false;
+  if (!ctx->h_epochs && cudaMallocHost(&ctx->h_epochs, kMaxSlices * sizeof(unsigned)) != cudaSuccess) return false;
   ctx->streamed = 1;
   return true;
 }
@@ -761,11 +763,32 @@ static int batch_resolve_streamed(ppg_ctx* ctx, const ppg_shapes* sh, const doub
     const char* v = std::getenv("PPG_SLICE_ENVS");  // experiments; default 16K envs per slice (measured best of 4K-32K)
     return v && std::atoi(v) >= 256 ? std::atoi(v) : 16384;
   }();
-  const int want = (E + per_slice - 1) / per_slice;
+  // PPG_SLICE_SCHED=0: uniform slices of PPG_SLICE_ENVS, each copied on its
+  // own.  Default (tapered): the kernel sees kMaxSlices small slices, copied
+  // in groups that shrink toward the end of the batch (big early groups,
+  // single slices last), so the envs that land last are few and the batch's
+  // tail (the heaviest env of the last-landing group) starts early.
+  static const bool tapered = [] {
+    const char* v = std::getenv("PPG_SLICE_SCHED");
+    return !(v && v[0] == '0');
+  }();
+  const int want = tapered ? (E + 2047) / 2048 : (E + per_slice - 1) / per_slice;
   const int slices = want < 2 ? 2 : (want > kMaxSlices ? kMaxSlices : want);
   // multiples of 16 envs: no cache line of any input array spans two slices
   const int slice_envs = ((E + slices - 1) / slices + 15) / 16 * 16;
   const int ns = (E + slice_envs - 1) / slice_envs;
+  int group_end[kMaxSlices];  // copy groups: slices [group_end[g-1], group_end[g])
+  int ng = 0;
+  if (tapered) {  // ns = 32: 8 8 6 4 3 2 1 slices
+    const int g0 = ns / 4 > 1 ? ns / 4 : 1;
+    for (int k = 0, g = g0, i = 0; k < ns; ++i) {
+      k = k + g < ns ? k + g : ns;
+      group_end[ng++] = k;
+      if (i > 0) g = g * 3 / 4 > 1 ? g * 3 / 4 : 1;
+    }
+  } else {
+    for (int k = 1; k <= ns; ++k) group_end[ng++] = k;
+  }
   CK(ctx->shape_in.ensure(static_cast<size_t>(E) * n * sizeof(double)));
   double* rad = ctx->shape_in.as<double>();
   unsigned* ready = ctx->b_pipe.as<unsigned>();
@@ -793,18 +816,32 @@ static int batch_resolve_streamed(ppg_ctx* ctx, const ppg_shapes* sh, const doub
   double* d_push = ctx->b_push.as<double>();
   int32_t* d_st = ctx->b_status.as<int32_t>();
   double* d_res = ctx->b_resid.as<double>();
-  for (int k = 0; k < ns; ++k) {
-    const size_t e0 = static_cast<size_t>(k) * slice_envs;
-    const size_t ek = (k + 1 == ns ? E : e0 + slice_envs) - e0;
+  // ready flags: one small pinned-host copy per group (default) or one
+  // cuStreamWriteValue32 per slice (PPG_SLICE_FLAGS=m); measured 1.5 % apart
+  static const bool flag_copy = [] {
+    const char* v = std::getenv("PPG_SLICE_FLAGS");
+    return !(v && v[0] == 'm');
+  }();
+  if (flag_copy)
+    for (int k = 0; k < kMaxSlices; ++k) ctx->h_epochs[k] = epoch;  // the previous call's copies are complete
+  for (int g = 0; g < ng; ++g) {
+    const int k0 = g ? group_end[g - 1] : 0, k1 = group_end[g];
+    const size_t e0 = static_cast<size_t>(k0) * slice_envs;
+    const size_t ek = (k1 == ns ? E : static_cast<size_t>(k1) * slice_envs) - e0;
     CK(cudaMemcpyAsync(d_in + e0 * row, poses_in + e0 * row, ek * row * 8, cudaMemcpyHostToDevice, in));
     CK(cudaMemcpyAsync(d_push + e0 * 4, pushes + e0 * 4, ek * 32, cudaMemcpyHostToDevice, in));
     CK(cudaMemcpyAsync(rad + e0 * n, sh->radius + e0 * n, ek * n * 8, cudaMemcpyHostToDevice, in));
-    if (write32(reinterpret_cast<CUstream>(in), reinterpret_cast<CUdeviceptr>(ready + k), epoch,
-                CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
-      ctx->err = "cuStreamWriteValue32 failed";
-      return PPG_ECUDA;
+    if (flag_copy) {  // the group's ready flags in one copy, ordered after its data on the stream
+      CK(cudaMemcpyAsync(ready + k0, ctx->h_epochs, (k1 - k0) * sizeof(unsigned), cudaMemcpyHostToDevice, in));
+    } else {
+      for (int k = k0; k < k1; ++k)
+        if (write32(reinterpret_cast<CUstream>(in), reinterpret_cast<CUdeviceptr>(ready + k), epoch,
+                    CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+          ctx->err = "cuStreamWriteValue32 failed";
+          return PPG_ECUDA;
+        }
     }
-    if (k == 0) CK(cudaEventRecord(ctx->pipe_ev, in));
+    if (g == 0) CK(cudaEventRecord(ctx->pipe_ev, in));
     mark(in);
   }
   // physics: one launch over all E envs once slice 0 is resident
@@ -870,7 +907,7 @@ static int batch_resolve_streamed(ppg_ctx* ctx, const ppg_shapes* sh, const doub
     for (int i = 1; i < ntev; ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, tev[0], tev[i]);
-      std::fprintf(stderr, i == ns + 1 ? " | kernel %.3f | out" : " %.3f", ms);
+      std::fprintf(stderr, i == ng + 1 ? " | kernel %.3f | out" : " %.3f", ms);
     }
     std::fprintf(stderr, "\n");
     for (int i = 0; i < ntev; ++i) cudaEventDestroy(tev[i]);

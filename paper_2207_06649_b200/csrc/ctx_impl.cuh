@@ -182,6 +182,7 @@ struct ppg_ctx {
   // signal "slice k resident" to the kernel and "slice k finished" to the
   // copy-back stream
   ppg::DevBuf b_pipe;                    // ready flags [kMaxSlices] | done counters [kMaxSlices]
+  unsigned* h_epochs = nullptr;          // pinned [kMaxSlices]: ready-flag values copied by the copy-in stream
   unsigned pipe_epoch = 0;
   int streamed = -1;                      // -1 not probed, 0 off (PPG_STREAMED=0 / no stream mem ops), 1 on
   void* fn_write32 = nullptr;             // cuStreamWriteValue32

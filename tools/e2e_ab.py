@@ -31,4 +31,6 @@ for _ in range(30):
     t = time.perf_counter(); step(); ts.append(time.perf_counter() - t)
 ts = np.array(ts)
 print(json.dumps({"E": E, "streamed": os.environ.get("PPG_STREAMED", "1"), "mean_ms": ts.mean() * 1e3, "min_ms": ts.min() * 1e3,
-                  "e2e_Msteps": E / ts.mean() / 1e6, "status0": int((h_st.numpy() == 0).sum())}))
+                  "e2e_Msteps": E / ts.mean() / 1e6, "status0": int((h_st.numpy() == 0).sum()),
+                  "sched": os.environ.get("PPG_SLICE_SCHED", "1"), "median_ms": float(np.median(ts)) * 1e3,
+                  "digest": hash(h_out.numpy().tobytes() + h_st.numpy().tobytes() + h_res.numpy().tobytes())}))
