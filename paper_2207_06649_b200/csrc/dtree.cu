@@ -127,29 +127,41 @@ constexpr unsigned kAll = 0xffffffffu;
 // pops the untried action and updates virtual visits / selectable counts.
 constexpr int kSelThreads = 256;
 
+// (score, insertion index, packed child) first-maximum merge; the packed
+// child is 2 * node + dt_self(node), carried so the winner needs no reload.
+__device__ __forceinline__ void sel_merge(double& bs, int& bk, int& bp, double os, int ok, int op) {
+  if (os > bs || (os == bs && ok < bk)) {
+    bs = os;
+    bk = ok;
+    bp = op;
+  }
+}
+
 __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
   constexpr int kWarps = kSelThreads / 32;
-  __shared__ double s_bs[kWarps];
-  __shared__ int s_bk[kWarps];
-  __shared__ int s_x;
-  __shared__ int s_path[kMaxTreeDepth];  // the draw's root path (node at each depth)
+  // per-level warp partials, double-buffered by level parity: ONE block
+  // barrier per level (every warp then reduces the partials itself)
+  __shared__ double s_bs[2][kWarps];
+  __shared__ int s_bk[2][kWarps], s_bp[2][kWarps];
   DTScal* sc = t.sc;
   const int tid = threadIdx.x, l = tid & 31, wid = tid >> 5;
   const int dT = sc->dT;
   const double cexp = sc->c_explore;
   int draws = 0;
   bool bad = false;
+  int parity = 0;
   if (sc->stop < 0) {
     for (; draws < t.n_envs; ++draws) {
       if (!dt_selectable(t, 0, dT)) break;  // every thread reads the same state
       int x = 0, lvl = 0;
-      if (tid == 0) s_path[0] = 0;
-      while (!dt_self(t, x, dT)) {  // descend_virtual (pmbs.cpp:30-48)
+      int my_node = 0;  // thread d keeps the root path's node at depth d
+      bool self = dt_self(t, 0, dT);
+      while (!self) {  // descend_virtual (pmbs.cpp:30-48)
         const long long co = t.u_off[x];
         const int cn = t.c_n[x];
         const double lg = t.logtab[t.visits[x] + t.vv[x]];  // log(n_parent)
         double bs = -INFINITY;
-        int bk = INT_MAX;
+        int bk = INT_MAX, bp = -2;
         constexpr int kScanU = 2;
         for (int k0 = 0; k0 < cn; k0 += kSelThreads * kScanU) {
           int ch[kScanU];
@@ -158,14 +170,17 @@ __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
             const int k = k0 + kSelThreads * u + tid;
             ch[u] = k < cn ? t.cpool[co + k] : -1;
           }
-          bool sel[kScanU];
+          bool sel[kScanU], slf[kScanU];
           long long nci[kScanU];
           double qc[kScanU];
 #pragma unroll
           for (int u = 0; u < kScanU; ++u) {
-            sel[u] = ch[u] >= 0 && dt_selectable(t, ch[u], dT);
-            nci[u] = ch[u] >= 0 ? t.visits[ch[u]] + t.vv[ch[u]] : 0;
-            qc[u] = ch[u] >= 0 ? t.q[ch[u]] : 0.0;
+            const int c = ch[u] >= 0 ? ch[u] : 0;
+            const bool ok = ch[u] >= 0 && t.flags[c] == 0;
+            slf[u] = ok && t.depth[c] < dT && t.u_head[c] < t.u_n[c];
+            sel[u] = slf[u] || (ok && t.selc[c] > 0);  // dt_selectable
+            nci[u] = ch[u] >= 0 ? t.visits[c] + t.vv[c] : 0;
+            qc[u] = ch[u] >= 0 ? t.q[c] : 0.0;
           }
 #pragma unroll
           for (int u = 0; u < kScanU; ++u) {
@@ -178,50 +193,39 @@ __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
             if (sv > bs) {
               bs = sv;
               bk = k0 + kSelThreads * u + tid;
+              bp = 2 * ch[u] + (slf[u] ? 1 : 0);
             }
           }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {  // first maximum in insertion order
-          const double os = __shfl_xor_sync(kAll, bs, o);
-          const int ok = __shfl_xor_sync(kAll, bk, o);
-          if (os > bs || (os == bs && ok < bk)) {
-            bs = os;
-            bk = ok;
-          }
-        }
+        for (int o = 16; o > 0; o >>= 1)  // first maximum in insertion order
+          sel_merge(bs, bk, bp, __shfl_xor_sync(kAll, bs, o), __shfl_xor_sync(kAll, bk, o),
+                    __shfl_xor_sync(kAll, bp, o));
         if (l == 0) {
-          s_bs[wid] = bs;
-          s_bk[wid] = bk;
+          s_bs[parity][wid] = bs;
+          s_bk[parity][wid] = bk;
+          s_bp[parity][wid] = bp;
         }
         __syncthreads();
-        if (wid == 0) {
-          bs = l < kWarps ? s_bs[l] : -INFINITY;
-          bk = l < kWarps ? s_bk[l] : INT_MAX;
+        bs = l < kWarps ? s_bs[parity][l] : -INFINITY;
+        bk = l < kWarps ? s_bk[parity][l] : INT_MAX;
+        bp = l < kWarps ? s_bp[parity][l] : -2;
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double os = __shfl_xor_sync(kAll, bs, o);
-            const int ok = __shfl_xor_sync(kAll, bk, o);
-            if (os > bs || (os == bs && ok < bk)) {
-              bs = os;
-              bk = ok;
-            }
-          }
-          if (l == 0) {
-            s_x = bk == INT_MAX ? -1 : t.cpool[co + bk];  // -1: impossible under the selc invariant
-            if (lvl + 1 < kMaxTreeDepth) s_path[lvl + 1] = s_x;
-          }
-        }
-        __syncthreads();
-        x = s_x;
+        for (int o = 16; o > 0; o >>= 1)
+          sel_merge(bs, bk, bp, __shfl_xor_sync(kAll, bs, o), __shfl_xor_sync(kAll, bk, o),
+                    __shfl_xor_sync(kAll, bp, o));
+        parity ^= 1;
         ++lvl;
-        if (x < 0) {
+        if (bk == INT_MAX) {  // impossible under the selc invariant
           bad = true;
           break;
         }
+        x = bp >> 1;
+        self = (bp & 1) != 0;
+        if (tid == lvl) my_node = x;
       }
       if (bad) break;
-      if (tid <= lvl) t.vv[s_path[tid]] += 1;  // virtual visit on the root path (one node per thread)
+      if (tid <= lvl) t.vv[my_node] += 1;  // virtual visit on the root path (one node per thread)
       if (tid == 0) {  // pop_untried (mcts.cpp:13-16)
         const int h = t.u_head[x];
         t.sel_node[draws] = x;
