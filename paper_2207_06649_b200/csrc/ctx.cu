@@ -3,6 +3,7 @@
 // kernels.  The PMBS tree planner that sits on top lives in planner.cpp.
 #include <cuda.h>  // stream memory operation types (entry points resolved at run time)
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <cmath>
 #include <cstdio>
@@ -572,6 +573,28 @@ static int launch_resolve_poly_t(ppg_ctx* ctx, const SimConst& C, ResolveArgs a,
     a.work_counter = ctx->b_counter.as<int>() + 4 * slot;
     CK(cudaMemsetAsync(a.work_counter, 0, 4, st));
     grid = cap;
+    // more envs than resident warps: fetch the likely-heavy envs first
+    // (poly_order_key_kernel; PPG_POLY_ORDER=0 keeps index order)
+    static const bool order = [] {
+      const char* v = std::getenv("PPG_POLY_ORDER");
+      return !(v && v[0] == '0');
+    }();
+    if (order && !a.idx && !a.E_dev) {
+      size_t scratch = 0;
+      CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, scratch, static_cast<const unsigned*>(nullptr),
+                                                   static_cast<unsigned*>(nullptr), static_cast<const int*>(nullptr),
+                                                   static_cast<int*>(nullptr), E, 0, 16, st));
+      const size_t En = (static_cast<size_t>(E) + 63) / 64 * 64;
+      CK(ctx->ord_buf[slot].ensure(4 * En * 4 + scratch));
+      unsigned* k_in = ctx->ord_buf[slot].as<unsigned>();
+      unsigned* k_out = k_in + En;
+      int* v_in = reinterpret_cast<int*>(k_out + En);
+      int* v_out = v_in + En;
+      poly_order_key_kernel<<<(E + 255) / 256, 256, 0, st>>>(a, k_in, v_in);
+      CK(cudaGetLastError());
+      CK(cub::DeviceRadixSort::SortPairsDescending(v_out + En, scratch, k_in, k_out, v_in, v_out, E, 0, 16, st));
+      a.idx = v_out;
+    }
   }
   resolve_warp_kernel<NW, true><<<grid, kWarpsPerBlock * 32, 0, st>>>(C, a);
   CK(cudaGetLastError());

@@ -28,6 +28,7 @@ __global__ void lock_step_kernel(const __grid_constant__ SimConst C, LockArgs a)
 __global__ void lock_step_count_kernel(const __grid_constant__ SimConst C, LockArgs a, unsigned long long* ops);
 __global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
+__global__ void poly_order_key_kernel(ResolveArgs a, unsigned* key, int* val);
 template <int NW, bool kPoly>
 __global__ void resolve_warp_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
 template <int NW, bool kPoly>
@@ -170,6 +171,7 @@ struct ppg_ctx {
   cudaStream_t chunk_stream[ppg::kChunks] = {};
   cudaEvent_t chunk_ev[ppg::kChunks] = {};  // slice k's host->device copies done
   DevBuf chunk_in[ppg::kChunks], chunk_buf[ppg::kChunks];
+  DevBuf ord_buf[ppg::kChunks];          // polygon batches: launch-order keys, env order, sort scratch
   ppg::DTreeState* dtree = nullptr;       // device-resident PMBS tree (dtree.cu)
   int planner = 0;                        // PPG_PLANNER_AUTO / _HOST / _DEVICE (PPG_PLANNER env)
   int warp_max_envs = 2048;             // batch_resolve on discs (n <= kDiscMaxN): latency mode up to this many envs; PPG_WARP_MAX

@@ -97,6 +97,37 @@ __global__ void __launch_bounds__(128) resolve_kernel(const __grid_constant__ Si
 }
 
 template __global__ void resolve_kernel<false>(const __grid_constant__ SimConst, ResolveArgs);
+// Launch-order key of a polygon batch (one warp per env, dynamic env fetch):
+// envs whose push path runs into many polygon vertices tend to need the most
+// projection iterations, and a heavy env fetched late is the launch's tail.
+// key = (sum of the vertex counts of polygons within 0.08 of the push
+// segment)^2 + objects within 0.08 — a scheduling hint only (results are
+// element-wise and independent of the order; tools/poly_sort_bound.py
+// measured this key against cost-ordered and index-ordered launches).
+__global__ void poly_order_key_kernel(ResolveArgs a, unsigned* key, int* val) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.E) return;
+  const int n = a.S.n;
+  const ShapeView S = a.S.view(a.S.T == 1 ? 0 : e);
+  const double* pu = a.pushes + static_cast<size_t>(e) * 4;
+  const float sx = static_cast<float>(pu[0]), sy = static_cast<float>(pu[1]);
+  const float dx = static_cast<float>(pu[2]) - sx, dy = static_cast<float>(pu[3]) - sy;
+  const float inv = 1.0f / fmaxf(dx * dx + dy * dy, 1e-30f);
+  const double* p = a.poses_in + static_cast<size_t>(e) * n * 3;
+  int cnt = 0, nvs = 0;
+  for (int i = 0; i < n; ++i) {
+    const float px = static_cast<float>(p[3 * i]) - sx, py = static_cast<float>(p[3 * i + 1]) - sy;
+    const float t = fminf(fmaxf((px * dx + py * dy) * inv, 0.0f), 1.0f);
+    const float qx = px - t * dx, qy = py - t * dy;
+    if (qx * qx + qy * qy < 0.08f * 0.08f) {
+      ++cnt;
+      if (S.kind_(i) != 0) nvs += S.nv_(i);
+    }
+  }
+  key[e] = static_cast<unsigned>(nvs * nvs + cnt);
+  val[e] = e;
+}
+
 template __global__ void resolve_kernel<true>(const __grid_constant__ SimConst, ResolveArgs);
 
 // Full ordered candidate list (object, angle) of sample_pushes.

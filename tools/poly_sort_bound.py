@@ -106,6 +106,16 @@ def main():
     keys = {"cost_pair_broad": c[:, 3], "cost_pair_narrow": c[:, 4] if c.shape[1] > 4 else c[:, 3],
             "near_count": near.sum(1).astype(np.float64),
             "near_polygons": (near & (table.kind != 0)).sum(1) * 16.0 + near.sum(1)}
+    poly = table.kind != 0
+    nv = np.where(poly, table.n_vertices, 0).astype(np.float64)
+    for th in (0.03, 0.05, 0.12, 0.2):
+        nr = dist < th
+        keys[f"np16_{th}"] = (nr & poly).sum(1) * 16.0 + nr.sum(1)
+    for th in (0.05, 0.08, 0.12):
+        nr = dist < th
+        keys[f"nvsum_{th}"] = (nr * nv).sum(1) + nr.sum(1)
+        keys[f"nvsq_{th}"] = ((nr * nv).sum(1)) ** 2 + nr.sum(1)
+    keys["all_polygons"] = poly.sum(1) * 16.0 + (dist < 0.08).sum(1)
     for name, key in keys.items():
         perm = np.argsort(-key, kind="stable")
         t = upload(perm)
