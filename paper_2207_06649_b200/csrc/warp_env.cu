@@ -317,8 +317,11 @@ __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockA
   if (tid < kRingCtr * kAsyncK) a.a_ctr[tid] = 0;
 }
 
+#ifndef PPG_ASYNC_BLOCKS
+#define PPG_ASYNC_BLOCKS 3  // resident blocks per SM the register budget is sized for
+#endif
 template <int NW, bool kPoly>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3) lock_async_kernel(const __grid_constant__ SimConst C,
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_async_kernel(const __grid_constant__ SimConst C,
                                                                            LockArgs a) {
   PPG_POLY_SMEM
   lock_dyn(a);
