@@ -361,3 +361,179 @@ def test_early_decisions_happen_with_one_dominant_node():
     got = asynchronous_early(nodes, 200, True, 10, 3, 16, random.Random(5))
     assert got[0] == ref[0] and sorted(got[1]) == sorted(ref[1]) and got[2] == ref[2]
     assert got[3] > 0
+
+
+def waves_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, switch_wave=None):
+    """The wave rounds (csrc/warp_env.cu wave_harvest / sample / physics /
+    post kernels) with early decisions, then — from `switch_wave` on — the
+    asynchronous kernel continuing from the wave state.  A wave = one harvest
+    pass (decide every robust round in order, apply the decisions to the
+    by-grasp envs listed so far, complete rounds in order) followed by one
+    step attempt of every READY env within the ring bound; a step may YIELD
+    (the physics budget ran out: it finishes in a later wave)."""
+    n_nodes = len(nodes)
+    used = n_envs if leaf_parallel else n_nodes
+    env_node = split(used, n_nodes)
+    tasks = [Cursor(env_node[e], e, nodes, cap, seed) for e in range(used)]
+    calls = [(env_node[e], e) for e in range(used)]
+    rewards = [0.0] * n_nodes
+    inc = [0] * used
+    W0 = [sum(t.max_remaining() for e, t in enumerate(tasks) if env_node[e] == i and not t.done)
+          for i in range(n_nodes)]
+    best0 = max(range(n_nodes), key=lambda i: (W0[i], -i))
+    best0 = best0 if W0[best0] > 0 else -1
+    for e in range(used):
+        if tasks[e].done:
+            rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+            if leaf_parallel and tasks[e].by_grasp and best0 >= 0:
+                env_node[e] = best0
+                inc[e] += 1
+                tasks[e] = Cursor(best0, e, nodes, cap, seed, inc[e])
+                calls.append((best0, e))
+    READY, AWAIT, GONE, PHYS = 0, 1, 2, 3
+    state = [GONE if tasks[e].done else READY for e in range(used)]
+    rnd = [0] * used
+    ring_W = defaultdict(lambda: [0] * n_nodes)
+    arrive, gone_at, done_list = defaultdict(int), defaultdict(int), defaultdict(list)
+    applied = defaultdict(int)
+    decided = {}
+    st = {"F": 0, "D": 0, "G": sum(1 for s in state if s == GONE),
+          "rounds": 1 if any(s == READY for s in state) else 0}
+
+    def robust(r):
+        gone_eff = st["G"] + sum(gone_at[q] for q in range(st["F"] + 1, r + 1))
+        strag = used - gone_eff - arrive[r]
+        W = ring_W[r]
+        m1 = max(W)
+        b = W.index(m1)
+        m2 = max([W[j] for j in range(n_nodes) if j != b], default=0)
+        ok = (strag > 0 or arrive[r] > 0) and (strag == 0 or (m1 > 0 and m2 + strag * (cap - 1) < m1))
+        return ok, (b if leaf_parallel and m1 > 0 else -1)
+
+    def apply(e):
+        b = decided[rnd[e]]
+        if b >= 0:
+            env_node[e] = b
+            inc[e] += 1
+            tasks[e] = Cursor(b, e, nodes, cap, seed, inc[e])
+            assert not tasks[e].done
+            calls.append((b, e))
+            state[e] = READY
+        else:
+            state[e] = GONE
+            gone_at[rnd[e] + 1] += 1
+
+    def finish_step(e):
+        r = rnd[e] + 1
+        tasks[e].step()
+        rnd[e] = r
+        if not tasks[e].done:
+            ring_W[r][env_node[e]] += tasks[e].max_remaining()
+            state[e] = READY
+        else:
+            rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)  # folded in at arrival
+            done_list[r].append(e)
+            if leaf_parallel and tasks[e].by_grasp:
+                state[e] = AWAIT
+            else:
+                state[e] = GONE
+                gone_at[r + 1] += 1
+        arrive[r] += 1
+
+    def complete(r):
+        st["G"] += gone_at.pop(r, 0)
+        arrive.pop(r, None)
+        ring_W.pop(r, None)
+        st["F"] = r
+        if st["G"] + gone_at[r + 1] < used:
+            st["rounds"] += 1
+
+    wave = 0
+    while st["G"] + gone_at[st["F"] + 1] < used:
+        if switch_wave is not None and wave >= switch_wave:
+            break
+        # harvest pass
+        while True:
+            prog = False
+            r = st["D"] + 1
+            if r <= st["F"] + K - 1:
+                ok, b = robust(r)
+                if ok:
+                    decided[r] = b
+                    st["D"] = r
+                    prog = True
+            for q in range(st["F"] + 1, st["D"] + 1):
+                lst = done_list[q]
+                for e in lst[applied[q]:]:
+                    if state[e] == AWAIT:
+                        apply(e)
+                applied[q] = len(lst)
+            rf = st["F"] + 1
+            if (st["G"] + gone_at[rf] < used and st["D"] >= rf
+                    and arrive[rf] == used - (st["G"] + gone_at[rf])):
+                complete(rf)
+                done_list.pop(rf, None)
+                applied.pop(rf, None)
+                prog = True
+            if not prog:
+                break
+        # the wave: every READY env within the ring steps; a physics step may yield
+        for e in range(used):
+            if state[e] == READY and rnd[e] + 1 <= st["F"] + K - 1:
+                state[e] = PHYS
+        for e in range(used):
+            if state[e] == PHYS and rng.random() < 0.7:
+                finish_step(e)
+        wave += 1
+        assert wave < 10000, "waves did not terminate"
+    # hand-over: pending physics finishes, then the asynchronous kernel (v2) continues
+    for e in range(used):
+        if state[e] == PHYS:
+            finish_step(e)
+    while True:
+        acts = []
+        F, D = st["F"], st["D"]
+        for e in range(used):
+            if state[e] == READY and rnd[e] + 1 <= F + K - 1:
+                acts.append(("step", e))
+            elif state[e] == AWAIT and rnd[e] in decided:
+                acts.append(("apply", e))
+        r = D + 1
+        if r <= F + K - 1 and r not in decided and robust(r)[0]:
+            acts.append(("decide", r))
+        if F + 1 in decided and arrive[F + 1] == used - (st["G"] + gone_at[F + 1]):
+            acts.append(("advance", F + 1))
+        if not acts:
+            assert st["G"] + gone_at[st["F"] + 1] >= used, "stalled"
+            break
+        kind, x = rng.choice(acts)
+        if kind == "step":
+            finish_step(x)
+        elif kind == "apply":
+            apply(x)
+        elif kind == "decide":
+            decided[x] = robust(x)[1]
+            st["D"] = x
+        else:
+            complete(x)
+    return rewards, calls, st["rounds"]
+
+
+@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("K", [2, 4, 16])
+def test_wave_rounds_with_early_decisions_equal_lockstep(seed, K):
+    """Wave rounds (yielding physics, harvest passes with early decisions) and
+    the hand-over to the asynchronous kernel at a random wave give the
+    reference's rewards, cursor creations and round count."""
+    cap = 10
+    nodes = _nodes(seed, 3 + seed % 9, cap)
+    n_envs = len(nodes) + 20 + 7 * seed
+    for leaf in (True, False):
+        ref = lockstep(nodes, n_envs, leaf, cap, seed)
+        for sched in range(3):
+            rng = random.Random(777 * seed + sched)
+            switch = None if sched == 0 else rng.randint(0, 12)
+            got = waves_early(nodes, n_envs, leaf, cap, seed, K, rng, switch)
+            assert got[0] == ref[0], (leaf, sched)
+            assert sorted(got[1]) == sorted(ref[1]), (leaf, sched)
+            assert got[2] == ref[2], (leaf, sched)
