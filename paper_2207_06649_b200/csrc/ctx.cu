@@ -303,7 +303,7 @@ void ppg_destroy(ppg_ctx* ctx) {
   if (ctx->h_epochs) cudaFreeHost(ctx->h_epochs);
   ctx->l_go.release();
   for (DevBuf* b : {&ctx->l_around, &ctx->l_astate, &ctx->l_aW, &ctx->l_actr, &ctx->l_adl, &ctx->l_actl, &ctx->trace_buf,
-                    &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract})
+                    &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract, &ctx->l_gring})
     b->release();
   if (ctx->h_go) cudaFreeHost(ctx->h_go);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -65,6 +65,7 @@ constexpr int warp_words(int n) { return n <= 8 ? 1 : n <= 11 ? 2 : n <= 16 ? 4 
 __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void wave_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
+__global__ void wave_pack_kernel(LockArgs a);
 __global__ void wave_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void wave_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 template <int NW, bool kPoly>
@@ -203,6 +204,7 @@ struct ppg_ctx {
   int wave_budget = 192;                  // projection iterations per env per wave (PPG_WAVE_BUDGET)
   int wave_switch = 12288;                // envs still running below which waves hand over to async (PPG_WAVE_SWITCH)
   ppg::DevBuf l_fin, l_rsi, l_ract;       // wave rounds: post list, resumable physics progress
+  ppg::DevBuf l_gring;                   // sharded wave rounds: the exchanged ring (LockArgs.g_ring)
   int32_t* h_go = nullptr;                // pinned copy
 };
 
@@ -252,6 +254,17 @@ int group_allreduce_sum_i64(ppg_ctx* ectx, Group* g, long long* const* bufs, siz
 // Waits for every member's stream (bounded by PPG_NCCL_TIMEOUT_S; a timeout
 // aborts the communicators and reports an error instead of hanging).
 int group_wait(ppg_ctx* ectx, Group* g);
+// Sharded wave rounds: after the round-0 harvest, every remaining round as
+// waves with ONE exchange per wave (multi.cu).  Member k runs la[k] / ra[k]
+// with constants C[k]; P = n_nodes of the call; work = grid sizing.
+struct ShardWave {
+  ppg_ctx* c;
+  const SimConst* C;
+  LockArgs la;
+  ResolveArgs ra;
+};
+bool shard_waves_enabled(const ppg_ctx* ctx);
+int sharded_wave_rounds(ppg_ctx* ectx, Group* g, std::vector<ShardWave>& sw, int P, int work);
 void group_destroy(ppg_ctx* ctx);
 int simulate_sharded(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
                      int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, double* rewards_out,

@@ -1290,6 +1290,8 @@ int run_pmbs_sharded(ppg_ctx* ctx, const double* root_poses, double* action_out,
     }
     set_shard(k);
   }
+  bool waves = true;
+  for (int k = 0; k < M; ++k) waves = waves && shard_waves_enabled(m[k]);
   std::vector<DTScal> h(M);
   std::vector<int32_t*> wb(M);
   std::vector<unsigned long long*> rb(M), vb(M);
@@ -1389,6 +1391,15 @@ int run_pmbs_sharded(ppg_ctx* ctx, const double* root_poses, double* action_out,
             return PPG_EINVAL;
           }
         if (!go) break;
+        if (waves) {  // every remaining round as waves, one exchange per wave (multi.cu)
+          std::vector<ShardWave> sw(M);
+          for (int k = 0; k < M; ++k) {
+            DTreeState& S = *m[k]->dtree;
+            sw[k] = ShardWave{m[k], &S.C, S.la, S.lra};
+          }
+          if ((rc = sharded_wave_rounds(ctx, g, sw, P, work)) != PPG_SUCCESS) return rc;
+          break;
+        }
         for (int k = 0; k < M; ++k) {
           DCK(cudaSetDevice(m[k]->device));
           DCK(cudaGraphLaunch(m[k]->dtree->exec_round, m[k]->stream));

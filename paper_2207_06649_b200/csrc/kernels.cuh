@@ -158,6 +158,10 @@ struct LockArgs {
   int32_t* a_ctr = nullptr;
   int32_t* a_dl = nullptr;
   int32_t* a_ctl = nullptr;
+  // sharded wave rounds (multi.cu / dtree.cu): every shard's W ring [K][n_nodes]
+  // and (arrived, gone) per ring slot [K][2], summed over the shards before
+  // each wave's harvest, which decides and completes rounds from these sums
+  int32_t* g_ring = nullptr;
   int a_wcap = 0;
   // wave rounds (warp_env.cu wave_*_kernel): envs whose physics finished in
   // this wave (post pending), and the resumable physics progress

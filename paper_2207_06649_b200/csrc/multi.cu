@@ -302,6 +302,72 @@ int ensure_go(ppg_ctx* c) {
 
 }  // namespace
 
+bool shard_waves_enabled(const ppg_ctx* ctx) {
+  static const bool on = [] {
+    const char* v = std::getenv("PPG_SHARD_WAVES");
+    return !(v && v[0] == '0');
+  }();
+  // the wave physics is the lane-per-env disc kernel
+  return on && wave_enabled(ctx) && ctx->scene_all_discs && ctx->scene.n <= kDiscMaxN && ctx->disc_kernels &&
+         !ctx->warp_max_explicit;
+}
+
+// Wave rounds over shards (warp_env.cu): per wave every shard packs its W ring
+// and per-round (arrived, gone) counts, ONE all-reduce sums them, and every
+// shard's harvest decides / completes rounds from the identical sums (so all
+// shards take the same decisions and stop at the same wave) while applying
+// the decisions to its own envs; then sample, budgeted physics, post.  No
+// hand-over to the asynchronous kernel (its exchange would be continuous).
+int sharded_wave_rounds(ppg_ctx* ctx, Group* g, std::vector<ShardWave>& sw, int P, int work) {
+  const int M = static_cast<int>(sw.size());
+  const size_t count = static_cast<size_t>(kAsyncK) * P + 2 * kAsyncK;
+  std::vector<int32_t*> gb(M);
+  for (int k = 0; k < M; ++k) {
+    ppg_ctx* c = sw[k].c;
+    CK(cudaSetDevice(c->device));
+    CK(c->l_gring.ensure(count * sizeof(int32_t)));
+    LockArgs& a = sw[k].la;
+    gb[k] = a.g_ring = c->l_gring.as<int32_t>();
+    a.round_mode = nullptr;
+    a.cond = 0;
+    a.go = a.a_ctl + 7;
+    a.wave_switch = 0;  // never hand over
+    a.wave_budget = c->wave_budget;
+  }
+  const int pack_grid = static_cast<int>(std::min<size_t>((count + 255) / 256, 1024));
+  for (int wave = 0;; ++wave) {
+    for (int k = 0; k < M; ++k) {
+      ppg_ctx* c = sw[k].c;
+      CK(cudaSetDevice(c->device));
+      wave_pack_kernel<<<pack_grid, 256, 0, c->stream>>>(sw[k].la);
+      CK(cudaGetLastError());
+    }
+    int rc = group_allreduce_sum_i32(ctx, g, gb.data(), count);
+    if (rc != PPG_SUCCESS) return rc;
+    for (int k = 0; k < M; ++k) {
+      ppg_ctx* c = sw[k].c;
+      CK(cudaSetDevice(c->device));
+      if ((rc = launch_wave(c, *sw[k].C, sw[k].la, sw[k].ra, work, c->stream)) != PPG_SUCCESS) {
+        ctx->err = c->err;
+        return rc;
+      }
+      CK(cudaMemcpyAsync(c->h_go, sw[k].la.a_ctl + 7, 4, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if ((rc = group_wait(ctx, g)) != PPG_SUCCESS) return rc;
+    const int go = sw[0].c->h_go[0];
+    for (int k = 1; k < M; ++k)
+      if (sw[k].c->h_go[0] != go) {
+        ctx->err = "sharded wave rounds: shards disagree on termination";
+        return PPG_EINVAL;
+      }
+    if (!go) return PPG_SUCCESS;
+    if (wave > 4 * kLockRoundLimit) {
+      ctx->err = "sharded wave rounds did not terminate";
+      return PPG_EINVAL;
+    }
+  }
+}
+
 int simulate_sharded(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int n_envs,
                      int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap, double* rewards_out,
                      int64_t* counters) {
@@ -328,6 +394,8 @@ int simulate_sharded(ppg_ctx* ctx, const double* node_poses, const int32_t* node
     c->la.go = c->l_go.as<int32_t>();
     c->lock_active_hint = hi - lo;
   }
+  bool waves = true;
+  for (int k = 0; k < M; ++k) waves = waves && shard_waves_enabled(g->m[k]);
   std::vector<int32_t*> wb(M);
   std::vector<unsigned long long*> rb(M);
   std::vector<long long*> cb(M);
@@ -362,6 +430,13 @@ int simulate_sharded(ppg_ctx* ctx, const double* node_poses, const int32_t* node
         return PPG_EINVAL;
       }
     if (!go) break;
+    if (waves) {  // every remaining round as waves, one exchange per wave
+      std::vector<ShardWave> sw(M);
+      for (int k = 0; k < M; ++k) sw[k] = ShardWave{g->m[k], &g->m[k]->lc, g->m[k]->la, g->m[k]->lra};
+      const int work = (used + G - 1) / G;
+      if ((rc = sharded_wave_rounds(ctx, g, sw, n_nodes, work)) != PPG_SUCCESS) return rc;
+      break;
+    }
     for (int k = 0; k < M; ++k) {
       ppg_ctx* c = g->m[k];
       CK(cudaSetDevice(c->device));

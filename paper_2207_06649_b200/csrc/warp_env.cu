@@ -591,6 +591,28 @@ PPG_DI void top2_merge(int& m1, int& b1, int& m2, int om1, int ob1, int om2) {
   }
 }
 
+// Sharded wave rounds: this shard's W ring and per-slot (arrived, gone)
+// counts into g_ring, which the host then all-reduces (sum) over the shards.
+// Before the call's first wave (nothing initialised yet) the contribution is 0.
+__global__ void wave_pack_kernel(LockArgs a) {
+  lock_dyn(a);
+  const int P = a.n_nodes;
+  const bool fresh = a.a_ctl[4] == 0;
+  const int total = kAsyncK * P + 2 * kAsyncK;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    int v = 0;
+    if (!fresh) {
+      if (i < kAsyncK * P) {
+        v = a.a_W[(i / P) * a.a_wcap + i % P];
+      } else {
+        const int k = i - kAsyncK * P;
+        v = a.a_ctr[kRingCtr * (k >> 1) + (k & 1)];
+      }
+    }
+    a.g_ring[i] = v;
+  }
+}
+
 // Between waves (one block): decide every round whose re-purposing target is
 // already fixed (the early decision of lock_async_kernel: max W_known > every
 // other W_known + stragglers * (cap - 1)), apply the decisions to the
@@ -605,7 +627,17 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
   const int tid = threadIdx.x, B = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int used = a.used;
   int32_t* ctl = a.a_ctl;
-  __shared__ int s_H, s_G, s_D, s_ns, s_np, s_prog, s_strag, s_try;
+  // decisions, completion and termination read the batch-wide values: this
+  // context's own ring, or (sharded) the ring summed over the shards
+  const bool sharded = a.g_ring != nullptr;
+  const int used_g = sharded ? a.used_global : used;
+  const int P = a.n_nodes;
+  auto W_of = [&](int r) -> const int32_t* {
+    return sharded ? a.g_ring + (r % kAsyncK) * P : a.a_W + (r % kAsyncK) * a.a_wcap;
+  };
+  auto arr_of = [&](int r) { return sharded ? a.g_ring[kAsyncK * P + 2 * (r % kAsyncK)] : ring_ctr(a, r)[0]; };
+  auto gone_of = [&](int r) { return sharded ? a.g_ring[kAsyncK * P + 2 * (r % kAsyncK) + 1] : ring_ctr(a, r)[1]; };
+  __shared__ int s_H, s_G, s_D, s_ns, s_np, s_prog, s_strag, s_try, s_F0;
   __shared__ int s_m1[32], s_b1[32], s_m2[32], s_rep[32], s_ret[32];
   if (ctl[4] == 0) {  // first wave of the call: every env READY or GONE at round 0
     if (tid == 0) s_G = 0;
@@ -623,7 +655,12 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
     __syncthreads();
     if (tid == 0) {
       ctl[0] = 0;
-      ctl[2] = s_G;
+      if (sharded) {  // the batch-wide count arrives with the next exchange: gone at round 1
+        ring_ctr(a, 1)[1] = s_G;
+        ctl[2] = 0;
+      } else {
+        ctl[2] = s_G;
+      }
       ctl[4] = 1;
       ctl[9] = 0;
     }
@@ -633,6 +670,7 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
     s_H = ctl[0];
     s_G = ctl[2];
     s_D = ctl[9];
+    s_F0 = s_H;
   }
   __syncthreads();
   for (;;) {
@@ -642,18 +680,20 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
       // (1) can round D + 1 be decided?
       const int r = s_D + 1;
       s_try = 0;
-      if (r <= s_H + kAsyncK - 1) {
+      // sharded: only rounds whose slot the exchange of this wave carried
+      // (a slot freed in this pass still holds its old round's sums)
+      if (r <= s_H + kAsyncK - 1 && (!sharded || r <= s_F0 + kAsyncK - 1)) {
         int gone_eff = s_G;
-        for (int q = s_H + 1; q <= r; ++q) gone_eff += ring_ctr(a, q)[1];
-        const int arr = ring_ctr(a, r)[0];
-        s_strag = used - gone_eff - arr;
+        for (int q = s_H + 1; q <= r; ++q) gone_eff += gone_of(q);
+        const int arr = arr_of(r);
+        s_strag = used_g - gone_eff - arr;
         s_try = (s_strag > 0 || arr > 0) ? 1 : 0;
       }
     }
     __syncthreads();
     if (s_try) {
       const int r = s_D + 1;
-      const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
+      const int32_t* W = W_of(r);
       int m1 = 0, b1 = -1, m2 = 0;
       for (int i = tid; i < a.n_nodes; i += B) top2_merge(m1, b1, m2, W[i], i, 0);
 #pragma unroll
@@ -735,8 +775,8 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
     // (3) complete round F + 1: decided, every env finished it or is gone, its done list applied
     const int r = s_H + 1;
     int32_t* rc = ring_ctr(a, r);
-    const int gone_r = s_G + rc[1];
-    if (gone_r >= used || s_D < r || rc[0] < used - gone_r) {
+    const int gone_r = s_G + gone_of(r);
+    if (gone_r >= used_g || s_D < r || arr_of(r) < used_g - gone_r) {
       if (!s_prog) break;
       continue;
     }
@@ -750,7 +790,10 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
       rc[5] = 0;
       s_G = gone_r;
       s_H = r;
-      if (s_G + ring_ctr(a, r + 1)[1] < used) a.counters[1] += 1;  // another round runs
+      // the lockstep harvest counts every round that runs.  Sharded, gone(r + 1)
+      // may still miss this pass's retirements, so round r itself is counted
+      // (round 1 by the initial harvest)
+      if (sharded ? (r >= 2 && arr_of(r) > 0) : (s_G + gone_of(r + 1) < used_g)) a.counters[1] += 1;
     }
     __syncthreads();
   }
@@ -787,12 +830,12 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
     ctl[9] = s_D;
     *a.n_active = s_ns;
     *a.n_stepping = s_np;
-    const bool finished = s_G + ring_ctr(a, s_H + 1)[1] >= used;
+    const bool finished = s_G + gone_of(s_H + 1) >= used_g;
     // a shrunken batch: finish the yielded pushes unbounded in this wave
     // (no new samples), then the asynchronous kernel continues the rounds
     // (switch on the envs still running, not on the in-flight count: envs
     // held back by the ring bound are still work for the batch)
-    const int remaining = used - (s_G + ring_ctr(a, s_H + 1)[1]);
+    const int remaining = used_g - (s_G + gone_of(s_H + 1));
     if (!finished && remaining < a.wave_switch) {
       ctl[5] = 2;
       ctl[8] = 0x7fffffff;
