@@ -537,3 +537,153 @@ def test_wave_rounds_with_early_decisions_equal_lockstep(seed, K):
             assert got[0] == ref[0], (leaf, sched)
             assert sorted(got[1]) == sorted(ref[1]), (leaf, sched)
             assert got[2] == ref[2], (leaf, sched)
+
+
+def sharded_waves(nodes, n_envs, leaf_parallel, cap, seed, K, rng, G):
+    """Sharded wave rounds (multi.cu sharded_wave_rounds): G shards own
+    contiguous env ranges; before each wave's harvest the shards' W rings and
+    per-round (arrived, gone) counts are SUMMED (the one exchange), and every
+    shard's harvest decides / completes rounds from that snapshot — which
+    lags this pass's retirements — applying the decisions to its own envs.
+    Returns the lockstep results and asserts the shards stay in agreement."""
+    n_nodes = len(nodes)
+    used = n_envs if leaf_parallel else n_nodes
+    env_node = split(used, n_nodes)
+    tasks = [Cursor(env_node[e], e, nodes, cap, seed) for e in range(used)]
+    calls = [(env_node[e], e) for e in range(used)]
+    rewards = [0.0] * n_nodes
+    inc = [0] * used
+    W0 = [sum(t.max_remaining() for e, t in enumerate(tasks) if env_node[e] == i and not t.done)
+          for i in range(n_nodes)]
+    best0 = max(range(n_nodes), key=lambda i: (W0[i], -i))
+    best0 = best0 if W0[best0] > 0 else -1
+    for e in range(used):
+        if tasks[e].done:
+            rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+            if leaf_parallel and tasks[e].by_grasp and best0 >= 0:
+                env_node[e] = best0
+                inc[e] += 1
+                tasks[e] = Cursor(best0, e, nodes, cap, seed, inc[e])
+                calls.append((best0, e))
+    READY, AWAIT, GONE, PHYS = 0, 1, 2, 3
+    state = [GONE if tasks[e].done else READY for e in range(used)]
+    rnd = [0] * used
+    owner = [min(G - 1, e * G // used) for e in range(used)]
+    # per-shard local rings (slot = round, cleared when the round completes)
+    Wl = [defaultdict(lambda: [0] * n_nodes) for _ in range(G)]
+    arr_l = [defaultdict(int) for _ in range(G)]
+    gone_l = [defaultdict(int) for _ in range(G)]
+    done_l = [defaultdict(list) for _ in range(G)]
+    applied = [defaultdict(int) for _ in range(G)]
+    for e in range(used):  # initial dones count as gone at round 1 (the device's sharded init)
+        if state[e] == GONE:
+            gone_l[owner[e]][1] += 1
+    sh = [{"F": 0, "D": 0, "G": 0, "rounds": 1 if any(s == READY for s in state) else 0, "decided": {}}
+          for _ in range(G)]
+
+    def finish_step(e):
+        s = owner[e]
+        r = rnd[e] + 1
+        tasks[e].step()
+        rnd[e] = r
+        if not tasks[e].done:
+            Wl[s][r][env_node[e]] += tasks[e].max_remaining()
+            state[e] = READY
+        else:
+            rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
+            done_l[s][r].append(e)
+            if leaf_parallel and tasks[e].by_grasp:
+                state[e] = AWAIT
+            else:
+                state[e] = GONE
+                gone_l[s][r + 1] += 1
+        arr_l[s][r] += 1
+
+    for wave in range(20000):
+        # the exchange: sums over the shards (a snapshot for this wave's harvests)
+        F0 = sh[0]["F"]
+        rounds_live = range(F0 + 1, F0 + K)
+        gW = {r: [sum(Wl[s][r][i] for s in range(G)) for i in range(n_nodes)] for r in rounds_live}
+        garr = {r: sum(arr_l[s][r] for s in range(G)) for r in rounds_live}
+        ggone = {r: sum(gone_l[s][r] for s in range(G)) for r in range(F0 + 1, F0 + K + 1)}
+        for s in range(G):
+            st = sh[s]
+            dec = st["decided"]
+            while True:
+                prog = False
+                r = st["D"] + 1
+                if r <= st["F"] + K - 1 and r <= F0 + K - 1:
+                    gone_eff = st["G"] + sum(ggone[q] for q in range(st["F"] + 1, r + 1))
+                    strag = used - gone_eff - garr[r]
+                    W = gW[r]
+                    m1 = max(W)
+                    b = W.index(m1)
+                    m2 = max([W[j] for j in range(n_nodes) if j != b], default=0)
+                    if (strag > 0 or garr[r] > 0) and (strag == 0 or (m1 > 0 and m2 + strag * (cap - 1) < m1)):
+                        dec[r] = b if leaf_parallel and m1 > 0 else -1
+                        st["D"] = r
+                        prog = True
+                for q in range(st["F"] + 1, st["D"] + 1):
+                    lst = done_l[s][q]
+                    for e in lst[applied[s][q]:]:
+                        if state[e] == AWAIT:
+                            bq = dec[q]
+                            if bq >= 0:
+                                env_node[e] = bq
+                                inc[e] += 1
+                                tasks[e] = Cursor(bq, e, nodes, cap, seed, inc[e])
+                                assert not tasks[e].done
+                                calls.append((bq, e))
+                                state[e] = READY
+                            else:
+                                state[e] = GONE
+                                gone_l[s][q + 1] += 1  # local: reaches the sums next wave
+                    applied[s][q] = len(lst)
+                rf = st["F"] + 1
+                gone_r = st["G"] + ggone.get(rf, 0)
+                if gone_r < used and st["D"] >= rf and rf in garr and garr[rf] == used - gone_r:
+                    st["G"] = gone_r
+                    st["F"] = rf
+                    Wl[s].pop(rf, None)
+                    arr_l[s].pop(rf, None)
+                    gone_l[s].pop(rf, None)
+                    done_l[s].pop(rf, None)
+                    applied[s].pop(rf, None)
+                    if rf >= 2 and garr[rf] > 0:
+                        st["rounds"] += 1
+                    prog = True
+                if not prog:
+                    break
+        for s in range(1, G):
+            assert (sh[s]["F"], sh[s]["D"], sh[s]["G"], sh[s]["rounds"]) == \
+                (sh[0]["F"], sh[0]["D"], sh[0]["G"], sh[0]["rounds"]), "shards diverged"
+        st = sh[0]
+        if st["G"] + ggone.get(st["F"] + 1, 0) >= used:
+            break
+        for e in range(used):
+            if state[e] == READY and rnd[e] + 1 <= sh[owner[e]]["F"] + K - 1:
+                state[e] = PHYS
+        for e in range(used):
+            if state[e] == PHYS and rng.random() < 0.7:
+                finish_step(e)
+    else:
+        raise AssertionError("sharded waves did not terminate")
+    assert all(s in (GONE, AWAIT) or tasks[e].done for e, s in enumerate(state))
+    return rewards, calls, sh[0]["rounds"]
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("K", [2, 4, 16])
+@pytest.mark.parametrize("G", [2, 3])
+def test_sharded_wave_rounds_equal_lockstep(seed, K, G):
+    """One exchange per wave with lagging sums: same rewards, cursor creations
+    and round count as the reference's lockstep, shards in agreement."""
+    cap = 10
+    nodes = _nodes(seed, 3 + seed % 9, cap)
+    n_envs = len(nodes) + 20 + 7 * seed
+    for leaf in (True, False):
+        ref = lockstep(nodes, n_envs, leaf, cap, seed)
+        got = sharded_waves(nodes, n_envs, leaf, cap, seed, K, random.Random(31 * seed + G), G)
+        assert got[0] == ref[0], leaf
+        assert sorted(got[1]) == sorted(ref[1]), leaf
+        assert got[2] == ref[2], leaf
