@@ -50,6 +50,66 @@ def formula_ops(counts: np.ndarray, n: int) -> np.ndarray:
             + 7 * n * (n - 1) / 2 + 15 * pf)
 
 
+class NvmlSampler:
+    """SM clock + clock-event reasons polled through NVML every 2 ms on a
+    thread during the timed region (a region of a few tens of ms gets several
+    samples; nvidia-smi's own loop needs ~50 ms per sample)."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, device: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = None
+        try:  # the CUDA device's own NVML handle (CUDA_VISIBLE_DEVICES renumbers devices)
+            import torch
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:  # noqa: BLE001
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [v for v in vis.split(",") if v.strip().isdigit()]
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(int(ids[device]) if device < len(ids) else device)
+        self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.sm, self.reasons = [], set()
+        self.run = False
+
+    def start(self):
+        self.run = True
+        self.thread = threading.Thread(target=self._poll, daemon=True)
+        self.thread.start()
+
+    def _poll(self):
+        nv = self.nv
+        while self.run:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS:
+                    if mask & getattr(nv, attr):
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001 - a failed poll is a missing sample
+                pass
+            time.sleep(0.002)
+
+    def stop(self):
+        self.run = False
+        self.thread.join(timeout=1)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": float(self.smax),
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 2 ms"}
+
+
+def clock_sampler(device: int):
+    """NVML polling when available, else nvidia-smi."""
+    try:
+        return NvmlSampler(device)
+    except Exception:  # noqa: BLE001 - NVML missing: fall back to nvidia-smi
+        return ClockSampler(device)
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region."""
 
@@ -527,7 +587,7 @@ def run_ours(args, world, rank, local):
         flush.zero_()
         step()
     torch.cuda.synchronize(dev)
-    clocks = ClockSampler(local)
+    clocks = clock_sampler(local)
     clocks.start()
     time.sleep(0.15)
     dist_barrier(world)
