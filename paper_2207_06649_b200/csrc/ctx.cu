@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -326,6 +327,16 @@ int ppg_set_scene(ppg_ctx* ctx, const ppg_shapes* shapes) {
   if (!ctx || !shapes || shapes->n_tables != 1) return PPG_EINVAL;
   CK(cudaSetDevice(ctx->device));
   const int n = shapes->n_objects;
+  if (ctx->has_scene && !ctx->group && static_cast<int>(ctx->h_kind.size()) == n && n > 0 &&
+      ctx->side == shapes->side_length && ctx->margin == shapes->boundary_margin &&
+      std::equal(ctx->h_kind.begin(), ctx->h_kind.end(), shapes->kind) &&
+      std::memcmp(ctx->h_radius.data(), shapes->radius, n * sizeof(double)) == 0 &&
+      ctx->h_target[0] == shapes->target_index[0] &&
+      (shapes->n_vertices ? std::equal(ctx->h_nv.begin(), ctx->h_nv.end(), shapes->n_vertices)
+                          : std::all_of(ctx->h_nv.begin(), ctx->h_nv.end(), [](int v) { return v == 0; })) &&
+      (shapes->vertices ? std::memcmp(ctx->h_verts.data(), shapes->vertices, ctx->h_verts.size() * sizeof(double)) == 0
+                        : std::all_of(ctx->h_verts.begin(), ctx->h_verts.end(), [](double v) { return v == 0.0; })))
+    return PPG_SUCCESS;  // the installed scene already (run_pmbs installs the state's scene on every call)
   ctx->h_kind.assign(shapes->kind, shapes->kind + n);
   ctx->h_radius.assign(shapes->radius, shapes->radius + n);
   ctx->h_nv.assign(n, 0);
@@ -1022,6 +1033,20 @@ int ppg_batch_resolve_count_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, cons
                         reinterpret_cast<long long*>(counts_dev), st);
 }
 
+// sample_pushes / graspable of small batches one warp per state
+// (sample_grasp_warp_kernel); large batches one lane per state.
+static bool sample_warp_ok(const ppg_ctx* ctx, bool all_discs, int n, int E) {
+  const char* v = std::getenv("PPG_SAMPLE_WARP_MAX");
+  const int emax = v ? std::atoi(v) : 8192;
+  return E <= emax && n <= (all_discs ? kWarpMaxN : kPolyMaxN) && n * ctx->params.pushes_per_object <= 32 * 32;
+}
+
+static void launch_sample_grasp(const SimConst& C, const SampleArgs& a, bool all_discs, int E, cudaStream_t st) {
+  const int grid = (E + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (all_discs) sample_grasp_warp_kernel<false><<<grid, kWarpsPerBlock * 32, 0, st>>>(C, a);
+  else sample_grasp_warp_kernel<true><<<grid, kWarpsPerBlock * 32, 0, st>>>(C, a);
+}
+
 int ppg_sample_pushes(ppg_ctx* ctx, const ppg_shapes* shapes, const double* poses, int E, double* out,
                       int32_t* count) {
   if (!ctx || E < 0) return PPG_EINVAL;
@@ -1053,10 +1078,57 @@ int ppg_sample_pushes(ppg_ctx* ctx, const ppg_shapes* shapes, const double* pose
   const SimConst C = make_const(ctx->params, n, side, margin);
   SampleArgs a{S, ctx->b_in.as<double>(), ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(),
                nullptr, nullptr, nullptr, nullptr, nullptr, E};
-  sample_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  const bool discs = shapes ? host_all_discs(shapes) : ctx->scene_all_discs;
+  if (sample_warp_ok(ctx, discs, n, E)) launch_sample_grasp(C, a, discs, E, st);
+  else sample_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, ctx->b_out.p, obytes, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(count, ctx->b_status.p, static_cast<size_t>(E) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return PPG_SUCCESS;
+}
+
+// The search root's sample_pushes + graspable (SearchTree::create,
+// mcts.cpp:28-39) in ONE launch and one synchronisation (run_pmbs setup).
+int ppg_root_sample_grasp(ppg_ctx* ctx, const double* poses, double* untried, int32_t* count, uint8_t* graspable,
+                          const double** untried_dev) {
+  if (untried_dev) *untried_dev = nullptr;
+  if (!ctx->has_scene) {
+    ctx->err = "no scene installed";
+    return PPG_EINVAL;
+  }
+  const int n = ctx->scene.n;
+  if (!sample_warp_ok(ctx, ctx->scene_all_discs, n, 1)) {
+    int rc = ppg_sample_pushes(ctx, nullptr, poses, 1, untried, count);
+    if (rc == PPG_SUCCESS) rc = ppg_graspable(ctx, poses, 1, graspable, nullptr, nullptr, nullptr, nullptr);
+    return rc;
+  }
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int na = ctx->params.pushes_per_object;
+  const size_t pbytes = static_cast<size_t>(n) * 3 * 8, obytes = static_cast<size_t>(n) * na * 4 * 8;
+  CK(ctx->b_in.ensure(pbytes));
+  CK(ctx->b_out.ensure(obytes));
+  CK(ctx->b_status.ensure(64));
+  CK(ctx->b_a.ensure(64));
+  CK(ctx->b_b.ensure(64));
+  CK(ctx->b_c.ensure(64));
+  CK(ctx->b_d.ensure(64));
+  CK(ctx->b_e.ensure(64));
+  CK(cudaMemcpyAsync(ctx->b_in.p, poses, pbytes, cudaMemcpyHostToDevice, st));
+  const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
+  SampleArgs a{ctx->scene, ctx->b_in.as<double>(), ctx->b_out.as<double>(), ctx->b_status.as<int32_t>(),
+               ctx->b_a.as<uint8_t>(), ctx->b_b.as<double>(), ctx->b_c.as<double>(), ctx->b_d.as<double>(),
+               ctx->b_e.as<int32_t>(), 1};
+  launch_sample_grasp(C, a, ctx->scene_all_discs, 1, st);
+  CK(cudaGetLastError());
+  if (untried_dev) {
+    *untried_dev = ctx->b_out.as<double>();  // the caller copies it on the device
+  } else {
+    CK(cudaMemcpyAsync(untried, ctx->b_out.p, obytes, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaMemcpyAsync(count, ctx->b_status.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(graspable, ctx->b_a.p, 1, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return PPG_SUCCESS;
 }
@@ -1083,7 +1155,8 @@ int ppg_graspable(ppg_ctx* ctx, const double* poses, int E, uint8_t* graspable, 
   const SimConst C = make_const(ctx->params, n, ctx->side, ctx->margin);
   SampleArgs a{ctx->scene, ctx->b_in.as<double>(), nullptr, nullptr, ctx->b_a.as<uint8_t>(),
                ctx->b_b.as<double>(), ctx->b_c.as<double>(), ctx->b_d.as<double>(), ctx->b_e.as<int32_t>(), E};
-  grasp_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
+  if (sample_warp_ok(ctx, ctx->scene_all_discs, n, E)) launch_sample_grasp(C, a, ctx->scene_all_discs, E, st);
+  else grasp_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(C, a);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(graspable, ctx->b_a.p, E, cudaMemcpyDeviceToHost, st));
   if (margin) CK(cudaMemcpyAsync(margin, ctx->b_b.p, static_cast<size_t>(E) * 8, cudaMemcpyDeviceToHost, st));

@@ -29,6 +29,8 @@ __global__ void lock_step_count_kernel(const __grid_constant__ SimConst C, LockA
 __global__ void lock_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
 __global__ void poly_order_key_kernel(ResolveArgs a, unsigned* key, int* val);
+template <bool kPoly>
+__global__ void sample_grasp_warp_kernel(const __grid_constant__ SimConst C, SampleArgs a);
 template <int NW, bool kPoly>
 __global__ void resolve_warp_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
 template <int NW, bool kPoly>
@@ -272,3 +274,8 @@ int simulate_sharded(ppg_ctx* ctx, const double* node_poses, const int32_t* node
 int run_pmbs_sharded(ppg_ctx* ctx, const double* root_poses, double* action_out, ppg_search_stats* stats,
                      char* sig_buf, int64_t sig_cap, int64_t* sig_len);
 }  // namespace ppg
+
+// internal (not in include/pushplan_gpu.h): the search root's sample_pushes +
+// graspable in one launch (ctx.cu), used by run_pmbs's setup (dtree.cu)
+extern "C" int ppg_root_sample_grasp(ppg_ctx* ctx, const double* poses, double* untried, int32_t* count,
+                                     uint8_t* graspable, const double** untried_dev);

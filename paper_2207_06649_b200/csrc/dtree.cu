@@ -31,6 +31,7 @@
 // The final tree is read back once for best_root_child (mcts.cpp:218-235)
 // and the tree signature (mcts.cpp:284-300).
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 
 #include <chrono>
 #include <climits>
@@ -40,6 +41,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ctx_impl.cuh"
@@ -247,6 +249,46 @@ __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
     sc->n_pairs = draws;
     if (bad) sc->stop = 3;
     else if (draws == 0 && sc->stop < 0) sc->stop = 1;  // TreeExhausted: explored
+  }
+}
+
+// The root node + the search scalars from one staged block (dt_begin):
+// [DTScal][root flags (int)][root poses n*3 doubles].
+__global__ void dt_root_kernel(DTree t, const char* stage, int n, int cnt, long long* counters) {
+  const int tid = threadIdx.x;
+  const DTScal* h = reinterpret_cast<const DTScal*>(stage);
+  const int rf = *reinterpret_cast<const int*>(stage + sizeof(DTScal));
+  const double* rp = reinterpret_cast<const double*>(stage + sizeof(DTScal) + 8);
+  if (tid == 0) {
+    t.parent[0] = -1;
+    t.depth[0] = 0;
+    t.q[0] = 0.0;
+    t.visits[0] = 0;
+    t.vv[0] = 0;
+    t.flags[0] = static_cast<uint8_t>(rf);
+    t.u_off[0] = 0;
+    t.u_n[0] = cnt;
+    t.u_head[0] = 0;
+    t.c_n[0] = 0;
+    t.selc[0] = 0;
+    t.anc[0] = 0;
+  }
+  if (tid < 4) t.action[tid] = 0.0;
+  if (tid < 4) counters[tid] = 0;
+  for (int i = tid; i < n * 3; i += blockDim.x) t.poses[i] = rp[i];
+  const int* src = reinterpret_cast<const int*>(h);
+  int* dst = reinterpret_cast<int*>(t.sc);
+  for (int i = tid; i < static_cast<int>(sizeof(DTScal) / 4); i += blockDim.x) dst[i] = src[i];
+}
+
+// The final read-back's children lists, dense: node x's children at
+// kids[coff[x] .. coff[x] + c_n[x]) (coff = exclusive scan of c_n), instead
+// of the whole action-sized children pool.
+__global__ void dt_kids_kernel(DTree t, int N, const int* coff, int* kids) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < N; x += gridDim.x * blockDim.x) {
+    const long long o = t.u_off[x];
+    const int b = coff[x], m = t.c_n[x];
+    for (int k = 0; k < m; ++k) kids[b + k] = t.cpool[o + k];
   }
 }
 
@@ -509,6 +551,24 @@ struct DTreeState {
   ResolveArgs lra{};
   SimConst C{};
   std::string key;  // configuration the graph was captured for
+  // pinned host staging: the search start's root block, the per-iteration
+  // scalars and the final tree read-back (one async copy each, no pageable
+  // round trips)
+  char* hpin = nullptr;
+  size_t hpin_cap = 0;
+  DTScal* hsc = nullptr;  // pinned copy of the scalars, read after every iteration
+  DevBuf dstage;
+  char* pinned(size_t bytes) {
+    if (bytes > hpin_cap) {
+      if (hpin) cudaFreeHost(hpin);
+      hpin = nullptr;
+      hpin_cap = 0;
+      const size_t want = bytes < 4096 ? 4096 : bytes + bytes / 2;
+      if (cudaMallocHost(&hpin, want) != cudaSuccess) return nullptr;
+      hpin_cap = want;
+    }
+    return hpin;
+  }
   // the last finished search (ppg_tree_export)
   bool last_valid = false;
   int last_nodes = 0, last_dT = 0, last_dS = 0, last_es = 0;
@@ -528,6 +588,12 @@ struct DTreeState {
     release_graph();
     if (st2) cudaStreamDestroy(st2);
     st2 = nullptr;
+    if (hpin) cudaFreeHost(hpin);
+    hpin = nullptr;
+    hpin_cap = 0;
+    if (hsc) cudaFreeHost(hsc);
+    hsc = nullptr;
+    dstage.release();
     DevBuf* bufs[] = {&parent, &depth, &q, &visits, &vv, &flags, &u_off, &u_n, &u_head, &c_n, &selc, &action,
                       &poses, &anc, &apool, &cpool, &sel_node, &sel_act, &gp, &ga, &cp, &st, &gr, &nu, &un,
                       &meta, &logtab, &sc, &l_node, &l_pushes, &l_done, &l_byg, &l_harv, &l_flag, &l_reward,
@@ -969,29 +1035,57 @@ int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
 
 std::string signature(const std::vector<int32_t>& depth, const std::vector<double>& action,
                       const std::vector<long long>& visits, const std::vector<double>& q,
-                      const std::vector<uint8_t>& flags, const std::vector<long long>& u_off,
-                      const std::vector<int32_t>& c_n, const std::vector<int32_t>& cpool) {
-  // pre-order, children in insertion order (mcts.cpp:284-300)
-  std::string out;
-  std::vector<std::pair<int, int>> stack{{0, -1}};
-  char buf[256];
-  while (!stack.empty()) {
-    auto& [x, k] = stack.back();
-    if (k < 0) {
-      std::snprintf(buf, sizeof buf, "%d|%.17g,%.17g,%.17g,%.17g|%ld|%.17g|%c%c\n", depth[x], action[x * 4],
-                    action[x * 4 + 1], action[x * 4 + 2], action[x * 4 + 3], static_cast<long>(visits[x]), q[x],
-                    (flags[x] & 1) ? 'g' : '.', (flags[x] & 2) ? 'd' : '.');
-      out += buf;
-      k = 0;
-    }
-    if (k < c_n[x]) {
-      const int ch = cpool[u_off[x] + k];
-      ++k;
-      stack.push_back({ch, -1});
-    } else {
-      stack.pop_back();
+                      const std::vector<uint8_t>& flags, const std::vector<long long>& coff,
+                      const std::vector<int32_t>& c_n, const std::vector<int32_t>& kids) {
+  // pre-order, children in insertion order (mcts.cpp:284-300): the node
+  // order first, then the lines formatted in parallel chunks (the %.17g
+  // formatting is the cost: ~28K nodes for a 64K-env C4 decision)
+  std::vector<int> order;
+  order.reserve(depth.size());
+  {
+    std::vector<std::pair<int, int>> stack{{0, 0}};
+    order.push_back(0);
+    while (!stack.empty()) {
+      auto& [x, k] = stack.back();
+      if (k < c_n[x]) {
+        const int ch = kids[coff[x] + k];
+        ++k;
+        order.push_back(ch);
+        stack.push_back({ch, 0});
+      } else {
+        stack.pop_back();
+      }
     }
   }
+  const size_t N = order.size();
+  auto format = [&](size_t lo, size_t hi, std::string& out) {
+    char buf[256];
+    out.reserve((hi - lo) * 112);
+    for (size_t i = lo; i < hi; ++i) {
+      const int x = order[i];
+      const int len = std::snprintf(buf, sizeof buf, "%d|%.17g,%.17g,%.17g,%.17g|%ld|%.17g|%c%c\n", depth[x],
+                                    action[x * 4], action[x * 4 + 1], action[x * 4 + 2], action[x * 4 + 3],
+                                    static_cast<long>(visits[x]), q[x], (flags[x] & 1) ? 'g' : '.',
+                                    (flags[x] & 2) ? 'd' : '.');
+      out.append(buf, static_cast<size_t>(len));
+    }
+  };
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t T = std::min<size_t>(std::min<size_t>(hw, 32), N / 1024);
+  if (T < 2) {
+    std::string out;
+    format(0, N, out);
+    return out;
+  }
+  std::vector<std::string> parts(T);
+  std::vector<std::thread> th;
+  for (size_t t = 0; t < T; ++t) th.emplace_back(format, N * t / T, N * (t + 1) / T, std::ref(parts[t]));
+  for (auto& x : th) x.join();
+  size_t total = 0;
+  for (const auto& p : parts) total += p.size();
+  std::string out;
+  out.reserve(total);
+  for (const auto& p : parts) out += p;
   return out;
 }
 
@@ -1019,10 +1113,9 @@ int dt_begin(ppg_ctx* ctx, const double* root_poses, bool sharded) {
   // root: sample_pushes + graspable (SearchTree::create, mcts.cpp:28-39)
   std::vector<double> root_untried(static_cast<size_t>(n) * na * 4);
   int32_t cnt = 0;
-  int rc = ppg_sample_pushes(ctx, nullptr, root_poses, 1, root_untried.data(), &cnt);
-  if (rc != PPG_SUCCESS) return rc;
   uint8_t rg = 0;
-  rc = ppg_graspable(ctx, root_poses, 1, &rg, nullptr, nullptr, nullptr, nullptr);
+  const double* root_list_dev = nullptr;  // the list left on the device (warp path), else in root_untried
+  int rc = ppg_root_sample_grasp(ctx, root_poses, root_untried.data(), &cnt, &rg, &root_list_dev);
   if (rc != PPG_SUCCESS) return rc;
   if (cnt == 0) {
     ctx->err = "no legal push action at the root";
@@ -1075,27 +1168,8 @@ int dt_begin(ppg_ctx* ctx, const double* root_poses, bool sharded) {
   }
   if ((rc = dt_batch(ctx, S)) != PPG_SUCCESS) return rc;
   dt_views(ctx, S);
-  // root node + scalars
+  // root node + scalars: one staged block, one copy, one kernel
   {
-    const int32_t zero = 0, m1 = -1;
-    const long long zl = 0;
-    const double zd = 0.0;
-    const uint8_t rf = static_cast<uint8_t>(rg ? 1 : 0);  // dead needs untried.empty(): cnt > 0 here
-    DCK(cudaMemcpyAsync(S.t.parent, &m1, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.depth, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.q, &zd, 8, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.visits, &zl, 8, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.vv, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.flags, &rf, 1, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.u_off, &zl, 8, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.u_n, &cnt, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.u_head, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.c_n, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.selc, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemsetAsync(S.t.action, 0, 32, st));
-    DCK(cudaMemcpyAsync(S.t.poses, root_poses, static_cast<size_t>(n) * 24, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.anc, &zero, 4, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemcpyAsync(S.t.apool, root_untried.data(), static_cast<size_t>(cnt) * 32, cudaMemcpyHostToDevice, st));
     DTScal h;
     std::memset(&h, 0, sizeof h);
     h.n_nodes = 1;
@@ -1111,8 +1185,27 @@ int dt_begin(ppg_ctx* ctx, const double* root_poses, bool sharded) {
     h.c_explore = p.c_explore;
     h.lock_dyn[4] = static_cast<int>(static_cast<uint32_t>(p.rng_seed));
     h.lock_dyn[5] = static_cast<int>(static_cast<uint32_t>(p.rng_seed >> 32));
-    DCK(cudaMemcpyAsync(S.t.sc, &h, sizeof h, cudaMemcpyHostToDevice, st));
-    DCK(cudaMemsetAsync(S.la.counters, 0, 32, st));
+    const size_t bytes = sizeof(DTScal) + 8 + static_cast<size_t>(n) * 24;
+    char* hp = S.pinned(bytes);
+    if (!hp) {
+      ctx->err = "device tree: pinned staging allocation failed";
+      return PPG_ECUDA;
+    }
+    DCK(cudaStreamSynchronize(st));  // the previous search's reads of the staging block are done
+    std::memcpy(hp, &h, sizeof h);
+    const int rf = rg ? 1 : 0;  // dead needs untried.empty(): cnt > 0 here
+    std::memcpy(hp + sizeof h, &rf, 4);
+    std::memcpy(hp + sizeof h + 8, root_poses, static_cast<size_t>(n) * 24);
+    DCK(S.dstage.ensure(bytes));
+    DCK(cudaMemcpyAsync(S.dstage.p, hp, bytes, cudaMemcpyHostToDevice, st));
+    dt_root_kernel<<<1, 128, 0, st>>>(S.t, S.dstage.as<char>(), n, cnt, S.la.counters);
+    DCK(cudaGetLastError());
+    if (root_list_dev) {
+      DCK(cudaMemcpyAsync(S.t.apool, root_list_dev, static_cast<size_t>(cnt) * 32, cudaMemcpyDeviceToDevice, st));
+    } else {
+      DCK(cudaMemcpyAsync(S.t.apool, root_untried.data(), static_cast<size_t>(cnt) * 32, cudaMemcpyHostToDevice,
+                          st));
+    }
   }
   return PPG_SUCCESS;
 }
@@ -1140,26 +1233,66 @@ int dt_finish(ppg_ctx* ctx, const DTScal& h, int stop, double elapsed_s, double 
   S.last_es = h.es_level;
   // read the tree back once
   const int N = h.n_nodes;
-  std::vector<int32_t> depth(N), c_n(N), parent(N);
+  std::vector<int32_t> depth(N), c_n(N), kids(static_cast<size_t>(N > 1 ? N - 1 : 1));
   std::vector<double> q(N), action(static_cast<size_t>(N) * 4);
-  std::vector<long long> visits(N), u_off(N);
+  std::vector<long long> visits(N), coff(N);
   std::vector<uint8_t> flags(N);
-  std::vector<int32_t> cpool(static_cast<size_t>(h.a_used));
-  DCK(cudaMemcpyAsync(depth.data(), S.t.depth, N * 4ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(c_n.data(), S.t.c_n, N * 4ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(q.data(), S.t.q, N * 8ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(action.data(), S.t.action, N * 32ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(visits.data(), S.t.visits, N * 8ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(u_off.data(), S.t.u_off, N * 8ull, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(flags.data(), S.t.flags, N, cudaMemcpyDeviceToHost, st));
-  DCK(cudaMemcpyAsync(cpool.data(), S.t.cpool, static_cast<size_t>(h.a_used) * 4, cudaMemcpyDeviceToHost, st));
-  DCK(cudaStreamSynchronize(st));
+  {  // one pinned staging block: every copy asynchronous, one synchronisation.
+     // Large trees: the children lists gathered densely on the device (the
+     // children pool is action-sized); small trees: the pool itself.
+    const bool dense = h.a_used > (1 << 18);
+    const size_t Nn = (static_cast<size_t>(N) + 63) / 64 * 64;
+    int* d_kids = nullptr;
+    if (dense) {
+      size_t scan_bytes = 0;
+      DCK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<const int*>(nullptr),
+                                        static_cast<int*>(nullptr), N, st));
+      DCK(S.dstage.ensure(Nn * 4 * 2 + scan_bytes));
+      int* d_coff = S.dstage.as<int>();
+      d_kids = d_coff + Nn;
+      DCK(cub::DeviceScan::ExclusiveSum(d_kids + Nn, scan_bytes, S.t.c_n, d_coff, N, st));
+      dt_kids_kernel<<<std::min(1024, (N + 255) / 256), 256, 0, st>>>(S.t, N, d_coff, d_kids);
+      DCK(cudaGetLastError());
+    }
+    std::vector<long long> u_off(dense ? 0 : N);
+    std::vector<int32_t> cpool(dense ? 0 : static_cast<size_t>(h.a_used));
+    const size_t nk = N > 1 ? static_cast<size_t>(N - 1) : 0;
+    const size_t seg[8] = {N * 4ull, N * 4ull, N * 8ull, N * 32ull, N * 8ull, static_cast<size_t>(N),
+                           dense ? nk * 4 : static_cast<size_t>(h.a_used) * 4, dense ? 0 : N * 8ull};
+    const void* dsrc[8] = {S.t.depth, S.t.c_n, S.t.q, S.t.action, S.t.visits, S.t.flags,
+                           dense ? static_cast<const void*>(d_kids) : static_cast<const void*>(S.t.cpool), S.t.u_off};
+    void* hdst[8] = {depth.data(), c_n.data(), q.data(), action.data(), visits.data(), flags.data(),
+                     dense ? static_cast<void*>(kids.data()) : static_cast<void*>(cpool.data()), u_off.data()};
+    size_t off[8], total = 0;
+    for (int i = 0; i < 8; ++i) {
+      off[i] = total;
+      total += (seg[i] + 15) / 16 * 16;
+    }
+    DCK(cudaStreamSynchronize(st));  // earlier users of the staging block are done
+    char* hp = S.pinned(total);
+    if (!hp) {
+      ctx->err = "device tree: pinned staging allocation failed";
+      return PPG_ECUDA;
+    }
+    for (int i = 0; i < 8; ++i)
+      if (seg[i]) DCK(cudaMemcpyAsync(hp + off[i], dsrc[i], seg[i], cudaMemcpyDeviceToHost, st));
+    DCK(cudaStreamSynchronize(st));
+    for (int i = 0; i < 8; ++i)
+      if (seg[i]) std::memcpy(hdst[i], hp + off[i], seg[i]);
+    long long acc = 0;
+    for (int x = 0; x < N; ++x) {
+      coff[x] = acc;
+      if (!dense)
+        for (int k = 0; k < c_n[x]; ++k) kids[acc + k] = cpool[u_off[x] + k];
+      acc += c_n[x];
+    }
+  }
   // best_root_child (mcts.cpp:218-235)
   int best = -1;
   double best_score = -std::numeric_limits<double>::infinity();
   long long best_visits = -1;
   for (int k = 0; k < c_n[0]; ++k) {
-    const int ch = cpool[u_off[0] + k];
+    const int ch = kids[coff[0] + k];
     if (visits[ch] == 0) continue;
     const double score = p.rank_by_ucb ? ucb_score_host(q[ch], static_cast<long>(visits[ch]), static_cast<long>(visits[0]),
                                                         p.c_explore)
@@ -1175,7 +1308,7 @@ int dt_finish(ppg_ctx* ctx, const DTScal& h, int stop, double elapsed_s, double 
     return PPG_EINVAL;
   }
   std::memcpy(action_out, &action[static_cast<size_t>(best) * 4], 32);
-  const std::string sig = signature(depth, action, visits, q, flags, u_off, c_n, cpool);
+  const std::string sig = signature(depth, action, visits, q, flags, coff, c_n, kids);
   if (stats) {
     ppg_search_stats s;
     std::memset(&s, 0, sizeof s);
@@ -1676,8 +1809,10 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     // capacity for one more iteration (the host learns the sizes after each)
     {
       const int prev_it = h.iteration, prev_nodes = h.n_nodes;
-      cudaError_t e = cudaMemcpyAsync(&h, S.t.sc, sizeof h, cudaMemcpyDeviceToHost, st);
+      cudaError_t e = S.hsc ? cudaSuccess : cudaMallocHost(&S.hsc, sizeof(DTScal));
+      if (e == cudaSuccess) e = cudaMemcpyAsync(S.hsc, S.t.sc, sizeof h, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) std::memcpy(&h, S.hsc, sizeof h);
       if (e != cudaSuccess) {
         char m[256];
         std::snprintf(m, sizeof m, "dtree: iteration after %d (nodes %d, cap %d, regrown %d): %s", prev_it,

@@ -105,6 +105,61 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kPoly ? 4 : 1) resolve_wa
   }
 }
 
+// sample_pushes (actions.cpp:51-73: the full ordered candidate list) and /
+// or graspable (actions.cpp:113-147) of E states, one warp per state: the
+// candidates' validity tests and the 16 grasp angles run across the lanes
+// (the one-lane kernels walk them in sequence: ~0.26 ms for one state).
+template <bool kPoly>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) sample_grasp_warp_kernel(const __grid_constant__ SimConst C,
+                                                                               SampleArgs a) {
+  __shared__ double blk[kWarpsPerBlock][160];
+  PPG_POLY_SMEM
+  __shared__ unsigned valid[kWarpsPerBlock][32];
+  const int wib = threadIdx.x >> 5;
+  const int e = blockIdx.x * kWarpsPerBlock + wib;
+  if (e >= a.E) return;
+  const int n = C.n, l = threadIdx.x & 31;
+  const int t = a.S.T == 1 ? 0 : e;
+  const ShapeView S = a.S.view(t);
+  WarpEnv W(blk[wib], n, l);
+  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  warp_load_any<kPoly>(W, G, a.poses + static_cast<size_t>(e) * n * 3, S);
+  if (a.out) {
+    const int count = warp_sample_mask(W, S, C, valid[wib]);
+    const int nw = (n * C.na + 31) >> 5;
+    double* out = a.out + static_cast<size_t>(e) * n * C.na * 4;
+    const PoseView PV = W.view();
+    int base = 0;
+    for (int w = 0; w < nw; ++w) {
+      const unsigned b = valid[wib][w];
+      if (b >> l & 1u) {
+        const int c = 32 * w + l;
+        V2 s0, t0;
+        push_candidate(PV, S, C, c / C.na, c % C.na, false, s0, t0);
+        double* q = out + static_cast<size_t>(base + __popc(b & ((1u << l) - 1u))) * 4;
+        q[0] = s0.x;
+        q[1] = s0.y;
+        q[2] = t0.x;
+        q[3] = t0.y;
+      }
+      base += __popc(b);
+    }
+    if (l == 0) a.count[e] = count;
+  }
+  if (a.grasp) {
+    const GraspOut g = warp_graspable(W, S, C, a.S.target[t]);
+    if (l == 0) {
+      a.grasp[e] = g.graspable ? 1 : 0;
+      a.margin[e] = g.margin;
+      a.bx[e] = g.x;
+      a.by[e] = g.y;
+      a.bk[e] = g.k;
+    }
+  }
+}
+template __global__ void sample_grasp_warp_kernel<false>(const __grid_constant__ SimConst, SampleArgs);
+template __global__ void sample_grasp_warp_kernel<true>(const __grid_constant__ SimConst, SampleArgs);
+
 // batch_expand prepare (pmbs.cpp:82-93), one warp per (node, action) pair.
 template <int NW, bool kPoly>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const __grid_constant__ SimConst C,
