@@ -177,7 +177,10 @@ struct LockArgs {
 };
 
 constexpr int kLockRoundLimit = 1 << 20;
-constexpr int kAsyncK = 16;  // ring depth: rounds an env may run ahead of the last complete round
+#ifndef PPG_ASYNC_K
+#define PPG_ASYNC_K 16
+#endif
+constexpr int kAsyncK = PPG_ASYNC_K;  // ring depth: rounds an env may run ahead of the last complete round
 constexpr int kRingCtr = 8;  // ints per ring slot: arrived, gone at this round, done-list length, decided round, decision
 
 // Applies the device-side per-iteration overrides (device tree mode).
