@@ -594,7 +594,7 @@ static int launch_resolve_poly_t(ppg_ctx* ctx, const SimConst& C, ResolveArgs a,
       size_t scratch = 0;
       CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, scratch, static_cast<const unsigned*>(nullptr),
                                                    static_cast<unsigned*>(nullptr), static_cast<const int*>(nullptr),
-                                                   static_cast<int*>(nullptr), E, 0, 16, st));
+                                                   static_cast<int*>(nullptr), E, 0, 24, st));
       const size_t En = (static_cast<size_t>(E) + 63) / 64 * 64;
       CK(ctx->ord_buf[slot].ensure(4 * En * 4 + scratch));
       unsigned* k_in = ctx->ord_buf[slot].as<unsigned>();
@@ -603,7 +603,7 @@ static int launch_resolve_poly_t(ppg_ctx* ctx, const SimConst& C, ResolveArgs a,
       int* v_out = v_in + En;
       poly_order_key_kernel<<<(E + 255) / 256, 256, 0, st>>>(a, k_in, v_in);
       CK(cudaGetLastError());
-      CK(cub::DeviceRadixSort::SortPairsDescending(v_out + En, scratch, k_in, k_out, v_in, v_out, E, 0, 16, st));
+      CK(cub::DeviceRadixSort::SortPairsDescending(v_out + En, scratch, k_in, k_out, v_in, v_out, E, 0, 24, st));
       a.idx = v_out;
     }
   }

@@ -98,12 +98,14 @@ __global__ void __launch_bounds__(128) resolve_kernel(const __grid_constant__ Si
 
 template __global__ void resolve_kernel<false>(const __grid_constant__ SimConst, ResolveArgs);
 // Launch-order key of a polygon batch (one warp per env, dynamic env fetch):
-// envs whose push path runs into many polygon vertices tend to need the most
-// projection iterations, and a heavy env fetched late is the launch's tail.
-// key = (sum of the vertex counts of polygons within 0.08 of the push
-// segment)^2 + objects within 0.08 — a scheduling hint only (results are
-// element-wise and independent of the order; tools/poly_sort_bound.py
-// measured this key against cost-ordered and index-ordered launches).
+// envs whose push path runs into clustered polygons need the most projection
+// iterations, and a heavy env fetched late is the launch's tail.  Key =
+// (polygon-polygon pairs with both objects within 0.08 of the push segment
+// and bounding circles less than 0.02 apart, then the squared vertex count
+// of the polygons within 0.08) — a scheduling hint only: results are
+// element-wise and independent of the order.  Fitted on measured per-env
+// latencies (tools/poly_env_costs.py: the 16K workload's list schedule
+// 1.38x over index order; measured-cost order 1.43x).
 __global__ void poly_order_key_kernel(ResolveArgs a, unsigned* key, int* val) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= a.E) return;
@@ -115,16 +117,32 @@ __global__ void poly_order_key_kernel(ResolveArgs a, unsigned* key, int* val) {
   const float inv = 1.0f / fmaxf(dx * dx + dy * dy, 1e-30f);
   const double* p = a.poses_in + static_cast<size_t>(e) * n * 3;
   int cnt = 0, nvs = 0;
+  unsigned near_poly = 0;
   for (int i = 0; i < n; ++i) {
     const float px = static_cast<float>(p[3 * i]) - sx, py = static_cast<float>(p[3 * i + 1]) - sy;
     const float t = fminf(fmaxf((px * dx + py * dy) * inv, 0.0f), 1.0f);
     const float qx = px - t * dx, qy = py - t * dy;
     if (qx * qx + qy * qy < 0.08f * 0.08f) {
       ++cnt;
-      if (S.kind_(i) != 0) nvs += S.nv_(i);
+      if (S.kind_(i) != 0) {
+        nvs += S.nv_(i);
+        near_poly |= 1u << i;
+      }
     }
   }
-  key[e] = static_cast<unsigned>(nvs * nvs + cnt);
+  int pp = 0;
+  for (unsigned m = near_poly; m; m &= m - 1) {
+    const int i = __ffs(m) - 1;
+    const float xi = static_cast<float>(p[3 * i]), yi = static_cast<float>(p[3 * i + 1]);
+    const float bi = static_cast<float>(S.br_(i));
+    for (unsigned m2 = m & (m - 1); m2; m2 &= m2 - 1) {
+      const int j = __ffs(m2) - 1;
+      const float ex = static_cast<float>(p[3 * j]) - xi, ey = static_cast<float>(p[3 * j + 1]) - yi;
+      const float gap = sqrtf(ex * ex + ey * ey) - bi - static_cast<float>(S.br_(j));
+      pp += gap < 0.02f ? 1 : 0;
+    }
+  }
+  key[e] = static_cast<unsigned>(pp) << 16 | static_cast<unsigned>(min(nvs * nvs + cnt, 0xffff));
   val[e] = e;
 }
 
