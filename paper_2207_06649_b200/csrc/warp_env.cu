@@ -31,8 +31,26 @@
 
 #include "warp_env.cuh"
 #include "warp_poly.cuh"
+#include "pushplan_gpu.h"  // status codes of the debug accessor
 
 namespace ppg {
+
+#ifdef PPG_PHASE_TRACE_BUILD
+// latency split of the asynchronous kernel's env-steps (experiments; build
+// with EXTRA_NVFLAGS=-DPPG_PHASE_TRACE_BUILD): globaltimer ns summed over
+// steps — [0] sample, [1] pick, [2] resolve, [3] graspable + bookkeeping,
+// [4] steps
+__device__ unsigned long long g_phase_ns[8];
+#define PPG_PHASE_MARK(slot, t_prev)                                          \
+  do {                                                                        \
+    if (l == 0) {                                                             \
+      unsigned long long t_now;                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));               \
+      atomicAdd(&g_phase_ns[slot], t_now - t_prev);                           \
+      t_prev = t_now;                                                         \
+    }                                                                         \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 
@@ -256,7 +274,15 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
     }
   } trace_guard{a, e, l, t_start};
 #endif
+#ifdef PPG_PHASE_TRACE_BUILD
+  unsigned long long t_ph = 0;
+  if (l == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ph));
+  if (l == 0) atomicAdd(&g_phase_ns[4], 1ull);
+#endif
   const int count = warp_sample_mask(W, S, C, valid);
+#ifdef PPG_PHASE_TRACE_BUILD
+  PPG_PHASE_MARK(0, t_ph);
+#endif
   if (count == 0) {  // no legal push: reward 0 (mcts.cpp:146-150)
     if (l == 0) {
       a.env_done[e] = 1;
@@ -278,7 +304,13 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
   push_candidate(W.view(), S, C, c / C.na, c % C.na, false, s, t);
   if (l == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), 1ull);
   double residual;
+#ifdef PPG_PHASE_TRACE_BUILD
+  PPG_PHASE_MARK(1, t_ph);
+#endif
   const int st = warp_resolve_any<NW, kPoly>(W, G, O, S, C, pij, s, t, false, &residual);
+#ifdef PPG_PHASE_TRACE_BUILD
+  PPG_PHASE_MARK(2, t_ph);
+#endif
   if (st != 0) {  // SimError: reward 0 (mcts.cpp:153-158)
     if (l == 0) {
       a.env_done[e] = 1;
@@ -287,6 +319,9 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
     return;
   }
   const GraspOut gr = warp_graspable(W, S, C, a.S.target[0]);
+#ifdef PPG_PHASE_TRACE_BUILD
+  PPG_PHASE_MARK(3, t_ph);
+#endif
   if (l == 0) {
     const int pushes = a.env_pushes[e] + 1;
     a.env_pushes[e] = pushes;
@@ -1101,3 +1136,18 @@ PPG_WARP_INST(4, true)
 #undef PPG_WARP_INST
 
 }  // namespace ppg
+
+// Latency split of the asynchronous kernel's env-steps (experiments): copies
+// the PPG_PHASE_TRACE_BUILD accumulators to out[8] and zeroes them; returns
+// PPG_EINVAL when the library was built without them.
+extern "C" int ppg_debug_phase_times(unsigned long long* out) {
+#ifdef PPG_PHASE_TRACE_BUILD
+  if (cudaMemcpyFromSymbol(out, ppg::g_phase_ns, sizeof(unsigned long long) * 8) != cudaSuccess) return PPG_ECUDA;
+  const unsigned long long zero[8] = {};
+  if (cudaMemcpyToSymbol(ppg::g_phase_ns, zero, sizeof zero) != cudaSuccess) return PPG_ECUDA;
+  return PPG_SUCCESS;
+#else
+  (void)out;
+  return PPG_EINVAL;
+#endif
+}
