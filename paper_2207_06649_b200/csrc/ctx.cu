@@ -304,7 +304,7 @@ void ppg_destroy(ppg_ctx* ctx) {
   if (ctx->h_epochs) cudaFreeHost(ctx->h_epochs);
   ctx->l_go.release();
   for (DevBuf* b : {&ctx->l_around, &ctx->l_astate, &ctx->l_aW, &ctx->l_actr, &ctx->l_adl, &ctx->l_actl, &ctx->trace_buf,
-                    &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract, &ctx->l_gring})
+                    &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract, &ctx->l_gring, &ctx->l_aP})
     b->release();
   if (ctx->h_go) cudaFreeHost(ctx->h_go);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1252,6 +1252,7 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   CK(ctx->l_around.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_astate.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_aW.ensure(static_cast<size_t>(kAsyncK) * n_nodes * 4));
+  CK(ctx->l_aP.ensure(static_cast<size_t>(kAsyncK) * n_nodes * 4));
   CK(ctx->l_actr.ensure(static_cast<size_t>(kAsyncK) * kRingCtr * 4));
   CK(ctx->l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   CK(ctx->l_actl.ensure(64));
@@ -1307,6 +1308,7 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   a.env_round = ctx->l_around.as<int32_t>();
   a.env_state = ctx->l_astate.as<int32_t>();
   a.a_W = ctx->l_aW.as<int32_t>();
+  a.a_P = ctx->l_aP.as<int32_t>();
   a.a_ctr = ctx->l_actr.as<int32_t>();
   a.a_dl = ctx->l_adl.as<int32_t>();
   a.a_ctl = ctx->l_actl.as<int32_t>();

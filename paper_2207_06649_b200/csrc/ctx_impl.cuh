@@ -207,6 +207,7 @@ struct ppg_ctx {
   int wave_switch = 12288;                // envs still running below which waves hand over to async (PPG_WAVE_SWITCH)
   ppg::DevBuf l_fin, l_rsi, l_ract;       // wave rounds: post list, resumable physics progress
   ppg::DevBuf l_gring;                   // sharded wave rounds: the exchanged ring (LockArgs.g_ring)
+  ppg::DevBuf l_aP;                      // asynchronous lockstep: pending bounds ring (LockArgs.a_P)
   int32_t* h_go = nullptr;                // pinned copy
 };
 

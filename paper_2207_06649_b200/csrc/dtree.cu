@@ -535,7 +535,7 @@ struct DTreeState {
   // lockstep state
   DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx, l_W, l_rew, l_active,
       l_nactive, l_counters, l_push, l_status, l_stepping, l_around, l_astate, l_aW, l_actr, l_adl, l_fin, l_rsi,
-      l_ract;
+      l_ract, l_aP;
   int cap_nodes = 0;
   long long cap_actions = 0;
   int n_envs = 0, n = 0, na = 0;
@@ -598,7 +598,7 @@ struct DTreeState {
                       &poses, &anc, &apool, &cpool, &sel_node, &sel_act, &gp, &ga, &cp, &st, &gr, &nu, &un,
                       &meta, &logtab, &sc, &l_node, &l_pushes, &l_done, &l_byg, &l_harv, &l_flag, &l_reward,
                       &l_poses, &l_mt, &l_mtidx, &l_W, &l_rew, &l_active, &l_nactive, &l_counters, &l_push,
-                      &l_status, &l_stepping, &l_around, &l_astate, &l_aW, &l_actr, &l_adl, &l_fin, &l_rsi, &l_ract};
+                      &l_status, &l_stepping, &l_around, &l_astate, &l_aW, &l_actr, &l_adl, &l_fin, &l_rsi, &l_ract, &l_aP};
     for (DevBuf* b : bufs) b->release();
   }
 };
@@ -737,6 +737,7 @@ int dt_batch(ppg_ctx* ctx, DTreeState& S) {
   DCK(S.l_around.ensure(static_cast<size_t>(E) * 4));
   DCK(S.l_astate.ensure(static_cast<size_t>(E) * 4));
   DCK(S.l_aW.ensure(static_cast<size_t>(kAsyncK) * E * 4));
+  DCK(S.l_aP.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_actr.ensure(static_cast<size_t>(kAsyncK) * kRingCtr * 4));
   DCK(S.l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_fin.ensure(static_cast<size_t>(E) * 4 + 16));
@@ -822,6 +823,7 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
   a.env_round = S.l_around.as<int32_t>();
   a.env_state = S.l_astate.as<int32_t>();
   a.a_W = S.l_aW.as<int32_t>();
+  a.a_P = S.l_aP.as<int32_t>();
   a.a_ctr = S.l_actr.as<int32_t>();
   a.a_dl = S.l_adl.as<int32_t>();
   a.a_ctl = t.sc->async_ctl;

@@ -162,6 +162,10 @@ struct LockArgs {
   // and (arrived, gone) per ring slot [K][2], summed over the shards before
   // each wave's harvest, which decides and completes rounds from these sums
   int32_t* g_ring = nullptr;
+  // asynchronous lockstep: per ring slot, per node, the most the envs that will
+  // step that round but have not finished it can still add to W [K][a_wcap]
+  // (count of those envs: ring slot field [6])
+  int32_t* a_P = nullptr;
   int a_wcap = 0;
   // wave rounds (warp_env.cu wave_*_kernel): envs whose physics finished in
   // this wave (post pending), and the resumable physics progress

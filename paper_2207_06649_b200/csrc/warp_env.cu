@@ -41,6 +41,7 @@ namespace ppg {
 // steps — [0] sample, [1] pick, [2] resolve, [3] graspable + bookkeeping,
 // [4] steps
 __device__ unsigned long long g_phase_ns[8];
+__device__ unsigned long long g_await_t0[65536];  // [5] / [6]: AWAIT wait ns / count
 #define PPG_PHASE_MARK(slot, t_prev)                                          \
   do {                                                                        \
     if (l == 0) {                                                             \
@@ -392,6 +393,12 @@ enum : int { kReady = 0, kAwait = 1, kGone = 2, kPhys = -1 };
 
 // Ring views
 PPG_DI int32_t* ring_ctr(const LockArgs& a, int r) { return a.a_ctr + kRingCtr * (r % kAsyncK); }
+PPG_DI int32_t* ring_P(const LockArgs& a, int r) { return a.a_P + (r % kAsyncK) * a.a_wcap; }
+PPG_DI int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockArgs a) {
   lock_dyn(a);
@@ -403,7 +410,10 @@ __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockA
     a.env_state[e] = a.env_done[e] ? 2 : 0;  // the lockstep harvest just harvested every done env
     if (a.env_done[e]) atomicAdd(&a.a_ctl[2], 1);
   }
-  for (int i = tid; i < kAsyncK * a.n_nodes; i += G) a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
+  for (int i = tid; i < kAsyncK * a.n_nodes; i += G) {
+    a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
+    a.a_P[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
+  }
   if (tid < kRingCtr * kAsyncK) a.a_ctr[tid] = 0;
 }
 
@@ -439,6 +449,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
     const int F0 = F;              // round F0 + 1 is already counted (lock / wave setup)
     int G = ld_volatile(&ctl[2]);  // envs gone through round F
     unsigned long long t_idle = now_ns();
+    {  // the workers' pending bounds of their READY envs are in place
+      const int nwk = gridDim.x * kWarpsPerBlock - 1, owners = nwk < used ? nwk : used;
+      while (ld_volatile(&ctl[10]) < owners) {
+        if (now_ns() - t_idle > kAsyncStallNs) {
+          if (l == 0) {
+            atomicExch(&ctl[3], 1);
+            atomicExch(&ctl[1], 1);
+            if (a.cond) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(a.cond), 0u);
+          }
+          return;
+        }
+        __nanosleep(64);
+      }
+      __threadfence();
+    }
     for (;;) {
       // finished when nothing will step in round F + 1.  Envs waiting on the
       // decision of round F add to gone(F + 1) only once they have applied it,
@@ -458,37 +483,54 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
         int32_t* rc = ring_ctr(a, r);
         int gone_eff = G;
         for (int q = F + 1; q <= r; ++q) gone_eff += ld_volatile(&ring_ctr(a, q)[1]);
-        const int arr = ld_volatile(&rc[0]);
+        const int arr = ld_acquire(&rc[0]);  // before near: a stale near may only over-count far
         const int strag = used - gone_eff - arr;
         if (strag > 0 || arr > 0) {
-          __threadfence();
+          // the envs that have not finished round r: those already READY for it
+          // ("near", their node and bound cap - 1 - pushes in P(r)) and the
+          // rest ("far": any node, at most cap - 1).  Read order: arrivals,
+          // near / P (acquire), then W — a worker publishes W, then drops its
+          // P bound, then counts its arrival, so every env is covered.
+          const int near = ld_acquire(&rc[6]);
+          const int far = strag - near;
           const int32_t* W = a.a_W + (r % kAsyncK) * a.a_wcap;
-          // first maximum (lowest node) and the largest other value
-          int m1 = 0, b1 = -1, m2 = 0;
+          const int32_t* Pr = ring_P(a, r);
+          int m1 = 0, b1 = -1;
           for (int i = l; i < a.n_nodes; i += 32) {
             const int w = ld_volatile(&W[i]);
             if (w > m1) {
-              m2 = max(m2, m1);
               m1 = w;
               b1 = i;
-            } else {
-              m2 = max(m2, w);
             }
           }
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) {
             const int om1 = __shfl_xor_sync(kFull, m1, off);
             const int ob1 = __shfl_xor_sync(kFull, b1, off);
-            const int om2 = __shfl_xor_sync(kFull, m2, off);
             if (om1 > m1 || (om1 == m1 && om1 > 0 && ob1 < b1)) {
-              m2 = max(m2, max(m1, om2));
               m1 = om1;
               b1 = ob1;
-            } else {
-              m2 = max(m2, max(om1, om2));
             }
           }
-          const bool robust = strag == 0 || (m1 > 0 && m2 + strag * (a.cap - 1) < m1);
+          // the most any other node can still reach, split by its side of b1
+          // (a tie goes to the lower node)
+          int lo = 0, hi = 0;
+          for (int i = l; i < a.n_nodes; i += 32) {
+            const int pi = ld_acquire(&Pr[i]);  // P before W
+            const int v = pi + ld_volatile(&W[i]);
+            if (i < b1) lo = max(lo, v);
+            else if (i > b1) hi = max(hi, v);
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            lo = max(lo, __shfl_xor_sync(kFull, lo, off));
+            hi = max(hi, __shfl_xor_sync(kFull, hi, off));
+          }
+          const int slack = far * (a.cap - 1);
+          // (m1 from the first pass is a lower bound of W(r)[b1]; with m1 = 0,
+          // hi covers every node with the fresher W of the second pass)
+          const bool robust = strag == 0 || !a.leaf_parallel ||  // (no re-purposing: the decision is -1 anyway)
+                              (far >= 0 && (m1 > 0 ? (lo + slack < m1 && hi + slack <= m1) : (far == 0 && hi == 0)));
           if (robust) {
             if (l == 0) {
               rc[4] = (a.leaf_parallel && m1 > 0) ? b1 : -1;
@@ -544,6 +586,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
   const int wk = gw - 1;
   if (wk >= used) return;  // owns no env
   const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  if (l == 0) {  // pending bounds of this warp's READY envs (fresh start or wave hand-over)
+    for (int e = wk; e < used; e += nwk)
+      if (a.env_state[e] == kReady) {
+        const int r1 = a.env_round[e] + 1;
+        atomicAdd(&ring_P(a, r1)[a.env_node[e]], a.cap - 1 - a.env_pushes[e]);
+        atomicAdd(&ring_ctr(a, r1)[6], 1);
+      }
+    __threadfence();
+    atomicAdd(&ctl[10], 1);
+  }
+  __syncwarp();
   unsigned long long t_idle = now_ns();
   for (;;) {
     int fin = 0, F = 0;
@@ -564,11 +617,21 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
           const int rho = a.env_round[e];
           const int32_t* rc = ring_ctr(a, rho);
           if (ld_volatile(&rc[3]) == rho) {
+#ifdef PPG_PHASE_TRACE_BUILD
+            {
+              unsigned long long t_now;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+              atomicAdd(&g_phase_ns[5], t_now - g_await_t0[e & 65535]);
+              atomicAdd(&g_phase_ns[6], 1ull);
+            }
+#endif
             __threadfence();
             b = ld_volatile(&rc[4]);
             if (b >= 0) {  // re-purpose (pmbs.cpp:181-185): RolloutCursor ctor at b, continues at round rho + 1
               cursor_init(C, a, e, b);
               a.env_harvested[e] = 0;
+              atomicAdd(&ring_P(a, rho + 1)[b], a.cap - 1 - a.env_pushes[e]);
+              atomicAdd(&ring_ctr(a, rho + 1)[6], 1);
               a.env_state[e] = kReady;
               atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[2]), 1ull);
             } else {
@@ -586,18 +649,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
       if (st != kReady) continue;
       const int r = a.env_round[e] + 1;
       if (r > F + kAsyncK - 1) continue;  // ring bound: at most K rounds past the last complete round
+      const int p_before = a.env_pushes[e];
       warp_rollout_step<NW, kPoly>(C, a, e, blk[wib], valid[wib], pij, G);
       __syncwarp();
       if (l == 0) {
         a.env_round[e] = r;
         int32_t* rc = ring_ctr(a, r);
+        const int node = a.env_node[e];
+        if (!a.env_done[e]) atomicAdd(&a.a_W[(r % kAsyncK) * a.a_wcap + node], a.cap - a.env_pushes[e]);
+        __threadfence();  // W before the pending bound is dropped
+        atomicSub(&ring_P(a, r)[node], a.cap - 1 - p_before);
+        atomicSub(&rc[6], 1);
         if (!a.env_done[e]) {
-          atomicAdd(&a.a_W[(r % kAsyncK) * a.a_wcap + a.env_node[e]], a.cap - a.env_pushes[e]);
+          atomicAdd(&ring_P(a, r + 1)[node], a.cap - 1 - a.env_pushes[e]);
+          atomicAdd(&ring_ctr(a, r + 1)[6], 1);
         } else {
           atomicMax(&a.rew[a.env_node[e]], static_cast<unsigned long long>(__double_as_longlong(a.env_reward[e])));
           a.env_harvested[e] = 1;
           if (a.leaf_parallel && a.env_bygrasp[e]) {
             a.env_state[e] = kAwait;  // waits for the decision of round r
+#ifdef PPG_PHASE_TRACE_BUILD
+            {
+              unsigned long long t_now;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_now));
+              g_await_t0[e & 65535] = t_now;
+            }
+#endif
           } else {
             a.env_state[e] = kGone;
             atomicAdd(&ring_ctr(a, r + 1)[1], 1);  // does not step in round r + 1
@@ -739,7 +816,10 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
       a.resume_si[e] = -1;
       g += a.env_done[e] ? 1 : 0;
     }
-    for (int i = tid; i < kAsyncK * a.n_nodes; i += B) a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
+    for (int i = tid; i < kAsyncK * a.n_nodes; i += B) {
+      a.a_W[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;
+      a.a_P[(i / a.n_nodes) * a.a_wcap + i % a.n_nodes] = 0;  // the asynchronous hand-over rebuilds it
+    }
     if (tid < kRingCtr * kAsyncK) a.a_ctr[tid] = 0;
     atomicAdd(&s_G, g);
     __syncthreads();

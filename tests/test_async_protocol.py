@@ -195,7 +195,7 @@ def asynchronous(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
     return rewards, calls, rounds
 
 
-def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
+def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=False):
     """Protocol v2 (the device's lock_async_kernel): the harvester DECIDES
     round r as soon as the argmax of W(r) is robust to the envs that have not
     finished round r yet (each can still add at most cap - 1 to one node):
@@ -227,6 +227,13 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
     rnd = [0] * used
     ring_W = defaultdict(lambda: [0] * n_nodes)
     arrive, gone_at = defaultdict(int), defaultdict(int)
+    # pending bounds (the kernel's a_P ring): per round, per node, the most the
+    # envs READY for that round can still add; near = their count
+    Pend, near_n = defaultdict(lambda: [0] * n_nodes), defaultdict(int)
+    for e in range(used):
+        if state[e] == READY:
+            Pend[1][env_node[e]] += cap - 1 - tasks[e].pushes
+            near_n[1] += 1
     decided = {}
     F = D = 0
     G = sum(1 for s in state if s == GONE)  # gone through round F
@@ -248,7 +255,18 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
             m1 = max(W) if n_nodes else 0
             b = W.index(m1) if n_nodes else -1
             m2 = max([W[j] for j in range(n_nodes) if j != b], default=0)
-            if (strag > 0 or arrive[r] > 0) and (strag == 0 or (m1 > 0 and m2 + strag * (cap - 1) < m1)):
+            if pending:  # the kernel's rule: near envs by node, the rest anywhere
+                far = strag - near_n[r]
+                slack = far * (cap - 1)
+                vals = [W[i] + Pend[r][i] for i in range(n_nodes)]
+                b1 = b if m1 > 0 else -1
+                lo = max([vals[i] for i in range(n_nodes) if i < b1], default=0)
+                hi = max([vals[i] for i in range(n_nodes) if i > b1], default=0)
+                ok = strag == 0 or not leaf_parallel or (
+                    far >= 0 and ((lo + slack < m1 and hi + slack <= m1) if m1 > 0 else (far == 0 and hi == 0)))
+            else:
+                ok = strag == 0 or (m1 > 0 and m2 + strag * (cap - 1) < m1)
+            if (strag > 0 or arrive[r] > 0) and ok:
                 acts.append(("decide", r))
         # harvester: advance F
         if F + 1 in decided and arrive[F + 1] == used - (G + gone_at[F + 1]):
@@ -260,10 +278,15 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
         if kind == "step":
             e = x
             r = rnd[e] + 1
+            p_before = tasks[e].pushes
             tasks[e].step()
             rnd[e] = r
+            Pend[r][env_node[e]] -= cap - 1 - p_before
+            near_n[r] -= 1
             if not tasks[e].done:
                 ring_W[r][env_node[e]] += tasks[e].max_remaining()
+                Pend[r + 1][env_node[e]] += cap - 1 - tasks[e].pushes
+                near_n[r + 1] += 1
             else:
                 rewards[env_node[e]] = max(rewards[env_node[e]], tasks[e].reward)
                 if leaf_parallel and tasks[e].by_grasp:
@@ -282,6 +305,8 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
                 assert not tasks[e].done
                 calls.append((b, e))
                 state[e] = READY
+                Pend[rnd[e] + 1][b] += cap - 1 - tasks[e].pushes
+                near_n[rnd[e] + 1] += 1
             else:
                 state[e] = GONE
                 gone_at[rnd[e] + 1] += 1
@@ -687,3 +712,22 @@ def test_sharded_wave_rounds_equal_lockstep(seed, K, G):
         assert got[0] == ref[0], leaf
         assert sorted(got[1]) == sorted(ref[1]), leaf
         assert got[2] == ref[2], leaf
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("K", [2, 4, 16])
+def test_pending_bound_decisions_equal_lockstep(seed, K):
+    """The kernel's per-node pending bounds (envs READY for the round bound
+    their own node's W, the rest any node) keep the decisions exact, on
+    search-like batches (many nodes, one or two envs each) and wide ones."""
+    cap = 10
+    for n_nodes, n_envs in ((3 + seed % 9, 3 + seed % 9 + 20 + 7 * seed), (20 + 3 * seed, 64)):
+        nodes = _nodes(seed, n_nodes, cap)
+        for leaf in (True, False):
+            ref = lockstep(nodes, n_envs, leaf, cap, seed)
+            for sched in range(3):
+                got = asynchronous_early(nodes, n_envs, leaf, cap, seed, K, random.Random(97 * seed + sched),
+                                         pending=True)
+                assert got[0] == ref[0], (leaf, sched)
+                assert sorted(got[1]) == sorted(ref[1]), (leaf, sched)
+                assert got[2] == ref[2], (leaf, sched)

@@ -26,4 +26,5 @@ for cid, ne in (("case_18", 64), ("case_13", 64), ("case_18", 1000)):
     steps = max(v[4], 1)
     tot = sum(v[:4])
     print(cid, ne, "steps", v[4], "us/step: sample %.1f pick %.1f resolve %.1f grasp %.1f" %
-          tuple(x / steps / 1e3 for x in v[:4]), "shares", [round(x / tot, 3) for x in v[:4]])
+          tuple(x / steps / 1e3 for x in v[:4]), "shares", [round(x / tot, 3) for x in v[:4]],
+          "await: %d waits, mean %.1f us, total %.1f ms" % (v[6], v[5] / max(v[6], 1) / 1e3, v[5] / 1e6))
