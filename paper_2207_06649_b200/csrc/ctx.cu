@@ -304,7 +304,7 @@ void ppg_destroy(ppg_ctx* ctx) {
   if (ctx->h_epochs) cudaFreeHost(ctx->h_epochs);
   ctx->l_go.release();
   for (DevBuf* b : {&ctx->l_around, &ctx->l_astate, &ctx->l_aW, &ctx->l_actr, &ctx->l_adl, &ctx->l_actl, &ctx->trace_buf,
-                    &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract, &ctx->l_gring, &ctx->l_aP})
+                    &ctx->l_fin, &ctx->l_rsi, &ctx->l_ract, &ctx->l_gring, &ctx->l_aP, &ctx->l_spec})
     b->release();
   if (ctx->h_go) cudaFreeHost(ctx->h_go);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -493,12 +493,17 @@ bool async_enabled(const ppg_ctx* ctx) {
 
 template <int NW, bool kPoly>
 static int launch_async_t(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, cudaStream_t st, bool cont) {
-  static int bps[2] = {-1, -1};
-  const void* fn = reinterpret_cast<const void*>(&lock_async_kernel<NW, kPoly>);
-  int& b = bps[kPoly ? 1 : 0];
+  static int bps[4] = {-1, -1, -1, -1};
+  // speculative re-purposing compiled in only where it is used (a_spec set:
+  // small batches); the plain instantiation keeps its registers
+  const bool spec = a.a_spec != nullptr;
+  const void* fn = spec ? reinterpret_cast<const void*>(&lock_async_kernel<NW, kPoly, true>)
+                        : reinterpret_cast<const void*>(&lock_async_kernel<NW, kPoly, false>);
+  int& b = bps[(kPoly ? 1 : 0) + (spec ? 2 : 0)];
   if (b < 0) {
     int v = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lock_async_kernel<NW, kPoly>, kWarpsPerBlock * 32, 0));
+    if (spec) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lock_async_kernel<NW, kPoly, true>, kWarpsPerBlock * 32, 0));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, lock_async_kernel<NW, kPoly, false>, kWarpsPerBlock * 32, 0));
     b = v > 0 ? v : 1;
   }
   const int want = (work + 1 + kWarpsPerBlock - 1) / kWarpsPerBlock;  // + the harvester warp
@@ -513,6 +518,14 @@ static int launch_async_t(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, in
   void* args[] = {&c_arg, &a_arg};
   CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kWarpsPerBlock * 32), args, 0, st));
   return PPG_SUCCESS;
+}
+
+bool speculate_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PPG_SPECULATE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 bool wave_enabled(const ppg_ctx* ctx) {
@@ -1253,6 +1266,7 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   CK(ctx->l_astate.ensure(static_cast<size_t>(E) * 4));
   CK(ctx->l_aW.ensure(static_cast<size_t>(kAsyncK) * n_nodes * 4));
   CK(ctx->l_aP.ensure(static_cast<size_t>(kAsyncK) * n_nodes * 4));
+  CK(ctx->l_spec.ensure(static_cast<size_t>(E) * 16 + 16));
   CK(ctx->l_actr.ensure(static_cast<size_t>(kAsyncK) * kRingCtr * 4));
   CK(ctx->l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   CK(ctx->l_actl.ensure(64));
@@ -1309,6 +1323,7 @@ int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta,
   a.env_state = ctx->l_astate.as<int32_t>();
   a.a_W = ctx->l_aW.as<int32_t>();
   a.a_P = ctx->l_aP.as<int32_t>();
+  a.a_spec = speculate_enabled() && E <= kSpecMaxEnvs ? ctx->l_spec.as<int4>() : nullptr;
   a.a_ctr = ctx->l_actr.as<int32_t>();
   a.a_dl = ctx->l_adl.as<int32_t>();
   a.a_ctl = ctx->l_actl.as<int32_t>();

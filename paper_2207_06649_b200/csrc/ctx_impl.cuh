@@ -70,7 +70,7 @@ __global__ void wave_harvest_kernel(const __grid_constant__ SimConst C, LockArgs
 __global__ void wave_pack_kernel(LockArgs a);
 __global__ void wave_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void wave_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
-template <int NW, bool kPoly>
+template <int NW, bool kPoly, bool kSpecul>
 __global__ void lock_async_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_sample_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void lock_post_warp_kernel(const __grid_constant__ SimConst C, LockArgs a);
@@ -208,6 +208,7 @@ struct ppg_ctx {
   ppg::DevBuf l_fin, l_rsi, l_ract;       // wave rounds: post list, resumable physics progress
   ppg::DevBuf l_gring;                   // sharded wave rounds: the exchanged ring (LockArgs.g_ring)
   ppg::DevBuf l_aP;                      // asynchronous lockstep: pending bounds ring (LockArgs.a_P)
+  ppg::DevBuf l_spec;                    // asynchronous lockstep: held speculative steps (LockArgs.a_spec)
   int32_t* h_go = nullptr;                // pinned copy
 };
 
@@ -232,6 +233,10 @@ int launch_async(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, int work, c
 // Wave rounds (warp_env.cu wave_*_kernel): one wave = harvest, sample,
 // budgeted lane physics, post.  PPG_WAVE=0 disables them (barrier hybrid rounds).
 bool wave_enabled(const ppg_ctx* ctx);
+bool speculate_enabled();  // PPG_SPECULATE=0 switches speculative re-purposing off
+// speculation pays where envs wait on decisions (small batches); wide batches
+// measured ~1 % slower with it (profiles/r2g_speculation_ab.txt)
+constexpr int kSpecMaxEnvs = 2048;
 int launch_wave(ppg_ctx* ctx, const SimConst& C, const LockArgs& a, const ResolveArgs& ra, int work, cudaStream_t st);
 int lock_setup(ppg_ctx* ctx, const double* node_poses, const int32_t* node_meta, int n_nodes, int used,
                int used_global, int env_lo, int leaf_parallel, uint64_t seed, uint64_t iteration, int depth_cap);

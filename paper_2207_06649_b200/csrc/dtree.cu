@@ -535,7 +535,7 @@ struct DTreeState {
   // lockstep state
   DevBuf l_node, l_pushes, l_done, l_byg, l_harv, l_flag, l_reward, l_poses, l_mt, l_mtidx, l_W, l_rew, l_active,
       l_nactive, l_counters, l_push, l_status, l_stepping, l_around, l_astate, l_aW, l_actr, l_adl, l_fin, l_rsi,
-      l_ract, l_aP;
+      l_ract, l_aP, l_spec;
   int cap_nodes = 0;
   long long cap_actions = 0;
   int n_envs = 0, n = 0, na = 0;
@@ -598,7 +598,8 @@ struct DTreeState {
                       &poses, &anc, &apool, &cpool, &sel_node, &sel_act, &gp, &ga, &cp, &st, &gr, &nu, &un,
                       &meta, &logtab, &sc, &l_node, &l_pushes, &l_done, &l_byg, &l_harv, &l_flag, &l_reward,
                       &l_poses, &l_mt, &l_mtidx, &l_W, &l_rew, &l_active, &l_nactive, &l_counters, &l_push,
-                      &l_status, &l_stepping, &l_around, &l_astate, &l_aW, &l_actr, &l_adl, &l_fin, &l_rsi, &l_ract, &l_aP};
+                      &l_status, &l_stepping, &l_around, &l_astate, &l_aW, &l_actr, &l_adl, &l_fin, &l_rsi, &l_ract, &l_aP,
+                      &l_spec};
     for (DevBuf* b : bufs) b->release();
   }
 };
@@ -738,6 +739,7 @@ int dt_batch(ppg_ctx* ctx, DTreeState& S) {
   DCK(S.l_astate.ensure(static_cast<size_t>(E) * 4));
   DCK(S.l_aW.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_aP.ensure(static_cast<size_t>(kAsyncK) * E * 4));
+  DCK(S.l_spec.ensure(static_cast<size_t>(E) * 16 + 16));
   DCK(S.l_actr.ensure(static_cast<size_t>(kAsyncK) * kRingCtr * 4));
   DCK(S.l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_fin.ensure(static_cast<size_t>(E) * 4 + 16));
@@ -824,6 +826,7 @@ void dt_views(ppg_ctx* ctx, DTreeState& S) {
   a.env_state = S.l_astate.as<int32_t>();
   a.a_W = S.l_aW.as<int32_t>();
   a.a_P = S.l_aP.as<int32_t>();
+  a.a_spec = speculate_enabled() && S.n_envs <= kSpecMaxEnvs ? S.l_spec.as<int4>() : nullptr;
   a.a_ctr = S.l_actr.as<int32_t>();
   a.a_dl = S.l_adl.as<int32_t>();
   a.a_ctl = t.sc->async_ctl;
@@ -1829,6 +1832,31 @@ int ppg_run_pmbs_device(ppg_ctx* ctx, const double* root_poses, double* action_o
     }
     if (h.async_ctl[3] != 0) {
       ctx->err = "device tree: asynchronous lockstep stalled (protocol error)";
+      if (std::getenv("PPG_ASYNC_DUMP")) {  // protocol state at the stall (debugging)
+        const int E = S.n_envs;
+        std::vector<int32_t> ctr(static_cast<size_t>(kAsyncK) * kRingCtr), st(E), rd(E), nd(E), pu(E);
+        std::vector<uint8_t> dn(E);
+        cudaMemcpy(ctr.data(), S.l_actr.p, ctr.size() * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(st.data(), S.l_astate.p, E * 4ull, cudaMemcpyDeviceToHost);
+        cudaMemcpy(rd.data(), S.l_around.p, E * 4ull, cudaMemcpyDeviceToHost);
+        cudaMemcpy(nd.data(), S.l_node.p, E * 4ull, cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "async stall: ctl");
+        for (int k = 0; k < 16; ++k) std::fprintf(stderr, " %d", h.async_ctl[k]);
+        std::fprintf(stderr, "\n");
+        for (int k = 0; k < kAsyncK; ++k) {
+          std::fprintf(stderr, " slot %d:", k);
+          for (int j = 0; j < 10; ++j) std::fprintf(stderr, " %d", ctr[k * kRingCtr + j]);
+          std::fprintf(stderr, "\n");
+        }
+        int cnt[8] = {};
+        for (int e = 0; e < h.lock_dyn[1] && e < E; ++e) {
+          const int v = st[e];
+          cnt[v >= 0 && v < 7 ? v : 7]++;
+          if (v != 2) std::fprintf(stderr, "  env %d state %d round %d node %d\n", e, v, rd[e], nd[e]);
+        }
+        std::fprintf(stderr, " states: ready %d await %d gone %d spec %d other %d\n", cnt[0], cnt[1], cnt[2], cnt[4],
+                     cnt[7]);
+      }
       return PPG_ECUDA;
     }
     if (h.err[0]) {

@@ -166,6 +166,8 @@ struct LockArgs {
   // step that round but have not finished it can still add to W [K][a_wcap]
   // (count of those envs: ring slot field [6])
   int32_t* a_P = nullptr;
+  // speculative re-purposing: per env (node, pushes before, saved mt_idx, resolve counted)
+  int4* a_spec = nullptr;
   int a_wcap = 0;
   // wave rounds (warp_env.cu wave_*_kernel): envs whose physics finished in
   // this wave (post pending), and the resumable physics progress
@@ -185,7 +187,8 @@ constexpr int kLockRoundLimit = 1 << 20;
 #define PPG_ASYNC_K 16
 #endif
 constexpr int kAsyncK = PPG_ASYNC_K;  // ring depth: rounds an env may run ahead of the last complete round
-constexpr int kRingCtr = 8;  // ints per ring slot: arrived, gone at this round, done-list length, decided round, decision
+constexpr int kRingCtr = 16;  // ints per ring slot: arrived, gone at this round, done-list length, decided round,
+                              // decision, applied, near count, -, provisional decision (u64 at [8])
 
 // Applies the device-side per-iteration overrides (device tree mode).
 __device__ __forceinline__ void lock_dyn(LockArgs& a) {

@@ -436,6 +436,7 @@ PPG_DI uint64_t mix_keys(uint64_t seed, uint64_t a, uint64_t b) {  // rng.hpp:15
 struct MtView {
   uint64_t* mt;  // &state[0][e]
   int stride;    // E
+  bool frozen = false;  // speculative use: a draw that needs a twist aborts (idx = kMtFrozen)
   PPG_DI uint64_t& w(int i) const { return mt[static_cast<size_t>(i) * stride]; }
 };
 

@@ -244,8 +244,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
 // sample + pick + resolve + graspable, state in HBM (env_*), the warp's
 // shared blocks `blk` / `valid` / the polygon caches as scratch.
 template <int NW, bool kPoly>
-PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, double* blk, unsigned* valid,
-                              const uint16_t* pij, const WarpPoly& G) {
+PPG_DI int warp_rollout_step(const SimConst& C, const LockArgs& a, int e, double* blk, unsigned* valid,
+                             const uint16_t* pij, const WarpPoly& G, bool frozen = false) {
   const int n = C.n, l = threadIdx.x & 31;
   WarpEnv W(blk, n, l);
   const ShapeView S = a.S.view(0);
@@ -289,9 +289,9 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
       a.env_done[e] = 1;
       a.env_reward[e] = 0.0;
     }
-    return;
+    return 0;
   }
-  const MtView g{a.mt + e, a.E};
+  const MtView g{a.mt + e, a.E, frozen};
   int idx = a.mt_idx[e];
   const uint64_t k = warp_mt_pick(g, idx, static_cast<uint64_t>(count), l);
   if (l == 0) a.mt_idx[e] = idx;
@@ -317,7 +317,7 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
       a.env_done[e] = 1;
       a.env_reward[e] = 0.0;
     }
-    return;
+    return 1;
   }
   const GraspOut gr = warp_graspable(W, S, C, a.S.target[0]);
 #ifdef PPG_PHASE_TRACE_BUILD
@@ -336,6 +336,7 @@ PPG_DI void warp_rollout_step(const SimConst& C, const LockArgs& a, int e, doubl
     }
   }
   warp_store(W, env);
+  return 1;
 }
 
 // RolloutCursor::step (mcts.cpp:142-171), one warp per active environment.
@@ -389,7 +390,7 @@ PPG_DI unsigned long long now_ns() {
 constexpr unsigned long long kAsyncStallNs = 20ull * 1000 * 1000 * 1000;  // 20 s without progress: error
 
 // env_state values of the asynchronous / wave protocols
-enum : int { kReady = 0, kAwait = 1, kGone = 2, kPhys = -1 };
+enum : int { kReady = 0, kAwait = 1, kGone = 2, kPhys = -1, kSpec = 4 };  // kSpec: a speculative step is held
 
 // Ring views
 PPG_DI int32_t* ring_ctr(const LockArgs& a, int r) { return a.a_ctr + kRingCtr * (r % kAsyncK); }
@@ -420,7 +421,7 @@ __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockA
 #ifndef PPG_ASYNC_BLOCKS
 #define PPG_ASYNC_BLOCKS 3  // resident blocks per SM the register budget is sized for
 #endif
-template <int NW, bool kPoly>
+template <int NW, bool kPoly, bool kSpecul>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_async_kernel(const __grid_constant__ SimConst C,
                                                                            LockArgs a) {
   PPG_POLY_SMEM
@@ -514,17 +515,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
           }
           // the most any other node can still reach, split by its side of b1
           // (a tie goes to the lower node)
-          int lo = 0, hi = 0;
+          int lo = 0, hi = 0, vb = 0, ib = -1;  // vb / ib: the likely outcome, argmax(W + P)
           for (int i = l; i < a.n_nodes; i += 32) {
             const int pi = ld_acquire(&Pr[i]);  // P before W
             const int v = pi + ld_volatile(&W[i]);
             if (i < b1) lo = max(lo, v);
             else if (i > b1) hi = max(hi, v);
+            if (v > vb) {
+              vb = v;
+              ib = i;
+            }
           }
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) {
             lo = max(lo, __shfl_xor_sync(kFull, lo, off));
             hi = max(hi, __shfl_xor_sync(kFull, hi, off));
+            const int ov = __shfl_xor_sync(kFull, vb, off), oi = __shfl_xor_sync(kFull, ib, off);
+            if (ov > vb || (ov == vb && ov > 0 && oi < ib)) {
+              vb = ov;
+              ib = oi;
+            }
           }
           const int slack = far * (a.cap - 1);
           // (m1 from the first pass is a lower bound of W(r)[b1]; with m1 = 0,
@@ -539,6 +549,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
             }
             D = r;
             progress = true;
+          } else if (kSpecul && l == 0 && a.leaf_parallel) {
+            // not fixed yet: the likely decision, for speculative re-purposing
+            const unsigned long long pv = static_cast<unsigned long long>(static_cast<unsigned>(r)) << 32 |
+                                          static_cast<unsigned>(vb > 0 ? ib : -1);
+            atomicExch(reinterpret_cast<unsigned long long*>(rc + 8), pv);
           }
         }
       }
@@ -611,11 +626,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
     for (int e = wk; e < used; e += nwk) {
       int st = l == 0 ? ld_volatile(&a.env_state[e]) : 0;
       st = __shfl_sync(kFull, st, 0);
-      if (st == kAwait) {  // finished by grasp in round rho: apply the decision of rho once published
-        int b = -2;
+      if (st == kAwait || st == kSpec) {
+        // finished by grasp in round rho: apply the decision of rho once
+        // published (pmbs.cpp:181-185); until then, step speculatively at the
+        // likely decision and hold the result (kSpec): kept when the decision
+        // agrees, discarded (cursor, RNG index and counters restored) when not
+        int b = -2, spec_node = -1;
         if (l == 0) {
           const int rho = a.env_round[e];
-          const int32_t* rc = ring_ctr(a, rho);
+          int32_t* rc = ring_ctr(a, rho);
           if (ld_volatile(&rc[3]) == rho) {
 #ifdef PPG_PHASE_TRACE_BUILD
             {
@@ -627,23 +646,88 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
 #endif
             __threadfence();
             b = ld_volatile(&rc[4]);
-            if (b >= 0) {  // re-purpose (pmbs.cpp:181-185): RolloutCursor ctor at b, continues at round rho + 1
-              cursor_init(C, a, e, b);
-              a.env_harvested[e] = 0;
-              atomicAdd(&ring_P(a, rho + 1)[b], a.cap - 1 - a.env_pushes[e]);
-              atomicAdd(&ring_ctr(a, rho + 1)[6], 1);
-              a.env_state[e] = kReady;
-              atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[2]), 1ull);
-            } else {
-              a.env_state[e] = kGone;
-              atomicAdd(&ring_ctr(a, rho + 1)[1], 1);  // does not step in round rho + 1
+            bool kept = false;
+            if (kSpecul && st == kSpec) {
+              const int4 sp = a.a_spec[e];
+              if (b == sp.x && a.mt_idx[e] < kMtFrozen) {  // the held step stands: publish it as round rho + 1
+                kept = true;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[2]), 1ull);
+                const int r = rho + 1;
+                int32_t* rc2 = ring_ctr(a, r);
+                a.env_round[e] = r;
+                const int node = a.env_node[e];
+                if (!a.env_done[e]) atomicAdd(&a.a_W[(r % kAsyncK) * a.a_wcap + node], a.cap - a.env_pushes[e]);
+                __threadfence();
+                if (!a.env_done[e]) {
+                  atomicAdd(&ring_P(a, r + 1)[node], a.cap - 1 - a.env_pushes[e]);
+                  atomicAdd(&ring_ctr(a, r + 1)[6], 1);
+                  a.env_state[e] = kReady;
+                } else {
+                  atomicMax(&a.rew[node], static_cast<unsigned long long>(__double_as_longlong(a.env_reward[e])));
+                  a.env_harvested[e] = 1;
+                  if (a.env_bygrasp[e]) {
+                    a.env_state[e] = kAwait;
+                  } else {
+                    a.env_state[e] = kGone;
+                    atomicAdd(&ring_ctr(a, r + 1)[1], 1);
+                  }
+                }
+                __threadfence();
+                atomicAdd(&rc2[0], 1);
+                b = -3;  // handled
+              } else {  // discard the held step: back to "finished by grasp, harvested"
+                a.mt_idx[e] = sp.z;
+                a.env_harvested[e] = 1;
+                a.env_done[e] = 1;
+                a.env_bygrasp[e] = 1;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[0]), ~0ull);
+                if (sp.w) atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[3]), ~0ull);
+              }
             }
+            if (!kept) {
+              if (b >= 0) {  // re-purpose: RolloutCursor ctor at b, continues at round rho + 1
+                cursor_init(C, a, e, b);
+                a.env_harvested[e] = 0;
+                atomicAdd(&ring_P(a, rho + 1)[b], a.cap - 1 - a.env_pushes[e]);
+                atomicAdd(&ring_ctr(a, rho + 1)[6], 1);
+                a.env_state[e] = kReady;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&a.counters[2]), 1ull);
+              } else {
+                a.env_state[e] = kGone;
+                atomicAdd(&ring_ctr(a, rho + 1)[1], 1);  // does not step in round rho + 1
+              }
+            }
+          } else if (kSpecul && st == kAwait && rho + 1 <= F + kAsyncK - 1 && a.mt_idx[e] < 312) {
+            const unsigned long long pv = *reinterpret_cast<volatile unsigned long long*>(rc + 8);
+            const int pn = static_cast<int>(static_cast<unsigned>(pv));
+            if (static_cast<int>(pv >> 32) == rho && pn >= 0) spec_node = pn;
           }
         }
         b = __shfl_sync(kFull, b, 0);
+        spec_node = __shfl_sync(kFull, spec_node, 0);
         __syncwarp();
+        if (kSpecul && b == -2 && spec_node >= 0) {  // speculative step at the likely decision
+          int p_before = 0, mt0 = 0;
+          if (l == 0) {
+            mt0 = a.mt_idx[e];
+            cursor_init(C, a, e, spec_node);
+            a.env_harvested[e] = 0;
+            p_before = a.env_pushes[e];
+          }
+          __syncwarp();
+          const int res = warp_rollout_step<NW, kPoly>(C, a, e, blk[wib], valid[wib], pij, G, true);
+          __syncwarp();
+          if (l == 0) {
+            a.a_spec[e] = make_int4(spec_node, p_before, mt0, res);
+            a.env_state[e] = kSpec;
+          }
+          __syncwarp();
+          progress = true;
+          continue;
+        }
         if (b == -2) continue;
         progress = true;
+        if (b == -3) continue;
         st = b >= 0 ? kReady : kGone;
       }
       if (st != kReady) continue;
@@ -1205,7 +1289,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) lock_post_warp_kernel(con
   template __global__ void resolve_warp_kernel<NW, P>(const __grid_constant__ SimConst, ResolveArgs);  \
   template __global__ void expand_warp_kernel<NW, P>(const __grid_constant__ SimConst, ExpandArgs);    \
   template __global__ void lock_step_warp_kernel<NW, P>(const __grid_constant__ SimConst, LockArgs);        \
-  template __global__ void lock_async_kernel<NW, P>(const __grid_constant__ SimConst, LockArgs);
+  template __global__ void lock_async_kernel<NW, P, false>(const __grid_constant__ SimConst, LockArgs); \
+  template __global__ void lock_async_kernel<NW, P, true>(const __grid_constant__ SimConst, LockArgs);
 PPG_WARP_INST(1, false)
 PPG_WARP_INST(2, false)
 PPG_WARP_INST(4, false)

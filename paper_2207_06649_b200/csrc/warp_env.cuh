@@ -470,8 +470,14 @@ PPG_DI void warp_twist(const MtView& g, int l) {
   __syncwarp();
 }
 
+constexpr int kMtFrozen = 1 << 20;  // idx after a frozen view needed a twist
+
 PPG_DI uint64_t warp_mt_next(const MtView& g, int& idx, int l) {
   if (idx >= 312) {
+    if (g.frozen) {  // the state must stay untouched: abort the draw
+      idx = kMtFrozen;
+      return 0;
+    }
     warp_twist(g, l);
     idx = 0;
   }
@@ -486,11 +492,13 @@ PPG_DI uint64_t warp_mt_next(const MtView& g, int& idx, int l) {
 // uniform_int_distribution<size_t>(0, n-1) (uniform_int_dist.h:255-280)
 PPG_DI uint64_t warp_mt_pick(const MtView& g, int& idx, uint64_t n, int l) {
   uint64_t xw = warp_mt_next(g, idx, l);
+  if (idx >= kMtFrozen) return 0;
   uint64_t low = xw * n, high = __umul64hi(xw, n);
   if (low < n) {
     const uint64_t thr = (0ull - n) % n;
     while (low < thr) {
       xw = warp_mt_next(g, idx, l);
+      if (idx >= kMtFrozen) return 0;
       low = xw * n;
       high = __umul64hi(xw, n);
     }
