@@ -208,6 +208,9 @@ int ppg_simulate_count(ppg_ctx* ctx, const double* node_poses, const int32_t* no
  * the per-node remaining work W (pmbs.cpp:157-163), all-reduced (sum) over
  * NVLink — so every shard re-purposes its own finished envs to the same
  * argmax node as the reference's sequential harvest (pmbs.cpp:165-187).
+ * Disc scenes run the rounds as waves: one all-reduce per wave of the ring
+ * of per-round W vectors and (arrived, gone) counts, from which every shard
+ * takes the same (early) decisions.
  * Per-node rewards are all-reduced (max) once per iteration.  Results
  * (decision, tree, rewards) are bit-identical for every G.  ppg_simulate and
  * ppg_run_pmbs* on such a context run sharded; every other call runs on the
