@@ -139,12 +139,93 @@ __device__ __forceinline__ void sel_merge(double& bs, int& bk, int& bp, double o
   }
 }
 
+// Children of node x scored by the calling thread (children k = tid,
+// tid + kSelThreads, ...; all loads of a chunk issued before any score):
+// the thread's first maximum (score, insertion index, packed child).
+__device__ __forceinline__ void dt_scan_children(const DTree& t, int x, double lg, int dT, double cexp, int tid,
+                                                 double& bs, int& bk, int& bp) {
+  const long long co = t.u_off[x];
+  const int cn = t.c_n[x];
+  constexpr int kScanU = 2;
+  for (int k0 = 0; k0 < cn; k0 += kSelThreads * kScanU) {
+    int ch[kScanU];
+#pragma unroll
+    for (int u = 0; u < kScanU; ++u) {
+      const int k = k0 + kSelThreads * u + tid;
+      ch[u] = k < cn ? t.cpool[co + k] : -1;
+    }
+    bool sel[kScanU], slf[kScanU];
+    long long nci[kScanU];
+    double qc[kScanU];
+#pragma unroll
+    for (int u = 0; u < kScanU; ++u) {
+      const int c = ch[u] >= 0 ? ch[u] : 0;
+      const bool ok = ch[u] >= 0 && t.flags[c] == 0;
+      slf[u] = ok && t.depth[c] < dT && t.u_head[c] < t.u_n[c];
+      sel[u] = slf[u] || (ok && t.selc[c] > 0);  // dt_selectable
+      nci[u] = ch[u] >= 0 ? t.visits[c] + t.vv[c] : 0;
+      qc[u] = ch[u] >= 0 ? t.q[c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kScanU; ++u) {
+      if (!sel[u]) continue;
+      double sv = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
+      if (nci[u] != 0) {
+        const double nc = static_cast<double>(nci[u]);
+        sv = qc[u] / nc + cexp * sqrt(2.0 * lg / nc);
+      }
+      if (sv > bs) {
+        bs = sv;
+        bk = k0 + kSelThreads * u + tid;
+        bp = 2 * ch[u] + (slf[u] ? 1 : 0);
+      }
+    }
+  }
+}
+
+// Block-wide first maximum of the threads' (score, index, packed child):
+// warp reduction, per-warp partials (double-buffered by `parity`, ONE block
+// barrier), then every warp reduces the partials itself.
+template <int kWarps>
+__device__ __forceinline__ void dt_block_best(double& bs, int& bk, int& bp, double (*s_bs)[kWarps],
+                                              int (*s_bk)[kWarps], int (*s_bp)[kWarps], int& parity, int l,
+                                              int wid) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)  // first maximum in insertion order
+    sel_merge(bs, bk, bp, __shfl_xor_sync(kAll, bs, o), __shfl_xor_sync(kAll, bk, o), __shfl_xor_sync(kAll, bp, o));
+  if (l == 0) {
+    s_bs[parity][wid] = bs;
+    s_bk[parity][wid] = bk;
+    s_bp[parity][wid] = bp;
+  }
+  __syncthreads();
+  bs = l < kWarps ? s_bs[parity][l] : -INFINITY;
+  bk = l < kWarps ? s_bk[parity][l] : INT_MAX;
+  bp = l < kWarps ? s_bp[parity][l] : -2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    sel_merge(bs, bk, bp, __shfl_xor_sync(kAll, bs, o), __shfl_xor_sync(kAll, bk, o), __shfl_xor_sync(kAll, bp, o));
+  parity ^= 1;
+}
+
+// The root and its children are the nodes every draw reads and updates
+// (virtual visits, untried heads, selectable counts): with up to
+// kSelCache children they live in shared memory for the whole kernel and are
+// written back at the end; deeper levels read the tree in HBM.
+constexpr int kSelCache = 512;
+
 __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
   constexpr int kWarps = kSelThreads / 32;
-  // per-level warp partials, double-buffered by level parity: ONE block
-  // barrier per level (every warp then reduces the partials itself)
   __shared__ double s_bs[2][kWarps];
   __shared__ int s_bk[2][kWarps], s_bp[2][kWarps];
+  // root-children cache (slot k = insertion index k of the root's children)
+  __shared__ int s_ch[kSelCache], s_vv[kSelCache], s_uh[kSelCache], s_un[kSelCache], s_selc[kSelCache],
+      s_dep[kSelCache];
+  __shared__ long long s_vis[kSelCache];
+  __shared__ double s_q[kSelCache];
+  __shared__ uint8_t s_fl[kSelCache];
+  __shared__ long long s_rvis;
+  __shared__ int s_r[6];  // root: vv, u_head, u_n, selc, flags, depth
   DTScal* sc = t.sc;
   const int tid = threadIdx.x, l = tid & 31, wid = tid >> 5;
   const int dT = sc->dT;
@@ -152,71 +233,160 @@ __global__ void __launch_bounds__(kSelThreads) dt_select_kernel(DTree t) {
   int draws = 0;
   bool bad = false;
   int parity = 0;
-  if (sc->stop < 0) {
+  const int cn0 = t.c_n[0];
+  const bool cached = cn0 <= kSelCache;
+  if (sc->stop < 0 && cached) {
+    const long long co0 = t.u_off[0];
+    for (int k = tid; k < cn0; k += kSelThreads) {
+      const int c = t.cpool[co0 + k];
+      s_ch[k] = c;
+      s_vv[k] = t.vv[c];
+      s_uh[k] = t.u_head[c];
+      s_un[k] = t.u_n[c];
+      s_selc[k] = t.selc[c];
+      s_dep[k] = t.depth[c];
+      s_vis[k] = t.visits[c];
+      s_q[k] = t.q[c];
+      s_fl[k] = t.flags[c];
+    }
+    if (tid == 0) {
+      s_rvis = t.visits[0];
+      s_r[0] = t.vv[0];
+      s_r[1] = t.u_head[0];
+      s_r[2] = t.u_n[0];
+      s_r[3] = t.selc[0];
+      s_r[4] = t.flags[0];
+      s_r[5] = t.depth[0];
+    }
+    __syncthreads();
+    for (; draws < t.n_envs; ++draws) {
+      // subtree_selectable(root) / is the root itself expandable
+      const bool rself = s_r[4] == 0 && s_r[5] < dT && s_r[1] < s_r[2];
+      if (!(rself || (s_r[4] == 0 && s_r[3] > 0))) break;
+      int x = 0, lvl = 0, slot1 = -1;
+      int my_node = 0;  // thread d keeps the root path's node at depth d
+      bool self = rself;
+      if (!self) {  // descend_virtual (pmbs.cpp:30-48), the root level from the cache
+        const double lg = t.logtab[s_rvis + s_r[0]];
+        double bs = -INFINITY;
+        int bk = INT_MAX, bp = -2;
+        for (int k = tid; k < cn0; k += kSelThreads) {
+          const bool ok = s_fl[k] == 0;
+          const bool slf = ok && s_dep[k] < dT && s_uh[k] < s_un[k];
+          if (!(slf || (ok && s_selc[k] > 0))) continue;
+          const long long nci = s_vis[k] + s_vv[k];
+          double sv = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
+          if (nci != 0) {
+            const double nc = static_cast<double>(nci);
+            sv = s_q[k] / nc + cexp * sqrt(2.0 * lg / nc);
+          }
+          if (sv > bs) {
+            bs = sv;
+            bk = k;
+            bp = 2 * s_ch[k] + (slf ? 1 : 0);
+          }
+        }
+        dt_block_best<kWarps>(bs, bk, bp, s_bs, s_bk, s_bp, parity, l, wid);
+        ++lvl;
+        if (bk == INT_MAX) {
+          bad = true;
+        } else {
+          x = bp >> 1;
+          self = (bp & 1) != 0;
+          slot1 = bk;
+          if (tid == 1) my_node = x;
+        }
+        while (!bad && !self) {  // deeper levels from HBM
+          const int vx = lvl == 1 ? s_vv[slot1] : t.vv[x];
+          const double lgx = t.logtab[t.visits[x] + vx];
+          bs = -INFINITY;
+          bk = INT_MAX;
+          bp = -2;
+          dt_scan_children(t, x, lgx, dT, cexp, tid, bs, bk, bp);
+          dt_block_best<kWarps>(bs, bk, bp, s_bs, s_bk, s_bp, parity, l, wid);
+          ++lvl;
+          if (bk == INT_MAX) {  // impossible under the selc invariant
+            bad = true;
+            break;
+          }
+          x = bp >> 1;
+          self = (bp & 1) != 0;
+          if (tid == lvl) my_node = x;
+        }
+      }
+      if (bad) break;
+      // virtual visit on the root path (one node per thread)
+      if (tid == 0) s_r[0] += 1;
+      else if (tid == 1 && lvl >= 1) s_vv[slot1] += 1;
+      else if (tid <= lvl) t.vv[my_node] += 1;
+      if (tid == 0) {  // pop_untried (mcts.cpp:13-16)
+        int h, un, dx;
+        if (lvl == 0) {
+          h = s_r[1]++;
+          un = s_r[2];
+          dx = s_r[5];
+        } else if (lvl == 1) {
+          h = s_uh[slot1]++;
+          un = s_un[slot1];
+          dx = s_dep[slot1];
+        } else {
+          h = t.u_head[x];
+          t.u_head[x] = h + 1;
+          un = t.u_n[x];
+          dx = t.depth[x];
+        }
+        t.sel_node[draws] = x;
+        t.sel_act[draws] = t.u_off[x] + h;
+        if (h + 1 == un) {  // now fully expanded
+          sc->unsettled[dx] -= 1;
+          const int sx = lvl == 0 ? s_r[3] : lvl == 1 ? s_selc[slot1] : t.selc[x];
+          if (sx == 0) {  // x left the selectable set: update its ancestors (all on this draw's path)
+            for (int d = lvl - 1; d >= 0; --d) {
+              bool still;
+              if (d == 0) {
+                s_r[3] -= 1;
+                still = s_r[4] == 0 && ((s_r[5] < dT && s_r[1] < s_r[2]) || s_r[3] > 0);
+              } else if (d == 1) {
+                s_selc[slot1] -= 1;
+                still = s_fl[slot1] == 0 && ((s_dep[slot1] < dT && s_uh[slot1] < s_un[slot1]) || s_selc[slot1] > 0);
+              } else {
+                // the ancestor at depth d: walk up from x
+                int p = x;
+                for (int k = lvl; k > d; --k) p = t.parent[p];
+                t.selc[p] -= 1;
+                still = dt_selectable(t, p, dT);
+              }
+              if (still) break;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // write the cached nodes back
+    if (tid == 0) {
+      t.vv[0] = s_r[0];
+      t.u_head[0] = s_r[1];
+      t.selc[0] = s_r[3];
+    }
+    for (int k = tid; k < cn0; k += kSelThreads) {
+      const int c = s_ch[k];
+      t.vv[c] = s_vv[k];
+      t.u_head[c] = s_uh[k];
+      t.selc[c] = s_selc[k];
+    }
+  } else if (sc->stop < 0) {
     for (; draws < t.n_envs; ++draws) {
       if (!dt_selectable(t, 0, dT)) break;  // every thread reads the same state
       int x = 0, lvl = 0;
-      int my_node = 0;  // thread d keeps the root path's node at depth d
+      int my_node = 0;
       bool self = dt_self(t, 0, dT);
       while (!self) {  // descend_virtual (pmbs.cpp:30-48)
-        const long long co = t.u_off[x];
-        const int cn = t.c_n[x];
         const double lg = t.logtab[t.visits[x] + t.vv[x]];  // log(n_parent)
         double bs = -INFINITY;
         int bk = INT_MAX, bp = -2;
-        constexpr int kScanU = 2;
-        for (int k0 = 0; k0 < cn; k0 += kSelThreads * kScanU) {
-          int ch[kScanU];
-#pragma unroll
-          for (int u = 0; u < kScanU; ++u) {
-            const int k = k0 + kSelThreads * u + tid;
-            ch[u] = k < cn ? t.cpool[co + k] : -1;
-          }
-          bool sel[kScanU], slf[kScanU];
-          long long nci[kScanU];
-          double qc[kScanU];
-#pragma unroll
-          for (int u = 0; u < kScanU; ++u) {
-            const int c = ch[u] >= 0 ? ch[u] : 0;
-            const bool ok = ch[u] >= 0 && t.flags[c] == 0;
-            slf[u] = ok && t.depth[c] < dT && t.u_head[c] < t.u_n[c];
-            sel[u] = slf[u] || (ok && t.selc[c] > 0);  // dt_selectable
-            nci[u] = ch[u] >= 0 ? t.visits[c] + t.vv[c] : 0;
-            qc[u] = ch[u] >= 0 ? t.q[c] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < kScanU; ++u) {
-            if (!sel[u]) continue;
-            double sv = INFINITY;  // ucb_virtual (pmbs.cpp:12-17)
-            if (nci[u] != 0) {
-              const double nc = static_cast<double>(nci[u]);
-              sv = qc[u] / nc + cexp * sqrt(2.0 * lg / nc);
-            }
-            if (sv > bs) {
-              bs = sv;
-              bk = k0 + kSelThreads * u + tid;
-              bp = 2 * ch[u] + (slf[u] ? 1 : 0);
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)  // first maximum in insertion order
-          sel_merge(bs, bk, bp, __shfl_xor_sync(kAll, bs, o), __shfl_xor_sync(kAll, bk, o),
-                    __shfl_xor_sync(kAll, bp, o));
-        if (l == 0) {
-          s_bs[parity][wid] = bs;
-          s_bk[parity][wid] = bk;
-          s_bp[parity][wid] = bp;
-        }
-        __syncthreads();
-        bs = l < kWarps ? s_bs[parity][l] : -INFINITY;
-        bk = l < kWarps ? s_bk[parity][l] : INT_MAX;
-        bp = l < kWarps ? s_bp[parity][l] : -2;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-          sel_merge(bs, bk, bp, __shfl_xor_sync(kAll, bs, o), __shfl_xor_sync(kAll, bk, o),
-                    __shfl_xor_sync(kAll, bp, o));
-        parity ^= 1;
+        dt_scan_children(t, x, lg, dT, cexp, tid, bs, bk, bp);
+        dt_block_best<kWarps>(bs, bk, bp, s_bs, s_bk, s_bp, parity, l, wid);
         ++lvl;
         if (bk == INT_MAX) {  // impossible under the selc invariant
           bad = true;
