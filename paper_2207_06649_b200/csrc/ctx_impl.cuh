@@ -68,6 +68,7 @@ __global__ void lock_post_kernel(const __grid_constant__ SimConst C, LockArgs a)
 __global__ void lock_async_init_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void wave_harvest_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void wave_pack_kernel(LockArgs a);
+__global__ void wave_pack_pending_kernel(LockArgs a);
 __global__ void wave_sample_kernel(const __grid_constant__ SimConst C, LockArgs a);
 __global__ void wave_post_kernel(const __grid_constant__ SimConst C, LockArgs a);
 template <int NW, bool kPoly, bool kSpecul>

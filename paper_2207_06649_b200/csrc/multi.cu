@@ -33,6 +33,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -320,7 +321,9 @@ bool shard_waves_enabled(const ppg_ctx* ctx) {
 // hand-over to the asynchronous kernel (its exchange would be continuous).
 int sharded_wave_rounds(ppg_ctx* ctx, Group* g, std::vector<ShardWave>& sw, int P, int work) {
   const int M = static_cast<int>(sw.size());
-  const size_t count = static_cast<size_t>(kAsyncK) * P + 2 * kAsyncK;
+  // W ring, per-round (arrived, gone), then the pending bounds of the next
+  // undecided round (round, near count, per node) — warp_env.cu wave_pack_kernel
+  const size_t count = static_cast<size_t>(kAsyncK) * P + 2 * kAsyncK + 2 + P;
   std::vector<int32_t*> gb(M);
   for (int k = 0; k < M; ++k) {
     ppg_ctx* c = sw[k].c;
@@ -340,6 +343,7 @@ int sharded_wave_rounds(ppg_ctx* ctx, Group* g, std::vector<ShardWave>& sw, int 
       ppg_ctx* c = sw[k].c;
       CK(cudaSetDevice(c->device));
       wave_pack_kernel<<<pack_grid, 256, 0, c->stream>>>(sw[k].la);
+      wave_pack_pending_kernel<<<std::max(1, std::min(4 * c->num_sms, (work + 255) / 256)), 256, 0, c->stream>>>(sw[k].la);
       CK(cudaGetLastError());
     }
     int rc = group_allreduce_sum_i32(ctx, g, gb.data(), count);

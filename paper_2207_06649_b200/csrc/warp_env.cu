@@ -540,6 +540,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPG_ASYNC_BLOCKS) lock_as
           // (m1 from the first pass is a lower bound of W(r)[b1]; with m1 = 0,
           // hi covers every node with the fresher W of the second pass)
           const bool robust = strag == 0 || !a.leaf_parallel ||  // (no re-purposing: the decision is -1 anyway)
+                              (a.n_nodes == 1 && m1 > 0) ||        // one node: nothing can overtake it
                               (far >= 0 && (m1 > 0 ? (lo + slack < m1 && hi + slack <= m1) : (far == 0 && hi == 0)));
           if (robust) {
             if (l == 0) {
@@ -849,19 +850,43 @@ __global__ void wave_pack_kernel(LockArgs a) {
   lock_dyn(a);
   const int P = a.n_nodes;
   const bool fresh = a.a_ctl[4] == 0;
-  const int total = kAsyncK * P + 2 * kAsyncK;
+  // [K][P] W | [K][2] (arrived, gone) | round r_p | near | P(r_p)[P]: the
+  // pending bounds of the envs READY for the next undecided round r_p
+  // (r_p from shard 0 only, so the sum is r_p; wave_pack_pending_kernel
+  // adds the bounds)
+  const int total = kAsyncK * P + 2 * kAsyncK + 2 + P;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     int v = 0;
     if (!fresh) {
       if (i < kAsyncK * P) {
         v = a.a_W[(i / P) * a.a_wcap + i % P];
-      } else {
+      } else if (i < kAsyncK * P + 2 * kAsyncK) {
         const int k = i - kAsyncK * P;
         v = a.a_ctr[kRingCtr * (k >> 1) + (k & 1)];
+      } else if (i == kAsyncK * P + 2 * kAsyncK && a.shard_r == 0) {
+        v = a.a_ctl[9] + 1;
       }
     }
     a.g_ring[i] = v;
   }
+}
+
+__global__ void wave_pack_pending_kernel(LockArgs a) {
+  lock_dyn(a);
+  if (a.a_ctl[4] == 0) return;
+  const int P = a.n_nodes;
+  const int rp = a.a_ctl[9] + 1;
+  int32_t* near = a.g_ring + kAsyncK * P + 2 * kAsyncK + 1;
+  int32_t* Pp = near + 1;
+  int cnt = 0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < a.used; e += gridDim.x * blockDim.x) {
+    const int st = a.env_state[e];
+    if ((st == kReady || st == kPhys) && a.env_round[e] + 1 == rp) {
+      atomicAdd(&Pp[a.env_node[e]], a.cap - 1 - a.env_pushes[e]);
+      ++cnt;
+    }
+  }
+  if (cnt) atomicAdd(near, cnt);
 }
 
 // Between waves (one block): decide every round whose re-purposing target is
@@ -888,8 +913,10 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
   };
   auto arr_of = [&](int r) { return sharded ? a.g_ring[kAsyncK * P + 2 * (r % kAsyncK)] : ring_ctr(a, r)[0]; };
   auto gone_of = [&](int r) { return sharded ? a.g_ring[kAsyncK * P + 2 * (r % kAsyncK) + 1] : ring_ctr(a, r)[1]; };
-  __shared__ int s_H, s_G, s_D, s_ns, s_np, s_prog, s_strag, s_try, s_F0;
-  __shared__ int s_m1[32], s_b1[32], s_m2[32], s_rep[32], s_ret[32];
+  __shared__ int s_H, s_G, s_D, s_ns, s_np, s_prog, s_strag, s_try, s_F0, s_near, s_usep;
+  __shared__ int s_m1[32], s_b1[32], s_m2[32], s_rep[32], s_ret[32], s_lo[32], s_hi[32];
+  constexpr int kWaveP = 4096;  // pending bounds kept per node in shared memory up to this many nodes
+  __shared__ int s_P[kWaveP];
   if (ctl[4] == 0) {  // first wave of the call: every env READY or GONE at round 0
     if (tid == 0) s_G = 0;
     __syncthreads();
@@ -948,6 +975,40 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
     if (s_try) {
       const int r = s_D + 1;
       const int32_t* W = W_of(r);
+      // pending bounds of the envs READY (or in physics) for round r: their
+      // node and cap - 1 - pushes (lock_async_kernel's rule); sharded, the
+      // summed bounds of the exchange when they are for this round
+      const int32_t* gP = nullptr;
+      if (tid == 0) {
+        s_usep = 0;
+        s_near = 0;
+        if (sharded) {
+          const int base = kAsyncK * P + 2 * kAsyncK;
+          if (a.g_ring[base] == r) {
+            s_usep = 2;
+            s_near = a.g_ring[base + 1];
+          }
+        } else if (a.leaf_parallel && a.n_nodes > 1 && a.n_nodes <= kWaveP) {
+          s_usep = 1;  // (one node: no competitor, decided below without the scan)
+        }
+      }
+      __syncthreads();
+      if (s_usep == 1) {
+        for (int i = tid; i < a.n_nodes; i += B) s_P[i] = 0;
+        __syncthreads();
+        int cnt = 0;
+        for (int e = tid; e < used; e += B) {
+          const int st = a.env_state[e];
+          if ((st == kReady || st == kPhys) && a.env_round[e] + 1 == r) {
+            atomicAdd(&s_P[a.env_node[e]], a.cap - 1 - a.env_pushes[e]);
+            ++cnt;
+          }
+        }
+        if (cnt) atomicAdd(&s_near, cnt);
+        __syncthreads();
+      } else if (s_usep == 2) {
+        gP = a.g_ring + kAsyncK * P + 2 * kAsyncK + 2;
+      }
       int m1 = 0, b1 = -1, m2 = 0;
       for (int i = tid; i < a.n_nodes; i += B) top2_merge(m1, b1, m2, W[i], i, 0);
 #pragma unroll
@@ -970,14 +1031,55 @@ __global__ void __launch_bounds__(1024) wave_harvest_kernel(const __grid_constan
           top2_merge(m1, b1, m2, __shfl_xor_sync(kFull, m1, off), __shfl_xor_sync(kFull, b1, off),
                      __shfl_xor_sync(kFull, m2, off));
         if (tid == 0) {
-          const int strag = s_strag;
-          if (strag == 0 || (m1 > 0 && m2 + strag * (a.cap - 1) < m1)) {
-            int32_t* rc = ring_ctr(a, r);
-            rc[4] = (a.leaf_parallel && m1 > 0) ? b1 : -1;
-            rc[3] = r;
-            s_D = r;
-            s_prog = 1;
+          s_m1[0] = m1;  // broadcast (m1, b1, m2) for the pending-bound pass
+          s_b1[0] = b1;
+          s_m2[0] = m2;
+        }
+      }
+      __syncthreads();
+      m1 = s_m1[0];
+      b1 = s_b1[0];
+      m2 = s_m2[0];
+      __syncthreads();
+      int lo = 0, hi = 0;
+      if (s_usep) {  // the most any other node can still reach, by its side of b1
+        for (int i = tid; i < a.n_nodes; i += B) {
+          const int v = W[i] + (s_usep == 1 ? s_P[i] : gP[i]);
+          if (i < b1) lo = max(lo, v);
+          else if (i > b1) hi = max(hi, v);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          lo = max(lo, __shfl_xor_sync(kFull, lo, off));
+          hi = max(hi, __shfl_xor_sync(kFull, hi, off));
+        }
+        if (lane == 0) {
+          s_lo[wid] = lo;
+          s_hi[wid] = hi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          for (int w = 1; w < (B >> 5); ++w) {
+            lo = max(lo, s_lo[w]);
+            hi = max(hi, s_hi[w]);
           }
+        }
+      }
+      if (tid == 0) {
+        const int strag = s_strag;
+        bool robust = strag == 0 || !a.leaf_parallel ||  // (no re-purposing: the decision is -1 anyway)
+                      (a.n_nodes == 1 && m1 > 0);          // one node: nothing can overtake it
+        if (!robust && s_usep) {
+          const int far = strag - s_near, slack = far * (a.cap - 1);
+          robust = far >= 0 && (m1 > 0 ? (lo + slack < m1 && hi + slack <= m1) : (far == 0 && hi == 0));
+        }
+        if (!robust) robust = m1 > 0 && m2 + strag * (a.cap - 1) < m1;
+        if (robust) {
+          int32_t* rc = ring_ctr(a, r);
+          rc[4] = (a.leaf_parallel && m1 > 0) ? b1 : -1;
+          rc[3] = r;
+          s_D = r;
+          s_prog = 1;
         }
       }
       __syncthreads();

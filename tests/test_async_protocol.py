@@ -262,7 +262,7 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=
                 b1 = b if m1 > 0 else -1
                 lo = max([vals[i] for i in range(n_nodes) if i < b1], default=0)
                 hi = max([vals[i] for i in range(n_nodes) if i > b1], default=0)
-                ok = strag == 0 or not leaf_parallel or (
+                ok = strag == 0 or not leaf_parallel or (n_nodes == 1 and m1 > 0) or (
                     far >= 0 and ((lo + slack < m1 and hi + slack <= m1) if m1 > 0 else (far == 0 and hi == 0)))
             else:
                 ok = strag == 0 or (m1 > 0 and m2 + strag * (cap - 1) < m1)
@@ -721,7 +721,7 @@ def test_pending_bound_decisions_equal_lockstep(seed, K):
     their own node's W, the rest any node) keep the decisions exact, on
     search-like batches (many nodes, one or two envs each) and wide ones."""
     cap = 10
-    for n_nodes, n_envs in ((3 + seed % 9, 3 + seed % 9 + 20 + 7 * seed), (20 + 3 * seed, 64)):
+    for n_nodes, n_envs in ((3 + seed % 9, 3 + seed % 9 + 20 + 7 * seed), (20 + 3 * seed, 64), (1, 40 + seed)):
         nodes = _nodes(seed, n_nodes, cap)
         for leaf in (True, False):
             ref = lockstep(nodes, n_envs, leaf, cap, seed)
