@@ -325,10 +325,12 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=
         else:  # advance F
             r = x
             G += gone_at.pop(r, 0)
-            arrive.pop(r, None)
+            ran = arrive.pop(r, 0) > 0
             ring_W.pop(r, None)
             F = r
-            if G + gone_at[F + 1] < used:
+            # the kernel counts round r when it completes (round 1 at the start):
+            # gone(r + 1) may still miss retirements of waiting envs here
+            if r >= 2 and ran:
                 rounds += 1
     return rewards, calls, rounds, early
 
