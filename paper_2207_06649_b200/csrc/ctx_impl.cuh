@@ -204,7 +204,7 @@ struct ppg_ctx {
   ppg::DevBuf l_around, l_astate, l_aW, l_actr, l_adl, l_actl;  // asynchronous lockstep state
   int async_mode = -1;                    // -1 not read, 0 off (PPG_ASYNC=0), 1 on
   int wave_mode = -1;                     // -1 not read, 0 off (PPG_WAVE=0), 1 on
-  int wave_budget = 192;                  // projection iterations per env per wave (PPG_WAVE_BUDGET)
+  int wave_budget = 160;                  // projection iterations per env per wave (PPG_WAVE_BUDGET)
   int wave_switch = 12288;                // envs still running below which waves hand over to async (PPG_WAVE_SWITCH)
   ppg::DevBuf l_fin, l_rsi, l_ract;       // wave rounds: post list, resumable physics progress
   ppg::DevBuf l_gring;                   // sharded wave rounds: the exchanged ring (LockArgs.g_ring)
