@@ -113,8 +113,17 @@ PPG_DI bool collides_gripper_start(const PoseView& P, const ShapeView& S, const 
   const double r = C.tip_r + C.tip_clear;
   const double h = C.side / 2.0;
   if (p.x - r < -h || p.x + r > h || p.y - r < -h || p.y + r > h) return true;
-  for (int i = 0; i < S.n; ++i)
+  for (int i = 0; i < S.n; ++i) {
+    if (S.kind_(i) == 0) {
+      // a disc farther than (r + radius)(1 + 1e-12) cannot pass the exact
+      // test (norm and the subtraction round by < 1e-15 relative): skip its
+      // square root; the rest take the reference's expression
+      const V2 dv = p - P.pos(i);
+      const double lim = r + S.rad_(i);
+      if (dv.x * dv.x + dv.y * dv.y > lim * lim * (1.0 + 1e-12)) continue;
+    }
     if (object_point_distance(P, S, i, p) < r) return true;
+  }
   return false;
 }
 
