@@ -693,7 +693,7 @@ def run_ours(args, world, rank, local):
                     "api": "ppg_batch_resolve (host C-ABI, pinned buffers): inputs copied in 16K-env slices "
                            "while ONE physics launch runs (stream-memop ready flags), results written by the "
                            "kernel straight to the pinned host buffers"},
-            "roofline": roof, "clocks": clk, "gpu_launches": 2 * args.steps,
+            "roofline": roof, "clocks": clk, "gpu_launches": args.steps,  # one resolve_disc_kernel per step
             "status_counts": np.bincount(status, minlength=3).tolist(), "sweep_env_steps_per_s": sweep,
             "workload_gen_s": gen_s}
     if not args.no_c5:

@@ -1025,10 +1025,24 @@ int ppg_batch_resolve_dev(ppg_ctx* ctx, const ppg_shapes* shapes_dev, const doub
   if (E == 0) return PPG_SUCCESS;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool discs = !shapes_dev->n_vertices && !shapes_dev->vertices;  // documented contract
+  const int n = shapes_dev->n_objects;
+  if (discs && shapes_dev->n_tables == E && n >= 1 && n <= kMaxObjects && use_disc(ctx, true, n) &&
+      !use_warp(ctx, true, n, E, false)) {
+    // the lane-per-env disc kernel reads the caller's [E][n] radius table as
+    // is (env-major strides): no shape-table transpose / vertex-table fill
+    ShapesDev S;
+    S.rad = const_cast<double*>(shapes_dev->radius);
+    S.T = E;
+    S.n = n;
+    ResolveArgs a{S, poses_in, pushes, poses_out, status, residual, nullptr, E};
+    a.rad_env_major = true;
+    const SimConst C = make_const(ctx->params, n, shapes_dev->side_length, shapes_dev->boundary_margin);
+    return launch_disc(ctx, C, a, n, E, st, true, 0, false);
+  }
   ShapesDev S;
   const int rc = upload_shapes(ctx, shapes_dev, true, ctx->shape_in, ctx->shape_buf, S, st);
   if (rc != PPG_SUCCESS) return rc;
-  const bool discs = !shapes_dev->n_vertices && !shapes_dev->vertices;  // documented contract
   return launch_resolve(ctx, S, discs, shapes_dev->side_length, shapes_dev->boundary_margin, poses_in, pushes, E,
                         poses_out, status, residual, nullptr, st);
 }
