@@ -6,7 +6,7 @@ reference's batch_resolve / batch_expand / batch_simulate behind a C-ABI
 default (csrc/dtree.cu: one CUDA-graph launch per PMBS iteration); the host
 C++ tree (csrc/planner.cpp) is selectable.  Multi-GPU contexts
 (Context.multi / Context.rank, csrc/multi.cu) shard the rollout batch over
-GPUs with one NCCL all-reduce per lockstep round.  This package is the thin
+GPUs with one NCCL all-reduce per wave (disc scenes) or per lockstep round.  This package is the thin
 Python binding.
 """
 from .abi import default_params, load_library  # noqa: F401
