@@ -195,7 +195,7 @@ def asynchronous(nodes, n_envs, leaf_parallel, cap, seed, K, rng):
     return rewards, calls, rounds
 
 
-def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=False):
+def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=False, speculate=False):
     """Protocol v2 (the device's lock_async_kernel): the harvester DECIDES
     round r as soon as the argmax of W(r) is robust to the envs that have not
     finished round r yet (each can still add at most cap - 1 to one node):
@@ -222,9 +222,10 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=
                 inc[e] += 1
                 tasks[e] = Cursor(best0, e, nodes, cap, seed, inc[e])
                 calls.append((best0, e))
-    READY, AWAIT, GONE = 0, 1, 2
+    READY, AWAIT, GONE, SPEC = 0, 1, 2, 3
     state = [GONE if tasks[e].done else READY for e in range(used)]
     rnd = [0] * used
+    held = {}  # speculation: env -> (likely node, the new cursor after its first step)
     ring_W = defaultdict(lambda: [0] * n_nodes)
     arrive, gone_at = defaultdict(int), defaultdict(int)
     # pending bounds (the kernel's a_P ring): per round, per node, the most the
@@ -241,11 +242,19 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=
     early = 0
     while True:
         acts = []
+        likely = -1  # the harvester's likely decision of round D + 1: argmax(W + P)
+        if speculate and leaf_parallel and D + 1 <= F + K - 1:
+            vals = [ring_W[D + 1][i] + Pend[D + 1][i] for i in range(n_nodes)]
+            vb = max(vals)
+            likely = vals.index(vb) if vb > 0 else -1
         for e in range(used):
             if state[e] == READY and rnd[e] + 1 <= F + K - 1:
                 acts.append(("step", e))
-            elif state[e] == AWAIT and rnd[e] in decided:
+            elif state[e] in (AWAIT, SPEC) and rnd[e] in decided:
                 acts.append(("apply", e))
+            elif (state[e] == AWAIT and likely >= 0 and rnd[e] == D + 1 and rnd[e] + 1 <= F + K - 1
+                  and D + 1 not in decided):
+                acts.append(("spec", e))
         # harvester: decide round D + 1 if robust
         r = D + 1
         if r <= F + K - 1 and (r not in decided):
@@ -295,21 +304,51 @@ def asynchronous_early(nodes, n_envs, leaf_parallel, cap, seed, K, rng, pending=
                     state[e] = GONE
                     gone_at[r + 1] += 1
             arrive[r] += 1
+        elif kind == "spec":  # a held step at the likely decision (nothing published)
+            e = x
+            c = Cursor(likely, e, nodes, cap, seed, inc[e] + 1)
+            assert not c.done
+            c.step()
+            held[e] = (likely, c)
+            state[e] = SPEC
         elif kind == "apply":
             e = x
             b = decided[rnd[e]]
-            if b >= 0:
-                env_node[e] = b
+            if state[e] == SPEC and held[e][0] == b:  # the held step stands: publish it as round rnd + 1
+                node, c = held.pop(e)
+                env_node[e] = node
                 inc[e] += 1
-                tasks[e] = Cursor(b, e, nodes, cap, seed, inc[e])
-                assert not tasks[e].done
-                calls.append((b, e))
-                state[e] = READY
-                Pend[rnd[e] + 1][b] += cap - 1 - tasks[e].pushes
-                near_n[rnd[e] + 1] += 1
+                tasks[e] = c
+                calls.append((node, e))
+                r = rnd[e] + 1
+                rnd[e] = r
+                if not c.done:
+                    ring_W[r][node] += c.max_remaining()
+                    Pend[r + 1][node] += cap - 1 - c.pushes
+                    near_n[r + 1] += 1
+                    state[e] = READY
+                else:
+                    rewards[node] = max(rewards[node], c.reward)
+                    if c.by_grasp:
+                        state[e] = AWAIT
+                    else:
+                        state[e] = GONE
+                        gone_at[r + 1] += 1
+                arrive[r] += 1
             else:
-                state[e] = GONE
-                gone_at[rnd[e] + 1] += 1
+                held.pop(e, None)  # discarded
+                if b >= 0:
+                    env_node[e] = b
+                    inc[e] += 1
+                    tasks[e] = Cursor(b, e, nodes, cap, seed, inc[e])
+                    assert not tasks[e].done
+                    calls.append((b, e))
+                    state[e] = READY
+                    Pend[rnd[e] + 1][b] += cap - 1 - tasks[e].pushes
+                    near_n[rnd[e] + 1] += 1
+                else:
+                    state[e] = GONE
+                    gone_at[rnd[e] + 1] += 1
         elif kind == "decide":
             r = x
             W = ring_W[r]
@@ -733,3 +772,21 @@ def test_pending_bound_decisions_equal_lockstep(seed, K):
                 assert got[0] == ref[0], (leaf, sched)
                 assert sorted(got[1]) == sorted(ref[1]), (leaf, sched)
                 assert got[2] == ref[2], (leaf, sched)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("K", [2, 4, 16])
+def test_speculative_repurposing_equals_lockstep(seed, K):
+    """Speculative re-purposing (the kernel's kSpec state): a waiting env
+    steps at the likely decision (argmax W + P) and holds the step; a step
+    published at the decision, or discarded, gives the reference's results."""
+    cap = 10
+    for n_nodes, n_envs in ((3 + seed % 9, 3 + seed % 9 + 20 + 7 * seed), (20 + 3 * seed, 64), (1, 40 + seed)):
+        nodes = _nodes(seed, n_nodes, cap)
+        ref = lockstep(nodes, n_envs, True, cap, seed)
+        for sched in range(3):
+            got = asynchronous_early(nodes, n_envs, True, cap, seed, K, random.Random(53 * seed + sched),
+                                     pending=True, speculate=True)
+            assert got[0] == ref[0], sched
+            assert sorted(got[1]) == sorted(ref[1]), sched
+            assert got[2] == ref[2], sched
