@@ -31,6 +31,8 @@ __global__ void expand_post_kernel(const __grid_constant__ SimConst C, ExpandArg
 __global__ void poly_order_key_kernel(ResolveArgs a, unsigned* key, int* val);
 template <bool kPoly>
 __global__ void sample_grasp_warp_kernel(const __grid_constant__ SimConst C, SampleArgs a);
+template <bool kPoly>
+__global__ void expand_post_warp_kernel(const __grid_constant__ SimConst C, ExpandArgs a);
 template <int NW, bool kPoly>
 __global__ void resolve_warp_kernel(const __grid_constant__ SimConst C, ResolveArgs a);
 template <int NW, bool kPoly>

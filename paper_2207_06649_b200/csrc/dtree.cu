@@ -1049,7 +1049,12 @@ int dt_round(ppg_ctx* ctx, DTreeState& S, cudaStream_t st, RoundMode m) {
 // iteration before batch_simulate (launched into a capturing stream).
 int dt_launch_pre(ppg_ctx* ctx, DTreeState& S, cudaStream_t st) {
   const int E = S.n_envs, n = S.n;
-  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E, true);
+  // large disc batches expand "hybrid": the pushes on the lane-per-env disc
+  // kernel (throughput), the children's untried lists and grasp flags one
+  // warp per pair (a lane-per-pair sampler walks its candidates serially)
+  const bool hybrid = ctx->scene_all_discs && n <= kDiscMaxN && ctx->disc_kernels && !ctx->warp_max_explicit &&
+                      ctx->hybrid_min_envs > 0 && E >= ctx->hybrid_min_envs;
+  const bool warp = !hybrid && use_warp(ctx, ctx->scene_all_discs, n, E, true);
   const bool disc = !warp && use_disc(ctx, ctx->scene_all_discs, n);
   const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
   const DTree& t = S.t;
@@ -1065,7 +1070,10 @@ int dt_launch_pre(ppg_ctx* ctx, DTreeState& S, cudaStream_t st) {
       ra.E_dev = &t.sc->n_pairs;
       const int rc = launch_disc(ctx, S.C, ra, n, E, st);
       if (rc != PPG_SUCCESS) return rc;
-      expand_post_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(S.C, a);
+      if (hybrid)
+        expand_post_warp_kernel<false><<<(E + kWarpsPerBlock - 1) / kWarpsPerBlock, kWarpsPerBlock * 32, 0, st>>>(S.C, a);
+      else
+        expand_post_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(S.C, a);
     } else {
       expand_kernel<<<(E + kBlock - 1) / kBlock, kBlock, smem_for(n), st>>>(S.C, a);
     }
@@ -1159,7 +1167,12 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
 int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
   cudaStream_t st = ctx->stream;
   const int E = S.n_envs, n = S.n;
-  const bool warp = use_warp(ctx, ctx->scene_all_discs, n, E, true);
+  // large disc batches expand "hybrid": the pushes on the lane-per-env disc
+  // kernel (throughput), the children's untried lists and grasp flags one
+  // warp per pair (a lane-per-pair sampler walks its candidates serially)
+  const bool hybrid = ctx->scene_all_discs && n <= kDiscMaxN && ctx->disc_kernels && !ctx->warp_max_explicit &&
+                      ctx->hybrid_min_envs > 0 && E >= ctx->hybrid_min_envs;
+  const bool warp = !hybrid && use_warp(ctx, ctx->scene_all_discs, n, E, true);
   const bool disc = !warp && use_disc(ctx, ctx->scene_all_discs, n);
   const int gg = std::max(1, std::min(4 * ctx->num_sms, (E * n * 3 + 255) / 256));
   const DTree& t = S.t;

@@ -240,6 +240,62 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_warp_kernel(const 
   }
 }
 
+// batch_expand prepare, hybrid (large batches of disc scenes): the pushes
+// were resolved in place on the child buffer by the lane-per-env disc kernel;
+// here one warp per (node, action) pair: dead child on failure, else the
+// child's full untried list and grasp flag (pmbs.cpp:82-93; the tail of
+// expand_warp_kernel).
+template <bool kPoly>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) expand_post_warp_kernel(const __grid_constant__ SimConst C,
+                                                                              ExpandArgs a) {
+  __shared__ double blk[kWarpsPerBlock][160];
+  PPG_POLY_SMEM
+  __shared__ unsigned valid[kWarpsPerBlock][32];
+  const int wib = threadIdx.x >> 5;
+  const int p = blockIdx.x * kWarpsPerBlock + wib;
+  if (p >= (a.P_dev ? *a.P_dev : a.P)) return;
+  const int n = C.n, l = threadIdx.x & 31;
+  double* child = a.child_poses + static_cast<size_t>(p) * n * 3;
+  if (a.status[p] != 0) {  // dead child: copy of the parent state (mcts.cpp:89-92)
+    const double* parent = a.parent_poses + static_cast<size_t>(p) * n * 3;
+    for (int i = l; i < n * 3; i += 32) child[i] = parent[i];
+    if (l == 0) {
+      a.grasp[p] = 0;
+      a.n_untried[p] = 0;
+    }
+    return;
+  }
+  WarpEnv W(blk[wib], n, l);
+  const ShapeView S = a.S.view(0);
+  const WarpPoly G{poly_wv[kPoly ? wib : 0], poly_cen[kPoly ? wib : 0]};
+  warp_load_any<kPoly>(W, G, child, S);
+  const int count = warp_sample_mask(W, S, C, valid[wib]);
+  const int nw = (n * C.na + 31) >> 5;
+  double* out = a.untried + static_cast<size_t>(p) * n * C.na * 4;
+  const PoseView PV = W.view();
+  int base = 0;
+  for (int w = 0; w < nw; ++w) {
+    const unsigned b = valid[wib][w];
+    if (b >> l & 1u) {
+      const int c = 32 * w + l;
+      V2 s0, t0;
+      push_candidate(PV, S, C, c / C.na, c % C.na, false, s0, t0);
+      double* q = out + static_cast<size_t>(base + __popc(b & ((1u << l) - 1u))) * 4;
+      q[0] = s0.x;
+      q[1] = s0.y;
+      q[2] = t0.x;
+      q[3] = t0.y;
+    }
+    base += __popc(b);
+  }
+  const GraspOut g = warp_graspable(W, S, C, a.S.target[0]);
+  if (l == 0) {
+    a.n_untried[p] = count;
+    a.grasp[p] = g.graspable ? 1 : 0;
+  }
+}
+template __global__ void expand_post_warp_kernel<false>(const __grid_constant__ SimConst, ExpandArgs);
+
 // RolloutCursor::step (mcts.cpp:142-171) of env e by the calling warp:
 // sample + pick + resolve + graspable, state in HBM (env_*), the warp's
 // shared blocks `blk` / `valid` / the polygon caches as scratch.
