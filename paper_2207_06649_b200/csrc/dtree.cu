@@ -31,6 +31,7 @@
 // The final tree is read back once for best_root_child (mcts.cpp:218-235)
 // and the tree signature (mcts.cpp:284-300).
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <chrono>
@@ -48,7 +49,8 @@
 
 namespace ppg {
 
-constexpr int kMaxTreeDepth = 32;  // ancestor row stride; node depths <= tree_depth < 32
+constexpr int kMaxTreeDepth = 32;
+constexpr int kWideBackprop = 8192;  // batches from this size backprop regrouped by ancestor  // ancestor row stride; node depths <= tree_depth < 32
 
 struct DTScal {
   int n_nodes;
@@ -679,6 +681,58 @@ __global__ void __launch_bounds__(32) dt_backprop_kernel(DTree t) {
   }
 }
 
+// Wide batches: the same backprop with the pairs regrouped by ancestor.
+// Entry (p, d) = (ancestor of new node p at depth d, p); a stable sort by
+// ancestor keeps each ancestor's pairs in batch order, and one thread folds
+// each ancestor's rewards in that order — the FP64 sums of the sequential
+// fold, without 32 lanes stepping through every pair.
+__global__ void dt_bp_keys_kernel(DTree t, int dmax, int* keys, int* vals) {
+  const DTScal* sc = t.sc;
+  const int P = sc->n_pairs, N = sc->n_nodes, base = N - P;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int E = t.n_envs;
+  if (i >= E * dmax) return;
+  const int p = i / dmax, d = i - p * dmax;
+  int key = INT_MAX;
+  if (p < P) {
+    const int id = base + p;
+    const int D = t.depth[id];
+    if (d == 0) {  // the new node itself
+      t.q[id] = 0.0 + __longlong_as_double(static_cast<long long>(t.rew[p]));
+      t.visits[id] = 1;
+    }
+    if (d < D) {
+      const int a = t.anc[static_cast<size_t>(id) * kMaxTreeDepth + d];
+      if (a < 0 || a >= N) {  // corrupt ancestor row: report, do not touch memory
+        if (atomicCAS(const_cast<int*>(&sc->err[0]), 0, 1) == 0) {
+          const_cast<DTScal*>(sc)->err[1] = id;
+          const_cast<DTScal*>(sc)->err[2] = d;
+          const_cast<DTScal*>(sc)->err[3] = a;
+        }
+      } else {
+        key = a;
+      }
+    }
+  }
+  keys[i] = key;
+  vals[i] = p;
+}
+
+__global__ void dt_bp_fold_kernel(DTree t, const int* keys, const int* vals, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int a = keys[i];
+  if (a == INT_MAX || (i > 0 && keys[i - 1] == a)) return;  // not the head of an ancestor's run
+  double cq = t.q[a];
+  long long cv = t.visits[a];
+  for (int j = i; j < n && keys[j] == a; ++j) {
+    cq += __longlong_as_double(static_cast<long long>(t.rew[vals[j]]));
+    cv += 1;
+  }
+  t.q[a] = cq;
+  t.visits[a] = cv;
+}
+
 // End of an iteration: early stop (mcts.cpp:211-216) then the iteration
 // budget (pmbs.cpp:282-290).
 __global__ void dt_stop_kernel(DTree t) {
@@ -728,6 +782,7 @@ struct DTreeState {
   size_t hpin_cap = 0;
   DTScal* hsc = nullptr;  // pinned copy of the scalars, read after every iteration
   DevBuf dstage;
+  DevBuf bp_buf;  // wide-batch backprop: keys / values (x2) + sort scratch
   char* pinned(size_t bytes) {
     if (bytes > hpin_cap) {
       if (hpin) cudaFreeHost(hpin);
@@ -764,6 +819,7 @@ struct DTreeState {
     if (hsc) cudaFreeHost(hsc);
     hsc = nullptr;
     dstage.release();
+    bp_buf.release();
     DevBuf* bufs[] = {&parent, &depth, &q, &visits, &vv, &flags, &u_off, &u_n, &u_head, &c_n, &selc, &action,
                       &poses, &anc, &apool, &cpool, &sel_node, &sel_act, &gp, &ga, &cp, &st, &gr, &nu, &un,
                       &meta, &logtab, &sc, &l_node, &l_pushes, &l_done, &l_byg, &l_harv, &l_flag, &l_reward,
@@ -910,6 +966,14 @@ int dt_batch(ppg_ctx* ctx, DTreeState& S) {
   DCK(S.l_aW.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_aP.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_spec.ensure(static_cast<size_t>(E) * 16 + 16));
+  if (E >= kWideBackprop) {  // wide-batch backprop: keys / values (x2) + sort scratch, sized before capture
+    const int nbp = E * (ctx->params.tree_depth > 0 ? ctx->params.tree_depth : 1);
+    size_t scratch = 0;
+    DCK(cub::DeviceRadixSort::SortPairs(nullptr, scratch, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                        static_cast<const int*>(nullptr), static_cast<int*>(nullptr), nbp, 0, 32));
+    const size_t nn = (static_cast<size_t>(nbp) + 63) / 64 * 64;
+    DCK(S.bp_buf.ensure(nn * 4 * 4 + scratch));
+  }
   DCK(S.l_actr.ensure(static_cast<size_t>(kAsyncK) * kRingCtr * 4));
   DCK(S.l_adl.ensure(static_cast<size_t>(kAsyncK) * E * 4));
   DCK(S.l_fin.ensure(static_cast<size_t>(E) * 4 + 16));
@@ -1086,6 +1150,39 @@ int dt_launch_pre(ppg_ctx* ctx, DTreeState& S, cudaStream_t st) {
   return PPG_SUCCESS;
 }
 
+// backprop of an iteration (pmbs.cpp:236-240): one warp stepping the pairs
+// in batch order, or for wide batches the pairs regrouped by ancestor
+// (dt_bp_keys_kernel + a stable radix sort + dt_bp_fold_kernel).  Called
+// while capturing: the sort's scratch is sized here.
+int dt_launch_backprop(ppg_ctx* ctx, DTreeState& S, cudaStream_t st) {
+  const int E = S.n_envs;
+  const int dmax = ctx->params.tree_depth > 0 ? ctx->params.tree_depth : 1;
+  if (E < kWideBackprop) {
+    dt_backprop_kernel<<<1, 32, 0, st>>>(S.t);
+    DCK(cudaGetLastError());
+    return PPG_SUCCESS;
+  }
+  const int n = E * dmax;
+  size_t scratch = 0;  // (the buffer was sized with this query before capture)
+  DCK(cub::DeviceRadixSort::SortPairs(nullptr, scratch, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                      static_cast<const int*>(nullptr), static_cast<int*>(nullptr), n, 0, 32, st));
+  const size_t nn = (static_cast<size_t>(n) + 63) / 64 * 64;
+  if (S.bp_buf.cap < nn * 4 * 4 + scratch) {
+    ctx->err = "device tree: backprop scratch not reserved";
+    return PPG_EINVAL;
+  }
+  int* k_in = S.bp_buf.as<int>();
+  int* k_out = k_in + nn;
+  int* v_in = k_out + nn;
+  int* v_out = v_in + nn;
+  dt_bp_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(S.t, dmax, k_in, v_in);
+  DCK(cudaGetLastError());
+  DCK(cub::DeviceRadixSort::SortPairs(v_out + nn, scratch, k_in, k_out, v_in, v_out, n, 0, 32, st));
+  dt_bp_fold_kernel<<<(n + 255) / 256, 256, 0, st>>>(S.t, k_out, v_out, n);
+  DCK(cudaGetLastError());
+  return PPG_SUCCESS;
+}
+
 // With a simulate hook installed (the sharded multi-GPU driver) an iteration
 // is two graphs around the host call: pre (above) and post (backprop, stop).
 int dt_capture_hooked(ppg_ctx* ctx, DTreeState& S) {
@@ -1104,7 +1201,7 @@ int dt_capture_hooked(ppg_ctx* ctx, DTreeState& S) {
   S.graph = g;
   DCK(cudaGraphInstantiate(&S.exec, S.graph, 0));
   DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  dt_backprop_kernel<<<1, 32, 0, st>>>(S.t);
+  if (const int brc = dt_launch_backprop(ctx, S, st); brc != PPG_SUCCESS) return brc;
   dt_stop_kernel<<<1, 1, 0, st>>>(S.t);
   DCK(cudaStreamEndCapture(st, &S.graph_post));
   DCK(cudaGraphInstantiate(&S.exec_post, S.graph_post, 0));
@@ -1153,7 +1250,7 @@ int dt_capture(ppg_ctx* ctx, DTreeState& S) {
   const cudaError_t e2 = cudaStreamEndCapture(S.st2, &body_out);
   if (rc != PPG_SUCCESS) return rc;
   DCK(e2);
-  dt_backprop_kernel<<<1, 32, 0, st>>>(t);
+  if (const int brc = dt_launch_backprop(ctx, S, st); brc != PPG_SUCCESS) return brc;
   dt_stop_kernel<<<1, 1, 0, st>>>(t);
   DCK(cudaGetLastError());
   DCK(cudaStreamEndCapture(st, &S.graph));
@@ -1215,7 +1312,7 @@ int dt_iteration_debug(ppg_ctx* ctx, DTreeState& S) {
     if (act == 0) break;
     DSTEP("round", dt_round(ctx, S, st, mode));
   }
-  DSTEP("backprop", (dt_backprop_kernel<<<1, 32, 0, st>>>(t)));
+  DSTEP("backprop", (dt_launch_backprop(ctx, S, st)));
   DSTEP("stop", (dt_stop_kernel<<<1, 1, 0, st>>>(t)));
 #undef DSTEP
   return PPG_SUCCESS;
@@ -1560,7 +1657,7 @@ int dt_capture_sharded(ppg_ctx* ctx, DTreeState& S, int work) {
   S.graph_round = g;
   DCK(cudaGraphInstantiate(&S.exec_round, S.graph_round, 0));
   DCK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  dt_backprop_kernel<<<1, 32, 0, st>>>(S.t);
+  if (const int brc = dt_launch_backprop(ctx, S, st); brc != PPG_SUCCESS) return brc;
   dt_stop_kernel<<<1, 1, 0, st>>>(S.t);
   DCK(cudaStreamEndCapture(st, &S.graph_post));
   DCK(cudaGraphInstantiate(&S.exec_post, S.graph_post, 0));
